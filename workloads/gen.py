@@ -1,0 +1,212 @@
+"""Seeded synthetic workloads C1-C5 (BASELINE.json `configs`).
+
+This module holds input generators ONLY: it contains none of the method's
+arithmetic (no distances, no greedy, no membership).  It is the one module that
+both the oracle (`oracle/`) and the CUDA path consume, so that both sides see
+identical bytes.
+
+Reproducibility / prefix property
+---------------------------------
+Rows are generated in fixed chunks of ``CHUNK`` rows; chunk ``c`` of config
+seed ``s`` draws from ``numpy.random.default_rng([s, c])`` and the per-config
+parameters (centres, sigmas, templates, rotation) from
+``default_rng([s, PARAM_STREAM])``.  Hence ``generate(w, n=m)`` is exactly the
+first ``m`` rows of ``generate(w)`` — the prefix property the parity tests use
+for C3/C5 (the greedy landmarks below ``m`` depend only on rows below ``m``).
+
+The paper's own datasets are unspecified ("Datasets were generated",
+PAPER.md:263); BASELINE.json's five configs stand in for them.  C4 is shaped
+like a 70,000 x 28x28 uint8 handwritten-image set but is produced purely by the
+stroke model below; no record of any real dataset is used.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+CHUNK = 1 << 16
+PARAM_STREAM = 0xFFFF
+
+# dtype / metric codes shared with the C ABI by *name* only (no arithmetic).
+DTYPES = ("f32", "i8", "u8")
+METRICS = ("l2", "l1", "cos")
+
+
+@dataclass(frozen=True)
+class Workload:
+    name: str
+    config: str       # c1..c5
+    n: int
+    d: int
+    dtype: str        # "f32" | "i8" | "u8"
+    metric: str       # "l2" | "l1" | "cos"
+    eps: float
+    seed: int
+    text: str         # BASELINE.json configs[] text this stands in for
+
+    @property
+    def eps_text(self) -> str:
+        return f"{self.eps!r}"
+
+
+_C1 = BASELINE_C1 = ("N=2,000 points, d=3, int8 coordinates: mixture of 4 isotropic Gaussians "
+                     "(sigma=6, centres uniform in [-40,40]^3, rounded and clamped to [-64,64]), "
+                     "Euclidean, eps^2=60.5")
+_C2 = ("N=100,000, d=10, fp32: noisy torus (R=3, r=1) embedded in 10-D by a seeded random "
+       "orthogonal map plus N(0,0.05^2) noise per coordinate, Euclidean, eps=0.4")
+_C3 = ("N=1,000,000, d=64, fp32: mixture of 32 Gaussians (centres N(0,4^2 I), per-cluster sigma "
+       "uniform in [0.5,1.5]), Euclidean, eps sweep {2.0, 4.0, 8.0}")
+_C4 = ("N=70,000, d=784 (28x28 image-shaped), uint8 0-255: ~80% zeros, 3-6 Gaussian strokes per "
+       "sample from 10 seeded stroke templates with jitter; Euclidean on exact integers, "
+       "eps^2 = 2.5e6 + 0.5")
+_C5 = ("N=10,000,000, d=16, fp32 uniform on [0,1]^16 mixed 50/50 with a 16-D Gaussian blob "
+       "(sigma=0.1, centred at 0.5); metrics L1 (eps=2.0) and cosine distance (eps=0.05)")
+
+WORKLOADS: dict[str, Workload] = {}
+
+
+def _reg(w: Workload) -> None:
+    WORKLOADS[w.name] = w
+
+
+_reg(Workload("c1", "c1", 2000, 3, "i8", "l2", math.sqrt(60.5), 1, _C1))
+_reg(Workload("c2", "c2", 100_000, 10, "f32", "l2", 0.4, 2, _C2))
+for _e in (2.0, 4.0, 8.0):
+    _reg(Workload(f"c3_e{int(_e)}", "c3", 1_000_000, 64, "f32", "l2", _e, 3, _C3))
+_reg(Workload("c4", "c4", 70_000, 784, "u8", "l2", math.sqrt(2.5e6 + 0.5), 4, _C4))
+_reg(Workload("c5_l1", "c5", 10_000_000, 16, "f32", "l1", 2.0, 5, _C5))
+_reg(Workload("c5_cos", "c5", 10_000_000, 16, "f32", "cos", 0.05, 5, _C5))
+
+
+def get(name: str) -> Workload:
+    if name not in WORKLOADS:
+        raise KeyError(f"unknown workload {name!r}; known: {sorted(WORKLOADS)}")
+    return WORKLOADS[name]
+
+
+def _params(seed: int) -> np.random.Generator:
+    return np.random.default_rng([seed, PARAM_STREAM])
+
+
+def _chunk_rng(seed: int, c: int) -> np.random.Generator:
+    return np.random.default_rng([seed, c])
+
+
+# --------------------------------------------------------------------------- C1
+def _c1_chunk(seed, c, rows):
+    centres = _params(seed).uniform(-40.0, 40.0, size=(4, 3))
+    rng = _chunk_rng(seed, c)
+    lab = rng.integers(0, 4, size=CHUNK)[:rows]
+    x = centres[lab] + rng.normal(0.0, 6.0, size=(CHUNK, 3))[:rows]
+    return np.clip(np.rint(x), -64, 64).astype(np.int8)
+
+
+# --------------------------------------------------------------------------- C2
+def _c2_chunk(seed, c, rows):
+    pr = _params(seed)
+    q, r = np.linalg.qr(pr.normal(size=(10, 10)))
+    q = q * np.sign(np.diag(r))[None, :]          # unique orthogonal factor
+    rng = _chunk_rng(seed, c)
+    th = rng.uniform(0.0, 2 * math.pi, size=CHUNK)[:rows]
+    ph = rng.uniform(0.0, 2 * math.pi, size=CHUNK)[:rows]
+    R, r_ = 3.0, 1.0
+    p = np.zeros((rows, 10))
+    p[:, 0] = (R + r_ * np.cos(th)) * np.cos(ph)
+    p[:, 1] = (R + r_ * np.cos(th)) * np.sin(ph)
+    p[:, 2] = r_ * np.sin(th)
+    x = p @ q.T + rng.normal(0.0, 0.05, size=(CHUNK, 10))[:rows]
+    return x.astype(np.float32)
+
+
+# --------------------------------------------------------------------------- C3
+def _c3_chunk(seed, c, rows):
+    pr = _params(seed)
+    mu = pr.normal(0.0, 4.0, size=(32, 64))
+    sig = pr.uniform(0.5, 1.5, size=32)
+    rng = _chunk_rng(seed, c)
+    lab = rng.integers(0, 32, size=CHUNK)[:rows]
+    x = mu[lab] + sig[lab, None] * rng.normal(size=(CHUNK, 64))[:rows]
+    return x.astype(np.float32)
+
+
+# --------------------------------------------------------------------------- C4
+C4_TAU = 40.0  # intensity floor zeroed (tau ~40-70 for ~75-80% zeros)
+
+
+def _c4_chunk(seed, c, rows):
+    pr = _params(seed)
+    tmpl_pts = pr.uniform(4.0, 24.0, size=(10, 4))        # (x0, y0, x1, y1)
+    tmpl_w = pr.uniform(0.8, 1.6, size=10)
+    rng = _chunk_rng(seed, c)
+    k = rng.integers(3, 7, size=CHUNK)[:rows]              # U{3..6}
+    t = rng.integers(0, 10, size=(CHUNK, 6))[:rows]
+    jit = rng.normal(0.0, 1.5, size=(CHUNK, 6, 4))[:rows]
+    seg = tmpl_pts[t] + jit                                # (rows, 6, 4)
+    w = tmpl_w[t]                                          # (rows, 6)
+    active = np.arange(6)[None, :] < k[:, None]            # (rows, 6)
+    yy, xx = np.meshgrid(np.arange(28, dtype=np.float32), np.arange(28, dtype=np.float32),
+                         indexing="ij")
+    px = xx.reshape(1, 1, -1)
+    py = yy.reshape(1, 1, -1)                              # 784 pixel centres, row-major
+    seg = seg.astype(np.float32)
+    out = np.empty((rows, 784), dtype=np.uint8)
+    B = 1024
+    for s in range(0, rows, B):
+        e = min(rows, s + B)
+        ax, ay = seg[s:e, :, 0:1], seg[s:e, :, 1:2]        # (b, 6, 1)
+        dx, dy = seg[s:e, :, 2:3] - ax, seg[s:e, :, 3:4] - ay
+        den = np.maximum(dx * dx + dy * dy, np.float32(1e-12))
+        qx, qy = px - ax, py - ay                          # (b, 6, 784)
+        tt = np.clip((qx * dx + qy * dy) / den, 0.0, 1.0)
+        ex, ey = qx - tt * dx, qy - tt * dy
+        ww = w[s:e, :, None].astype(np.float32)
+        inten = np.exp(-(ex * ex + ey * ey) / (2.0 * ww * ww)) * active[s:e, :, None]
+        img = np.clip(255.0 * inten.sum(1), 0.0, 255.0)
+        img[img < C4_TAU] = 0.0
+        out[s:e] = np.rint(img).astype(np.uint8)
+    return out
+
+
+# --------------------------------------------------------------------------- C5
+def _c5_chunk(seed, c, rows):
+    rng = _chunk_rng(seed, c)
+    which = rng.random(CHUNK)[:rows] < 0.5
+    uni = rng.random((CHUNK, 16))[:rows]
+    blob = 0.5 + 0.1 * rng.normal(size=(CHUNK, 16))[:rows]
+    return np.where(which[:, None], uni, blob).astype(np.float32)
+
+
+_CHUNK_FN = {"c1": _c1_chunk, "c2": _c2_chunk, "c3": _c3_chunk, "c4": _c4_chunk, "c5": _c5_chunk}
+
+
+def generate(w: Workload | str, n: int | None = None) -> np.ndarray:
+    """Return the first ``n`` rows (default: all ``w.n``) of workload ``w``,
+    C-contiguous, dtype float32 / int8 / uint8, shape (n, d)."""
+    if isinstance(w, str):
+        w = get(w)
+    n = w.n if n is None else int(n)
+    if n < 0:
+        raise ValueError("n must be >= 0")
+    fn = _CHUNK_FN[w.config]
+    np_dtype = {"f32": np.float32, "i8": np.int8, "u8": np.uint8}[w.dtype]
+    out = np.empty((n, w.d), dtype=np_dtype)
+    for c in range((n + CHUNK - 1) // CHUNK):
+        s = c * CHUNK
+        rows = min(CHUNK, n - s)
+        out[s:s + rows] = fn(w.seed, c, rows)
+    return out
+
+
+def random_cloud(n: int, d: int, dtype: str = "f32", seed: int = 0, scale: float = 1.0,
+                 lo: int = -8, hi: int = 8) -> np.ndarray:
+    """Small generic seeded clouds for unit tests (uniform floats or integers)."""
+    rng = np.random.default_rng([seed, n, d])
+    if dtype == "f32":
+        return (rng.random((n, d)) * scale).astype(np.float32)
+    if dtype == "i8":
+        return rng.integers(max(lo, -128), min(hi, 127) + 1, size=(n, d)).astype(np.int8)
+    if dtype == "u8":
+        return rng.integers(max(lo, 0), min(hi, 255) + 1, size=(n, d)).astype(np.uint8)
+    raise ValueError(dtype)
