@@ -1,0 +1,301 @@
+"""Thin ctypes binding of include/bm.h (argument marshalling only).
+
+Every step of the cover construction runs inside libbm_b200.so; this module
+only converts torch / numpy buffers to pointers and wraps the returned
+``bm_cover``.  There is no CPU fallback: if the library is missing, importing
+or calling raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libbm_b200.so")
+
+BM_OK, BM_EINVAL, BM_EUNSUPPORTED, BM_ENOMEM, BM_ECUDA, BM_EOVERFLOW = range(6)
+STATUS_NAMES = {0: "BM_OK", 1: "BM_EINVAL", 2: "BM_EUNSUPPORTED", 3: "BM_ENOMEM",
+                4: "BM_ECUDA", 5: "BM_EOVERFLOW"}
+METRIC = {"l2": 0, "l1": 1, "cos": 2, "cosine": 2}
+DTYPE = {"f32": 0, "i8": 1, "u8": 2}
+PATH = {"auto": 0, "cuda_core": 1, "tensor": 2}
+STEPS = ("prep", "greedy", "member", "csr", "edges", "total")
+
+EXPORTED = ("bm_cover_build", "bm_cover_build_ex", "bm_cover_build_host", "bm_free",
+            "bm_last_error", "bm_version", "bm_debug_radix_sort_u64",
+            "bm_debug_exclusive_scan_i64", "bm_debug_resolve_tile")
+
+
+class BMError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+class _Options(ctypes.Structure):
+    _fields_ = [("struct_size", ctypes.c_int32), ("tile", ctypes.c_int32),
+                ("path", ctypes.c_int32), ("timing", ctypes.c_int32),
+                ("near_tie_cap", ctypes.c_int64), ("reserved", ctypes.c_int32 * 8)]
+
+
+class _Cover(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("d", ctypes.c_int32), ("dtype", ctypes.c_int32),
+                ("metric", ctypes.c_int32), ("on_host", ctypes.c_int32), ("eps", ctypes.c_double),
+                ("n_landmarks", ctypes.c_int64), ("landmarks", ctypes.c_void_p),
+                ("n_members", ctypes.c_int64), ("ball_ptr", ctypes.c_void_p),
+                ("ball_idx", ctypes.c_void_p), ("pt_ptr", ctypes.c_void_p),
+                ("pt_lm", ctypes.c_void_p),
+                ("n_edges", ctypes.c_int64), ("edges", ctypes.c_void_p),
+                ("n_pair_evals", ctypes.c_int64), ("n_greedy_evals", ctypes.c_int64),
+                ("n_band_pairs", ctypes.c_int64), ("n_near_ties", ctypes.c_int64),
+                ("n_near_ties_stored", ctypes.c_int64),
+                ("near_tie_pairs", ctypes.POINTER(ctypes.c_int64)),
+                ("n_greedy_tiles", ctypes.c_int64), ("n_launches", ctypes.c_int64),
+                ("path_used", ctypes.c_int32), ("tile_used", ctypes.c_int32),
+                ("step_ms", ctypes.c_float * 8), ("priv", ctypes.c_void_p)]
+
+
+_lib = None
+
+
+def load() -> ctypes.CDLL:
+    """Load libbm_b200.so (raises if it was not built — no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_2601_01405_b200.build` "
+                          "(there is no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    vp, i64, i32, dbl = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_double
+    pc = ctypes.POINTER(ctypes.POINTER(_Cover))
+    lib.bm_cover_build.argtypes = [vp, i32, i64, i32, i32, dbl, vp, pc]
+    lib.bm_cover_build_ex.argtypes = [vp, i32, i64, i32, i32, dbl, vp,
+                                      ctypes.POINTER(_Options), pc]
+    lib.bm_cover_build_host.argtypes = [vp, i32, i64, i32, i32, dbl, vp,
+                                        ctypes.POINTER(_Options), pc]
+    for f in (lib.bm_cover_build, lib.bm_cover_build_ex, lib.bm_cover_build_host):
+        f.restype = i32
+    lib.bm_free.argtypes = [ctypes.POINTER(_Cover)]
+    lib.bm_free.restype = None
+    lib.bm_last_error.restype = ctypes.c_char_p
+    lib.bm_version.restype = i32
+    lib.bm_debug_radix_sort_u64.argtypes = [vp, i64, i32, vp]
+    lib.bm_debug_radix_sort_u64.restype = i32
+    lib.bm_debug_exclusive_scan_i64.argtypes = [vp, vp, i64, ctypes.POINTER(i64), vp]
+    lib.bm_debug_exclusive_scan_i64.restype = i32
+    lib.bm_debug_resolve_tile.argtypes = [vp, i32, vp, vp]
+    lib.bm_debug_resolve_tile.restype = i32
+    _lib = lib
+    return lib
+
+
+def _check(rc: int):
+    if rc != BM_OK:
+        raise BMError(rc, load().bm_last_error().decode())
+
+
+def _options(tile=0, path="auto", timing=False, near_tie_cap=0) -> _Options:
+    o = _Options()
+    o.struct_size = ctypes.sizeof(_Options)
+    o.tile = int(tile)
+    o.path = PATH[path] if isinstance(path, str) else int(path)
+    o.timing = 1 if timing else 0
+    o.near_tie_cap = int(near_tie_cap)
+    return o
+
+
+class _DevArray:
+    """__cuda_array_interface__ view of a library-owned device array."""
+
+    def __init__(self, ptr, shape, typestr):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
+                                         "data": (int(ptr or 0), False), "version": 3,
+                                         "strides": None}
+
+
+@dataclass
+class CoverStats:
+    n_pair_evals: int
+    n_greedy_evals: int
+    n_band_pairs: int
+    n_near_ties: int
+    n_greedy_tiles: int
+    n_launches: int
+    path_used: int
+    tile_used: int
+    step_ms: dict
+
+
+class Cover:
+    """Owns one bm_cover.  Device arrays are exposed as torch tensors that
+    alias library memory (valid until .free()); .numpy() copies to host."""
+
+    def __init__(self, ptr):
+        self._ptr = ptr
+        c = ptr.contents
+        self.n, self.d, self.eps = c.n, c.d, c.eps
+        self.L, self.M, self.E = c.n_landmarks, c.n_members, c.n_edges
+        self.on_host = bool(c.on_host)
+        self.stats = CoverStats(c.n_pair_evals, c.n_greedy_evals, c.n_band_pairs,
+                                c.n_near_ties, c.n_greedy_tiles, c.n_launches, c.path_used,
+                                c.tile_used, {k: float(c.step_ms[i]) for i, k in
+                                              enumerate(STEPS[:5])} |
+                                {"total": float(c.step_ms[5])})
+        k = c.n_near_ties_stored
+        if k > 0:
+            self.near_ties = np.ctypeslib.as_array(c.near_tie_pairs, shape=(k, 3)).copy()
+        else:
+            self.near_ties = np.zeros((0, 3), dtype=np.int64)
+
+    def _spec(self):
+        c = self._ptr.contents
+        return {"landmarks": (c.landmarks, (self.L,), "<i4"),
+                "ball_ptr": (c.ball_ptr, (self.L + 1,), "<i8"),
+                "ball_idx": (c.ball_idx, (self.M,), "<i4"),
+                "pt_ptr": (c.pt_ptr, (self.n + 1,), "<i8"),
+                "pt_lm": (c.pt_lm, (self.M,), "<i4"),
+                "edges": (c.edges, (self.E, 2), "<i4")}
+
+    def tensors(self) -> dict:
+        """Zero-copy torch views of the device arrays (device covers only)."""
+        if self.on_host:
+            raise ValueError("host cover: use .numpy()")
+        import torch
+        out = {}
+        for name, (p, shape, ts) in self._spec().items():
+            if int(np.prod(shape)) == 0:
+                dt = torch.int32 if ts == "<i4" else torch.int64
+                out[name] = torch.zeros(shape, dtype=dt, device="cuda")
+            else:
+                out[name] = torch.as_tensor(_DevArray(p, shape, ts), device="cuda")
+        return out
+
+    def numpy(self) -> dict:
+        if self.on_host:
+            out = {}
+            for name, (p, shape, ts) in self._spec().items():
+                ct = ctypes.c_int32 if ts == "<i4" else ctypes.c_int64
+                n = int(np.prod(shape))
+                if n == 0:
+                    out[name] = np.zeros(shape, dtype=np.dtype(ts))
+                else:
+                    arr = np.ctypeslib.as_array(ctypes.cast(p, ctypes.POINTER(ct)), shape=(n,))
+                    out[name] = arr.copy().reshape(shape)
+            return out
+        return {k: v.cpu().numpy() for k, v in self.tensors().items()}
+
+    def free(self):
+        if self._ptr is not None:
+            load().bm_free(self._ptr)
+            self._ptr = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def _dtype_of(t) -> str:
+    s = str(t.dtype)
+    if s.endswith("float32"):
+        return "f32"
+    if s.endswith("uint8"):
+        return "u8"
+    if s.endswith("int8"):
+        return "i8"
+    raise ValueError(f"unsupported dtype {t.dtype}")
+
+
+def cover_build(points, metric: str, eps: float, stream=None, tile: int = 0,
+                path: str = "auto", timing: bool = False, near_tie_cap: int = 0) -> Cover:
+    """bm_cover_build_ex on a CUDA torch tensor [n, d] (row-major, contiguous)."""
+    import torch
+    if not (isinstance(points, torch.Tensor) and points.is_cuda):
+        raise TypeError("points must be a CUDA torch tensor (use cover_build_host for host data)")
+    if points.dim() != 2:
+        raise ValueError("points must be 2-D [n, d]")
+    points = points.contiguous()
+    n, d = points.shape
+    if stream is None:
+        stream = torch.cuda.current_stream(points.device)
+    sp = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+    out = ctypes.POINTER(_Cover)()
+    o = _options(tile, path, timing, near_tie_cap)
+    lib = load()
+    with torch.cuda.device(points.device):
+        rc = lib.bm_cover_build_ex(ctypes.c_void_p(points.data_ptr()), DTYPE[_dtype_of(points)],
+                                   n, d, METRIC[metric], float(eps), ctypes.c_void_p(sp),
+                                   ctypes.byref(o), ctypes.byref(out))
+    _check(rc)
+    return Cover(out)
+
+
+def cover_build_host(points: np.ndarray, metric: str, eps: float, stream=None, tile: int = 0,
+                     path: str = "auto", timing: bool = False, near_tie_cap: int = 0) -> Cover:
+    """bm_cover_build_host on a host buffer (numpy array or CPU torch tensor,
+    ideally pinned): copies in, builds, copies every result back to host."""
+    import torch
+    if isinstance(points, torch.Tensor):
+        if points.is_cuda:
+            raise TypeError("cover_build_host takes host memory")
+        points = points.contiguous()
+        ptr, (n, d), dt = points.data_ptr(), points.shape, _dtype_of(points)
+    else:
+        points = np.ascontiguousarray(points)
+        ptr, (n, d) = points.ctypes.data, points.shape
+        dt = {np.dtype(np.float32): "f32", np.dtype(np.int8): "i8",
+              np.dtype(np.uint8): "u8"}[points.dtype]
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    sp = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+    out = ctypes.POINTER(_Cover)()
+    o = _options(tile, path, timing, near_tie_cap)
+    rc = load().bm_cover_build_host(ctypes.c_void_p(ptr), DTYPE[dt], n, d, METRIC[metric],
+                                    float(eps), ctypes.c_void_p(sp), ctypes.byref(o),
+                                    ctypes.byref(out))
+    _check(rc)
+    return Cover(out)
+
+
+def raw_build(ptr: int, dtype: str, n: int, d: int, metric: str, eps: float, stream: int = 0):
+    """bm_cover_build with raw arguments (ABI tests: NULL pointers, bad sizes)."""
+    out = ctypes.POINTER(_Cover)()
+    rc = load().bm_cover_build(ctypes.c_void_p(ptr), DTYPE.get(dtype, dtype) if isinstance(
+        dtype, str) else dtype, n, d, METRIC.get(metric, metric) if isinstance(metric, str)
+        else metric, float(eps), ctypes.c_void_p(stream), ctypes.byref(out))
+    return rc, (Cover(out) if rc == BM_OK else None)
+
+
+def radix_sort_u64(keys, bits: int):
+    """In-place device radix sort (diagnostic entry point)."""
+    import torch
+    assert keys.is_cuda and keys.dtype == torch.int64 and keys.is_contiguous()
+    _check(load().bm_debug_radix_sort_u64(ctypes.c_void_p(keys.data_ptr()), keys.numel(), bits,
+                                          ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    return keys
+
+
+def exclusive_scan_i64(x):
+    import torch
+    out = torch.empty_like(x)
+    tot = ctypes.c_int64()
+    _check(load().bm_debug_exclusive_scan_i64(
+        ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(out.data_ptr()), x.numel(),
+        ctypes.byref(tot), ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    return out, tot.value
+
+
+def resolve_tile(adj_words: np.ndarray, nc: int) -> np.ndarray:
+    """A3 on the device from a host [nc, ceil(nc/32)] uint32 lower-triangular adjacency."""
+    import torch
+    adj_words = np.ascontiguousarray(adj_words, dtype=np.uint32)
+    out = np.zeros(nc, dtype=np.uint8)
+    _check(load().bm_debug_resolve_tile(
+        ctypes.c_void_p(adj_words.ctypes.data), nc, ctypes.c_void_p(out.ctypes.data),
+        ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    return out

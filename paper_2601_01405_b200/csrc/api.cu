@@ -1,0 +1,647 @@
+// api.cu — C ABI (include/bm.h) and host orchestration of the cover build.
+//
+// Sequence on the caller's stream:
+//   A0 prep -> greedy tiles {A2 adjacency, A3 resolve, A4 coverage, compaction}
+//   (device-resident counts; the host checks termination once per batch of
+//   tiles) -> B membership (+B' fp64 band) -> C sort + CSR both ways ->
+//   D1 pair emission -> D2 radix sort -> D3 unique.
+// Host<->device synchronisation: one count read-back per greedy batch, then
+// M (membership count), P (pair count) and E (edge count).
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <string>
+#include <vector>
+
+#include "internal.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+bm_status set_err(bm_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+#define CK(expr)                                                                      \
+  do {                                                                                \
+    cudaError_t _e = (expr);                                                          \
+    if (_e != cudaSuccess) {                                                          \
+      cudaGetLastError();                                                             \
+      return set_err(BM_ECUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(_e),       \
+                     __FILE__, __LINE__);                                             \
+    }                                                                                 \
+  } while (0)
+
+// Stream-ordered allocations owned by one build call.
+struct Pool {
+  cudaStream_t s;
+  std::vector<void*> ptrs;
+  explicit Pool(cudaStream_t st) : s(st) {}
+  ~Pool() {
+    for (void* p : ptrs)
+      if (p) cudaFreeAsync(p, s);
+  }
+  template <class T>
+  bm_status alloc(T** out, size_t count) {
+    void* p = nullptr;
+    size_t bytes = count * sizeof(T);
+    if (bytes < 256) bytes = 256;
+    cudaError_t e = cudaMallocAsync(&p, bytes, s);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      *out = nullptr;
+      return set_err(e == cudaErrorMemoryAllocation ? BM_ENOMEM : BM_ECUDA,
+                     "cudaMallocAsync(%zu bytes): %s", bytes, cudaGetErrorString(e));
+    }
+    ptrs.push_back(p);
+    *out = (T*)p;
+    return BM_OK;
+  }
+  // remove from the pool (ownership moves to the bm_cover)
+  void release(void* p) {
+    for (auto& q : ptrs)
+      if (q == p) q = nullptr;
+  }
+  void free_now(void* p) {
+    for (auto& q : ptrs)
+      if (q == p) {
+        cudaFreeAsync(q, s);
+        q = nullptr;
+      }
+  }
+};
+
+#define TRY(expr)                      \
+  do {                                 \
+    bm_status _st = (expr);            \
+    if (_st != BM_OK) return _st;      \
+  } while (0)
+
+struct Priv {
+  cudaStream_t stream;
+};
+
+int bits_for(int64_t v) {  // number of bits to represent 0..v (>= 1)
+  int b = 1;
+  while (b < 63 && (v >> b) != 0) ++b;
+  return b;
+}
+
+float round_down_f(double v) {
+  float f = (float)v;
+  if ((double)f > v) f = nextafterf(f, -INFINITY);
+  return f;
+}
+float round_up_f(double v) {
+  float f = (float)v;
+  if ((double)f < v) f = nextafterf(f, INFINITY);
+  return f;
+}
+
+// Rigorous fp32 classification band.
+bm::Thresh make_thresh(int kind, int d, double eps) {
+  bm::Thresh t{};
+  const double u = ldexp(1.0, -24);
+  const double tie = 1e-6;
+  t.eps = eps;
+  t.eps2 = eps * eps;
+  t.tie_rel = tie;
+  if (kind == bm::K_L2F) {
+    // |s - D| <= (d+3) u D (difference rounding, squaring, fp32 accumulation),
+    // near tie |d-eps| <= 1e-6 eps  <=>  |D - eps^2| <= 2.000001e-6 eps^2
+    double eta = (d + 3) * u * 1.01 + 1e-12;
+    double tie2 = 2.000001e-6;
+    t.lo_f = round_down_f(t.eps2 * (1.0 - tie2 - 2.0 * eta));
+    t.hi_f = round_up_f(t.eps2 * (1.0 + tie2 + 2.0 * eta));
+  } else if (kind == bm::K_L1F) {
+    double eta = (d + 1) * u * 1.01 + 1e-12;
+    t.lo_f = round_down_f(eps * (1.0 - tie - 2.0 * eta));
+    t.hi_f = round_up_f(eps * (1.0 + tie + 2.0 * eta));
+  } else if (kind == bm::K_COSF) {
+    // |c_hat - c| <= (d+3) u (normalisation + fp32 dot), absolute
+    double eta = (d + 3) * u * 1.01 + 1e-12;
+    double c_in = (1.0 - eps) + tie * eps + 2.0 * eta;   // in  if c_hat >  c_in
+    double c_out = (1.0 - eps) - tie * eps - 2.0 * eta;  // out if c_hat <= c_out
+    t.lo_f = round_down_f(-c_in);                        // score = -c_hat
+    t.hi_f = round_up_f(-c_out);
+  } else if (kind == bm::K_L2I) {
+    double K = ceil(t.eps2) - 1.0;  // largest integer d2 with (double)d2 < eps*eps
+    double lo = K + 1.0;
+    t.lo_i = lo > 2147483647.0 ? 2147483647 : (int32_t)lo;
+  } else {
+    double lo = ceil(eps);          // in iff s < ceil(eps)  <=>  (double)s < eps
+    t.lo_i = lo > 2147483647.0 ? 2147483647 : (int32_t)lo;
+  }
+  return t;
+}
+
+__global__ void k_iota(int32_t* a, int64_t n) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) a[i] = (int32_t)i;
+}
+
+struct Timer {
+  bool on;
+  cudaStream_t s;
+  cudaEvent_t ev[BM_NUM_STEPS + 1];
+  int n = 0;
+  Timer(bool o, cudaStream_t st) : on(o), s(st) {
+    if (on)
+      for (auto& e : ev) cudaEventCreate(&e);
+  }
+  ~Timer() {
+    if (on)
+      for (auto& e : ev) cudaEventDestroy(e);
+  }
+  void mark(int i) {
+    if (on) cudaEventRecord(ev[i], s);
+  }
+};
+
+bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, bm_metric metric,
+                     double eps, cudaStream_t s, const bm_options* opts, bool host_in,
+                     bm_cover** out) {
+  using namespace bm;
+  if (!out) return set_err(BM_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (!points) return set_err(BM_EINVAL, "points is NULL");
+  if (n < 1) return set_err(BM_EINVAL, "n must be >= 1 (got %lld)", (long long)n);
+  if (d < 1) return set_err(BM_EINVAL, "d must be >= 1 (got %d)", d);
+  if (!(eps > 0.0) || !isfinite(eps)) return set_err(BM_EINVAL, "eps must be finite and > 0");
+  if (n > 2147483646LL) return set_err(BM_EOVERFLOW, "n exceeds INT32_MAX-1");
+  if (dtype != BM_F32 && dtype != BM_I8 && dtype != BM_U8)
+    return set_err(BM_EUNSUPPORTED, "unsupported dtype %d", (int)dtype);
+  if (metric != BM_L2 && metric != BM_L1 && metric != BM_COSINE)
+    return set_err(BM_EUNSUPPORTED, "unsupported metric %d", (int)metric);
+  if (dtype != BM_F32 && metric == BM_COSINE)
+    return set_err(BM_EUNSUPPORTED, "cosine is supported for BM_F32 only");
+  if (dtype != BM_F32 && d > 32768)
+    return set_err(BM_EOVERFLOW, "integer path needs d <= 32768 for exact int32 arithmetic");
+  bm_options o{};
+  if (opts) {
+    size_t sz = opts->struct_size > 0 && (size_t)opts->struct_size < sizeof o
+                    ? (size_t)opts->struct_size : sizeof o;
+    memcpy(&o, opts, sz);
+  }
+  int T = o.tile > 0 ? o.tile : 1024;
+  if (T < 32 || T > 1024 || (T % 32) != 0)
+    return set_err(BM_EINVAL, "tile must be a multiple of 32 in [32, 1024]");
+  if (o.path == BM_PATH_TENSOR)
+    return set_err(BM_EUNSUPPORTED, "tensor-core path not available in this build");
+  const int64_t tie_cap = o.near_tie_cap > 0 ? o.near_tie_cap : 65536;
+
+  const int kind = dtype == BM_F32
+                       ? (metric == BM_L2 ? K_L2F : (metric == BM_L1 ? K_L1F : K_COSF))
+                       : (metric == BM_L2 ? K_L2I : K_L1I);
+  const int nu_needed = dtype == BM_F32 ? (d + 1) / 2 : (d + 7) / 8;
+  int nu = pick_nu(nu_needed);
+  if (nu == 0) nu = nu_needed;
+  const Thresh th = make_thresh(kind, d, eps);
+
+  int64_t launches = 0;
+  Pool pool(s);
+  Timer tm(o.timing != 0, s);
+  tm.mark(0);
+
+  // ---- A0 prep
+  const void* dpoints = points;
+  if (host_in) {
+    size_t esz = dtype == BM_F32 ? 4 : 1;
+    void* buf;
+    TRY(pool.alloc((uint8_t**)&buf, (size_t)n * d * esz));
+    CK(cudaMemcpyAsync(buf, points, (size_t)n * d * esz, cudaMemcpyHostToDevice, s));
+    dpoints = buf;
+  }
+  uint2* rows = nullptr;
+  uint2* xhat = nullptr;
+  int32_t* inorm = nullptr;
+  DevStats* stats = nullptr;
+  TRY(pool.alloc(&rows, (size_t)n * nu));
+  if (kind == K_COSF) TRY(pool.alloc(&xhat, (size_t)n * nu));
+  if (kind == K_L2I) TRY(pool.alloc(&inorm, (size_t)n));
+  TRY(pool.alloc(&stats, 1));
+  CK(cudaMemsetAsync(stats, 0, sizeof(DevStats), s));
+  CK(launch_prep(dpoints, dtype, n, d, kind, nu, rows, xhat, inorm, stats, s, &launches));
+  if (host_in) pool.free_now((void*)dpoints);
+  tm.mark(1);
+
+  // ---- A1-A4 greedy
+  const int adj_words = T / 32;
+  const int cov_rows = cover_rows_per_cta(nu);
+  const int nblk = (int)((n + cov_rows - 1) / cov_rows);
+  int32_t *cnt = nullptr, *unc0 = nullptr, *unc1 = nullptr, *lm = nullptr, *new_lm = nullptr;
+  int32_t *blk_count = nullptr, *blk_off = nullptr;
+  uint32_t* adj = nullptr;
+  uint8_t* keep = nullptr;
+  TRY(pool.alloc(&cnt, 8));  // [0],[1] n_unc ping-pong; [2] L; [3] dL
+  TRY(pool.alloc(&unc0, (size_t)n));
+  TRY(pool.alloc(&unc1, (size_t)n));
+  TRY(pool.alloc(&lm, (size_t)n));
+  TRY(pool.alloc(&new_lm, (size_t)T));
+  TRY(pool.alloc(&adj, (size_t)T * adj_words));
+  TRY(pool.alloc(&keep, (size_t)n));
+  TRY(pool.alloc(&blk_count, (size_t)nblk));
+  TRY(pool.alloc(&blk_off, (size_t)nblk));
+  {
+    int32_t init[8] = {(int32_t)n, 0, 0, 0, 0, 0, 0, 0};
+    CK(cudaMemcpyAsync(cnt, init, sizeof init, cudaMemcpyHostToDevice, s));
+    k_iota<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(unc0, n);
+    ++launches;
+    CK(cudaGetLastError());
+  }
+  int32_t* uncb[2] = {unc0, unc1};
+  const uint2* score_rows = kind == K_COSF ? xhat : rows;
+
+  PairArgs base{};
+  base.rows = score_rows;
+  base.xrows = rows;
+  base.inorm = inorm;
+  base.n = n;
+  base.nu = nu;
+  base.d = d;
+  base.th = th;
+  base.stats = stats;
+
+  int64_t tile = 0;
+  int batch = 1;
+  int nonfinite_checked = 0;
+  for (;;) {
+    for (int b = 0; b < batch; ++b, ++tile) {
+      const int cur = (int)(tile & 1), nxt = cur ^ 1;
+      // A2: adjacency among the candidates unc[0 .. nc)
+      PairArgs a = base;
+      a.qidx = uncb[cur];
+      a.q_begin = 0;
+      a.q_end = T;
+      a.q_end_dev = cnt + cur;
+      a.lidx = uncb[cur];
+      a.l_begin = 0;
+      a.l_end = T;
+      a.l_end_dev = cnt + cur;
+      a.adj = adj;
+      a.adj_words = adj_words;
+      CK(launch_pairs(kind, MODE_ADJ, a, T, s, &launches));
+      // A3: in-order resolve, append landmarks
+      CK(launch_resolve(adj, adj_words, uncb[cur], cnt + cur, T, lm, cnt + 2, new_lm, cnt + 3,
+                        stats, s, &launches));
+      // A4: coverage of unc[nc .. n_unc) by the new landmarks
+      PairArgs c = base;
+      c.qidx = uncb[cur];
+      c.q_begin = T;
+      c.q_begin_dev = cnt + cur;
+      c.q_end = n;
+      c.q_end_dev = cnt + cur;
+      c.lidx = new_lm;
+      c.l_begin = 0;
+      c.l_end = T;
+      c.l_end_dev = cnt + 3;
+      c.keep = keep;
+      c.blk_count = blk_count;
+      CK(launch_pairs(kind, MODE_COVER, c, n, s, &launches));
+      CK(launch_compact_unc(keep, blk_count, nblk, cov_rows, uncb[cur], cnt + cur, T, blk_off,
+                            uncb[nxt], cnt + nxt, s, &launches));
+    }
+    int32_t hc[4];
+    CK(cudaMemcpyAsync(hc, cnt, sizeof hc, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (!nonfinite_checked) {
+      int nf = 0;
+      CK(cudaMemcpy(&nf, &stats->nonfinite, sizeof nf, cudaMemcpyDeviceToHost));
+      if (nf) return set_err(BM_EINVAL, "points contain a non-finite coordinate");
+      nonfinite_checked = 1;
+    }
+    if (hc[tile & 1] == 0) break;
+    if (batch < 32) batch *= 2;
+  }
+  tm.mark(2);
+
+  int32_t hL = 0;
+  CK(cudaMemcpyAsync(&hL, cnt + 2, sizeof hL, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const int64_t L = hL;
+  pool.free_now(unc0);
+  pool.free_now(unc1);
+  pool.free_now(keep);
+
+  // ---- B membership (+ B' band recheck, near ties)
+  const int lbits = bits_for(L > 1 ? L - 1 : 1);
+  const int pbits = bits_for(n > 1 ? n - 1 : 1);
+  int64_t* ties_dev = nullptr;
+  TRY(pool.alloc(&ties_dev, (size_t)tie_cap * 3));
+  DevStats hs{};
+  CK(cudaMemcpyAsync(&hs, stats, sizeof hs, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const unsigned long long greedy_band = hs.band_pairs;
+  int64_t key_cap = n * 4 > (1 << 20) ? n * 4 : (1 << 20);
+  unsigned long long* keys = nullptr;
+  int64_t M = 0;
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    TRY(pool.alloc(&keys, (size_t)key_cap));
+    PairArgs m = base;
+    m.qidx = nullptr;
+    m.q_begin = 0;
+    m.q_end = n;
+    m.lidx = lm;
+    m.l_begin = 0;
+    m.l_end = L;
+    m.lpos0 = 0;
+    const int R = nu <= 8 ? 4 : (nu <= 16 ? 2 : 1);
+    const int64_t gx = (n + 256 * R - 1) / (256 * R);
+    int64_t want_gy = (148 * 8 + gx - 1) / gx;
+    if (want_gy < 1) want_gy = 1;
+    int64_t lch = (L + want_gy - 1) / want_gy;
+    lch = ((lch + 63) / 64) * 64;
+    if (lch < 64) lch = 64;
+    while ((L + lch - 1) / lch > 65535) lch *= 2;
+    m.l_chunk = lch;
+    m.keys = keys;
+    m.key_cap = key_cap;
+    m.lbits = lbits;
+    m.ties = ties_dev;
+    m.tie_cap = tie_cap;
+    CK(launch_pairs(kind, MODE_MEMBER, m, n, s, &launches));
+    CK(cudaMemcpyAsync(&hs, stats, sizeof hs, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    M = (int64_t)hs.key_count;
+    if (M <= key_cap) break;
+    // overflow: resize exactly and recompute
+    pool.free_now(keys);
+    key_cap = M;
+    unsigned long long zero3[3] = {0, 0, 0};
+    CK(cudaMemcpyAsync(&stats->key_count, zero3, sizeof(unsigned long long), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(&stats->near_ties, zero3, sizeof(unsigned long long), cudaMemcpyHostToDevice, s));
+    unsigned long long gb = greedy_band;
+    CK(cudaMemcpyAsync(&stats->band_pairs, &gb, sizeof gb, cudaMemcpyHostToDevice, s));
+    CK(cudaStreamSynchronize(s));
+  }
+  tm.mark(3);
+
+  // ---- C CSR both ways
+  unsigned long long* alt = nullptr;
+  void* rtemp = nullptr;
+  int64_t* pt_ptr = nullptr;
+  int32_t* pt_lm = nullptr;
+  int64_t* ball_ptr = nullptr;
+  int32_t* ball_idx = nullptr;
+  TRY(pool.alloc(&alt, (size_t)(M > 0 ? M : 1)));
+  TRY(pool.alloc((uint8_t**)&rtemp, radix_temp_bytes(M)));
+  TRY(pool.alloc(&pt_ptr, (size_t)n + 1));
+  TRY(pool.alloc(&pt_lm, (size_t)(M > 0 ? M : 1)));
+  TRY(pool.alloc(&ball_ptr, (size_t)L + 1));
+  TRY(pool.alloc(&ball_idx, (size_t)(M > 0 ? M : 1)));
+  CK(radix_sort_u64(&keys, &alt, M, 0, pbits + lbits, rtemp, s, &launches));
+  const unsigned long long lmask = (1ull << lbits) - 1ull, pmask = (1ull << pbits) - 1ull;
+  CK(launch_unpack_low(keys, M, lmask, pt_lm, s, &launches));
+  CK(launch_segment_ptr(keys, M, lbits, pmask, n, pt_ptr, s, &launches));
+  CK(launch_rekey_landmark_major(keys, M, lbits, pbits, alt, s, &launches));
+  {
+    unsigned long long* k2 = alt;
+    unsigned long long* a2 = keys;
+    CK(radix_sort_u64(&k2, &a2, M, pbits, pbits + lbits, rtemp, s, &launches));
+    CK(launch_unpack_low(k2, M, pmask, ball_idx, s, &launches));
+    CK(launch_segment_ptr(k2, M, pbits, lmask, L, ball_ptr, s, &launches));
+  }
+  pool.free_now(keys);
+  pool.free_now(alt);
+  pool.free_now(rtemp);
+  tm.mark(4);
+
+  // ---- D1-D3 edges
+  int64_t *pcnt = nullptr, *poff = nullptr, *ptot = nullptr;
+  void* stemp = nullptr;
+  TRY(pool.alloc(&pcnt, (size_t)n));
+  TRY(pool.alloc(&poff, (size_t)n));
+  TRY(pool.alloc(&ptot, 2));
+  TRY(pool.alloc((uint8_t**)&stemp, scan_temp_bytes(n)));
+  CK(launch_pair_counts(pt_ptr, n, pcnt, s, &launches));
+  CK(exclusive_scan_i64(pcnt, poff, n, stemp, ptot, s, &launches));
+  int64_t P = 0;
+  CK(cudaMemcpyAsync(&P, ptot, sizeof P, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  int64_t E = 0;
+  int32_t* edges = nullptr;
+  if (P > 0) {
+    unsigned long long *ek = nullptr, *ea = nullptr;
+    int64_t *flags = nullptr, *pos = nullptr;
+    void *et = nullptr, *ft = nullptr;
+    TRY(pool.alloc(&ek, (size_t)P));
+    TRY(pool.alloc(&ea, (size_t)P));
+    TRY(pool.alloc((uint8_t**)&et, radix_temp_bytes(P)));
+    CK(launch_pair_emit(pt_ptr, pt_lm, n, poff, lbits, ek, s, &launches));
+    CK(radix_sort_u64(&ek, &ea, P, 0, 2 * lbits, et, s, &launches));
+    TRY(pool.alloc(&flags, (size_t)P));
+    TRY(pool.alloc(&pos, (size_t)P));
+    TRY(pool.alloc((uint8_t**)&ft, scan_temp_bytes(P)));
+    CK(launch_unique_flags(ek, P, flags, s, &launches));
+    CK(exclusive_scan_i64(flags, pos, P, ft, ptot + 1, s, &launches));
+    CK(cudaMemcpyAsync(&E, ptot + 1, sizeof E, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    TRY(pool.alloc(&edges, (size_t)(2 * E > 0 ? 2 * E : 1)));
+    CK(launch_unique_scatter(ek, P, pos, lbits, edges, s, &launches));
+    pool.free_now(ek);
+    pool.free_now(ea);
+    pool.free_now(flags);
+    pool.free_now(pos);
+    pool.free_now(et);
+    pool.free_now(ft);
+  } else {
+    TRY(pool.alloc(&edges, 1));
+  }
+  int32_t* landmarks = nullptr;
+  TRY(pool.alloc(&landmarks, (size_t)(L > 0 ? L : 1)));
+  CK(launch_copy_i32(lm, landmarks, L, s, &launches));
+  tm.mark(5);
+
+  // ---- results
+  CK(cudaMemcpyAsync(&hs, stats, sizeof hs, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  bm_cover* c = (bm_cover*)calloc(1, sizeof(bm_cover));
+  Priv* pv = (Priv*)calloc(1, sizeof(Priv));
+  if (!c || !pv) {
+    free(c);
+    free(pv);
+    return set_err(BM_ENOMEM, "host allocation failed");
+  }
+  pv->stream = s;
+  c->priv = pv;
+  c->n = n;
+  c->d = d;
+  c->dtype = dtype;
+  c->metric = metric;
+  c->eps = eps;
+  c->n_landmarks = L;
+  c->n_members = M;
+  c->n_edges = E;
+  c->n_pair_evals = n * L;
+  c->n_greedy_evals = (int64_t)hs.greedy_evals;
+  c->n_band_pairs = (int64_t)hs.band_pairs;
+  c->n_near_ties = (int64_t)hs.near_ties;
+  c->n_greedy_tiles = (int64_t)hs.tiles;
+  c->path_used = BM_PATH_CUDA_CORE;
+  c->tile_used = T;
+  const int64_t nst = c->n_near_ties < tie_cap ? c->n_near_ties : tie_cap;
+  c->n_near_ties_stored = nst;
+  if (nst > 0) {
+    c->near_tie_pairs = (int64_t*)malloc(sizeof(int64_t) * 3 * nst);
+    if (c->near_tie_pairs)
+      CK(cudaMemcpy(c->near_tie_pairs, ties_dev, sizeof(int64_t) * 3 * nst,
+                    cudaMemcpyDeviceToHost));
+  }
+  if (tm.on) {
+    for (int i = 0; i < 5; ++i) cudaEventElapsedTime(&c->step_ms[i], tm.ev[i], tm.ev[i + 1]);
+    cudaEventElapsedTime(&c->step_ms[BM_STEP_TOTAL], tm.ev[0], tm.ev[5]);
+  }
+  c->n_launches = launches;
+  if (host_in) {
+    c->on_host = 1;
+    auto h2 = [&](void* dsrc, size_t bytes) -> void* {
+      void* h = malloc(bytes > 0 ? bytes : 1);
+      if (h && bytes) cudaMemcpy(h, dsrc, bytes, cudaMemcpyDeviceToHost);
+      return h;
+    };
+    c->landmarks = (int32_t*)h2(landmarks, sizeof(int32_t) * L);
+    c->ball_ptr = (int64_t*)h2(ball_ptr, sizeof(int64_t) * (L + 1));
+    c->ball_idx = (int32_t*)h2(ball_idx, sizeof(int32_t) * M);
+    c->pt_ptr = (int64_t*)h2(pt_ptr, sizeof(int64_t) * (n + 1));
+    c->pt_lm = (int32_t*)h2(pt_lm, sizeof(int32_t) * M);
+    c->edges = (int32_t*)h2(edges, sizeof(int32_t) * 2 * E);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess || !c->landmarks || !c->ball_ptr || !c->ball_idx || !c->pt_ptr ||
+        !c->pt_lm || !c->edges) {
+      bm_free(c);
+      return set_err(BM_ECUDA, "device-to-host copy of the results failed");
+    }
+  } else {
+    c->landmarks = landmarks;
+    c->ball_ptr = ball_ptr;
+    c->ball_idx = ball_idx;
+    c->pt_ptr = pt_ptr;
+    c->pt_lm = pt_lm;
+    c->edges = edges;
+    for (void* p : {(void*)landmarks, (void*)ball_ptr, (void*)ball_idx, (void*)pt_ptr,
+                    (void*)pt_lm, (void*)edges})
+      pool.release(p);
+  }
+  *out = c;
+  g_err.clear();
+  return BM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+bm_status bm_cover_build_ex(const void* points, bm_dtype dtype, int64_t n, int32_t d,
+                            bm_metric metric, double eps, void* stream, const bm_options* opts,
+                            bm_cover** out) {
+  try {
+    return build_impl(points, dtype, n, d, metric, eps, (cudaStream_t)stream, opts, false, out);
+  } catch (...) {
+    return set_err(BM_ENOMEM, "unexpected host exception");
+  }
+}
+
+bm_status bm_cover_build(const void* points, bm_dtype dtype, int64_t n, int32_t d,
+                         bm_metric metric, double eps, void* stream, bm_cover** out) {
+  return bm_cover_build_ex(points, dtype, n, d, metric, eps, stream, nullptr, out);
+}
+
+bm_status bm_cover_build_host(const void* host_points, bm_dtype dtype, int64_t n, int32_t d,
+                              bm_metric metric, double eps, void* stream,
+                              const bm_options* opts, bm_cover** out) {
+  try {
+    return build_impl(host_points, dtype, n, d, metric, eps, (cudaStream_t)stream, opts, true,
+                      out);
+  } catch (...) {
+    return set_err(BM_ENOMEM, "unexpected host exception");
+  }
+}
+
+void bm_free(bm_cover* c) {
+  if (!c) return;
+  Priv* pv = (Priv*)c->priv;
+  if (c->on_host) {
+    free(c->landmarks);
+    free(c->ball_ptr);
+    free(c->ball_idx);
+    free(c->pt_ptr);
+    free(c->pt_lm);
+    free(c->edges);
+  } else {
+    cudaStream_t s = pv ? pv->stream : nullptr;
+    for (void* p : {(void*)c->landmarks, (void*)c->ball_ptr, (void*)c->ball_idx,
+                    (void*)c->pt_ptr, (void*)c->pt_lm, (void*)c->edges})
+      if (p) cudaFreeAsync(p, s);
+  }
+  free(c->near_tie_pairs);
+  free(pv);
+  free(c);
+}
+
+const char* bm_last_error(void) { return g_err.c_str(); }
+
+int32_t bm_version(void) { return (BM_VERSION_MAJOR << 16) | BM_VERSION_MINOR; }
+
+bm_status bm_debug_radix_sort_u64(uint64_t* keys, int64_t n, int32_t bits, void* stream) {
+  if (!keys || n < 0 || bits < 1 || bits > 64) return set_err(BM_EINVAL, "bad arguments");
+  cudaStream_t s = (cudaStream_t)stream;
+  Pool pool(s);
+  unsigned long long* alt = nullptr;
+  void* temp = nullptr;
+  TRY(pool.alloc(&alt, (size_t)(n > 0 ? n : 1)));
+  TRY(pool.alloc((uint8_t**)&temp, bm::radix_temp_bytes(n)));
+  int64_t launches = 0;
+  unsigned long long* k = (unsigned long long*)keys;
+  CK(bm::radix_sort_u64(&k, &alt, n, 0, bits, temp, s, &launches));
+  if (k != (unsigned long long*)keys)
+    CK(cudaMemcpyAsync(keys, k, sizeof(uint64_t) * n, cudaMemcpyDeviceToDevice, s));
+  CK(cudaStreamSynchronize(s));
+  return BM_OK;
+}
+
+bm_status bm_debug_exclusive_scan_i64(const int64_t* in, int64_t* out, int64_t n, int64_t* total,
+                                      void* stream) {
+  if (!in || !out || n < 0) return set_err(BM_EINVAL, "bad arguments");
+  cudaStream_t s = (cudaStream_t)stream;
+  Pool pool(s);
+  void* temp = nullptr;
+  int64_t* tot = nullptr;
+  TRY(pool.alloc((uint8_t**)&temp, bm::scan_temp_bytes(n)));
+  TRY(pool.alloc(&tot, 1));
+  int64_t launches = 0;
+  CK(bm::exclusive_scan_i64(in, out, n, temp, tot, s, &launches));
+  int64_t h = 0;
+  CK(cudaMemcpyAsync(&h, tot, sizeof h, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (total) *total = h;
+  return BM_OK;
+}
+
+bm_status bm_debug_resolve_tile(const uint32_t* adj, int32_t nc, uint8_t* lm_out, void* stream) {
+  if (!adj || !lm_out || nc < 1 || nc > 1024) return set_err(BM_EINVAL, "bad arguments");
+  cudaStream_t s = (cudaStream_t)stream;
+  Pool pool(s);
+  const int words = (nc + 31) / 32;
+  uint32_t* dadj = nullptr;
+  uint8_t* dlm = nullptr;
+  TRY(pool.alloc(&dadj, (size_t)nc * words));
+  TRY(pool.alloc(&dlm, (size_t)nc));
+  CK(cudaMemcpyAsync(dadj, adj, sizeof(uint32_t) * nc * words, cudaMemcpyHostToDevice, s));
+  int64_t launches = 0;
+  CK(bm::launch_resolve_debug(dadj, words, nc, dlm, s, &launches));
+  CK(cudaMemcpyAsync(lm_out, dlm, nc, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return BM_OK;
+}
+
+}  // extern "C"

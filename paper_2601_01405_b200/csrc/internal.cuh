@@ -1,0 +1,147 @@
+// internal.cuh — shared declarations of the CUDA implementation behind include/bm.h.
+//
+// Layout in HBM:
+//   rows   : prepped point rows, NU 8-byte units per row (fp32: 2 coords/unit,
+//            int8: 8 coords/unit), zero padded, 16-B aligned base.  For fp32
+//            these are the input values bit-for-bit, so they also serve the
+//            fp64 recheck.
+//   xhat   : cosine only — rows normalised by their fp64 norm, rounded to fp32
+//            (a zero row holds NaN in unit 0 so every pair with it is sent to the
+//            fp64 recheck, which applies the zero-vector rule).
+//   inorm  : integer L2 only — exact int32 squared norms.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/bm.h"
+
+namespace bm {
+
+// ---------------------------------------------------------------- kinds
+enum Kind : int { K_L2F = 0, K_L1F = 1, K_COSF = 2, K_L2I = 3, K_L1I = 4 };
+
+enum PairMode : int { MODE_ADJ = 0, MODE_COVER = 1, MODE_MEMBER = 2 };
+
+// Thresholds for the classification "score < lo -> in, score >= hi -> out,
+// else band (fp64 recheck)".  Score = d^2 (L2F), L1 sum (L1F), -cos (COSF),
+// exact integer d^2 / L1 (int kinds; lo == hi, no band).
+struct Thresh {
+  float lo_f, hi_f;
+  int32_t lo_i;          // in iff score <= lo_i - 1 (i.e. score < lo_i)
+  double eps, eps2;      // fp64 truth: L2 d2 < eps2, L1 s < eps, cos 1-c < eps
+  double tie_rel;        // near-tie band (1e-6)
+};
+
+struct Dev;   // per-call device workspace (api.cu)
+
+// Statistics counters living in device memory (one struct per call).
+struct DevStats {
+  unsigned long long key_count;      // membership pairs emitted
+  unsigned long long band_pairs;     // fp64 rechecks (all modes)
+  unsigned long long near_ties;      // near ties found in MODE_MEMBER
+  unsigned long long greedy_evals;   // in-tile + coverage evaluations
+  unsigned long long tiles;          // greedy tiles with nc > 0
+  int nonfinite;                     // prep: a NaN/Inf coordinate was seen
+  int pad;
+};
+
+struct PairArgs {
+  const uint2* rows;        // [n][nu] scoring rows (xhat for cosine)
+  const uint2* xrows;       // [n][nu] fp32 rows for the fp64 recheck (== rows except cosine)
+  const int32_t* inorm;     // [n] exact int L2 norms (K_L2I)
+  int64_t n;
+  int nu;                   // units per row (runtime copy of the template NU)
+  int d;                    // true dimension (recheck loop bound)
+  Thresh th;
+  // queries: contiguous [q_begin, q_end) or list qidx[q_begin .. q_end)
+  const int32_t* qidx;
+  int64_t q_begin, q_end;
+  const int32_t* q_end_dev;   // if non-null: q_end = min(q_end, *q_end_dev)
+  const int32_t* q_begin_dev; // if non-null: q_begin = min(q_begin, *q_begin_dev)
+  // landmarks: point indices lidx[l_begin .. l_end); positions are l_begin-relative + lpos0
+  const int32_t* lidx;
+  int64_t l_begin, l_end;
+  const int32_t* l_end_dev;   // if non-null: l_end = min(l_end, *l_end_dev)
+  int64_t lpos0;
+  int64_t l_chunk;          // landmarks per grid.y slice (MODE_MEMBER)
+  // outputs
+  uint32_t* adj; int adj_words;                 // MODE_ADJ
+  uint8_t* keep; int32_t* blk_count;            // MODE_COVER: keep[i - q_begin], per-CTA counts
+  unsigned long long* keys; int64_t key_cap; int lbits;   // MODE_MEMBER: (p << lbits) | j
+  int64_t* ties; int64_t tie_cap;               // MODE_MEMBER near-tie triples (host-mapped)
+  DevStats* stats;
+};
+
+// ------------------------------------------------------------ launchers
+// All return cudaError_t of the launch; `launches` is incremented per kernel.
+cudaError_t launch_prep(const void* X, int dtype, int64_t n, int d, int kind, int nu,
+                        uint2* rows, uint2* xhat, int32_t* inorm, DevStats* stats,
+                        cudaStream_t s, int64_t* launches);
+
+cudaError_t launch_pairs(int kind, int mode, const PairArgs& a, int64_t q_rows_max,
+                         cudaStream_t s, int64_t* launches);
+
+cudaError_t launch_resolve(const uint32_t* adj, int adj_words, const int32_t* unc,
+                           const int32_t* n_unc, int T, int32_t* lm_out, int32_t* L_dev,
+                           int32_t* new_lm, int32_t* dL_dev, DevStats* stats,
+                           cudaStream_t s, int64_t* launches);
+
+cudaError_t launch_compact_unc(const uint8_t* keep, const int32_t* blk_count, int nblk,
+                               int blk_rows, const int32_t* unc, const int32_t* n_unc, int T,
+                               int32_t* blk_off, int32_t* unc_next, int32_t* n_unc_next,
+                               cudaStream_t s, int64_t* launches);
+
+// scan / sort (sort.cu)
+size_t scan_temp_bytes(int64_t n);
+cudaError_t exclusive_scan_i64(const int64_t* in, int64_t* out, int64_t n, void* temp,
+                               int64_t* total_dev, cudaStream_t s, int64_t* launches);
+size_t radix_temp_bytes(int64_t n);
+// Stable LSD sort of keys over bit range [lo_bit, hi_bit); result in *keys (may swap with alt).
+cudaError_t radix_sort_u64(unsigned long long** keys, unsigned long long** alt, int64_t n,
+                           int lo_bit, int hi_bit, void* temp, cudaStream_t s,
+                           int64_t* launches);
+
+// csr / edges (csr.cu)
+cudaError_t launch_segment_ptr(const unsigned long long* keys, int64_t m, int shift,
+                               unsigned long long mask, int64_t nseg, int64_t* ptr,
+                               cudaStream_t s, int64_t* launches);
+cudaError_t launch_unpack_low(const unsigned long long* keys, int64_t m,
+                              unsigned long long mask, int32_t* out, cudaStream_t s,
+                              int64_t* launches);
+cudaError_t launch_rekey_landmark_major(const unsigned long long* pm_keys, int64_t m, int lbits,
+                                        int pbits, unsigned long long* out, cudaStream_t s,
+                                        int64_t* launches);
+cudaError_t launch_pair_counts(const int64_t* pt_ptr, int64_t n, int64_t* cnt, cudaStream_t s,
+                               int64_t* launches);
+cudaError_t launch_pair_emit(const int64_t* pt_ptr, const int32_t* pt_lm, int64_t n,
+                             const int64_t* off, int lbits, unsigned long long* keys,
+                             cudaStream_t s, int64_t* launches);
+cudaError_t launch_unique_flags(const unsigned long long* keys, int64_t m, int64_t* flags,
+                                cudaStream_t s, int64_t* launches);
+cudaError_t launch_unique_scatter(const unsigned long long* keys, int64_t m,
+                                  const int64_t* pos, int lbits, int32_t* edges,
+                                  cudaStream_t s, int64_t* launches);
+cudaError_t launch_copy_i32(const int32_t* src, int32_t* dst, int64_t n, cudaStream_t s,
+                            int64_t* launches);
+
+// resolve-only diagnostic kernel
+cudaError_t launch_resolve_debug(const uint32_t* adj, int adj_words, int nc, uint8_t* lm,
+                                 cudaStream_t s, int64_t* launches);
+
+}  // namespace bm
+
+namespace bm {
+// Instantiated register-row widths of the CUDA-core pair kernel (8-byte units);
+// 0 = wide variant (rows re-read from L1/global).
+inline int pick_nu(int nu_needed) {
+  static const int widths[] = {1, 2, 4, 5, 8, 12, 16, 24, 32};
+  for (int w : widths)
+    if (nu_needed <= w) return w;
+  return 0;
+}
+// Rows a MODE_COVER CTA handles (must match launch_pairs_nu's R choice).
+inline int cover_rows_per_cta(int nu) {
+  int R = nu == 0 ? 1 : (nu <= 8 ? 4 : (nu <= 16 ? 2 : 1));
+  return 256 * R;
+}
+}  // namespace bm

@@ -1,0 +1,6 @@
+// pairs_cosf.cu — instantiation of the CUDA-core pair kernel for kind K_COSF
+// (split per kind so the kernel variants compile in parallel).
+#include "pairs_impl.cuh"
+namespace bm {
+BM_INSTANTIATE_PAIRS(K_COSF)
+}

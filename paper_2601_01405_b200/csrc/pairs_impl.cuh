@@ -1,0 +1,371 @@
+// pairs_impl.cuh — CUDA-core point x landmark predicate kernel (steps A2, A4, B).
+//
+// One kernel template serves the three places the method evaluates the ball
+// predicate d(x_p, l) < eps (open ball):
+//   MODE_ADJ    A2: candidate x candidate bits of the greedy tile (b < a)
+//   MODE_COVER  A4: "mark all points within eps of x as covered"
+//               for the still-uncovered points after the tile, with a per-CTA
+//               kept-count for the order-preserving compaction
+//   MODE_MEMBER B : ball membership of every point in every ball,
+//               emitting packed (point << lbits | landmark position) keys with
+//               warp-aggregated atomics
+//
+// Layout: each thread keeps R query rows in registers (NU 8-byte units each);
+// LC landmark rows at a time are staged in shared memory and read as warp
+// broadcasts.  Float kinds are scored in fp32 (direct difference form for L2
+// and L1, normalised dot for cosine) and classified against a rigorous band
+// (DESIGN.md "Float exactness"): score < lo -> in, score >= hi -> out, else the
+// pair is re-decided with the fp64 formula of the oracle (same operation order,
+// no FMA contraction), which is bit-identical to the CPU oracle's decision.
+// Integer kinds are exact: int32 Gram form via dp4a for L2,
+// byte |x-y| via vabsdiffs4 + dp4a for L1.
+#pragma once
+#include <math.h>
+
+#include "internal.cuh"
+
+namespace bm {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+template <int KIND>
+struct KindTraits;
+template <> struct KindTraits<K_L2F> { using acc_t = float; static constexpr bool is_float = true; };
+template <> struct KindTraits<K_L1F> { using acc_t = float; static constexpr bool is_float = true; };
+template <> struct KindTraits<K_COSF> { using acc_t = float; static constexpr bool is_float = true; };
+template <> struct KindTraits<K_L2I> { using acc_t = int; static constexpr bool is_float = false; };
+template <> struct KindTraits<K_L1I> { using acc_t = int; static constexpr bool is_float = false; };
+
+template <int KIND>
+__device__ __forceinline__ void acc_unit(typename KindTraits<KIND>::acc_t& a, uint2 q, uint2 l) {
+  if constexpr (KIND == K_L2F) {
+    float t0 = __uint_as_float(q.x) - __uint_as_float(l.x);
+    float t1 = __uint_as_float(q.y) - __uint_as_float(l.y);
+    a = fmaf(t0, t0, a);
+    a = fmaf(t1, t1, a);
+  } else if constexpr (KIND == K_L1F) {
+    a += fabsf(__uint_as_float(q.x) - __uint_as_float(l.x));
+    a += fabsf(__uint_as_float(q.y) - __uint_as_float(l.y));
+  } else if constexpr (KIND == K_COSF) {
+    a = fmaf(__uint_as_float(q.x), __uint_as_float(l.x), a);
+    a = fmaf(__uint_as_float(q.y), __uint_as_float(l.y), a);
+  } else if constexpr (KIND == K_L2I) {
+    a = __dp4a((int)q.x, (int)l.x, a);
+    a = __dp4a((int)q.y, (int)l.y, a);
+  } else {
+    a = (int)__dp4a(__vabsdiffs4(q.x, l.x), 0x01010101u, (unsigned)a);
+    a = (int)__dp4a(__vabsdiffs4(q.y, l.y), 0x01010101u, (unsigned)a);
+  }
+}
+
+// fp64 re-decision, operation-for-operation the oracle's formula
+// (oracle/bm_oracle.c oracle_distance; reading A6/A7).
+// Returns in-ball; *dist = fp64 distance (Euclidean, not squared, for L2).
+template <int KIND>
+__device__ __noinline__ bool recheck64(const uint2* __restrict__ xrows, int nu, int d,
+                                       double eps, double eps2, int64_t p, int64_t q,
+                                       double* dist) {
+  const float* x = reinterpret_cast<const float*>(xrows + p * (int64_t)nu);
+  const float* y = reinterpret_cast<const float*>(xrows + q * (int64_t)nu);
+  if constexpr (KIND == K_L2F) {
+    double s = 0.0;
+    for (int j = 0; j < d; ++j) {
+      double t = __dsub_rn((double)x[j], (double)y[j]);
+      s = __dadd_rn(s, __dmul_rn(t, t));
+    }
+    *dist = __dsqrt_rn(s);
+    return s < eps2;
+  } else if constexpr (KIND == K_L1F) {
+    double s = 0.0;
+    for (int j = 0; j < d; ++j) s = __dadd_rn(s, fabs(__dsub_rn((double)x[j], (double)y[j])));
+    *dist = s;
+    return s < eps;
+  } else {
+    double dot = 0.0, xx = 0.0, yy = 0.0;
+    for (int j = 0; j < d; ++j) {
+      double a = (double)x[j], b = (double)y[j];
+      dot = __dadd_rn(dot, __dmul_rn(a, b));
+      xx = __dadd_rn(xx, __dmul_rn(a, a));
+      yy = __dadd_rn(yy, __dmul_rn(b, b));
+    }
+    double v;
+    if (xx == 0.0 && yy == 0.0) v = 0.0;
+    else if (xx == 0.0 || yy == 0.0) v = 1.0;
+    else v = __dsub_rn(1.0, __ddiv_rn(dot, __dmul_rn(__dsqrt_rn(xx), __dsqrt_rn(yy))));
+    *dist = v;
+    return v < eps;
+  }
+}
+
+// Classification of a score: 1 = in, 0 = out, 2 = band.
+template <int KIND>
+__device__ __forceinline__ int classify(typename KindTraits<KIND>::acc_t acc, int32_t nq,
+                                        int32_t nl, const Thresh& th) {
+  if constexpr (KIND == K_L2I) {
+    int s = nq + nl - 2 * acc;
+    return s < th.lo_i ? 1 : 0;
+  } else if constexpr (KIND == K_L1I) {
+    return acc < th.lo_i ? 1 : 0;
+  } else {
+    float s = (KIND == K_COSF) ? -acc : acc;
+    // NaN (cosine zero row) fails both comparisons -> band
+    return s < th.lo_f ? 1 : (s >= th.hi_f ? 0 : 2);
+  }
+}
+
+// NU > 0: query rows live in registers (NU units).  NU == 0 ("wide"): rows of
+// any length; the query row is re-read from global/L1 for every landmark.
+template <int KIND, int NU, int R, int MODE, int LC>
+__global__ void __launch_bounds__(256) k_pairs(PairArgs A) {
+  constexpr int NT = 256;
+  constexpr int QU = NU > 0 ? NU : 1;   // register units per query row
+  using acc_t = typename KindTraits<KIND>::acc_t;
+  extern __shared__ uint2 sl[];          // [LC][nu]
+  const int nu = NU > 0 ? NU : A.nu;
+  __shared__ int32_t sln[LC];
+  __shared__ int32_t slp[LC];
+  __shared__ int32_t s_red[NT / 32];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // device-resident counts act as caps on the host bounds: actual = min(host, *dev)
+  int64_t q_end = A.q_end_dev ? min(A.q_end, (int64_t)*A.q_end_dev) : A.q_end;
+  int64_t q_begin = A.q_begin_dev ? min(A.q_begin, (int64_t)*A.q_begin_dev) : A.q_begin;
+  q_begin = min(q_begin, q_end);
+  const int64_t blk_q0 = q_begin + (int64_t)blockIdx.x * (NT * R);
+
+  int64_t l_end = A.l_end_dev ? min(A.l_end, (int64_t)*A.l_end_dev) : A.l_end;
+  int64_t l0 = A.l_begin, l1 = l_end;
+  if (MODE == MODE_MEMBER) {
+    l0 = A.l_begin + (int64_t)blockIdx.y * A.l_chunk;
+    l1 = min(l_end, l0 + A.l_chunk);
+  } else if (MODE == MODE_ADJ) {
+    l0 = A.l_begin + (int64_t)blockIdx.y * 32;
+    l1 = min(l_end, l0 + 32);
+  }
+  if (MODE == MODE_COVER) {
+    if (blk_q0 >= q_end) {
+      if (tid == 0 && A.blk_count) A.blk_count[blockIdx.x] = 0;
+      return;
+    }
+  } else {
+    if (blk_q0 >= q_end || l0 >= l1) return;
+    // adjacency: only b < a is needed
+    if (MODE == MODE_ADJ && l0 >= min(q_end, blk_q0 + NT * R)) return;
+  }
+
+  // ---- query rows into registers
+  uint2 q[R][QU];
+  int64_t qp[R];
+  int64_t qi[R];
+  int32_t qn[R];
+  bool act[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    qi[r] = blk_q0 + r * NT + tid;
+    act[r] = qi[r] < q_end;
+    qp[r] = act[r] ? (A.qidx ? (int64_t)A.qidx[qi[r]] : qi[r]) : 0;
+    const uint2* src = A.rows + qp[r] * (int64_t)nu;
+#pragma unroll
+    for (int u = 0; u < QU; ++u) q[r][u] = (act[r] && NU > 0) ? src[u] : make_uint2(0u, 0u);
+    qn[r] = (KIND == K_L2I && act[r]) ? A.inorm[qp[r]] : 0;
+  }
+
+  bool covered[R];
+  uint32_t word[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) { covered[r] = false; word[r] = 0u; }
+
+  for (int64_t lb = l0; lb < l1; lb += LC) {
+    const int nl = (int)min((int64_t)LC, l1 - lb);
+    if (MODE == MODE_COVER) {
+      bool done = true;
+#pragma unroll
+      for (int r = 0; r < R; ++r) done = done && (covered[r] || !act[r]);
+      if (__syncthreads_and(done)) break;
+    } else {
+      __syncthreads();
+    }
+    for (int t = tid; t < nl * nu; t += NT) {
+      int jj = t / nu, u = t - jj * nu;
+      int32_t pt = A.lidx[lb + jj];
+      sl[jj * nu + u] = A.rows[(int64_t)pt * nu + u];
+    }
+    for (int t = tid; t < nl; t += NT) {
+      int32_t pt = A.lidx[lb + t];
+      slp[t] = pt;
+      sln[t] = (KIND == K_L2I) ? A.inorm[pt] : 0;
+    }
+    __syncthreads();
+
+    bool warp_done = false;
+    for (int jj = 0; jj < nl; ++jj) {
+      if (MODE == MODE_COVER) {
+        if (warp_done) break;
+      }
+      uint2 l[QU];
+#pragma unroll
+      for (int u = 0; u < QU; ++u) l[u] = NU > 0 ? sl[jj * nu + u] : make_uint2(0u, 0u);
+      int cls[R];
+      bool special = false;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        acc_t a = 0;
+        if constexpr (NU > 0) {
+#pragma unroll
+          for (int u = 0; u < NU; ++u) acc_unit<KIND>(a, q[r][u], l[u]);
+        } else {
+          const uint2* src = A.rows + qp[r] * (int64_t)nu;
+          const uint2* ls = sl + jj * nu;
+          for (int u = 0; u < nu; ++u) acc_unit<KIND>(a, __ldg(src + u), ls[u]);
+        }
+        int c = classify<KIND>(a, qn[r], sln[jj], A.th);
+        c = act[r] ? c : 0;
+        if (MODE == MODE_ADJ) {
+          int64_t b = lb + jj;
+          if (b >= qi[r]) c = 0;               // strictly lower triangle
+        }
+        cls[r] = c;
+        if (MODE == MODE_MEMBER) special = special || (c != 0);
+        else special = special || (c == 2);
+        if (MODE == MODE_COVER) covered[r] = covered[r] || (c == 1);
+        if (MODE == MODE_ADJ) word[r] |= (c == 1 ? 1u : 0u) << (int)(lb + jj - l0);
+      }
+      const unsigned ball = __ballot_sync(FULL, special);
+      if (ball) {                               // rare, warp-uniform slow path
+        const int64_t lpt = slp[jj];
+        int nemit = 0;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          if (KindTraits<KIND>::is_float && cls[r] == 2) {
+            double dist;
+            bool in = recheck64<KIND>(A.xrows, A.nu, A.d, A.th.eps, A.th.eps2, qp[r], lpt, &dist);
+            atomicAdd(&A.stats->band_pairs, 1ull);
+            cls[r] = in ? 1 : 0;
+            if (MODE == MODE_MEMBER && fabs(dist - A.th.eps) <= A.th.tie_rel * A.th.eps) {
+              unsigned long long k = atomicAdd(&A.stats->near_ties, 1ull);
+              if ((int64_t)k < A.tie_cap && A.ties) {
+                A.ties[3 * k + 0] = qp[r];
+                A.ties[3 * k + 1] = lpt;
+                A.ties[3 * k + 2] = in ? 1 : 0;
+              }
+            }
+            if (MODE == MODE_COVER) covered[r] = covered[r] || in;
+            if (MODE == MODE_ADJ) word[r] |= (in ? 1u : 0u) << (int)(lb + jj - l0);
+          }
+          if (MODE == MODE_MEMBER) nemit += (cls[r] == 1);
+        }
+        if (MODE == MODE_MEMBER) {
+          int incl = nemit;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            int v = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += v;
+          }
+          const int wtot = __shfl_sync(FULL, incl, 31);
+          unsigned long long base = 0;
+          if (wtot > 0) {
+            if (lane == 31) base = atomicAdd(&A.stats->key_count, (unsigned long long)wtot);
+            base = __shfl_sync(FULL, base, 31);
+            unsigned long long k = base + (unsigned long long)(incl - nemit);
+            const unsigned long long jpos =
+                (unsigned long long)(A.lpos0 + (lb + jj - A.l_begin));
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+              if (cls[r] == 1) {
+                if ((int64_t)k < A.key_cap)
+                  A.keys[k] = ((unsigned long long)qp[r] << A.lbits) | jpos;
+                ++k;
+              }
+            }
+          }
+        }
+      }
+      if (MODE == MODE_COVER) {
+        bool done = true;
+#pragma unroll
+        for (int r = 0; r < R; ++r) done = done && (covered[r] || !act[r]);
+        warp_done = __all_sync(FULL, done);
+      }
+    }
+  }
+
+  if (MODE == MODE_ADJ) {
+    const int64_t wcol = l0 / 32;
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (act[r]) A.adj[qi[r] * (int64_t)A.adj_words + wcol] = word[r];
+  }
+  if (MODE == MODE_COVER) {
+    int cnt = 0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (act[r]) A.keep[qi[r] - q_begin] = covered[r] ? 0 : 1;
+      cnt += (act[r] && !covered[r]) ? 1 : 0;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(FULL, cnt, o);
+    if (lane == 0) s_red[warp] = cnt;
+    __syncthreads();
+    if (tid == 0) {
+      int tot = 0;
+      for (int w = 0; w < NT / 32; ++w) tot += s_red[w];
+      A.blk_count[blockIdx.x] = tot;
+    }
+  }
+  if (MODE == MODE_ADJ || MODE == MODE_COVER) {
+    // greedy evaluation statistics are accumulated by the resolve kernel
+  }
+}
+
+template <int KIND, int NU, int MODE>
+cudaError_t launch_pairs_nu(const PairArgs& a, int64_t q_rows_max, cudaStream_t s) {
+  constexpr int R = (MODE == MODE_ADJ || NU == 0) ? 1 : (NU <= 8 ? 4 : (NU <= 16 ? 2 : 1));
+  constexpr int LC = NU == 0 ? 32 : 64;
+  constexpr int NT = 256;
+  size_t smem = (size_t)LC * a.nu * sizeof(uint2);
+  auto kern = k_pairs<KIND, NU, R, MODE, LC>;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  int64_t gx = (q_rows_max + NT * R - 1) / (NT * R);
+  if (gx < 1) gx = 1;
+  int64_t gy = 1;
+  if (MODE == MODE_ADJ) gy = (a.l_end - a.l_begin + 31) / 32;
+  if (MODE == MODE_MEMBER) gy = (a.l_end - a.l_begin + a.l_chunk - 1) / a.l_chunk;
+  if (gy < 1) gy = 1;
+  if (gx > 0x7fffffffLL || gy > 65535) return cudaErrorInvalidConfiguration;
+  kern<<<dim3((unsigned)gx, (unsigned)gy), NT, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+template <int KIND, int NU>
+cudaError_t launch_pairs_mode(int mode, const PairArgs& a, int64_t q_rows_max, cudaStream_t s) {
+  if (mode == MODE_ADJ) return launch_pairs_nu<KIND, NU, MODE_ADJ>(a, q_rows_max, s);
+  if (mode == MODE_COVER) return launch_pairs_nu<KIND, NU, MODE_COVER>(a, q_rows_max, s);
+  return launch_pairs_nu<KIND, NU, MODE_MEMBER>(a, q_rows_max, s);
+}
+
+// Runtime NU dispatch for one kind (NU must be one of the instantiated widths,
+// see pick_nu in internal.cuh; 0 = wide).
+template <int KIND>
+cudaError_t launch_pairs_kind(int mode, const PairArgs& a, int64_t q_rows_max, cudaStream_t s) {
+  switch (a.nu) {
+    case 1: return launch_pairs_mode<KIND, 1>(mode, a, q_rows_max, s);
+    case 2: return launch_pairs_mode<KIND, 2>(mode, a, q_rows_max, s);
+    case 4: return launch_pairs_mode<KIND, 4>(mode, a, q_rows_max, s);
+    case 5: return launch_pairs_mode<KIND, 5>(mode, a, q_rows_max, s);
+    case 8: return launch_pairs_mode<KIND, 8>(mode, a, q_rows_max, s);
+    case 12: return launch_pairs_mode<KIND, 12>(mode, a, q_rows_max, s);
+    case 16: return launch_pairs_mode<KIND, 16>(mode, a, q_rows_max, s);
+    case 24: return launch_pairs_mode<KIND, 24>(mode, a, q_rows_max, s);
+    case 32: return launch_pairs_mode<KIND, 32>(mode, a, q_rows_max, s);
+    default: return launch_pairs_mode<KIND, 0>(mode, a, q_rows_max, s);
+  }
+}
+
+#define BM_INSTANTIATE_PAIRS(KIND)                                                       \
+  template cudaError_t launch_pairs_kind<KIND>(int, const PairArgs&, int64_t, cudaStream_t);
+
+}  // namespace bm

@@ -1,0 +1,6 @@
+// pairs_l2f.cu — instantiation of the CUDA-core pair kernel for kind K_L2F
+// (split per kind so the kernel variants compile in parallel).
+#include "pairs_impl.cuh"
+namespace bm {
+BM_INSTANTIATE_PAIRS(K_L2F)
+}

@@ -1,0 +1,87 @@
+// prep.cu — step A0: pack rows into 8-byte units, norms, finite check.
+//
+// fp32 rows are copied bit-for-bit (zero padded to NU units): the CUDA-core
+// kernels score them in fp32 and the fp64 recheck reads the same values.  For
+// cosine, xhat = x / ||x|| (norm in fp64) rounded to fp32; a
+// zero row gets NaN so that every pair touching it lands in the fp64 band.
+// Integer rows are packed as int8 (uint8 shifted by -128: exact, distances are
+// translation invariant) with exact int32 squared norms for the Gram form
+// d^2 = |x|^2 + |y|^2 - 2 x.y.
+#include <math.h>
+
+#include "internal.cuh"
+
+namespace bm {
+
+__global__ void k_prep_f32(const float* __restrict__ X, int64_t n, int d, int nu, int cosine,
+                           uint2* __restrict__ rows, uint2* __restrict__ xhat,
+                           DevStats* stats) {
+  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const float* x = X + p * (int64_t)d;
+  float2* r = reinterpret_cast<float2*>(rows) + p * (int64_t)nu;
+  double ss = 0.0;
+  bool finite = true;
+  for (int u = 0; u < nu; ++u) {
+    int j = 2 * u;
+    float a = j < d ? x[j] : 0.f;
+    float b = j + 1 < d ? x[j + 1] : 0.f;
+    finite = finite && isfinite(a) && isfinite(b);
+    r[u] = make_float2(a, b);
+    ss = __dadd_rn(ss, __dmul_rn((double)a, (double)a));
+    ss = __dadd_rn(ss, __dmul_rn((double)b, (double)b));
+  }
+  if (!finite) atomicExch(&stats->nonfinite, 1);
+  if (cosine) {
+    float2* h = reinterpret_cast<float2*>(xhat) + p * (int64_t)nu;
+    if (ss == 0.0) {
+      for (int u = 0; u < nu; ++u) h[u] = make_float2(0.f, 0.f);
+      h[0] = make_float2(__int_as_float(0x7fc00000), __int_as_float(0x7fc00000));
+    } else {
+      double inv = 1.0 / sqrt(ss);
+      for (int u = 0; u < nu; ++u) {
+        float2 v = r[u];
+        h[u] = make_float2((float)((double)v.x * inv), (float)((double)v.y * inv));
+      }
+    }
+  }
+}
+
+__global__ void k_prep_int(const uint8_t* __restrict__ X, int64_t n, int d, int nu, int is_u8,
+                           uint2* __restrict__ rows, int32_t* __restrict__ inorm) {
+  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const uint8_t* x = X + p * (int64_t)d;
+  uint2* r = rows + p * (int64_t)nu;
+  int32_t ss = 0;
+  for (int u = 0; u < nu; ++u) {
+    uint32_t w[2] = {0u, 0u};
+    for (int k = 0; k < 8; ++k) {
+      int j = 8 * u + k;
+      int v = 0;
+      if (j < d) v = is_u8 ? (int)x[j] - 128 : (int)(int8_t)x[j];
+      ss += v * v;
+      w[k >> 2] |= ((uint32_t)(uint8_t)(int8_t)v) << (8 * (k & 3));
+    }
+    r[u] = make_uint2(w[0], w[1]);
+  }
+  if (inorm) inorm[p] = ss;
+}
+
+cudaError_t launch_prep(const void* X, int dtype, int64_t n, int d, int kind, int nu,
+                        uint2* rows, uint2* xhat, int32_t* inorm, DevStats* stats,
+                        cudaStream_t s, int64_t* launches) {
+  int bs = 256;
+  int64_t g = (n + bs - 1) / bs;
+  if (dtype == BM_F32) {
+    k_prep_f32<<<(unsigned)g, bs, 0, s>>>((const float*)X, n, d, nu, kind == K_COSF, rows, xhat,
+                                          stats);
+  } else {
+    k_prep_int<<<(unsigned)g, bs, 0, s>>>((const uint8_t*)X, n, d, nu, dtype == BM_U8, rows,
+                                          inorm);
+  }
+  ++*launches;
+  return cudaGetLastError();
+}
+
+}  // namespace bm
