@@ -69,6 +69,7 @@ enum {
   BM_STEP_CSR = 3,      /* C: compaction into both CSRs                           */
   BM_STEP_EDGES = 4,    /* D1-D3: pair emission, radix sort, unique               */
   BM_STEP_TOTAL = 5,
+  BM_STEP_MEMBER_KERNEL = 6,  /* the membership contraction kernel alone (last launch) */
   BM_NUM_STEPS = 8
 };
 

@@ -22,7 +22,7 @@ STATUS_NAMES = {0: "BM_OK", 1: "BM_EINVAL", 2: "BM_EUNSUPPORTED", 3: "BM_ENOMEM"
 METRIC = {"l2": 0, "l1": 1, "cos": 2, "cosine": 2}
 DTYPE = {"f32": 0, "i8": 1, "u8": 2}
 PATH = {"auto": 0, "cuda_core": 1, "tensor": 2}
-STEPS = ("prep", "greedy", "member", "csr", "edges", "total")
+STEPS = ("prep", "greedy", "member", "csr", "edges", "total", "member_kernel")
 
 EXPORTED = ("bm_cover_build", "bm_cover_build_ex", "bm_cover_build_host", "bm_free",
             "bm_last_error", "bm_version", "bm_debug_radix_sort_u64",
@@ -143,8 +143,7 @@ class Cover:
         self.stats = CoverStats(c.n_pair_evals, c.n_greedy_evals, c.n_band_pairs,
                                 c.n_near_ties, c.n_greedy_tiles, c.n_launches, c.path_used,
                                 c.tile_used, {k: float(c.step_ms[i]) for i, k in
-                                              enumerate(STEPS[:5])} |
-                                {"total": float(c.step_ms[5])})
+                                              enumerate(STEPS)})
         k = c.n_near_ties_stored
         if k > 0:
             self.near_ties = np.ctypeslib.as_array(c.near_tie_pairs, shape=(k, 3)).copy()

@@ -153,7 +153,7 @@ __global__ void k_iota(int32_t* a, int64_t n) {
 struct Timer {
   bool on;
   cudaStream_t s;
-  cudaEvent_t ev[BM_NUM_STEPS + 1];
+  cudaEvent_t ev[BM_NUM_STEPS];
   int n = 0;
   Timer(bool o, cudaStream_t st) : on(o), s(st) {
     if (on)
@@ -369,7 +369,9 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
     m.lbits = lbits;
     m.ties = ties_dev;
     m.tie_cap = tie_cap;
+    tm.mark(6);
     CK(launch_pairs(kind, MODE_MEMBER, m, n, s, &launches));
+    tm.mark(7);
     CK(cudaMemcpyAsync(&hs, stats, sizeof hs, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     M = (int64_t)hs.key_count;
@@ -500,6 +502,7 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
   if (tm.on) {
     for (int i = 0; i < 5; ++i) cudaEventElapsedTime(&c->step_ms[i], tm.ev[i], tm.ev[i + 1]);
     cudaEventElapsedTime(&c->step_ms[BM_STEP_TOTAL], tm.ev[0], tm.ev[5]);
+    cudaEventElapsedTime(&c->step_ms[BM_STEP_MEMBER_KERNEL], tm.ev[6], tm.ev[7]);
   }
   c->n_launches = launches;
   if (host_in) {
