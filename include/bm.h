@@ -193,6 +193,14 @@ bm_status bm_debug_exclusive_scan_i64(const int64_t *in, int64_t *out, int64_t n
  * selected candidates.  nc <= 1024. */
 bm_status bm_debug_resolve_tile(const uint32_t *adj, int32_t nc, uint8_t *lm_out, void *stream);
 
+/* Raw tcgen05 Gram accumulators of the membership contraction (step B):
+ * out[p*L + j] = bits of sum_k x_p[k] * x_{lm[j]}[k] as accumulated by the
+ * tensor core (fp32 bits of the tf32 products for BM_F32, int32 for
+ * BM_U8 / BM_I8).  points, lm and out are DEVICE pointers; d*elem <= 512
+ * bytes (F32) or 896 bytes (int8). */
+bm_status bm_debug_tc_gram(const void *points, bm_dtype dtype, int64_t n, int32_t d,
+                           const int32_t *lm, int64_t L, uint32_t *out, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

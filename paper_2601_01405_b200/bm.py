@@ -26,7 +26,7 @@ STEPS = ("prep", "greedy", "member", "csr", "edges", "total", "member_kernel")
 
 EXPORTED = ("bm_cover_build", "bm_cover_build_ex", "bm_cover_build_host", "bm_free",
             "bm_last_error", "bm_version", "bm_debug_radix_sort_u64",
-            "bm_debug_exclusive_scan_i64", "bm_debug_resolve_tile")
+            "bm_debug_exclusive_scan_i64", "bm_debug_resolve_tile", "bm_debug_tc_gram")
 
 
 class BMError(RuntimeError):
@@ -89,6 +89,8 @@ def load() -> ctypes.CDLL:
     lib.bm_debug_exclusive_scan_i64.restype = i32
     lib.bm_debug_resolve_tile.argtypes = [vp, i32, vp, vp]
     lib.bm_debug_resolve_tile.restype = i32
+    lib.bm_debug_tc_gram.argtypes = [vp, i32, i64, i32, vp, i64, vp, vp]
+    lib.bm_debug_tc_gram.restype = i32
     _lib = lib
     return lib
 
@@ -298,3 +300,18 @@ def resolve_tile(adj_words: np.ndarray, nc: int) -> np.ndarray:
         ctypes.c_void_p(adj_words.ctypes.data), nc, ctypes.c_void_p(out.ctypes.data),
         ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
     return out
+
+
+def tc_gram(points, landmarks):
+    """Raw tcgen05 accumulators [n, L] (diagnostic; float32 for f32 input,
+    int32 for int8 input) of points @ points[landmarks].T."""
+    import torch
+    assert points.is_cuda and landmarks.is_cuda and landmarks.dtype == torch.int32
+    n, d = points.shape
+    L = landmarks.numel()
+    out = torch.empty((n, L), dtype=torch.int32, device=points.device)
+    _check(load().bm_debug_tc_gram(
+        ctypes.c_void_p(points.data_ptr()), DTYPE[_dtype_of(points)], n, d,
+        ctypes.c_void_p(landmarks.data_ptr()), L, ctypes.c_void_p(out.data_ptr()),
+        ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    return out.view(torch.float32) if _dtype_of(points) == "f32" else out

@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "internal.cuh"
+#include "tc.cuh"
 
 namespace {
 
@@ -196,8 +197,6 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
   int T = o.tile > 0 ? o.tile : 1024;
   if (T < 32 || T > 1024 || (T % 32) != 0)
     return set_err(BM_EINVAL, "tile must be a multiple of 32 in [32, 1024]");
-  if (o.path == BM_PATH_TENSOR)
-    return set_err(BM_EUNSUPPORTED, "tensor-core path not available in this build");
   const int64_t tie_cap = o.near_tie_cap > 0 ? o.near_tie_cap : 65536;
 
   const int kind = dtype == BM_F32
@@ -207,6 +206,22 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
   int nu = pick_nu(nu_needed);
   if (nu == 0) nu = nu_needed;
   const Thresh th = make_thresh(kind, d, eps);
+
+  // Tensor-core membership contraction (tc.cu): Euclidean only, K up to the
+  // configured atom counts; AUTO picks it for d >= 32.
+  tc::TcPlan P{};
+  P.kind = dtype == BM_F32 ? tc::TC_TF32 : (dtype == BM_U8 ? tc::TC_U8 : tc::TC_S8);
+  {
+    const int esz = dtype == BM_F32 ? 4 : 1;
+    P.row_bytes = (((int64_t)d * esz + 15) / 16) * 16;
+    P.k_elems = P.row_bytes / esz;
+    P.katoms = (int)((P.row_bytes + 127) / 128);
+  }
+  bool use_tc = metric == BM_L2 && tc::tc_supported(P.kind, P.katoms) &&
+                (o.path == BM_PATH_TENSOR || (o.path == BM_PATH_AUTO && d >= 32));
+  if (o.path == BM_PATH_TENSOR && !use_tc)
+    return set_err(BM_EUNSUPPORTED, "tensor-core path supports L2 with d*elem <= %d bytes",
+                   dtype == BM_F32 ? 512 : 896);
 
   int64_t launches = 0;
   Pool pool(s);
@@ -232,6 +247,19 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
   TRY(pool.alloc(&stats, 1));
   CK(cudaMemsetAsync(stats, 0, sizeof(DevStats), s));
   CK(launch_prep(dpoints, dtype, n, d, kind, nu, rows, xhat, inorm, stats, s, &launches));
+  void* tc_nrm = nullptr;
+  if (use_tc) {
+    uint8_t* xop = nullptr;
+    TRY(pool.alloc(&xop, (size_t)n * P.row_bytes));
+    if (dtype == BM_F32) TRY(pool.alloc((double**)&tc_nrm, (size_t)n));
+    else TRY(pool.alloc((int32_t**)&tc_nrm, (size_t)n));
+    P.xop = xop;
+    P.n_rows = n;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&P.num_sms, cudaDevAttrMultiProcessorCount, dev));
+    CK(tc::launch_tc_prep(dpoints, dtype, n, d, P, tc_nrm, stats, s, &launches));
+  }
   if (host_in) pool.free_now((void*)dpoints);
   tm.mark(1);
 
@@ -345,7 +373,90 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
   int64_t key_cap = n * 4 > (1 << 20) ? n * 4 : (1 << 20);
   unsigned long long* keys = nullptr;
   int64_t M = 0;
-  for (int attempt = 0; attempt < 2; ++attempt) {
+  if (use_tc) {
+    // ---- B on tcgen05 (tc.cu) + B' fp64 recheck of the queued band pairs
+    const int BN = tc::tc_bn_for(P.kind, P.katoms);
+    const int RB = tc::tc_rows_for(P.kind, P.katoms);
+    P.l_rows = ((L + BN - 1) / BN) * BN;
+    P.n_pad = ((n + RB - 1) / RB) * RB;
+    tc::TcArgs ta{};
+    ta.n = n;
+    ta.L = L;
+    ta.ksteps = (int)(((int64_t)d * (dtype == BM_F32 ? 4 : 1) + 31) / 32);
+    ta.lbits = lbits;
+    TRY(pool.alloc((uint8_t**)&P.lop, (size_t)P.l_rows * P.row_bytes));
+    double C2 = 0.0, tau = 0.0;
+    int32_t lo_i = th.lo_i;
+    if (P.kind == tc::TC_TF32) {
+      float *rlo, *rhi, *ca, *cb;
+      TRY(pool.alloc(&rlo, (size_t)P.n_pad));
+      TRY(pool.alloc(&rhi, (size_t)P.n_pad));
+      TRY(pool.alloc(&ca, (size_t)P.l_rows));
+      TRY(pool.alloc(&cb, (size_t)P.l_rows));
+      ta.row_lo = rlo;
+      ta.row_hi = rhi;
+      ta.col_a = ca;
+      ta.col_b = cb;
+      // |acc - x.l| <= c1 |x||l|, c1 = operand
+      // rounding (2u_t + u_t^2) + fp32 accumulation (4 K 2^-23, safety 2);
+      // epilogue roundings add 2^-22; |x||l| <= (n_p + n_l)/2.
+      const double ut = ldexp(1.0, -11);
+      const double K = 8.0 * ta.ksteps;
+      const double c1 = 2.0 * ut + ut * ut + 4.0 * K * ldexp(1.0, -23) * (1.0 + ut) * (1.0 + ut);
+      C2 = 1.25 * 0.5 * (c1 + ldexp(1.0, -22));
+      tau = 1.0000005e-6 * th.eps2 + th.eps2 * ldexp(1.0, -21);
+    } else {
+      int32_t *rr, *cc;
+      TRY(pool.alloc(&rr, (size_t)P.n_pad));
+      TRY(pool.alloc(&cc, (size_t)P.l_rows));
+      ta.row_r = rr;
+      ta.col_c = cc;
+    }
+    CK(tc::launch_tc_rows(P, tc_nrm, n, C2, th.eps2, tau, lo_i, ta, s, &launches));
+    CK(tc::launch_tc_landmarks(P, tc_nrm, lm, L, C2, ta, s, &launches));
+    int64_t band_cap = n * 4 > (1 << 22) ? n * 4 : (1 << 22);
+    unsigned long long *band = nullptr, *bcount = nullptr;
+    TRY(pool.alloc(&bcount, 1));
+    for (int attempt = 0; attempt < 3; ++attempt) {
+      TRY(pool.alloc(&keys, (size_t)key_cap));
+      TRY(pool.alloc(&band, (size_t)band_cap));
+      CK(cudaMemsetAsync(bcount, 0, sizeof(unsigned long long), s));
+      CK(cudaMemsetAsync(&stats->key_count, 0, sizeof(unsigned long long), s));
+      ta.keys = keys;
+      ta.key_count = &stats->key_count;
+      ta.key_cap = key_cap;
+      ta.band = band;
+      ta.band_count = bcount;
+      ta.band_cap = band_cap;
+      tm.mark(6);
+      CK(tc::launch_tc(P, ta, s, &launches));
+      tm.mark(7);
+      unsigned long long hb = 0;
+      CK(cudaMemcpyAsync(&hs, stats, sizeof hs, cudaMemcpyDeviceToHost, s));
+      CK(cudaMemcpyAsync(&hb, bcount, sizeof hb, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      const int64_t K1 = (int64_t)hs.key_count, B = (int64_t)hb;
+      if (B <= band_cap && K1 + B <= key_cap) {
+        CK(tc::launch_tc_recheck(band, B, (const float*)rows, 2 * nu, d, lm, th, lbits, keys,
+                                 &stats->key_count, key_cap, ties_dev, tie_cap, stats, s,
+                                 &launches));
+        unsigned long long tot = greedy_band + (unsigned long long)B;
+        CK(cudaMemcpyAsync(&stats->band_pairs, &tot, sizeof tot, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(&hs, stats, sizeof hs, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        M = (int64_t)hs.key_count;
+        break;
+      }
+      pool.free_now(keys);
+      pool.free_now(band);
+      if (B > band_cap) band_cap = B;
+      if (K1 + B > key_cap) key_cap = K1 + B;
+      if (attempt == 2) return set_err(BM_ENOMEM, "membership buffers kept overflowing");
+    }
+    pool.free_now(band);
+    pool.free_now((void*)P.lop);
+  }
+  for (int attempt = 0; attempt < 2 && !use_tc; ++attempt) {
     TRY(pool.alloc(&keys, (size_t)key_cap));
     PairArgs m = base;
     m.qidx = nullptr;
@@ -427,29 +538,29 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
   TRY(pool.alloc((uint8_t**)&stemp, scan_temp_bytes(n)));
   CK(launch_pair_counts(pt_ptr, n, pcnt, s, &launches));
   CK(exclusive_scan_i64(pcnt, poff, n, stemp, ptot, s, &launches));
-  int64_t P = 0;
-  CK(cudaMemcpyAsync(&P, ptot, sizeof P, cudaMemcpyDeviceToHost, s));
+  int64_t NP = 0;  // P = sum_p C(t_p, 2) witnessed pairs
+  CK(cudaMemcpyAsync(&NP, ptot, sizeof NP, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   int64_t E = 0;
   int32_t* edges = nullptr;
-  if (P > 0) {
+  if (NP > 0) {
     unsigned long long *ek = nullptr, *ea = nullptr;
     int64_t *flags = nullptr, *pos = nullptr;
     void *et = nullptr, *ft = nullptr;
-    TRY(pool.alloc(&ek, (size_t)P));
-    TRY(pool.alloc(&ea, (size_t)P));
-    TRY(pool.alloc((uint8_t**)&et, radix_temp_bytes(P)));
+    TRY(pool.alloc(&ek, (size_t)NP));
+    TRY(pool.alloc(&ea, (size_t)NP));
+    TRY(pool.alloc((uint8_t**)&et, radix_temp_bytes(NP)));
     CK(launch_pair_emit(pt_ptr, pt_lm, n, poff, lbits, ek, s, &launches));
-    CK(radix_sort_u64(&ek, &ea, P, 0, 2 * lbits, et, s, &launches));
-    TRY(pool.alloc(&flags, (size_t)P));
-    TRY(pool.alloc(&pos, (size_t)P));
-    TRY(pool.alloc((uint8_t**)&ft, scan_temp_bytes(P)));
-    CK(launch_unique_flags(ek, P, flags, s, &launches));
-    CK(exclusive_scan_i64(flags, pos, P, ft, ptot + 1, s, &launches));
+    CK(radix_sort_u64(&ek, &ea, NP, 0, 2 * lbits, et, s, &launches));
+    TRY(pool.alloc(&flags, (size_t)NP));
+    TRY(pool.alloc(&pos, (size_t)NP));
+    TRY(pool.alloc((uint8_t**)&ft, scan_temp_bytes(NP)));
+    CK(launch_unique_flags(ek, NP, flags, s, &launches));
+    CK(exclusive_scan_i64(flags, pos, NP, ft, ptot + 1, s, &launches));
     CK(cudaMemcpyAsync(&E, ptot + 1, sizeof E, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     TRY(pool.alloc(&edges, (size_t)(2 * E > 0 ? 2 * E : 1)));
-    CK(launch_unique_scatter(ek, P, pos, lbits, edges, s, &launches));
+    CK(launch_unique_scatter(ek, NP, pos, lbits, edges, s, &launches));
     pool.free_now(ek);
     pool.free_now(ea);
     pool.free_now(flags);
@@ -489,7 +600,7 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
   c->n_band_pairs = (int64_t)hs.band_pairs;
   c->n_near_ties = (int64_t)hs.near_ties;
   c->n_greedy_tiles = (int64_t)hs.tiles;
-  c->path_used = BM_PATH_CUDA_CORE;
+  c->path_used = use_tc ? BM_PATH_TENSOR : BM_PATH_CUDA_CORE;
   c->tile_used = T;
   const int64_t nst = c->n_near_ties < tie_cap ? c->n_near_ties : tie_cap;
   c->n_near_ties_stored = nst;
@@ -627,6 +738,54 @@ bm_status bm_debug_exclusive_scan_i64(const int64_t* in, int64_t* out, int64_t n
   CK(cudaMemcpyAsync(&h, tot, sizeof h, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   if (total) *total = h;
+  return BM_OK;
+}
+
+bm_status bm_debug_tc_gram(const void* points, bm_dtype dtype, int64_t n, int32_t d,
+                           const int32_t* lm, int64_t L, uint32_t* out, void* stream) {
+  using namespace bm;
+  if (!points || !lm || !out || n < 1 || d < 1 || L < 1) return set_err(BM_EINVAL, "bad arguments");
+  cudaStream_t s = (cudaStream_t)stream;
+  tc::TcPlan P{};
+  P.kind = dtype == BM_F32 ? tc::TC_TF32 : (dtype == BM_U8 ? tc::TC_U8 : tc::TC_S8);
+  const int esz = dtype == BM_F32 ? 4 : 1;
+  P.row_bytes = (((int64_t)d * esz + 15) / 16) * 16;
+  P.k_elems = P.row_bytes / esz;
+  P.katoms = (int)((P.row_bytes + 127) / 128);
+  if (!tc::tc_supported(P.kind, P.katoms)) return set_err(BM_EUNSUPPORTED, "d too large");
+  Pool pool(s);
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&P.num_sms, cudaDevAttrMultiProcessorCount, dev));
+  uint8_t* xop = nullptr;
+  void* nrm = nullptr;
+  DevStats* stats = nullptr;
+  TRY(pool.alloc(&xop, (size_t)n * P.row_bytes));
+  TRY(pool.alloc((double**)&nrm, (size_t)n));
+  TRY(pool.alloc(&stats, 1));
+  CK(cudaMemsetAsync(stats, 0, sizeof(DevStats), s));
+  P.xop = xop;
+  P.n_rows = n;
+  int64_t launches = 0;
+  CK(tc::launch_tc_prep(points, dtype, n, d, P, nrm, stats, s, &launches));
+  const int BN = tc::tc_bn_for(P.kind, P.katoms), RB = tc::tc_rows_for(P.kind, P.katoms);
+  P.l_rows = ((L + BN - 1) / BN) * BN;
+  P.n_pad = ((n + RB - 1) / RB) * RB;
+  TRY(pool.alloc((uint8_t**)&P.lop, (size_t)P.l_rows * P.row_bytes));
+  tc::TcArgs ta{};
+  ta.n = n;
+  ta.L = L;
+  ta.ksteps = (int)(((int64_t)d * esz + 31) / 32);
+  float *fa, *fb;
+  TRY(pool.alloc(&fa, (size_t)P.l_rows * 2));
+  fb = fa + P.l_rows;
+  ta.col_a = fa;
+  ta.col_b = fb;
+  ta.col_c = (const int32_t*)fa;
+  CK(tc::launch_tc_landmarks(P, nrm, lm, L, 0.0, ta, s, &launches));
+  ta.gram = out;
+  CK(tc::launch_tc(P, ta, s, &launches));
+  CK(cudaStreamSynchronize(s));
   return BM_OK;
 }
 

@@ -1,0 +1,734 @@
+// tc.cu — step B on the 5th-gen tensor cores: the Gram-trick membership
+// contraction (d^2(q,x) = d^2(q,0) + d^2(x,0) - 2 sum_j q_j x_j,
+// with the norms "precomputed and stored").
+//
+// Structure (one persistent CTA per SM, 8 warps):
+//   warp 0      TMA producer: the CTA's resident A block (RA x 128 point rows,
+//               all K atoms) once per work unit, then B (landmark) tiles of
+//               BN rows one 128-byte K atom per pipeline stage.
+//   warp 1      MMA issuer (one elected thread): tcgen05.mma kind::tf32 (fp32
+//               data pre-rounded to tf32) or kind::i8 (exact int32), A and B
+//               from 128B-swizzled K-major shared memory, D in TMEM; two TMEM
+//               accumulator buffers of RA x BN columns so the epilogue of tile
+//               t overlaps the MMAs of tile t+1.
+//   warp 2      TMEM allocator.
+//   warps 4-7   epilogue: tcgen05.ld 32 columns at a time, per pair one add and
+//               one max against a per-row / per-column constant ("out for sure"
+//               test); the rare survivors are classified in / band and staged
+//               in shared memory, flushed to global with one atomic per flush.
+// Float exactness: with x, l rounded to tf32 and
+// fp32 accumulation, |acc - x.l| <= C (|x|^2 + |l|^2)/2 with a global constant
+// C; the per-row/per-column thresholds fold that bound in, so "out" and "in"
+// decisions are certain and every other pair is queued for the fp64 recheck
+// (k_tc_recheck) that reproduces the oracle's formula exactly.
+#include <cuda.h>
+#include <math.h>
+
+#include "internal.cuh"
+#include "tc.cuh"
+
+namespace bm {
+namespace tc {
+
+constexpr unsigned FULLM = 0xffffffffu;
+
+__device__ __forceinline__ uint32_t su32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE_%=;\n\t"
+      "bra WAIT_%=;\n"
+      "DONE_%=:\n\t}" ::"r"(su32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, uint64_t* bar, int x,
+                                            int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(su32(dst)),
+      "l"(tm), "r"(x), "r"(y), "r"(su32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   su32(bar))
+               : "memory");
+}
+template <int KIND>
+__device__ __forceinline__ void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
+                                    uint32_t acc) {
+  if constexpr (KIND == TC_TF32) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, "
+      "%28, %29, %30, %31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+        "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
+        "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+        "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
+        "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// Shared-memory matrix descriptor: K-major, 128-byte swizzle, 8-row groups
+// 1024 B apart (SBO), sm_100 descriptor version 1.
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)1u << 16;
+  d |= (uint64_t)(1024u >> 4) << 32;
+  d |= (uint64_t)1u << 46;
+  d |= (uint64_t)2u << 61;
+  return d;
+}
+
+template <int KIND>
+constexpr uint32_t make_idesc(int M, int N) {
+  // c_format [4,6): 1 = F32, 2 = S32; a/b format [7,10)/[10,13): TF32 = 2,
+  // u8 = 0, s8 = 1; a/b major bits 15/16 = 0 (K-major); N>>3 at 17; M>>4 at 24.
+  return (KIND == TC_TF32 ? (1u << 4) | (2u << 7) | (2u << 10)
+                          : (2u << 4) | ((KIND == TC_S8 ? 1u : 0u) << 7) |
+                                ((KIND == TC_S8 ? 1u : 0u) << 10)) |
+         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+template <int RA, int BN, int KATOMS, int STAGES>
+struct Smem {
+  static constexpr int A_ATOM = 128 * 128;                 // 128 rows x 128 B
+  static constexpr int A_BYTES = RA * KATOMS * A_ATOM;
+  static constexpr int B_STAGE = BN * 128;
+  static constexpr int B_BYTES = STAGES * B_STAGE;
+  static constexpr int KEYCAP = 1024, BANDCAP = 1024;
+  static constexpr int BAR_OFF = A_BYTES + B_BYTES;
+  static constexpr int NBARS = 2 * STAGES + 2 + 4;
+  static constexpr int BUF_OFF = BAR_OFF + NBARS * 8 + 16;
+  static constexpr int TOTAL = BUF_OFF + (KEYCAP + BANDCAP) * 8 + 1024;  // + align slack
+};
+
+// ------------------------------------------------------------------ kernel
+template <int KIND, int RA, int BN, int KATOMS, int STAGES, int MODE>
+__global__ void __launch_bounds__(256, 1)
+    k_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+         TcArgs args) {
+  using S = Smem<RA, BN, KATOMS, STAGES>;
+  constexpr int BUFCOLS = RA * BN;
+  static_assert(2 * BUFCOLS <= 512, "TMEM: two accumulator buffers must fit 512 columns");
+  static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "BN");
+  constexpr int ATOM_ELEMS = KIND == TC_TF32 ? 32 : 128;
+  constexpr uint32_t IDESC = make_idesc<KIND>(128, BN);
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sA = sm;
+  uint8_t* sB = sm + S::A_BYTES;
+  uint64_t* bars = (uint64_t*)(sm + S::BAR_OFF);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + STAGES;
+  uint64_t* a_full = bars + 2 * STAGES;
+  uint64_t* a_empty = a_full + 1;
+  uint64_t* t_full = a_full + 2;   // [2]
+  uint64_t* t_empty = a_full + 4;  // [2]
+  uint32_t* tmem_slot = (uint32_t*)(bars + S::NBARS);
+  uint32_t* kcount = tmem_slot + 1;
+  uint32_t* bcount = tmem_slot + 2;
+  unsigned long long* kbuf = (unsigned long long*)(sm + S::BUF_OFF);
+  unsigned long long* bbuf = kbuf + S::KEYCAP;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(a_full, 1);
+    mbar_init(a_empty, 1);
+    mbar_init(&t_full[0], 1);
+    mbar_init(&t_full[1], 1);
+    mbar_init(&t_empty[0], 4);
+    mbar_init(&t_empty[1], 4);
+    *kcount = 0;
+    *bcount = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     su32(tmem_slot)),
+                 "r"(512)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  const int64_t n_tiles = args.n_tiles;           // BN-wide landmark tiles
+  const int64_t tiles_per_chunk = args.tiles_per_chunk;
+  const int64_t n_chunks = (n_tiles + tiles_per_chunk - 1) / tiles_per_chunk;
+  const int64_t n_units = args.n_mblk * n_chunks;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer
+      int stage = 0;
+      uint32_t phase = 0, a_ph = 0;
+      bool first = true;
+      for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
+        const int64_t mb = u / n_chunks, ch = u % n_chunks;
+        const int64_t t0 = ch * tiles_per_chunk, t1 = min(n_tiles, t0 + tiles_per_chunk);
+        if (!first) {
+          mbar_wait(a_empty, a_ph);
+          a_ph ^= 1u;
+        }
+        first = false;
+        mbar_expect_tx(a_full, (uint32_t)S::A_BYTES);
+        for (int r = 0; r < RA; ++r)
+          for (int ka = 0; ka < KATOMS; ++ka)
+            tma_load_2d(sA + (r * KATOMS + ka) * S::A_ATOM, &tmA, a_full, ka * ATOM_ELEMS,
+                        (int)(mb * RA * 128 + r * 128));
+        for (int64_t t = t0; t < t1; ++t) {
+          for (int ka = 0; ka < KATOMS; ++ka) {
+            mbar_wait(&empty[stage], phase ^ 1u);
+            mbar_expect_tx(&full[stage], (uint32_t)S::B_STAGE);
+            tma_load_2d(sB + stage * S::B_STAGE, &tmB, &full[stage], ka * ATOM_ELEMS,
+                        (int)(t * BN));
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1u;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer
+      int stage = 0;
+      uint32_t phase = 0, a_ph = 0;
+      uint32_t use[2] = {0u, 0u};
+      int buf = 0;
+      const int ksteps = args.ksteps;  // 32-byte K steps actually needed
+      for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
+        const int64_t ch = u % n_chunks;
+        const int64_t t0 = ch * tiles_per_chunk, t1 = min(n_tiles, t0 + tiles_per_chunk);
+        mbar_wait(a_full, a_ph);
+        a_ph ^= 1u;
+        fence_after();
+        for (int64_t t = t0; t < t1; ++t) {
+          mbar_wait(&t_empty[buf], (use[buf] & 1u) ^ 1u);
+          fence_after();
+          const uint32_t dcol = tmem + (uint32_t)(buf * BUFCOLS);
+          for (int ka = 0; ka < KATOMS; ++ka) {
+            mbar_wait(&full[stage], phase);
+            fence_after();
+            const uint32_t bbase = su32(sB + stage * S::B_STAGE);
+#pragma unroll
+            for (int r = 0; r < RA; ++r) {
+              const uint32_t abase = su32(sA + (r * KATOMS + ka) * S::A_ATOM);
+#pragma unroll
+              for (int ks = 0; ks < 4; ++ks) {
+                if (ka * 4 + ks < ksteps)
+                  mma<KIND>(dcol + (uint32_t)(r * BN), sdesc(abase + ks * 32),
+                            sdesc(bbase + ks * 32), IDESC, (ka | ks) != 0 ? 1u : 0u);
+              }
+            }
+            mma_commit(&empty[stage]);
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1u;
+            }
+          }
+          mma_commit(&t_full[buf]);
+          ++use[buf];
+          buf ^= 1;
+        }
+        mma_commit(a_empty);
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue (warps 4..7 -> TMEM lane quarters 0..3)
+    const int q = warp & 3;
+    uint32_t use[2] = {0u, 0u};
+    int buf = 0;
+    for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
+      const int64_t mb = u / n_chunks, ch = u % n_chunks;
+      const int64_t t0 = ch * tiles_per_chunk, t1 = min(n_tiles, t0 + tiles_per_chunk);
+      int64_t prow[RA];
+      float rlo[RA], rhi[RA];
+      int32_t rint[RA];
+#pragma unroll
+      for (int r = 0; r < RA; ++r) {
+        prow[r] = mb * RA * 128 + r * 128 + q * 32 + lane;   // < n_pad
+        if constexpr (KIND == TC_TF32) {
+          rlo[r] = args.row_lo[prow[r]];
+          rhi[r] = args.row_hi[prow[r]];
+        } else {
+          rint[r] = args.row_r[prow[r]];
+        }
+      }
+      for (int64_t t = t0; t < t1; ++t) {
+        mbar_wait(&t_full[buf], use[buf] & 1u);
+        ++use[buf];
+        fence_after();
+#pragma unroll
+        for (int r = 0; r < RA; ++r) {
+#pragma unroll 1
+          for (int cc = 0; cc < BN / 32; ++cc) {
+            uint32_t v[32];
+            const uint32_t taddr =
+                tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * BUFCOLS + r * BN + cc * 32);
+            tmem_ld32(taddr, v);
+            const int64_t j0 = t * BN + cc * 32;
+            if constexpr (MODE == TC_MODE_GRAM) {
+              if (prow[r] < args.n) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                  if (j0 + i < args.L) args.gram[prow[r] * args.L + j0 + i] = v[i];
+              }
+              continue;
+            }
+            bool surv;
+            if constexpr (KIND == TC_TF32) {
+              const float4* cb = reinterpret_cast<const float4*>(args.col_b + j0);
+              float m = -INFINITY;
+#pragma unroll
+              for (int i4 = 0; i4 < 8; ++i4) {
+                const float4 b = __ldg(cb + i4);
+                m = fmaxf(m, __uint_as_float(v[4 * i4 + 0]) - b.x);
+                m = fmaxf(m, __uint_as_float(v[4 * i4 + 1]) - b.y);
+                m = fmaxf(m, __uint_as_float(v[4 * i4 + 2]) - b.z);
+                m = fmaxf(m, __uint_as_float(v[4 * i4 + 3]) - b.w);
+              }
+              surv = m > rlo[r];
+            } else {
+              const int4* cc4 = reinterpret_cast<const int4*>(args.col_c + j0);
+              int m = INT_MIN;
+#pragma unroll
+              for (int i4 = 0; i4 < 8; ++i4) {
+                const int4 c = __ldg(cc4 + i4);
+                m = max(m, 2 * (int)v[4 * i4 + 0] - c.x);
+                m = max(m, 2 * (int)v[4 * i4 + 1] - c.y);
+                m = max(m, 2 * (int)v[4 * i4 + 2] - c.z);
+                m = max(m, 2 * (int)v[4 * i4 + 3] - c.w);
+              }
+              surv = m > rint[r];
+            }
+            if (__any_sync(FULLM, surv)) {
+              // rare path: classify the surviving columns of this lane
+              if (surv) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                  const int64_t j = j0 + i;
+                  int cls = 0;  // 0 out, 1 in, 2 band
+                  if constexpr (KIND == TC_TF32) {
+                    const float a = __uint_as_float(v[i]);
+                    if (a - args.col_b[j] > rlo[r]) cls = (a - args.col_a[j] > rhi[r]) ? 1 : 2;
+                  } else {
+                    cls = (2 * (int)v[i] - args.col_c[j] > rint[r]) ? 1 : 0;
+                  }
+                  if (cls == 0) continue;
+                  const unsigned long long key =
+                      cls == 1 ? (((unsigned long long)prow[r] << args.lbits) |
+                                  (unsigned long long)j)
+                               : (((unsigned long long)prow[r] << 32) | (unsigned long long)j);
+                  uint32_t* cnt = cls == 1 ? kcount : bcount;
+                  unsigned long long* buf_s = cls == 1 ? kbuf : bbuf;
+                  const uint32_t cap = cls == 1 ? S::KEYCAP : S::BANDCAP;
+                  const uint32_t k = atomicAdd(cnt, 1u);
+                  if (k < cap) {
+                    buf_s[k] = key;
+                  } else {
+                    unsigned long long* gcnt = cls == 1 ? args.key_count : args.band_count;
+                    unsigned long long* gbuf = cls == 1 ? args.keys : args.band;
+                    const int64_t gcap = cls == 1 ? args.key_cap : args.band_cap;
+                    const unsigned long long g = atomicAdd(gcnt, 1ull);
+                    if ((int64_t)g < gcap) gbuf[g] = key;
+                  }
+                }
+              }
+            }
+          }
+        }
+        fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&t_empty[buf]);
+        buf ^= 1;
+        // flush the shared staging buffers when half full (epilogue warps only)
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        const uint32_t kc = *kcount, bc = *bcount;
+        const bool last = (t + 1 == t1) && (u + gridDim.x >= n_units);
+        if (kc > S::KEYCAP / 2 || bc > S::BANDCAP / 2 || last) {
+          __shared__ unsigned long long gbase[2];
+          const int et = threadIdx.x - 128;
+          const uint32_t kn = min(kc, (uint32_t)S::KEYCAP), bn = min(bc, (uint32_t)S::BANDCAP);
+          if (et == 0) {
+            gbase[0] = kn ? atomicAdd(args.key_count, (unsigned long long)kn) : 0ull;
+            gbase[1] = bn ? atomicAdd(args.band_count, (unsigned long long)bn) : 0ull;
+          }
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          for (uint32_t i = et; i < kn; i += 128)
+            if ((int64_t)(gbase[0] + i) < args.key_cap) args.keys[gbase[0] + i] = kbuf[i];
+          for (uint32_t i = et; i < bn; i += 128)
+            if ((int64_t)(gbase[1] + i) < args.band_cap) args.band[gbase[1] + i] = bbuf[i];
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          if (et == 0) {
+            *kcount = 0;
+            *bcount = 0;
+          }
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  if (warp == 2) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512)
+                 : "memory");
+  }
+}
+
+// ------------------------------------------------------------ host helpers
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)p;
+  }
+  return fn;
+}
+
+// 2-D K-major operand [rows][row_bytes], box = (128 bytes of K) x box_rows, 128B swizzle.
+static cudaError_t make_tmap(CUtensorMap* tm, const void* base, int kind, int64_t k_elems,
+                             int64_t rows, int64_t row_bytes, int box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return cudaErrorNotSupported;
+  const int esz = kind == TC_TF32 ? 4 : 1;
+  cuuint64_t dims[2] = {(cuuint64_t)k_elems, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)row_bytes};
+  cuuint32_t box[2] = {(cuuint32_t)(128 / esz), (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(tm, kind == TC_TF32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_UINT8,
+                  2, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+template <int KIND, int RA, int BN, int KATOMS, int STAGES, int MODE>
+static cudaError_t launch_cfg(const TcPlan& P, TcArgs a, cudaStream_t s) {
+  using S = Smem<RA, BN, KATOMS, STAGES>;
+  CUtensorMap tA, tB;
+  cudaError_t e = make_tmap(&tA, P.xop, KIND, P.k_elems, P.n_rows, P.row_bytes, 128);
+  if (e != cudaSuccess) return e;
+  e = make_tmap(&tB, P.lop, KIND, P.k_elems, P.l_rows, P.row_bytes, BN);
+  if (e != cudaSuccess) return e;
+  auto kern = k_tc<KIND, RA, BN, KATOMS, STAGES, MODE>;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::TOTAL);
+  if (e != cudaSuccess) return e;
+  a.n_tiles = P.l_rows / BN;
+  a.n_mblk = (P.n_rows + RA * 128 - 1) / (RA * 128);
+  // work units: (m-block, chunk of landmark tiles); enough units to balance 148 SMs
+  int64_t chunks = (4 * P.num_sms + a.n_mblk - 1) / a.n_mblk;
+  if (chunks < 1) chunks = 1;
+  if (chunks > a.n_tiles) chunks = a.n_tiles;
+  a.tiles_per_chunk = (a.n_tiles + chunks - 1) / chunks;
+  chunks = (a.n_tiles + a.tiles_per_chunk - 1) / a.tiles_per_chunk;
+  int64_t units = a.n_mblk * chunks;
+  int grid = (int)(units < P.num_sms ? units : P.num_sms);
+  kern<<<grid, 256, S::TOTAL, s>>>(tA, tB, a);
+  return cudaGetLastError();
+}
+
+// Configuration table:
+//   tf32, K <= 64 floats (2 atoms): A-stationary 512 rows (RA=4), BN=64, 8 stages
+//   tf32, K <= 128 floats:          RA=2, BN=64
+//   int8, K <= 896 bytes (7 atoms): RA=1, BN=256, 3 stages
+template <int MODE>
+static cudaError_t dispatch(const TcPlan& P, const TcArgs& a, cudaStream_t s) {
+  if (P.kind == TC_TF32) {
+    if (P.katoms <= 2) return launch_cfg<TC_TF32, 4, 64, 2, 8, MODE>(P, a, s);
+    if (P.katoms <= 4) return launch_cfg<TC_TF32, 2, 64, 4, 8, MODE>(P, a, s);
+    return cudaErrorNotSupported;
+  }
+  if (P.kind == TC_U8) {
+    if (P.katoms <= 2) return launch_cfg<TC_U8, 4, 64, 2, 8, MODE>(P, a, s);
+    if (P.katoms <= 7) return launch_cfg<TC_U8, 1, 256, 7, 3, MODE>(P, a, s);
+    return cudaErrorNotSupported;
+  }
+  if (P.katoms <= 2) return launch_cfg<TC_S8, 4, 64, 2, 8, MODE>(P, a, s);
+  if (P.katoms <= 7) return launch_cfg<TC_S8, 1, 256, 7, 3, MODE>(P, a, s);
+  return cudaErrorNotSupported;
+}
+
+int tc_bn_for(int kind, int katoms) {
+  if (kind == TC_TF32) return 64;
+  return katoms <= 2 ? 64 : 256;
+}
+int tc_rows_for(int kind, int katoms) {
+  if (kind == TC_TF32) return katoms <= 2 ? 512 : 256;
+  return katoms <= 2 ? 512 : 128;
+}
+bool tc_supported(int kind, int katoms) {
+  return kind == TC_TF32 ? katoms <= 4 : katoms <= 7;
+}
+
+cudaError_t launch_tc(const TcPlan& P, const TcArgs& a, cudaStream_t s, int64_t* launches) {
+  ++*launches;
+  if (a.gram) return dispatch<TC_MODE_GRAM>(P, a, s);
+  return dispatch<TC_MODE_MEMBER>(P, a, s);
+}
+
+// ------------------------------------------------------------ prep kernels
+// Operand rows: fp32 rounded to tf32 (cvt.rna) or raw int8 bytes, K padded
+// with zeros to row_bytes; norms in fp64 (float) / int32 (int).
+__global__ void k_tc_prep_f32(const float* __restrict__ X, int64_t n, int d, int row_elems,
+                              float* __restrict__ xop, double* __restrict__ nrm,
+                              DevStats* stats) {
+  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const float* x = X + p * (int64_t)d;
+  float* o = xop + p * (int64_t)row_elems;
+  double ss = 0.0;
+  bool fin = true;
+  for (int j = 0; j < row_elems; ++j) {
+    float v = j < d ? x[j] : 0.f;
+    fin = fin && isfinite(v);
+    uint32_t t;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(t) : "f"(v));
+    o[j] = __uint_as_float(t);
+    ss = __dadd_rn(ss, __dmul_rn((double)v, (double)v));
+  }
+  if (!fin) atomicExch(&stats->nonfinite, 1);
+  nrm[p] = ss;
+}
+
+__global__ void k_tc_prep_int(const uint8_t* __restrict__ X, int64_t n, int d, int row_bytes,
+                              int is_u8, uint8_t* __restrict__ xop, int32_t* __restrict__ nrm) {
+  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const uint8_t* x = X + p * (int64_t)d;
+  uint8_t* o = xop + p * (int64_t)row_bytes;
+  int32_t ss = 0;
+  for (int j = 0; j < row_bytes; ++j) {
+    uint8_t v = j < d ? x[j] : 0;
+    o[j] = v;
+    int iv = is_u8 ? (int)v : (int)(int8_t)v;
+    ss += iv * iv;
+  }
+  nrm[p] = ss;
+}
+
+// per-row constants; rows >= n get +inf / INT_MAX
+__global__ void k_tc_rows_f32(const double* __restrict__ nrm, int64_t n, int64_t n_pad, double C2,
+                              double eps2, double tau, float* __restrict__ lo,
+                              float* __restrict__ hi) {
+  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n_pad) return;
+  if (p >= n) {
+    lo[p] = INFINITY;
+    hi[p] = INFINITY;
+    return;
+  }
+  const double np = nrm[p];
+  const double g = 0.5 * (np - eps2);
+  lo[p] = __double2float_rd(g - C2 * np - tau);
+  hi[p] = __double2float_ru(g + C2 * np + tau);
+}
+
+__global__ void k_tc_rows_int(const int32_t* __restrict__ nrm, int64_t n, int64_t n_pad,
+                              int32_t lo_i, int32_t* __restrict__ r) {
+  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n_pad) return;
+  // in iff n_p + n_l - 2 acc < lo_i  <=>  2 acc - n_l > n_p - lo_i
+  r[p] = p < n ? nrm[p] - lo_i : INT_MAX;
+}
+
+// gather landmark operand rows + per-column constants; columns >= L are inert
+__global__ void k_tc_gather_lm(const uint8_t* __restrict__ xop, int64_t row_bytes,
+                               const int32_t* __restrict__ lm, int64_t L, int64_t l_pad,
+                               uint8_t* __restrict__ lop) {
+  const int64_t j = blockIdx.x;
+  const uint4* src = j < L ? reinterpret_cast<const uint4*>(xop + (int64_t)lm[j] * row_bytes)
+                           : nullptr;
+  uint4* dst = reinterpret_cast<uint4*>(lop + j * row_bytes);
+  for (int64_t i = threadIdx.x; i < row_bytes / 16; i += blockDim.x)
+    dst[i] = src ? src[i] : make_uint4(0, 0, 0, 0);
+}
+
+__global__ void k_tc_cols_f32(const double* __restrict__ nrm, const int32_t* __restrict__ lm,
+                              int64_t L, int64_t l_pad, double C2, float* __restrict__ ca,
+                              float* __restrict__ cb) {
+  int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= l_pad) return;
+  if (j >= L) {
+    ca[j] = INFINITY;
+    cb[j] = INFINITY;
+    return;
+  }
+  const double nl = nrm[lm[j]];
+  ca[j] = __double2float_ru(0.5 * nl + C2 * nl);
+  cb[j] = __double2float_rd(0.5 * nl - C2 * nl);
+}
+
+__global__ void k_tc_cols_int(const int32_t* __restrict__ nrm, const int32_t* __restrict__ lm,
+                              int64_t L, int64_t l_pad, int32_t* __restrict__ cc) {
+  int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= l_pad) return;
+  cc[j] = j < L ? nrm[lm[j]] : (1 << 30);
+}
+
+// B': exact fp64 decision for every queued band pair (p << 32 | j), the
+// oracle's formula operation for operation; in-ball pairs join the keys.
+__global__ void k_tc_recheck(const unsigned long long* __restrict__ band, int64_t nb,
+                             const float* __restrict__ X, int xstride, int d,
+                             const int32_t* __restrict__ lm,
+                             double eps, double eps2, double tie_rel, int lbits,
+                             unsigned long long* keys, unsigned long long* key_count,
+                             int64_t key_cap, int64_t* ties, int64_t tie_cap,
+                             DevStats* stats) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  bool in = false;
+  int64_t p = 0, j = 0;
+  if (i < nb) {
+    p = (int64_t)(band[i] >> 32);
+    j = (int64_t)(band[i] & 0xffffffffull);
+    const int64_t q = lm[j];
+    const float* x = X + p * (int64_t)xstride;
+    const float* y = X + q * (int64_t)xstride;
+    double s = 0.0;
+    for (int k = 0; k < d; ++k) {
+      double t = __dsub_rn((double)x[k], (double)y[k]);
+      s = __dadd_rn(s, __dmul_rn(t, t));
+    }
+    in = s < eps2;
+    const double dist = __dsqrt_rn(s);
+    if (fabs(dist - eps) <= tie_rel * eps) {
+      unsigned long long k = atomicAdd(&stats->near_ties, 1ull);
+      if ((int64_t)k < tie_cap && ties) {
+        ties[3 * k] = p;
+        ties[3 * k + 1] = q;
+        ties[3 * k + 2] = in ? 1 : 0;
+      }
+    }
+  }
+  const unsigned m = __ballot_sync(FULLM, in);
+  if (m) {
+    const int lane = threadIdx.x & 31;
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(key_count, (unsigned long long)__popc(m));
+    base = __shfl_sync(FULLM, base, 0);
+    if (in) {
+      const unsigned long long k = base + __popc(m & ((1u << lane) - 1u));
+      if ((int64_t)k < key_cap) keys[k] = ((unsigned long long)p << lbits) | (unsigned long long)j;
+    }
+  }
+}
+
+cudaError_t launch_tc_prep(const void* X, int dtype, int64_t n, int d, const TcPlan& P,
+                           void* nrm, DevStats* stats, cudaStream_t s, int64_t* launches) {
+  ++*launches;
+  const unsigned g = (unsigned)((n + 255) / 256);
+  if (dtype == BM_F32)
+    k_tc_prep_f32<<<g, 256, 0, s>>>((const float*)X, n, d, (int)(P.row_bytes / 4),
+                                    (float*)P.xop, (double*)nrm, stats);
+  else
+    k_tc_prep_int<<<g, 256, 0, s>>>((const uint8_t*)X, n, d, (int)P.row_bytes, dtype == BM_U8,
+                                    (uint8_t*)P.xop, (int32_t*)nrm);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tc_rows(const TcPlan& P, const void* nrm, int64_t n, double C2, double eps2,
+                           double tau, int32_t lo_i, TcArgs& a, cudaStream_t s,
+                           int64_t* launches) {
+  ++*launches;
+  const unsigned g = (unsigned)((P.n_pad + 255) / 256);
+  if (P.kind == TC_TF32)
+    k_tc_rows_f32<<<g, 256, 0, s>>>((const double*)nrm, n, P.n_pad, C2, eps2, tau,
+                                    (float*)a.row_lo, (float*)a.row_hi);
+  else
+    k_tc_rows_int<<<g, 256, 0, s>>>((const int32_t*)nrm, n, P.n_pad, lo_i, (int32_t*)a.row_r);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tc_landmarks(const TcPlan& P, const void* nrm, const int32_t* lm, int64_t L,
+                                double C2, TcArgs& a, cudaStream_t s, int64_t* launches) {
+  *launches += 2;
+  k_tc_gather_lm<<<(unsigned)P.l_rows, 128, 0, s>>>((const uint8_t*)P.xop, P.row_bytes, lm, L,
+                                                    P.l_rows, (uint8_t*)P.lop);
+  const unsigned g = (unsigned)((P.l_rows + 255) / 256);
+  if (P.kind == TC_TF32)
+    k_tc_cols_f32<<<g, 256, 0, s>>>((const double*)nrm, lm, L, P.l_rows, C2,
+                                    (float*)a.col_a, (float*)a.col_b);
+  else
+    k_tc_cols_int<<<g, 256, 0, s>>>((const int32_t*)nrm, lm, L, P.l_rows, (int32_t*)a.col_c);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tc_recheck(const unsigned long long* band, int64_t nb, const float* X,
+                              int xstride, int d, const int32_t* lm, const Thresh& th, int lbits,
+                              unsigned long long* keys, unsigned long long* key_count,
+                              int64_t key_cap, int64_t* ties, int64_t tie_cap, DevStats* stats,
+                              cudaStream_t s, int64_t* launches) {
+  if (nb <= 0) return cudaSuccess;
+  ++*launches;
+  k_tc_recheck<<<(unsigned)((nb + 255) / 256), 256, 0, s>>>(
+      band, nb, X, xstride, d, lm, th.eps, th.eps2, th.tie_rel, lbits, keys, key_count, key_cap, ties,
+      tie_cap, stats);
+  return cudaGetLastError();
+}
+
+}  // namespace tc
+}  // namespace bm

@@ -1,0 +1,69 @@
+// tc.cuh — interface of the tcgen05 membership contraction (tc.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "internal.cuh"
+
+namespace bm {
+namespace tc {
+
+enum TcKind : int { TC_TF32 = 0, TC_U8 = 1, TC_S8 = 2 };
+enum TcMode : int { TC_MODE_MEMBER = 0, TC_MODE_GRAM = 1 };
+
+// Operand geometry (host side).
+struct TcPlan {
+  int kind;            // TcKind
+  const void* xop;     // [n][row_bytes] point operand (tf32-rounded fp32 or int8 bytes)
+  void* lop;           // [l_rows][row_bytes] landmark operand (gathered rows, zero padded)
+  int64_t n_rows;      // n (TMA zero-fills rows beyond)
+  int64_t n_pad;       // row-constant array length (multiple of the CTA row block)
+  int64_t l_rows;      // padded landmark count (multiple of BN)
+  int64_t row_bytes;   // bytes per operand row (multiple of 16)
+  int64_t k_elems;     // row_bytes / element size
+  int katoms;          // ceil(row_bytes / 128)
+  int num_sms;
+};
+
+struct TcArgs {
+  int64_t n, L;
+  int64_t n_tiles, n_mblk, tiles_per_chunk;  // filled by the launcher
+  int ksteps;                                // 32-byte K steps to issue
+  int lbits;
+  // per-row / per-column constants
+  const float* row_lo;
+  const float* row_hi;
+  const int32_t* row_r;
+  const float* col_a;
+  const float* col_b;
+  const int32_t* col_c;
+  // outputs
+  unsigned long long* keys;
+  unsigned long long* key_count;
+  int64_t key_cap;
+  unsigned long long* band;
+  unsigned long long* band_count;
+  int64_t band_cap;
+  uint32_t* gram;      // debug: raw accumulators [n][L]
+};
+
+int tc_bn_for(int kind, int katoms);
+int tc_rows_for(int kind, int katoms);
+bool tc_supported(int kind, int katoms);
+
+cudaError_t launch_tc_prep(const void* X, int dtype, int64_t n, int d, const TcPlan& P,
+                           void* nrm, DevStats* stats, cudaStream_t s, int64_t* launches);
+cudaError_t launch_tc_rows(const TcPlan& P, const void* nrm, int64_t n, double C2, double eps2,
+                           double tau, int32_t lo_i, TcArgs& a, cudaStream_t s,
+                           int64_t* launches);
+cudaError_t launch_tc_landmarks(const TcPlan& P, const void* nrm, const int32_t* lm, int64_t L,
+                                double C2, TcArgs& a, cudaStream_t s, int64_t* launches);
+cudaError_t launch_tc(const TcPlan& P, const TcArgs& a, cudaStream_t s, int64_t* launches);
+cudaError_t launch_tc_recheck(const unsigned long long* band, int64_t nb, const float* X,
+                              int xstride, int d, const int32_t* lm, const Thresh& th, int lbits,
+                              unsigned long long* keys, unsigned long long* key_count,
+                              int64_t key_cap, int64_t* ties, int64_t tie_cap, DevStats* stats,
+                              cudaStream_t s, int64_t* launches);
+
+}  // namespace tc
+}  // namespace bm
