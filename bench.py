@@ -108,7 +108,43 @@ def load_peaks():
             "sm_max_mhz": 1965.0}, "fallback"
 
 
-def roofline_for(w, L, kernel_ms, n, peaks):
+def roofline_for(w, L, kernel_ms, n, peaks, path_used, step_ms):
+    if path_used == 2:
+        return roofline_tensor(w, L, kernel_ms, n, peaks, step_ms)
+    return roofline_alu(w, L, kernel_ms, n, peaks)
+
+
+def _traffic(w):
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        try:
+            return json.load(open(tp)).get(w.name, {}).get("member_kernel_dram_bytes")
+        except Exception:
+            return None
+    return None
+
+
+def roofline_tensor(w, L, kernel_ms, n, peaks, step_ms):
+    """tcgen05 contraction: 2*d algorithmic ops per pair (true d, not the
+    padded K).  Peak: measured bf16 x nominal ratio (tf32 0.5, int8 2.0);
+    burst figure for short steps, sustained for steps > 0.5 s."""
+    sustained = step_ms > 500.0
+    bf16 = float(peaks["bf16_tflops_sustained" if sustained else "bf16_tflops"])
+    ratio = 0.5 if w.dtype == "f32" else 2.0
+    peak = bf16 * ratio
+    ops = 2.0 * w.d * float(n) * L
+    achieved = ops / (kernel_ms * 1e-3) / 1e12 if kernel_ms > 0 else 0.0
+    return {"bound": "tensor", "kernel": "k_tc (tcgen05 " + ("tf32" if w.dtype == "f32"
+                                                             else "int8") + ")",
+            "achieved": round(achieved, 3), "peak": round(peak, 3), "unit": "TFLOP/s",
+            "frac": round(achieved / peak, 4), "traffic": _traffic(w),
+            "ops_per_pair": 2 * w.d, "kernel_ms": round(kernel_ms, 5),
+            "peak_basis": f"measured bf16 {'sustained' if sustained else 'burst'} "
+                          f"{bf16} x {ratio} (nominal {'tf32' if ratio == 0.5 else 'int8'} "
+                          f"ratio)"}
+
+
+def roofline_alu(w, L, kernel_ms, n, peaks):
     """Dominant kernel = the membership pass (step B).  CUDA-core path:
     bound 'alu' — algorithmic FP32/INT lane-instructions per pair (DESIGN.md
     §Roofline): L2 f32 direct 2d (sub + fma), L1 f32 2d (sub + abs-add),
@@ -123,13 +159,7 @@ def roofline_for(w, L, kernel_ms, n, peaks):
     peak = 148 * 128 * clk / 1e12
     ops = float(n) * L * per_pair
     achieved = ops / (kernel_ms * 1e-3) / 1e12 if kernel_ms > 0 else 0.0
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tp):
-        try:
-            traffic = json.load(open(tp)).get(w.name, {}).get("member_kernel_dram_bytes")
-        except Exception:
-            traffic = None
+    traffic = _traffic(w)
     return {"bound": "alu", "kernel": "k_pairs<MODE_MEMBER>", "achieved": round(achieved, 4),
             "peak": round(peak, 4), "unit": "Tinst/s", "frac": round(achieved / peak, 4),
             "traffic": traffic, "ops_per_pair": per_pair,
@@ -275,7 +305,7 @@ def run_ours(args):
     breakdown = {k: round(sorted(s.step_ms[k] for s in covs_stats)[len(covs_stats) // 2], 4)
                  for k in ("prep", "greedy", "member", "csr", "edges", "member_kernel")}
     peaks, peak_src = load_peaks()
-    roof = roofline_for(w, L, kern_ms, n, peaks)
+    roof = roofline_for(w, L, kern_ms, n, peaks, covs_stats[-1].path_used, ms)
     roof["peak_source"] = peak_src
     roof["share_of_step"] = round(kern_ms / ms, 4) if ms > 0 else None
 
