@@ -64,12 +64,13 @@ typedef enum bm_dtype {
 /* Per-step device timings, indices into bm_cover.step_ms. */
 enum {
   BM_STEP_PREP = 0,     /* A0: packing, norms, finite check                      */
-  BM_STEP_GREEDY = 1,   /* A1-A4: blocked greedy eps-net                          */
-  BM_STEP_MEMBER = 2,   /* B, B': membership contraction + fp64 band recheck      */
+  BM_STEP_GREEDY = 1,   /* A1-A4 + B, B': blocked greedy eps-net; each tile's new   */
+                        /* balls are filled over all points in the same loop      */
+  BM_STEP_MEMBER = 2,   /* B fallback: exact-capacity membership recount (normally ~0) */
   BM_STEP_CSR = 3,      /* C: compaction into both CSRs                           */
   BM_STEP_EDGES = 4,    /* D1-D3: pair emission, radix sort, unique               */
   BM_STEP_TOTAL = 5,
-  BM_STEP_MEMBER_KERNEL = 6,  /* the membership contraction kernel alone (last launch) */
+  BM_STEP_MEMBER_KERNEL = 6,  /* membership contraction kernels alone, summed over tiles */
   BM_NUM_STEPS = 8
 };
 
@@ -87,7 +88,11 @@ typedef struct bm_options {
   int32_t path;          /* bm_path                                                             */
   int32_t timing;        /* 1 = record per-step CUDA events into step_ms                        */
   int64_t near_tie_cap;  /* max near-tie pairs stored (0 = default 65536); all are counted      */
-  int32_t reserved[8];
+  int32_t key_cap;       /* initial membership key capacity (0 = default 16 n); a smaller M
+                            fits, a larger one costs one exact-capacity recount             */
+  int32_t band_cap;      /* tensor path: per-tile fp64 band queue capacity (0 = default);
+                            an overflow re-runs the build on the CUDA-core path             */
+  int32_t reserved[6];
 } bm_options;
 
 /*
@@ -116,6 +121,7 @@ typedef struct bm_cover {
   int64_t n_edges;           /* E                                                        */
   int32_t *edges;            /* [E][2] landmark positions (i, j), i < j, lexicographic   */
 
+  int64_t n_witness_pairs;   /* P = sum_p C(t_p, 2): landmark pairs witnessed by points  */
   int64_t n_pair_evals;      /* n * L: point-landmark distance evaluations of step B     */
   int64_t n_greedy_evals;    /* extra evaluations inside the greedy (tiles + coverage)   */
   int64_t n_band_pairs;      /* float paths: pairs re-decided in fp64                    */
@@ -124,6 +130,7 @@ typedef struct bm_cover {
   int64_t *near_tie_pairs;   /* [n_near_ties_stored][3] (point, landmark point, decision); HOST */
   int64_t n_greedy_tiles;    /* candidate tiles resolved                                 */
   int64_t n_launches;        /* library kernels launched by this call                    */
+  int64_t n_member_launches; /* membership-contraction launches (one per greedy tile)    */
   int32_t path_used;         /* bm_path actually used for the contraction                */
   int32_t tile_used;         /* greedy tile T                                            */
   float step_ms[BM_NUM_STEPS];/* per-step device time (ms) when options.timing = 1       */
@@ -166,6 +173,11 @@ bm_status bm_cover_build_host(const void *host_points, bm_dtype dtype, int64_t n
 
 /* Release a cover and every array it owns.  NULL-safe. */
 void bm_free(bm_cover *c);
+
+/* Return the device memory the library keeps cached between calls (its
+ * stream-ordered pool on the current device) to the system.  Memory still
+ * owned by live covers is unaffected. */
+bm_status bm_trim_memory(void);
 
 /* Thread-local message for the last non-OK status of this thread ("" if none). */
 const char *bm_last_error(void);

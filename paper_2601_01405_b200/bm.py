@@ -25,7 +25,7 @@ PATH = {"auto": 0, "cuda_core": 1, "tensor": 2}
 STEPS = ("prep", "greedy", "member", "csr", "edges", "total", "member_kernel")
 
 EXPORTED = ("bm_cover_build", "bm_cover_build_ex", "bm_cover_build_host", "bm_free",
-            "bm_last_error", "bm_version", "bm_debug_radix_sort_u64",
+            "bm_last_error", "bm_version", "bm_trim_memory", "bm_debug_radix_sort_u64",
             "bm_debug_exclusive_scan_i64", "bm_debug_resolve_tile", "bm_debug_tc_gram")
 
 
@@ -38,7 +38,8 @@ class BMError(RuntimeError):
 class _Options(ctypes.Structure):
     _fields_ = [("struct_size", ctypes.c_int32), ("tile", ctypes.c_int32),
                 ("path", ctypes.c_int32), ("timing", ctypes.c_int32),
-                ("near_tie_cap", ctypes.c_int64), ("reserved", ctypes.c_int32 * 8)]
+                ("near_tie_cap", ctypes.c_int64), ("key_cap", ctypes.c_int32),
+                ("band_cap", ctypes.c_int32), ("reserved", ctypes.c_int32 * 6)]
 
 
 class _Cover(ctypes.Structure):
@@ -49,11 +50,13 @@ class _Cover(ctypes.Structure):
                 ("ball_idx", ctypes.c_void_p), ("pt_ptr", ctypes.c_void_p),
                 ("pt_lm", ctypes.c_void_p),
                 ("n_edges", ctypes.c_int64), ("edges", ctypes.c_void_p),
+                ("n_witness_pairs", ctypes.c_int64),
                 ("n_pair_evals", ctypes.c_int64), ("n_greedy_evals", ctypes.c_int64),
                 ("n_band_pairs", ctypes.c_int64), ("n_near_ties", ctypes.c_int64),
                 ("n_near_ties_stored", ctypes.c_int64),
                 ("near_tie_pairs", ctypes.POINTER(ctypes.c_int64)),
                 ("n_greedy_tiles", ctypes.c_int64), ("n_launches", ctypes.c_int64),
+                ("n_member_launches", ctypes.c_int64),
                 ("path_used", ctypes.c_int32), ("tile_used", ctypes.c_int32),
                 ("step_ms", ctypes.c_float * 8), ("priv", ctypes.c_void_p)]
 
@@ -83,6 +86,7 @@ def load() -> ctypes.CDLL:
     lib.bm_free.restype = None
     lib.bm_last_error.restype = ctypes.c_char_p
     lib.bm_version.restype = i32
+    lib.bm_trim_memory.restype = i32
     lib.bm_debug_radix_sort_u64.argtypes = [vp, i64, i32, vp]
     lib.bm_debug_radix_sort_u64.restype = i32
     lib.bm_debug_exclusive_scan_i64.argtypes = [vp, vp, i64, ctypes.POINTER(i64), vp]
@@ -100,13 +104,16 @@ def _check(rc: int):
         raise BMError(rc, load().bm_last_error().decode())
 
 
-def _options(tile=0, path="auto", timing=False, near_tie_cap=0) -> _Options:
+def _options(tile=0, path="auto", timing=False, near_tie_cap=0, key_cap=0,
+             band_cap=0) -> _Options:
     o = _Options()
     o.struct_size = ctypes.sizeof(_Options)
     o.tile = int(tile)
     o.path = PATH[path] if isinstance(path, str) else int(path)
     o.timing = 1 if timing else 0
     o.near_tie_cap = int(near_tie_cap)
+    o.key_cap = int(key_cap)
+    o.band_cap = int(band_cap)
     return o
 
 
@@ -127,6 +134,7 @@ class CoverStats:
     n_near_ties: int
     n_greedy_tiles: int
     n_launches: int
+    n_member_launches: int
     path_used: int
     tile_used: int
     step_ms: dict
@@ -141,9 +149,11 @@ class Cover:
         c = ptr.contents
         self.n, self.d, self.eps = c.n, c.d, c.eps
         self.L, self.M, self.E = c.n_landmarks, c.n_members, c.n_edges
+        self.P = c.n_witness_pairs
         self.on_host = bool(c.on_host)
         self.stats = CoverStats(c.n_pair_evals, c.n_greedy_evals, c.n_band_pairs,
-                                c.n_near_ties, c.n_greedy_tiles, c.n_launches, c.path_used,
+                                c.n_near_ties, c.n_greedy_tiles, c.n_launches,
+                                c.n_member_launches, c.path_used,
                                 c.tile_used, {k: float(c.step_ms[i]) for i, k in
                                               enumerate(STEPS)})
         k = c.n_near_ties_stored
@@ -213,7 +223,8 @@ def _dtype_of(t) -> str:
 
 
 def cover_build(points, metric: str, eps: float, stream=None, tile: int = 0,
-                path: str = "auto", timing: bool = False, near_tie_cap: int = 0) -> Cover:
+                path: str = "auto", timing: bool = False, near_tie_cap: int = 0,
+                key_cap: int = 0, band_cap: int = 0) -> Cover:
     """bm_cover_build_ex on a CUDA torch tensor [n, d] (row-major, contiguous)."""
     import torch
     if not (isinstance(points, torch.Tensor) and points.is_cuda):
@@ -226,7 +237,7 @@ def cover_build(points, metric: str, eps: float, stream=None, tile: int = 0,
         stream = torch.cuda.current_stream(points.device)
     sp = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
     out = ctypes.POINTER(_Cover)()
-    o = _options(tile, path, timing, near_tie_cap)
+    o = _options(tile, path, timing, near_tie_cap, key_cap, band_cap)
     lib = load()
     with torch.cuda.device(points.device):
         rc = lib.bm_cover_build_ex(ctypes.c_void_p(points.data_ptr()), DTYPE[_dtype_of(points)],
@@ -237,7 +248,8 @@ def cover_build(points, metric: str, eps: float, stream=None, tile: int = 0,
 
 
 def cover_build_host(points: np.ndarray, metric: str, eps: float, stream=None, tile: int = 0,
-                     path: str = "auto", timing: bool = False, near_tie_cap: int = 0) -> Cover:
+                     path: str = "auto", timing: bool = False, near_tie_cap: int = 0,
+                     key_cap: int = 0, band_cap: int = 0) -> Cover:
     """bm_cover_build_host on a host buffer (numpy array or CPU torch tensor,
     ideally pinned): copies in, builds, copies every result back to host."""
     import torch
@@ -255,7 +267,7 @@ def cover_build_host(points: np.ndarray, metric: str, eps: float, stream=None, t
         stream = torch.cuda.current_stream()
     sp = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
     out = ctypes.POINTER(_Cover)()
-    o = _options(tile, path, timing, near_tie_cap)
+    o = _options(tile, path, timing, near_tie_cap, key_cap, band_cap)
     rc = load().bm_cover_build_host(ctypes.c_void_p(ptr), DTYPE[dt], n, d, METRIC[metric],
                                     float(eps), ctypes.c_void_p(sp), ctypes.byref(o),
                                     ctypes.byref(out))
@@ -315,3 +327,8 @@ def tc_gram(points, landmarks):
         ctypes.c_void_p(landmarks.data_ptr()), L, ctypes.c_void_p(out.data_ptr()),
         ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
     return out.view(torch.float32) if _dtype_of(points) == "f32" else out
+
+
+def trim_memory():
+    """Return the library's cached device memory (its stream-ordered pool) to the system."""
+    _check(load().bm_trim_memory())

@@ -13,6 +13,7 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -43,11 +44,40 @@ bm_status set_err(bm_status st, const char* fmt, ...) {
     }                                                                                 \
   } while (0)
 
+// The library's own stream-ordered memory pool per device: freed blocks stay
+// reserved for the next call (release threshold = unlimited) instead of
+// being unmapped at every synchronisation; bm_trim_memory() returns them.
+std::mutex g_pool_mu;
+cudaMemPool_t g_pools[64] = {};
+
+cudaMemPool_t device_pool() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  if (!g_pools[dev]) {
+    cudaMemPoolProps pr{};
+    pr.allocType = cudaMemAllocationTypePinned;
+    pr.handleTypes = cudaMemHandleTypeNone;
+    pr.location.type = cudaMemLocationTypeDevice;
+    pr.location.id = dev;
+    cudaMemPool_t mp = nullptr;
+    if (cudaMemPoolCreate(&mp, &pr) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &thr);
+    g_pools[dev] = mp;
+  }
+  return g_pools[dev];
+}
+
 // Stream-ordered allocations owned by one build call.
 struct Pool {
   cudaStream_t s;
+  cudaMemPool_t mp;
   std::vector<void*> ptrs;
-  explicit Pool(cudaStream_t st) : s(st) {}
+  explicit Pool(cudaStream_t st) : s(st), mp(device_pool()) {}
   ~Pool() {
     for (void* p : ptrs)
       if (p) cudaFreeAsync(p, s);
@@ -57,7 +87,7 @@ struct Pool {
     void* p = nullptr;
     size_t bytes = count * sizeof(T);
     if (bytes < 256) bytes = 256;
-    cudaError_t e = cudaMallocAsync(&p, bytes, s);
+    cudaError_t e = mp ? cudaMallocFromPoolAsync(&p, bytes, mp, s) : cudaMallocAsync(&p, bytes, s);
     if (e != cudaSuccess) {
       cudaGetLastError();
       *out = nullptr;
@@ -146,6 +176,35 @@ bm::Thresh make_thresh(int kind, int d, double eps) {
   return t;
 }
 
+// Initial capacity of the membership key buffer (8 B per key): M is unknown
+// until the greedy ends.  16 keys per point covers every BASELINE config
+// (C5: M/n ~ 10); a larger M triggers one exact-capacity recount
+// (membership_full).  Bounded by a quarter of the free device memory.
+int64_t initial_key_cap(int64_t n) {
+  int64_t cap = n * 16 > (1 << 20) ? n * 16 : (1 << 20);
+  static int64_t lim = -1;   // an eighth of the device memory, in keys (queried once)
+  if (lim < 0) {
+    int dev = 0;
+    cudaDeviceProp pr;
+    lim = (cudaGetDevice(&dev) == cudaSuccess &&
+           cudaGetDeviceProperties(&pr, dev) == cudaSuccess)
+              ? (int64_t)(pr.totalGlobalMem / 8 / sizeof(unsigned long long))
+              : (int64_t)1 << 28;
+  }
+  return cap > lim && lim > (1 << 20) ? lim : cap;
+}
+
+// Tensor-core band constant: |acc - x.l| <= c1
+// |x||l|, c1 = operand rounding to tf32 (2u_t + u_t^2) + fp32 accumulation
+// (4 K 2^-23, safety 2); the epilogue's roundings add 2^-22; |x||l| <=
+// (n_p + n_l)/2, and 1.25 is a further safety factor.
+double tc_band_c2(int ksteps) {
+  const double ut = ldexp(1.0, -11);
+  const double K = 8.0 * ksteps;
+  const double c1 = 2.0 * ut + ut * ut + 4.0 * K * ldexp(1.0, -23) * (1.0 + ut) * (1.0 + ut);
+  return 1.25 * 0.5 * (c1 + ldexp(1.0, -22));
+}
+
 __global__ void k_iota(int32_t* a, int64_t n) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) a[i] = (int32_t)i;
@@ -168,6 +227,104 @@ struct Timer {
     if (on) cudaEventRecord(ev[i], s);
   }
 };
+
+// Step B over all n points x all L landmarks in one pass (used only when the
+// fused loop's key buffer overflowed: M is then known exactly and `keys` has
+// room for it).  Keys are point << 32 | landmark position, as in the loop.
+bm_status membership_full(Pool& pool, int kind, const bm::PairArgs& base, bm::tc::TcPlan P,
+                          bool use_tc, const void* tc_nrm, const int32_t* lm, int64_t L,
+                          int64_t n, int d, bm_dtype dtype, int nu, const bm::Thresh& th,
+                          double C2, unsigned long long* keys, int64_t key_cap,
+                          int64_t* ties_dev, int64_t tie_cap, bm::DevStats* stats,
+                          cudaStream_t s, int64_t* launches, int64_t* M_out) {
+  using namespace bm;
+  CK(cudaMemsetAsync(&stats->key_count, 0, sizeof(unsigned long long), s));
+  CK(cudaMemsetAsync(&stats->near_ties, 0, sizeof(unsigned long long), s));
+  if (use_tc) {
+    const int BN = tc::tc_bn_for(P.kind, P.katoms);
+    P.l_rows = ((L + BN - 1) / BN) * BN;
+    tc::TcArgs ta{};
+    ta.n = n;
+    ta.L = L;
+    ta.ksteps = (int)(((int64_t)d * (dtype == BM_F32 ? 4 : 1) + 31) / 32);
+    ta.lbits = 32;
+    TRY(pool.alloc((uint8_t**)&P.lop, (size_t)P.l_rows * P.row_bytes));
+    const int RB = tc::tc_rows_for(P.kind, P.katoms);
+    P.n_pad = ((n + RB - 1) / RB) * RB;
+    double tau = 0.0;
+    if (P.kind == tc::TC_TF32) {
+      float *rlo, *rhi, *ca, *cb;
+      TRY(pool.alloc(&rlo, (size_t)P.n_pad));
+      TRY(pool.alloc(&rhi, (size_t)P.n_pad));
+      TRY(pool.alloc(&ca, (size_t)P.l_rows));
+      TRY(pool.alloc(&cb, (size_t)P.l_rows));
+      ta.row_lo = rlo;
+      ta.row_hi = rhi;
+      ta.col_a = ca;
+      ta.col_b = cb;
+      tau = 1.0000005e-6 * th.eps2 + th.eps2 * ldexp(1.0, -21);
+    } else {
+      int32_t *rr, *cc;
+      TRY(pool.alloc(&rr, (size_t)P.n_pad));
+      TRY(pool.alloc(&cc, (size_t)P.l_rows));
+      ta.row_r = rr;
+      ta.col_c = cc;
+    }
+    CK(tc::launch_tc_rows(P, tc_nrm, n, C2, th.eps2, tau, th.lo_i, ta, s, launches));
+    CK(tc::launch_tc_landmarks(P, tc_nrm, lm, L, C2, ta, s, launches));
+    int64_t band_cap = n * 4 > (1 << 22) ? n * 4 : (1 << 22);
+    unsigned long long* bcount = nullptr;
+    TRY(pool.alloc(&bcount, 1));
+    for (int attempt = 0; attempt < 2; ++attempt) {
+      unsigned long long* band = nullptr;
+      TRY(pool.alloc(&band, (size_t)band_cap));
+      CK(cudaMemsetAsync(bcount, 0, sizeof(unsigned long long), s));
+      CK(cudaMemsetAsync(&stats->key_count, 0, sizeof(unsigned long long), s));
+      ta.keys = keys;
+      ta.key_count = &stats->key_count;
+      ta.key_cap = key_cap;
+      ta.band = band;
+      ta.band_count = bcount;
+      ta.band_cap = band_cap;
+      CK(tc::launch_tc(P, ta, s, launches));
+      unsigned long long hb = 0;
+      CK(cudaMemcpyAsync(&hb, bcount, sizeof hb, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      if ((int64_t)hb <= band_cap) {
+        CK(tc::launch_tc_recheck(band, (int64_t)hb, (const float*)base.xrows, 2 * nu, d, lm, th,
+                                 32, keys, &stats->key_count, key_cap, ties_dev, tie_cap, stats,
+                                 s, launches));
+        pool.free_now(band);
+        break;
+      }
+      pool.free_now(band);
+      band_cap = (int64_t)hb;
+      if (attempt == 1) return set_err(BM_ENOMEM, "band queue kept overflowing");
+    }
+    pool.free_now((void*)P.lop);
+  } else {
+    PairArgs m = base;
+    m.qidx = nullptr;
+    m.q_begin = 0;
+    m.q_end = n;
+    m.lidx = lm;
+    m.l_begin = 0;
+    m.l_end = L;
+    m.lpos0 = 0;
+    m.keys = keys;
+    m.key_cap = key_cap;
+    m.lbits = 32;
+    m.ties = ties_dev;
+    m.tie_cap = tie_cap;
+    CK(launch_pairs(kind, MODE_MEMBER, m, n, s, launches));
+  }
+  unsigned long long kc = 0;
+  CK(cudaMemcpyAsync(&kc, &stats->key_count, sizeof kc, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if ((int64_t)kc > key_cap) return set_err(BM_ECUDA, "membership recount exceeded its exact size");
+  *M_out = (int64_t)kc;
+  return BM_OK;
+}
 
 bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, bm_metric metric,
                      double eps, cudaStream_t s, const bm_options* opts, bool host_in,
@@ -261,25 +418,29 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
     CK(tc::launch_tc_prep(dpoints, dtype, n, d, P, tc_nrm, stats, s, &launches));
   }
   if (host_in) pool.free_now((void*)dpoints);
-  tm.mark(1);
 
-  // ---- A1-A4 greedy
+  // ---- buffers of the fused greedy + membership loop
+  const int64_t nL_max = n;  // L <= n
+  int64_t key_cap = o.key_cap > 0 ? (int64_t)o.key_cap : initial_key_cap(n);
   const int adj_words = T / 32;
-  const int cov_rows = cover_rows_per_cta(nu);
-  const int nblk = (int)((n + cov_rows - 1) / cov_rows);
   int32_t *cnt = nullptr, *unc0 = nullptr, *unc1 = nullptr, *lm = nullptr, *new_lm = nullptr;
-  int32_t *blk_count = nullptr, *blk_off = nullptr;
   uint32_t* adj = nullptr;
-  uint8_t* keep = nullptr;
-  TRY(pool.alloc(&cnt, 8));  // [0],[1] n_unc ping-pong; [2] L; [3] dL
+  uint8_t* covered = nullptr;
+  unsigned long long* cstate = nullptr;
+  unsigned long long* keys = nullptr;
+  int64_t* ties_dev = nullptr;
+  TRY(pool.alloc(&cnt, 8));  // [0],[1] n_unc ping-pong; [2] L; [3] dL; [4] compaction ticket
   TRY(pool.alloc(&unc0, (size_t)n));
   TRY(pool.alloc(&unc1, (size_t)n));
-  TRY(pool.alloc(&lm, (size_t)n));
+  TRY(pool.alloc(&lm, (size_t)nL_max));
   TRY(pool.alloc(&new_lm, (size_t)T));
   TRY(pool.alloc(&adj, (size_t)T * adj_words));
-  TRY(pool.alloc(&keep, (size_t)n));
-  TRY(pool.alloc(&blk_count, (size_t)nblk));
-  TRY(pool.alloc(&blk_off, (size_t)nblk));
+  TRY(pool.alloc(&covered, (size_t)n));
+  TRY(pool.alloc(&cstate, (size_t)compact_state_words(n)));
+  TRY(pool.alloc(&keys, (size_t)key_cap));
+  TRY(pool.alloc(&ties_dev, (size_t)tie_cap * 3));
+  CK(cudaMemsetAsync(covered, 0, (size_t)n, s));
+  CK(cudaMemsetAsync(cstate, 0, sizeof(unsigned long long) * compact_state_words(n), s));
   {
     int32_t init[8] = {(int32_t)n, 0, 0, 0, 0, 0, 0, 0};
     CK(cudaMemcpyAsync(cnt, init, sizeof init, cudaMemcpyHostToDevice, s));
@@ -300,8 +461,80 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
   base.th = th;
   base.stats = stats;
 
+  // tensor path: tile landmark operand [T_pad][row_bytes], column constants, band queue
+  tc::TcArgs ta{};
+  unsigned long long *band = nullptr, *bcount = nullptr;
+  int64_t band_cap = 0;
+  double C2 = 0.0;
+  if (use_tc) {
+    const int BN = tc::tc_bn_for(P.kind, P.katoms);
+    const int RB = tc::tc_rows_for(P.kind, P.katoms);
+    P.l_rows = ((T + BN - 1) / BN) * BN;
+    P.n_pad = ((n + RB - 1) / RB) * RB;
+    ta.n = n;
+    ta.L = T;
+    ta.ksteps = (int)(((int64_t)d * (dtype == BM_F32 ? 4 : 1) + 31) / 32);
+    ta.lbits = 32;
+    ta.l_count_dev = cnt + 3;
+    ta.l_total_dev = cnt + 2;
+    ta.covered = covered;
+    TRY(pool.alloc((uint8_t**)&P.lop, (size_t)P.l_rows * P.row_bytes));
+    double tau = 0.0;
+    if (P.kind == tc::TC_TF32) {
+      float *rlo, *rhi, *ca, *cb;
+      TRY(pool.alloc(&rlo, (size_t)P.n_pad));
+      TRY(pool.alloc(&rhi, (size_t)P.n_pad));
+      TRY(pool.alloc(&ca, (size_t)P.l_rows));
+      TRY(pool.alloc(&cb, (size_t)P.l_rows));
+      ta.row_lo = rlo;
+      ta.row_hi = rhi;
+      ta.col_a = ca;
+      ta.col_b = cb;
+      C2 = tc_band_c2(ta.ksteps);
+      tau = 1.0000005e-6 * th.eps2 + th.eps2 * ldexp(1.0, -21);
+      band_cap = o.band_cap > 0 ? (int64_t)o.band_cap : (n * 4 > (1 << 22) ? n * 4 : (1 << 22));
+      TRY(pool.alloc(&band, (size_t)band_cap));
+      TRY(pool.alloc(&bcount, 1));
+      CK(cudaMemsetAsync(bcount, 0, sizeof(unsigned long long), s));
+    } else {
+      int32_t *rr, *cc;
+      TRY(pool.alloc(&rr, (size_t)P.n_pad));
+      TRY(pool.alloc(&cc, (size_t)P.l_rows));
+      ta.row_r = rr;
+      ta.col_c = cc;
+    }
+    CK(tc::launch_tc_rows(P, tc_nrm, n, C2, th.eps2, tau, th.lo_i, ta, s, &launches));
+    ta.keys = keys;
+    ta.key_count = &stats->key_count;
+    ta.key_cap = key_cap;
+    ta.band = band;
+    ta.band_count = bcount;
+    ta.band_cap = band_cap;
+  }
+  tm.mark(1);
+
+  // ---- A1-A4 + B: blocked greedy, each tile's membership pass over all points
+  // (SURVEY §3 (iii) variant: total membership work is exactly n * L).
+  std::vector<cudaEvent_t> mev;   // per-tile membership kernel brackets (timing only)
+  auto mark_member = [&](void) -> cudaError_t {
+    if (!tm.on) return cudaSuccess;
+    cudaEvent_t e;
+    cudaError_t r = cudaEventCreate(&e);
+    if (r != cudaSuccess) return r;
+    mev.push_back(e);
+    return cudaEventRecord(e, s);
+  };
+  struct EvGuard {
+    std::vector<cudaEvent_t>& v;
+    ~EvGuard() {
+      for (auto e : v) cudaEventDestroy(e);
+    }
+  } evguard{mev};
+
+  // tiles are issued in batches between host termination checks (a tile after
+  // the last one costs a few empty launches; a check costs a round trip)
   int64_t tile = 0;
-  int batch = 1;
+  int batch = 4;
   int nonfinite_checked = 0;
   for (;;) {
     for (int b = 0; b < batch; ++b, ++tile) {
@@ -319,25 +552,43 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
       a.adj = adj;
       a.adj_words = adj_words;
       CK(launch_pairs(kind, MODE_ADJ, a, T, s, &launches));
-      // A3: in-order resolve, append landmarks
+      // A3: in-order resolve, append landmarks (resets the tile's counters)
       CK(launch_resolve(adj, adj_words, uncb[cur], cnt + cur, T, lm, cnt + 2, new_lm, cnt + 3,
-                        stats, s, &launches));
-      // A4: coverage of unc[nc .. n_unc) by the new landmarks
-      PairArgs c = base;
-      c.qidx = uncb[cur];
-      c.q_begin = T;
-      c.q_begin_dev = cnt + cur;
-      c.q_end = n;
-      c.q_end_dev = cnt + cur;
-      c.lidx = new_lm;
-      c.l_begin = 0;
-      c.l_end = T;
-      c.l_end_dev = cnt + 3;
-      c.keep = keep;
-      c.blk_count = blk_count;
-      CK(launch_pairs(kind, MODE_COVER, c, n, s, &launches));
-      CK(launch_compact_unc(keep, blk_count, nblk, cov_rows, uncb[cur], cnt + cur, T, blk_off,
-                            uncb[nxt], cnt + nxt, s, &launches));
+                        stats, cnt + 4, bcount, s, &launches));
+      // B (+A4 marks): membership of every point in the new balls
+      if (use_tc) {
+        CK(tc::launch_tc_tile_landmarks(P, tc_nrm, new_lm, cnt + 3, C2, ta, s, &launches));
+        CK(mark_member());
+        CK(tc::launch_tc(P, ta, s, &launches));
+        CK(mark_member());
+        if (P.kind == tc::TC_TF32)
+          CK(tc::launch_tc_recheck_tile(band, bcount, band_cap, (const float*)rows, 2 * nu, d,
+                                        new_lm, cnt + 3, cnt + 2, th, keys, &stats->key_count,
+                                        key_cap, covered, ties_dev, tie_cap, stats, P.num_sms, s,
+                                        &launches));
+      } else {
+        PairArgs m = base;
+        m.qidx = nullptr;
+        m.q_begin = 0;
+        m.q_end = n;
+        m.lidx = new_lm;
+        m.l_begin = 0;
+        m.l_end = T;
+        m.l_end_dev = cnt + 3;
+        m.l_total_dev = cnt + 2;
+        m.keys = keys;
+        m.key_cap = key_cap;
+        m.lbits = 32;
+        m.ties = ties_dev;
+        m.tie_cap = tie_cap;
+        m.covered = covered;
+        CK(mark_member());
+        CK(launch_pairs(kind, MODE_MEMBER, m, n, s, &launches));
+        CK(mark_member());
+      }
+      // A4: keep the still-uncovered points after the tile, in order
+      CK(launch_compact_unc(covered, uncb[cur], cnt + cur, T, uncb[nxt], cnt + nxt, cstate,
+                            cnt + 4, (uint32_t)(tile + 1), n, s, &launches));
     }
     int32_t hc[4];
     CK(cudaMemcpyAsync(hc, cnt, sizeof hc, cudaMemcpyDeviceToHost, s));
@@ -349,157 +600,49 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
       nonfinite_checked = 1;
     }
     if (hc[tile & 1] == 0) break;
-    if (batch < 32) batch *= 2;
+    if (batch < 64) batch *= 2;
   }
   tm.mark(2);
 
+  DevStats hs{};
+  CK(cudaMemcpyAsync(&hs, stats, sizeof hs, cudaMemcpyDeviceToHost, s));
   int32_t hL = 0;
   CK(cudaMemcpyAsync(&hL, cnt + 2, sizeof hL, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   const int64_t L = hL;
+  if (hs.overflow) {
+    // a tile's band queue overflowed (adversarial input): redo on the CUDA-core
+    // path, whose band is re-decided inline and cannot overflow
+    bm_options o2 = o;
+    o2.path = BM_PATH_CUDA_CORE;
+    return build_impl(points, dtype, n, d, metric, eps, s, &o2, host_in, out);
+  }
   pool.free_now(unc0);
   pool.free_now(unc1);
-  pool.free_now(keep);
+  pool.free_now(covered);
+  pool.free_now(cstate);
+  if (band) pool.free_now(band);
 
-  // ---- B membership (+ B' band recheck, near ties)
+  // ---- B fallback: the key buffer overflowed; recompute the membership alone
+  // with the exact capacity (the greedy's coverage decisions were unaffected)
   const int lbits = bits_for(L > 1 ? L - 1 : 1);
   const int pbits = bits_for(n > 1 ? n - 1 : 1);
-  int64_t* ties_dev = nullptr;
-  TRY(pool.alloc(&ties_dev, (size_t)tie_cap * 3));
-  DevStats hs{};
-  CK(cudaMemcpyAsync(&hs, stats, sizeof hs, cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
-  const unsigned long long greedy_band = hs.band_pairs;
-  int64_t key_cap = n * 4 > (1 << 20) ? n * 4 : (1 << 20);
-  unsigned long long* keys = nullptr;
-  int64_t M = 0;
-  if (use_tc) {
-    // ---- B on tcgen05 (tc.cu) + B' fp64 recheck of the queued band pairs
-    const int BN = tc::tc_bn_for(P.kind, P.katoms);
-    const int RB = tc::tc_rows_for(P.kind, P.katoms);
-    P.l_rows = ((L + BN - 1) / BN) * BN;
-    P.n_pad = ((n + RB - 1) / RB) * RB;
-    tc::TcArgs ta{};
-    ta.n = n;
-    ta.L = L;
-    ta.ksteps = (int)(((int64_t)d * (dtype == BM_F32 ? 4 : 1) + 31) / 32);
-    ta.lbits = lbits;
-    TRY(pool.alloc((uint8_t**)&P.lop, (size_t)P.l_rows * P.row_bytes));
-    double C2 = 0.0, tau = 0.0;
-    int32_t lo_i = th.lo_i;
-    if (P.kind == tc::TC_TF32) {
-      float *rlo, *rhi, *ca, *cb;
-      TRY(pool.alloc(&rlo, (size_t)P.n_pad));
-      TRY(pool.alloc(&rhi, (size_t)P.n_pad));
-      TRY(pool.alloc(&ca, (size_t)P.l_rows));
-      TRY(pool.alloc(&cb, (size_t)P.l_rows));
-      ta.row_lo = rlo;
-      ta.row_hi = rhi;
-      ta.col_a = ca;
-      ta.col_b = cb;
-      // |acc - x.l| <= c1 |x||l|, c1 = operand
-      // rounding (2u_t + u_t^2) + fp32 accumulation (4 K 2^-23, safety 2);
-      // epilogue roundings add 2^-22; |x||l| <= (n_p + n_l)/2.
-      const double ut = ldexp(1.0, -11);
-      const double K = 8.0 * ta.ksteps;
-      const double c1 = 2.0 * ut + ut * ut + 4.0 * K * ldexp(1.0, -23) * (1.0 + ut) * (1.0 + ut);
-      C2 = 1.25 * 0.5 * (c1 + ldexp(1.0, -22));
-      tau = 1.0000005e-6 * th.eps2 + th.eps2 * ldexp(1.0, -21);
-    } else {
-      int32_t *rr, *cc;
-      TRY(pool.alloc(&rr, (size_t)P.n_pad));
-      TRY(pool.alloc(&cc, (size_t)P.l_rows));
-      ta.row_r = rr;
-      ta.col_c = cc;
-    }
-    CK(tc::launch_tc_rows(P, tc_nrm, n, C2, th.eps2, tau, lo_i, ta, s, &launches));
-    CK(tc::launch_tc_landmarks(P, tc_nrm, lm, L, C2, ta, s, &launches));
-    int64_t band_cap = n * 4 > (1 << 22) ? n * 4 : (1 << 22);
-    unsigned long long *band = nullptr, *bcount = nullptr;
-    TRY(pool.alloc(&bcount, 1));
-    for (int attempt = 0; attempt < 3; ++attempt) {
-      TRY(pool.alloc(&keys, (size_t)key_cap));
-      TRY(pool.alloc(&band, (size_t)band_cap));
-      CK(cudaMemsetAsync(bcount, 0, sizeof(unsigned long long), s));
-      CK(cudaMemsetAsync(&stats->key_count, 0, sizeof(unsigned long long), s));
-      ta.keys = keys;
-      ta.key_count = &stats->key_count;
-      ta.key_cap = key_cap;
-      ta.band = band;
-      ta.band_count = bcount;
-      ta.band_cap = band_cap;
-      tm.mark(6);
-      CK(tc::launch_tc(P, ta, s, &launches));
-      tm.mark(7);
-      unsigned long long hb = 0;
-      CK(cudaMemcpyAsync(&hs, stats, sizeof hs, cudaMemcpyDeviceToHost, s));
-      CK(cudaMemcpyAsync(&hb, bcount, sizeof hb, cudaMemcpyDeviceToHost, s));
-      CK(cudaStreamSynchronize(s));
-      const int64_t K1 = (int64_t)hs.key_count, B = (int64_t)hb;
-      if (B <= band_cap && K1 + B <= key_cap) {
-        CK(tc::launch_tc_recheck(band, B, (const float*)rows, 2 * nu, d, lm, th, lbits, keys,
-                                 &stats->key_count, key_cap, ties_dev, tie_cap, stats, s,
-                                 &launches));
-        unsigned long long tot = greedy_band + (unsigned long long)B;
-        CK(cudaMemcpyAsync(&stats->band_pairs, &tot, sizeof tot, cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(&hs, stats, sizeof hs, cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-        M = (int64_t)hs.key_count;
-        break;
-      }
-      pool.free_now(keys);
-      pool.free_now(band);
-      if (B > band_cap) band_cap = B;
-      if (K1 + B > key_cap) key_cap = K1 + B;
-      if (attempt == 2) return set_err(BM_ENOMEM, "membership buffers kept overflowing");
-    }
-    pool.free_now(band);
-    pool.free_now((void*)P.lop);
-  }
-  for (int attempt = 0; attempt < 2 && !use_tc; ++attempt) {
-    TRY(pool.alloc(&keys, (size_t)key_cap));
-    PairArgs m = base;
-    m.qidx = nullptr;
-    m.q_begin = 0;
-    m.q_end = n;
-    m.lidx = lm;
-    m.l_begin = 0;
-    m.l_end = L;
-    m.lpos0 = 0;
-    const int R = nu <= 8 ? 4 : (nu <= 16 ? 2 : 1);
-    const int64_t gx = (n + 256 * R - 1) / (256 * R);
-    int64_t want_gy = (148 * 8 + gx - 1) / gx;
-    if (want_gy < 1) want_gy = 1;
-    int64_t lch = (L + want_gy - 1) / want_gy;
-    lch = ((lch + 63) / 64) * 64;
-    if (lch < 64) lch = 64;
-    while ((L + lch - 1) / lch > 65535) lch *= 2;
-    m.l_chunk = lch;
-    m.keys = keys;
-    m.key_cap = key_cap;
-    m.lbits = lbits;
-    m.ties = ties_dev;
-    m.tie_cap = tie_cap;
-    tm.mark(6);
-    CK(launch_pairs(kind, MODE_MEMBER, m, n, s, &launches));
-    tm.mark(7);
-    CK(cudaMemcpyAsync(&hs, stats, sizeof hs, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    M = (int64_t)hs.key_count;
-    if (M <= key_cap) break;
-    // overflow: resize exactly and recompute
+  int64_t M = (int64_t)hs.key_count;
+  if (M > key_cap) {
     pool.free_now(keys);
     key_cap = M;
-    unsigned long long zero3[3] = {0, 0, 0};
-    CK(cudaMemcpyAsync(&stats->key_count, zero3, sizeof(unsigned long long), cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(&stats->near_ties, zero3, sizeof(unsigned long long), cudaMemcpyHostToDevice, s));
-    unsigned long long gb = greedy_band;
-    CK(cudaMemcpyAsync(&stats->band_pairs, &gb, sizeof gb, cudaMemcpyHostToDevice, s));
+    TRY(pool.alloc(&keys, (size_t)key_cap));
+    TRY(membership_full(pool, kind, base, P, use_tc, tc_nrm, lm, L, n, d, dtype, nu, th, C2,
+                        keys, key_cap, ties_dev, tie_cap, stats, s, &launches, &M));
+    CK(cudaMemcpyAsync(&hs, stats, sizeof hs, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
   }
   tm.mark(3);
 
-  // ---- C CSR both ways
+  // ---- C CSR both ways.  keys = point << 32 | landmark position: a stable
+  // sort on the position bits and then the point bits gives the point-major
+  // order; a further stable sort on the position bits alone gives the
+  // landmark-major order with the points of each ball still ascending.
   unsigned long long* alt = nullptr;
   void* rtemp = nullptr;
   int64_t* pt_ptr = nullptr;
@@ -512,18 +655,15 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
   TRY(pool.alloc(&pt_lm, (size_t)(M > 0 ? M : 1)));
   TRY(pool.alloc(&ball_ptr, (size_t)L + 1));
   TRY(pool.alloc(&ball_idx, (size_t)(M > 0 ? M : 1)));
-  CK(radix_sort_u64(&keys, &alt, M, 0, pbits + lbits, rtemp, s, &launches));
-  const unsigned long long lmask = (1ull << lbits) - 1ull, pmask = (1ull << pbits) - 1ull;
-  CK(launch_unpack_low(keys, M, lmask, pt_lm, s, &launches));
-  CK(launch_segment_ptr(keys, M, lbits, pmask, n, pt_ptr, s, &launches));
-  CK(launch_rekey_landmark_major(keys, M, lbits, pbits, alt, s, &launches));
-  {
-    unsigned long long* k2 = alt;
-    unsigned long long* a2 = keys;
-    CK(radix_sort_u64(&k2, &a2, M, pbits, pbits + lbits, rtemp, s, &launches));
-    CK(launch_unpack_low(k2, M, pmask, ball_idx, s, &launches));
-    CK(launch_segment_ptr(k2, M, pbits, lmask, L, ball_ptr, s, &launches));
-  }
+  const unsigned long long lo32 = 0xffffffffull;
+  const BitRange pm[2] = {{0, lbits}, {32, 32 + pbits}};
+  const BitRange lmaj[1] = {{0, lbits}};
+  CK(radix_sort_u64(&keys, &alt, M, pm, 2, rtemp, s, &launches));
+  CK(launch_unpack_low(keys, M, lo32, pt_lm, s, &launches));
+  CK(launch_segment_ptr(keys, M, 32, lo32, n, pt_ptr, s, &launches));
+  CK(radix_sort_u64(&keys, &alt, M, lmaj, 1, rtemp, s, &launches));
+  CK(launch_unpack_high(keys, M, ball_idx, s, &launches));
+  CK(launch_segment_ptr(keys, M, 0, lo32, L, ball_ptr, s, &launches));
   pool.free_now(keys);
   pool.free_now(alt);
   pool.free_now(rtemp);
@@ -551,7 +691,8 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
     TRY(pool.alloc(&ea, (size_t)NP));
     TRY(pool.alloc((uint8_t**)&et, radix_temp_bytes(NP)));
     CK(launch_pair_emit(pt_ptr, pt_lm, n, poff, lbits, ek, s, &launches));
-    CK(radix_sort_u64(&ek, &ea, NP, 0, 2 * lbits, et, s, &launches));
+    const BitRange er[1] = {{0, 2 * lbits}};
+    CK(radix_sort_u64(&ek, &ea, NP, er, 1, et, s, &launches));
     TRY(pool.alloc(&flags, (size_t)NP));
     TRY(pool.alloc(&pos, (size_t)NP));
     TRY(pool.alloc((uint8_t**)&ft, scan_temp_bytes(NP)));
@@ -595,6 +736,7 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
   c->n_landmarks = L;
   c->n_members = M;
   c->n_edges = E;
+  c->n_witness_pairs = NP;
   c->n_pair_evals = n * L;
   c->n_greedy_evals = (int64_t)hs.greedy_evals;
   c->n_band_pairs = (int64_t)hs.band_pairs;
@@ -613,8 +755,15 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
   if (tm.on) {
     for (int i = 0; i < 5; ++i) cudaEventElapsedTime(&c->step_ms[i], tm.ev[i], tm.ev[i + 1]);
     cudaEventElapsedTime(&c->step_ms[BM_STEP_TOTAL], tm.ev[0], tm.ev[5]);
-    cudaEventElapsedTime(&c->step_ms[BM_STEP_MEMBER_KERNEL], tm.ev[6], tm.ev[7]);
+    float km = 0.f;
+    for (size_t i = 0; i + 1 < mev.size(); i += 2) {
+      float t = 0.f;
+      cudaEventElapsedTime(&t, mev[i], mev[i + 1]);
+      km += t;
+    }
+    c->step_ms[BM_STEP_MEMBER_KERNEL] = km;
   }
+  c->n_member_launches = (int64_t)(mev.size() / 2);
   c->n_launches = launches;
   if (host_in) {
     c->on_host = 1;
@@ -704,6 +853,12 @@ void bm_free(bm_cover* c) {
 
 const char* bm_last_error(void) { return g_err.c_str(); }
 
+bm_status bm_trim_memory(void) {
+  cudaMemPool_t mp = device_pool();
+  if (mp) CK(cudaMemPoolTrimTo(mp, 0));
+  return BM_OK;
+}
+
 int32_t bm_version(void) { return (BM_VERSION_MAJOR << 16) | BM_VERSION_MINOR; }
 
 bm_status bm_debug_radix_sort_u64(uint64_t* keys, int64_t n, int32_t bits, void* stream) {
@@ -716,7 +871,8 @@ bm_status bm_debug_radix_sort_u64(uint64_t* keys, int64_t n, int32_t bits, void*
   TRY(pool.alloc((uint8_t**)&temp, bm::radix_temp_bytes(n)));
   int64_t launches = 0;
   unsigned long long* k = (unsigned long long*)keys;
-  CK(bm::radix_sort_u64(&k, &alt, n, 0, bits, temp, s, &launches));
+  const bm::BitRange r[1] = {{0, bits}};
+  CK(bm::radix_sort_u64(&k, &alt, n, r, 1, temp, s, &launches));
   if (k != (unsigned long long*)keys)
     CK(cudaMemcpyAsync(keys, k, sizeof(uint64_t) * n, cudaMemcpyDeviceToDevice, s));
   CK(cudaStreamSynchronize(s));

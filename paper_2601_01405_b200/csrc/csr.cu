@@ -52,6 +52,20 @@ cudaError_t launch_unpack_low(const unsigned long long* keys, int64_t m, unsigne
   return cudaGetLastError();
 }
 
+__global__ void k_unpack_high(const unsigned long long* __restrict__ keys, int64_t m,
+                              int32_t* __restrict__ out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < m) out[i] = (int32_t)(keys[i] >> 32);
+}
+
+cudaError_t launch_unpack_high(const unsigned long long* keys, int64_t m, int32_t* out,
+                               cudaStream_t s, int64_t* launches) {
+  if (m <= 0) return cudaSuccess;
+  ++*launches;
+  k_unpack_high<<<grid_for(m, 256), 256, 0, s>>>(keys, m, out);
+  return cudaGetLastError();
+}
+
 __global__ void k_rekey(const unsigned long long* __restrict__ pm, int64_t m, int lbits, int pbits,
                         unsigned long long* __restrict__ out) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -85,7 +99,9 @@ cudaError_t launch_pair_counts(const int64_t* pt_ptr, int64_t n, int64_t* cnt, c
   return cudaGetLastError();
 }
 
-// One warp per point: lanes stride over the C(t,2) pairs of the point's row.
+// One warp per point: the C(t,2) pairs (a, c), a < c, of the point's row in
+// row-major order over the strict upper triangle; the warp walks the rows and
+// its lanes stride over the columns of each row (O(1) per pair).
 __global__ void k_pair_emit(const int64_t* __restrict__ pt_ptr, const int32_t* __restrict__ pt_lm,
                             int64_t n, const int64_t* __restrict__ off, int lbits,
                             unsigned long long* __restrict__ keys) {
@@ -94,17 +110,12 @@ __global__ void k_pair_emit(const int64_t* __restrict__ pt_ptr, const int32_t* _
   if (p >= n) return;
   const int64_t b = pt_ptr[p], t = pt_ptr[p + 1] - b;
   if (t < 2) return;
-  const int64_t npairs = t * (t - 1) / 2;
-  const int64_t o = off[p];
-  for (int64_t k = lane; k < npairs; k += 32) {
-    // unrank k -> (a, c), a < c, row-major over the strict upper triangle
-    int64_t a = 0, rem = k;
-    while (rem >= t - 1 - a) {
-      rem -= t - 1 - a;
-      ++a;
-    }
-    const int64_t c = a + 1 + rem;
-    keys[o + k] = ((unsigned long long)pt_lm[b + a] << lbits) | (unsigned long long)pt_lm[b + c];
+  int64_t o = off[p];
+  for (int64_t a = 0; a + 1 < t; ++a) {
+    const unsigned long long hi = (unsigned long long)pt_lm[b + a] << lbits;
+    for (int64_t c = a + 1 + lane; c < t; c += 32)
+      keys[o + (c - a - 1)] = hi | (unsigned long long)pt_lm[b + c];
+    o += t - 1 - a;
   }
 }
 

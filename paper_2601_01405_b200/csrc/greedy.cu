@@ -1,4 +1,4 @@
-// greedy.cu — steps A1/A3 of the blocked greedy eps-net.
+// greedy.cu — steps A1/A3/A4 of the blocked greedy eps-net.
 //
 // The paper's greedy walks the points in order and makes the
 // next uncovered point a landmark.  Blocked form: the list `unc` holds the
@@ -9,9 +9,10 @@
 // candidate landmark b < a is adjacent to it — which is exactly the greedy
 // restricted to the tile, because every landmark from earlier tiles has
 // already removed its ball from `unc`.  The result is independent of T
-// (lexicographically-first maximal independent set).  A4 (MODE_COVER) marks
-// the remaining unc[nc..) against the new landmarks and k_scan_blocks /
-// k_compact keep the survivors in order.
+// (lexicographically-first maximal independent set).  The tile's membership
+// pass (step B for the new landmarks, over all points) sets covered[p] for
+// every point in a new ball; k_compact keeps the survivors unc[nc..) with
+// covered == 0, in order (A4), in one pass with a decoupled look-back.
 #include "internal.cuh"
 
 namespace bm {
@@ -68,13 +69,19 @@ __global__ void __launch_bounds__(1024) k_resolve(const uint32_t* __restrict__ a
                                                   int32_t* __restrict__ lm_out,
                                                   int32_t* __restrict__ L_dev,
                                                   int32_t* __restrict__ new_lm,
-                                                  int32_t* __restrict__ dL_dev, DevStats* stats) {
+                                                  int32_t* __restrict__ dL_dev, DevStats* stats,
+                                                  int32_t* __restrict__ ticket,
+                                                  unsigned long long* __restrict__ band_count) {
   __shared__ volatile uint32_t lmw[32];
   __shared__ volatile int ready[32];
   __shared__ int wpre[33];
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
   const int n_unc = *n_unc_dev;
   const int nc = min(T, n_unc);
+  if (tid == 0) {
+    if (ticket) *ticket = 0;
+    if (band_count) *band_count = 0ull;
+  }
   if (nc == 0) {
     if (tid == 0) *dL_dev = 0;
     return;
@@ -111,19 +118,18 @@ __global__ void __launch_bounds__(1024) k_resolve(const uint32_t* __restrict__ a
     const int dL = wpre[nb];
     *dL_dev = dL;
     *L_dev = L0 + dL;
-    stats->greedy_evals += (unsigned long long)nc * (unsigned long long)(nc - 1) / 2ull +
-                           (unsigned long long)(n_unc - nc) * (unsigned long long)dL;
+    stats->greedy_evals += (unsigned long long)nc * (unsigned long long)(nc - 1) / 2ull;
     stats->tiles += 1ull;
   }
 }
 
 cudaError_t launch_resolve(const uint32_t* adj, int adj_words, const int32_t* unc,
                            const int32_t* n_unc, int T, int32_t* lm_out, int32_t* L_dev,
-                           int32_t* new_lm, int32_t* dL_dev, DevStats* stats, cudaStream_t s,
-                           int64_t* launches) {
+                           int32_t* new_lm, int32_t* dL_dev, DevStats* stats, int32_t* ticket,
+                           unsigned long long* band_count, cudaStream_t s, int64_t* launches) {
   ++*launches;
   k_resolve<<<1, 1024, 0, s>>>(adj, adj_words, unc, n_unc, T, lm_out, L_dev, new_lm, dL_dev,
-                               stats);
+                               stats, ticket, band_count);
   return cudaGetLastError();
 }
 
@@ -146,93 +152,111 @@ cudaError_t launch_resolve_debug(const uint32_t* adj, int adj_words, int nc, uin
   return cudaGetLastError();
 }
 
-// Exclusive scan of the per-CTA kept counts of the coverage pass (one CTA).
-__global__ void __launch_bounds__(1024) k_scan_blocks(const int32_t* __restrict__ cnt, int nblk,
-                                                      int32_t* __restrict__ off,
-                                                      int32_t* __restrict__ total) {
-  __shared__ int wsum[32];
-  __shared__ int carry;
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  if (tid == 0) carry = 0;
-  __syncthreads();
-  for (int base = 0; base < nblk; base += 1024) {
-    const int i = base + tid;
-    const int v = i < nblk ? cnt[i] : 0;
-    int incl = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      int t = __shfl_up_sync(FULLMASK, incl, o);
-      if (lane >= o) incl += t;
-    }
-    if (lane == 31) wsum[w] = incl;
-    __syncthreads();
-    if (w == 0) {
-      int s = wsum[lane];
-      int si = s;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        int t = __shfl_up_sync(FULLMASK, si, o);
-        if (lane >= o) si += t;
-      }
-      wsum[lane] = si - s;
-    }
-    __syncthreads();
-    const int excl = carry + wsum[w] + incl - v;
-    if (i < nblk) off[i] = excl;
-    __syncthreads();
-    if (tid == 1023) carry = excl + v;
-    __syncthreads();
-  }
-  if (tid == 0) *total = carry;
+// A4 compaction: unc_next = [unc[i] for nc <= i < n_unc if !covered[unc[i]]],
+// in order.  Each CTA takes the next CP_TILE items by ticket (so a CTA only
+// ever waits on CTAs that already started), ranks its survivors with ballots,
+// publishes its count, and derives its output offset by looking back over the
+// predecessors' published (aggregate | inclusive prefix) words.  Words carry the
+// launch tag, so the state array never needs clearing between tiles.
+constexpr int CP_NT = 256, CP_ROUNDS = 16, CP_TILE = CP_NT * CP_ROUNDS;
+constexpr unsigned long long CP_AGG = 1ull, CP_INC = 2ull;
+
+__device__ __forceinline__ unsigned long long cp_pack(uint32_t tag, unsigned long long flag,
+                                                      uint32_t v) {
+  return ((unsigned long long)tag << 34) | (flag << 32) | (unsigned long long)v;
 }
 
-// Order-preserving scatter of the survivors: unc_next[off[b] + rank] = unc[nc + i].
-__global__ void __launch_bounds__(256) k_compact(const uint8_t* __restrict__ keep,
-                                                 const int32_t* __restrict__ off, int blk_rows,
-                                                 const int32_t* __restrict__ unc,
-                                                 const int32_t* __restrict__ n_unc_dev, int T,
-                                                 int32_t* __restrict__ unc_next) {
-  __shared__ int wsum[8];
+__global__ void __launch_bounds__(CP_NT) k_compact(const uint8_t* __restrict__ covered,
+                                                   const int32_t* __restrict__ unc,
+                                                   const int32_t* __restrict__ n_unc_dev, int T,
+                                                   int32_t* __restrict__ unc_next,
+                                                   int32_t* __restrict__ n_unc_next,
+                                                   unsigned long long* state,
+                                                   int32_t* ticket, uint32_t tag) {
+  __shared__ int s_bid;
+  __shared__ int s_wcnt[CP_ROUNDS][CP_NT / 32];
+  __shared__ int s_excl;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  if (tid == 0) s_bid = atomicAdd(ticket, 1);
+  __syncthreads();
+  const int bid = s_bid;
   const int n_unc = *n_unc_dev;
   const int nc = min(T, n_unc);
-  const int64_t m = n_unc - nc;
-  const int64_t b0 = (int64_t)blockIdx.x * blk_rows;
-  if (b0 >= m) return;
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int per = blk_rows / 256;     // consecutive items per thread
-  const int64_t i0 = b0 + (int64_t)tid * per;
-  int c = 0;
-  for (int k = 0; k < per; ++k) {
-    const int64_t i = i0 + k;
-    if (i < m) c += keep[i];
+  const int64_t m = (int64_t)n_unc - nc;
+  const int64_t i0 = (int64_t)bid * CP_TILE;
+  if (i0 >= m) {
+    if (bid == 0 && tid == 0) *n_unc_next = 0;   // nothing left after this tile
+    return;
   }
-  int incl = c;
+  // survivors of this CTA's items, round r covers [i0 + r*NT, i0 + (r+1)*NT)
+  int32_t pt[CP_ROUNDS];
+  unsigned keepm = 0u;
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    int t = __shfl_up_sync(FULLMASK, incl, o);
-    if (lane >= o) incl += t;
+  for (int r = 0; r < CP_ROUNDS; ++r) {
+    const int64_t i = i0 + r * CP_NT + tid;
+    pt[r] = i < m ? unc[nc + i] : 0;
+    const bool keep = i < m && covered[pt[r]] == 0;
+    keepm |= (keep ? 1u : 0u) << r;
+    const unsigned b = __ballot_sync(FULLMASK, keep);
+    if (lane == 0) s_wcnt[r][w] = __popc(b);
   }
-  if (lane == 31) wsum[w] = incl;
   __syncthreads();
-  int wpre = 0;
-  for (int k = 0; k < w; ++k) wpre += wsum[k];
-  int pos = off[blockIdx.x] + wpre + incl - c;
-  for (int k = 0; k < per; ++k) {
-    const int64_t i = i0 + k;
-    if (i < m && keep[i]) unc_next[pos++] = unc[nc + i];
+  if (tid < 32) {
+    // CTA aggregate, then the look-back (warp 0, lane 0 walks the predecessors)
+    int agg = 0;
+    for (int k = lane; k < CP_ROUNDS * (CP_NT / 32); k += 32) agg += (&s_wcnt[0][0])[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) agg += __shfl_xor_sync(FULLMASK, agg, o);
+    if (lane == 0) {
+      volatile unsigned long long* st = state;
+      int excl = 0;
+      if (bid == 0) {
+        st[0] = cp_pack(tag, CP_INC, (uint32_t)agg);
+      } else {
+        st[bid] = cp_pack(tag, CP_AGG, (uint32_t)agg);
+        __threadfence();
+        for (int j = bid - 1; j >= 0; --j) {
+          unsigned long long v;
+          do {
+            v = st[j];
+          } while ((uint32_t)(v >> 34) != tag || ((v >> 32) & 3ull) == 0ull);
+          excl += (int)(uint32_t)v;
+          if (((v >> 32) & 3ull) == CP_INC) break;
+        }
+        __threadfence();
+        st[bid] = cp_pack(tag, CP_INC, (uint32_t)(excl + agg));
+      }
+      s_excl = excl;
+      if (i0 + CP_TILE >= m) *n_unc_next = excl + agg;   // the last CTA holds the total
+    }
+  }
+  __syncthreads();
+  // scatter in item order: offset = excl + all earlier rounds + earlier warps + lane rank
+  int base = s_excl;
+#pragma unroll
+  for (int r = 0; r < CP_ROUNDS; ++r) {
+    const bool keep = (keepm >> r) & 1u;
+    const unsigned b = __ballot_sync(FULLMASK, keep);
+    int pre = 0;
+    for (int k = 0; k < w; ++k) pre += s_wcnt[r][k];
+    if (keep) unc_next[base + pre + __popc(b & ((1u << lane) - 1u))] = pt[r];
+    int tot = 0;
+#pragma unroll
+    for (int k = 0; k < CP_NT / 32; ++k) tot += s_wcnt[r][k];
+    base += tot;
   }
 }
 
-cudaError_t launch_compact_unc(const uint8_t* keep, const int32_t* blk_count, int nblk,
-                               int blk_rows, const int32_t* unc, const int32_t* n_unc, int T,
-                               int32_t* blk_off, int32_t* unc_next, int32_t* n_unc_next,
-                               cudaStream_t s, int64_t* launches) {
-  k_scan_blocks<<<1, 1024, 0, s>>>(blk_count, nblk, blk_off, n_unc_next);
+int64_t compact_state_words(int64_t n) { return (n + CP_TILE - 1) / CP_TILE + 1; }
+
+cudaError_t launch_compact_unc(const uint8_t* covered, const int32_t* unc, const int32_t* n_unc,
+                               int T, int32_t* unc_next, int32_t* n_unc_next,
+                               unsigned long long* state, int32_t* ticket, uint32_t tag,
+                               int64_t n, cudaStream_t s, int64_t* launches) {
+  const int64_t nblk = (n + CP_TILE - 1) / CP_TILE;
   ++*launches;
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
-  k_compact<<<nblk, 256, 0, s>>>(keep, blk_off, blk_rows, unc, n_unc, T, unc_next);
-  ++*launches;
+  k_compact<<<(unsigned)(nblk > 0 ? nblk : 1), CP_NT, 0, s>>>(covered, unc, n_unc, T, unc_next,
+                                                               n_unc_next, state, ticket, tag);
   return cudaGetLastError();
 }
 

@@ -20,7 +20,7 @@ namespace bm {
 // ---------------------------------------------------------------- kinds
 enum Kind : int { K_L2F = 0, K_L1F = 1, K_COSF = 2, K_L2I = 3, K_L1I = 4 };
 
-enum PairMode : int { MODE_ADJ = 0, MODE_COVER = 1, MODE_MEMBER = 2 };
+enum PairMode : int { MODE_ADJ = 0, MODE_MEMBER = 2 };
 
 // Thresholds for the classification "score < lo -> in, score >= hi -> out,
 // else band (fp64 recheck)".  Score = d^2 (L2F), L1 sum (L1F), -cos (COSF),
@@ -42,7 +42,7 @@ struct DevStats {
   unsigned long long greedy_evals;   // in-tile + coverage evaluations
   unsigned long long tiles;          // greedy tiles with nc > 0
   int nonfinite;                     // prep: a NaN/Inf coordinate was seen
-  int pad;
+  int overflow;                      // fused greedy: a tile's band queue overflowed
 };
 
 struct PairArgs {
@@ -63,10 +63,11 @@ struct PairArgs {
   int64_t l_begin, l_end;
   const int32_t* l_end_dev;   // if non-null: l_end = min(l_end, *l_end_dev)
   int64_t lpos0;
-  int64_t l_chunk;          // landmarks per grid.y slice (MODE_MEMBER)
+  const int32_t* l_total_dev; // if non-null: lpos0 = *l_total_dev - (l_end - l_begin)
+                              // (fused greedy tile: the new landmarks are the last ones)
   // outputs
   uint32_t* adj; int adj_words;                 // MODE_ADJ
-  uint8_t* keep; int32_t* blk_count;            // MODE_COVER: keep[i - q_begin], per-CTA counts
+  uint8_t* covered;                             // MODE_MEMBER: covered[p] = 1 for in-ball pairs
   unsigned long long* keys; int64_t key_cap; int lbits;   // MODE_MEMBER: (p << lbits) | j
   int64_t* ties; int64_t tie_cap;               // MODE_MEMBER near-tie triples (host-mapped)
   DevStats* stats;
@@ -81,24 +82,36 @@ cudaError_t launch_prep(const void* X, int dtype, int64_t n, int d, int kind, in
 cudaError_t launch_pairs(int kind, int mode, const PairArgs& a, int64_t q_rows_max,
                          cudaStream_t s, int64_t* launches);
 
+// A3; also resets the per-tile device counters (*ticket = 0, *band_count = 0).
 cudaError_t launch_resolve(const uint32_t* adj, int adj_words, const int32_t* unc,
                            const int32_t* n_unc, int T, int32_t* lm_out, int32_t* L_dev,
                            int32_t* new_lm, int32_t* dL_dev, DevStats* stats,
+                           int32_t* ticket, unsigned long long* band_count,
                            cudaStream_t s, int64_t* launches);
 
-cudaError_t launch_compact_unc(const uint8_t* keep, const int32_t* blk_count, int nblk,
-                               int blk_rows, const int32_t* unc, const int32_t* n_unc, int T,
-                               int32_t* blk_off, int32_t* unc_next, int32_t* n_unc_next,
-                               cudaStream_t s, int64_t* launches);
+// Order-preserving compaction of the uncovered list after a tile: keeps
+// unc[i], nc <= i < n_unc, with covered[unc[i]] == 0 (single pass, decoupled
+// look-back; `state` holds compact_state_words(n) zero-initialised words,
+// `ticket` is reset by the resolve kernel of the same tile, `tag` is unique
+// per launch within a call and non-zero).
+int64_t compact_state_words(int64_t n);
+cudaError_t launch_compact_unc(const uint8_t* covered, const int32_t* unc, const int32_t* n_unc,
+                               int T, int32_t* unc_next, int32_t* n_unc_next,
+                               unsigned long long* state, int32_t* ticket, uint32_t tag,
+                               int64_t n, cudaStream_t s, int64_t* launches);
 
 // scan / sort (sort.cu)
 size_t scan_temp_bytes(int64_t n);
 cudaError_t exclusive_scan_i64(const int64_t* in, int64_t* out, int64_t n, void* temp,
                                int64_t* total_dev, cudaStream_t s, int64_t* launches);
 size_t radix_temp_bytes(int64_t n);
-// Stable LSD sort of keys over bit range [lo_bit, hi_bit); result in *keys (may swap with alt).
+// Stable LSD sort of keys on the concatenation of bit ranges (ranges[0] least
+// significant, at most 64 bits in total); result in *keys (may swap with alt).
+struct BitRange {
+  int lo, hi;  // bits [lo, hi)
+};
 cudaError_t radix_sort_u64(unsigned long long** keys, unsigned long long** alt, int64_t n,
-                           int lo_bit, int hi_bit, void* temp, cudaStream_t s,
+                           const BitRange* ranges, int nranges, void* temp, cudaStream_t s,
                            int64_t* launches);
 
 // csr / edges (csr.cu)
@@ -108,6 +121,8 @@ cudaError_t launch_segment_ptr(const unsigned long long* keys, int64_t m, int sh
 cudaError_t launch_unpack_low(const unsigned long long* keys, int64_t m,
                               unsigned long long mask, int32_t* out, cudaStream_t s,
                               int64_t* launches);
+cudaError_t launch_unpack_high(const unsigned long long* keys, int64_t m, int32_t* out,
+                               cudaStream_t s, int64_t* launches);
 cudaError_t launch_rekey_landmark_major(const unsigned long long* pm_keys, int64_t m, int lbits,
                                         int pbits, unsigned long long* out, cudaStream_t s,
                                         int64_t* launches);
@@ -138,10 +153,5 @@ inline int pick_nu(int nu_needed) {
   for (int w : widths)
     if (nu_needed <= w) return w;
   return 0;
-}
-// Rows a MODE_COVER CTA handles (must match launch_pairs_nu's R choice).
-inline int cover_rows_per_cta(int nu) {
-  int R = nu == 0 ? 1 : (nu <= 8 ? 4 : (nu <= 16 ? 2 : 1));
-  return 256 * R;
 }
 }  // namespace bm

@@ -1,14 +1,14 @@
 // pairs_impl.cuh — CUDA-core point x landmark predicate kernel (steps A2, A4, B).
 //
-// One kernel template serves the three places the method evaluates the ball
+// One kernel template serves the two places the method evaluates the ball
 // predicate d(x_p, l) < eps (open ball):
 //   MODE_ADJ    A2: candidate x candidate bits of the greedy tile (b < a)
-//   MODE_COVER  A4: "mark all points within eps of x as covered"
-//               for the still-uncovered points after the tile, with a per-CTA
-//               kept-count for the order-preserving compaction
-//   MODE_MEMBER B : ball membership of every point in every ball,
-//               emitting packed (point << lbits | landmark position) keys with
-//               warp-aggregated atomics
+//   MODE_MEMBER B (+A4): ball membership of every point in the balls of a
+//               block of landmarks (the range queries), emitting
+//               packed (point << lbits | landmark position) keys with
+//               warp-aggregated atomics and, in the fused greedy, setting
+//               covered[p] ("mark all points within eps of x as covered",
+//               PAPER.md:104) for every in-ball pair
 //
 // Layout: each thread keeps R query rows in registers (NU 8-byte units each);
 // LC landmark rows at a time are staged in shared memory and read as warp
@@ -115,43 +115,17 @@ __device__ __forceinline__ int classify(typename KindTraits<KIND>::acc_t acc, in
 
 // NU > 0: query rows live in registers (NU units).  NU == 0 ("wide"): rows of
 // any length; the query row is re-read from global/L1 for every landmark.
+// One call = one block of NT*R query rows [blk_q0, ..) against landmarks
+// lidx[l0 .. l1) (positions lpos0 + (l - l_begin)).
 template <int KIND, int NU, int R, int MODE, int LC>
-__global__ void __launch_bounds__(256) k_pairs(PairArgs A) {
+__device__ __forceinline__ void pairs_block(const PairArgs& A, uint2* sl, int32_t* sln,
+                                            int32_t* slp, int64_t blk_q0, int64_t q_end,
+                                            int64_t l0, int64_t l1, int64_t lpos0) {
   constexpr int NT = 256;
   constexpr int QU = NU > 0 ? NU : 1;   // register units per query row
   using acc_t = typename KindTraits<KIND>::acc_t;
-  extern __shared__ uint2 sl[];          // [LC][nu]
   const int nu = NU > 0 ? NU : A.nu;
-  __shared__ int32_t sln[LC];
-  __shared__ int32_t slp[LC];
-  __shared__ int32_t s_red[NT / 32];
-
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  // device-resident counts act as caps on the host bounds: actual = min(host, *dev)
-  int64_t q_end = A.q_end_dev ? min(A.q_end, (int64_t)*A.q_end_dev) : A.q_end;
-  int64_t q_begin = A.q_begin_dev ? min(A.q_begin, (int64_t)*A.q_begin_dev) : A.q_begin;
-  q_begin = min(q_begin, q_end);
-  const int64_t blk_q0 = q_begin + (int64_t)blockIdx.x * (NT * R);
-
-  int64_t l_end = A.l_end_dev ? min(A.l_end, (int64_t)*A.l_end_dev) : A.l_end;
-  int64_t l0 = A.l_begin, l1 = l_end;
-  if (MODE == MODE_MEMBER) {
-    l0 = A.l_begin + (int64_t)blockIdx.y * A.l_chunk;
-    l1 = min(l_end, l0 + A.l_chunk);
-  } else if (MODE == MODE_ADJ) {
-    l0 = A.l_begin + (int64_t)blockIdx.y * 32;
-    l1 = min(l_end, l0 + 32);
-  }
-  if (MODE == MODE_COVER) {
-    if (blk_q0 >= q_end) {
-      if (tid == 0 && A.blk_count) A.blk_count[blockIdx.x] = 0;
-      return;
-    }
-  } else {
-    if (blk_q0 >= q_end || l0 >= l1) return;
-    // adjacency: only b < a is needed
-    if (MODE == MODE_ADJ && l0 >= min(q_end, blk_q0 + NT * R)) return;
-  }
+  const int tid = threadIdx.x, lane = tid & 31;
 
   // ---- query rows into registers
   uint2 q[R][QU];
@@ -170,21 +144,13 @@ __global__ void __launch_bounds__(256) k_pairs(PairArgs A) {
     qn[r] = (KIND == K_L2I && act[r]) ? A.inorm[qp[r]] : 0;
   }
 
-  bool covered[R];
   uint32_t word[R];
 #pragma unroll
-  for (int r = 0; r < R; ++r) { covered[r] = false; word[r] = 0u; }
+  for (int r = 0; r < R; ++r) word[r] = 0u;
 
   for (int64_t lb = l0; lb < l1; lb += LC) {
     const int nl = (int)min((int64_t)LC, l1 - lb);
-    if (MODE == MODE_COVER) {
-      bool done = true;
-#pragma unroll
-      for (int r = 0; r < R; ++r) done = done && (covered[r] || !act[r]);
-      if (__syncthreads_and(done)) break;
-    } else {
-      __syncthreads();
-    }
+    __syncthreads();
     for (int t = tid; t < nl * nu; t += NT) {
       int jj = t / nu, u = t - jj * nu;
       int32_t pt = A.lidx[lb + jj];
@@ -197,11 +163,7 @@ __global__ void __launch_bounds__(256) k_pairs(PairArgs A) {
     }
     __syncthreads();
 
-    bool warp_done = false;
     for (int jj = 0; jj < nl; ++jj) {
-      if (MODE == MODE_COVER) {
-        if (warp_done) break;
-      }
       uint2 l[QU];
 #pragma unroll
       for (int u = 0; u < QU; ++u) l[u] = NU > 0 ? sl[jj * nu + u] : make_uint2(0u, 0u);
@@ -227,7 +189,6 @@ __global__ void __launch_bounds__(256) k_pairs(PairArgs A) {
         cls[r] = c;
         if (MODE == MODE_MEMBER) special = special || (c != 0);
         else special = special || (c == 2);
-        if (MODE == MODE_COVER) covered[r] = covered[r] || (c == 1);
         if (MODE == MODE_ADJ) word[r] |= (c == 1 ? 1u : 0u) << (int)(lb + jj - l0);
       }
       const unsigned ball = __ballot_sync(FULL, special);
@@ -249,10 +210,10 @@ __global__ void __launch_bounds__(256) k_pairs(PairArgs A) {
                 A.ties[3 * k + 2] = in ? 1 : 0;
               }
             }
-            if (MODE == MODE_COVER) covered[r] = covered[r] || in;
             if (MODE == MODE_ADJ) word[r] |= (in ? 1u : 0u) << (int)(lb + jj - l0);
           }
           if (MODE == MODE_MEMBER) nemit += (cls[r] == 1);
+          if (MODE == MODE_MEMBER && A.covered && cls[r] == 1) A.covered[qp[r]] = 1;
         }
         if (MODE == MODE_MEMBER) {
           int incl = nemit;
@@ -268,7 +229,7 @@ __global__ void __launch_bounds__(256) k_pairs(PairArgs A) {
             base = __shfl_sync(FULL, base, 31);
             unsigned long long k = base + (unsigned long long)(incl - nemit);
             const unsigned long long jpos =
-                (unsigned long long)(A.lpos0 + (lb + jj - A.l_begin));
+                (unsigned long long)(lpos0 + (lb + jj - A.l_begin));
 #pragma unroll
             for (int r = 0; r < R; ++r) {
               if (cls[r] == 1) {
@@ -280,12 +241,6 @@ __global__ void __launch_bounds__(256) k_pairs(PairArgs A) {
           }
         }
       }
-      if (MODE == MODE_COVER) {
-        bool done = true;
-#pragma unroll
-        for (int r = 0; r < R; ++r) done = done && (covered[r] || !act[r]);
-        warp_done = __all_sync(FULL, done);
-      }
     }
   }
 
@@ -295,25 +250,56 @@ __global__ void __launch_bounds__(256) k_pairs(PairArgs A) {
     for (int r = 0; r < R; ++r)
       if (act[r]) A.adj[qi[r] * (int64_t)A.adj_words + wcol] = word[r];
   }
-  if (MODE == MODE_COVER) {
-    int cnt = 0;
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      if (act[r]) A.keep[qi[r] - q_begin] = covered[r] ? 0 : 1;
-      cnt += (act[r] && !covered[r]) ? 1 : 0;
+}
+
+// Device-side decomposition of MODE_MEMBER work into (query block, landmark
+// chunk) items; the landmark count may live on the device (fused greedy tile).
+struct MemberSched {
+  int64_t nrb, nch, chunk;
+};
+__device__ __forceinline__ MemberSched member_sched(int64_t nq, int64_t nl, int rows_per_blk,
+                                                    int64_t grid) {
+  MemberSched m;
+  m.nrb = (nq + rows_per_blk - 1) / rows_per_blk;
+  const int64_t n32 = (nl + 31) / 32;
+  int64_t merge = (m.nrb * n32 + 8 * grid - 1) / (8 * grid);
+  if (merge < 1) merge = 1;
+  m.chunk = 32 * merge;
+  m.nch = nl > 0 ? (nl + m.chunk - 1) / m.chunk : 0;
+  return m;
+}
+
+template <int KIND, int NU, int R, int MODE, int LC>
+__global__ void __launch_bounds__(256) k_pairs(PairArgs A) {
+  constexpr int NT = 256;
+  extern __shared__ uint2 sl[];          // [LC][nu]
+  __shared__ int32_t sln[LC];
+  __shared__ int32_t slp[LC];
+  // device-resident counts act as caps on the host bounds: actual = min(host, *dev)
+  int64_t q_end = A.q_end_dev ? min(A.q_end, (int64_t)*A.q_end_dev) : A.q_end;
+  int64_t q_begin = A.q_begin_dev ? min(A.q_begin, (int64_t)*A.q_begin_dev) : A.q_begin;
+  q_begin = min(q_begin, q_end);
+  const int64_t l_end = A.l_end_dev ? min(A.l_end, (int64_t)*A.l_end_dev) : A.l_end;
+  if (MODE == MODE_ADJ) {
+    const int64_t blk_q0 = q_begin + (int64_t)blockIdx.x * (NT * R);
+    const int64_t l0 = A.l_begin + (int64_t)blockIdx.y * 32;
+    const int64_t l1 = min(l_end, l0 + 32);
+    if (blk_q0 >= q_end || l0 >= l1) return;
+    if (l0 >= min(q_end, blk_q0 + NT * R)) return;   // only b < a is needed
+    pairs_block<KIND, NU, R, MODE, LC>(A, sl, sln, slp, blk_q0, q_end, l0, l1, A.lpos0);
+  } else {
+    const int64_t nl = l_end - A.l_begin;
+    const int64_t lpos0 = A.l_total_dev ? (int64_t)*A.l_total_dev - nl : A.lpos0;
+    const MemberSched m = member_sched(q_end - q_begin, nl, NT * R, gridDim.x);
+    const int64_t items = m.nrb * m.nch;
+    for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+      const int64_t rb = it % m.nrb, ch = it / m.nrb;
+      const int64_t l0 = A.l_begin + ch * m.chunk;
+      const int64_t l1 = min(l_end, l0 + m.chunk);
+      pairs_block<KIND, NU, R, MODE, LC>(A, sl, sln, slp, q_begin + rb * (NT * R), q_end, l0,
+                                         l1, lpos0);
+      __syncthreads();   // the next item restages the landmark rows
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(FULL, cnt, o);
-    if (lane == 0) s_red[warp] = cnt;
-    __syncthreads();
-    if (tid == 0) {
-      int tot = 0;
-      for (int w = 0; w < NT / 32; ++w) tot += s_red[w];
-      A.blk_count[blockIdx.x] = tot;
-    }
-  }
-  if (MODE == MODE_ADJ || MODE == MODE_COVER) {
-    // greedy evaluation statistics are accumulated by the resolve kernel
   }
 }
 
@@ -332,9 +318,25 @@ cudaError_t launch_pairs_nu(const PairArgs& a, int64_t q_rows_max, cudaStream_t 
   int64_t gx = (q_rows_max + NT * R - 1) / (NT * R);
   if (gx < 1) gx = 1;
   int64_t gy = 1;
-  if (MODE == MODE_ADJ) gy = (a.l_end - a.l_begin + 31) / 32;
-  if (MODE == MODE_MEMBER) gy = (a.l_end - a.l_begin + a.l_chunk - 1) / a.l_chunk;
-  if (gy < 1) gy = 1;
+  if (MODE == MODE_ADJ) {
+    gy = (a.l_end - a.l_begin + 31) / 32;
+    if (gy < 1) gy = 1;
+  } else {
+    // persistent: as many CTAs as fit on the GPU at once (or fewer if there
+    // is less work than that); the kernel strides over the work items
+    static int per_sm = 0, sms = 0;
+    if (per_sm == 0) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem);
+      if (per_sm < 1) per_sm = 1;
+    }
+    const int64_t items = gx * ((a.l_end - a.l_begin + 31) / 32);
+    gx = (int64_t)per_sm * sms;
+    if (items < gx) gx = items;
+    if (gx < 1) gx = 1;
+  }
   if (gx > 0x7fffffffLL || gy > 65535) return cudaErrorInvalidConfiguration;
   kern<<<dim3((unsigned)gx, (unsigned)gy), NT, smem, s>>>(a);
   return cudaGetLastError();
@@ -343,7 +345,6 @@ cudaError_t launch_pairs_nu(const PairArgs& a, int64_t q_rows_max, cudaStream_t 
 template <int KIND, int NU>
 cudaError_t launch_pairs_mode(int mode, const PairArgs& a, int64_t q_rows_max, cudaStream_t s) {
   if (mode == MODE_ADJ) return launch_pairs_nu<KIND, NU, MODE_ADJ>(a, q_rows_max, s);
-  if (mode == MODE_COVER) return launch_pairs_nu<KIND, NU, MODE_COVER>(a, q_rows_max, s);
   return launch_pairs_nu<KIND, NU, MODE_MEMBER>(a, q_rows_max, s);
 }
 

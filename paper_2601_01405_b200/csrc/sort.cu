@@ -1,19 +1,33 @@
 // sort.cu — device-wide exclusive scan and stable LSD radix sort (steps C, D2).
 //
-// Scan: three phases (tile sums -> one-CTA scan of the sums -> tile scan +
-// offset), 4096 elements per tile.
-// Radix sort: 8-bit digits, per pass (1) per-tile 256-bin histograms stored
-// digit-major, (2) exclusive scan of the histogram matrix, (3) stable scatter
-// where each tile is processed in 16 rounds of 256 keys; ranks inside a round
-// come from __match_any_sync (peers with the same digit in the warp) plus
-// per-warp digit counts in shared memory, so equal keys keep their input
-// order (LSD stability).
+// Both are single-pass-per-level designs with decoupled look-back:
+//
+// Scan: one kernel.  Each CTA takes the next 4096-element tile by ticket
+// (a CTA only ever waits on tiles whose owners already started), publishes
+// its tile aggregate, walks back over its predecessors' (aggregate |
+// inclusive-prefix) descriptors to find its exclusive offset, publishes its
+// inclusive prefix, and writes its outputs.
+//
+// Radix sort ("onesweep" structure): 8-bit digits over a list of bit ranges.
+// (1) one histogram kernel reads the keys once and counts every pass's
+// digits; (2) one CTA turns them into global digit offsets; (3) one scatter
+// kernel per pass: a CTA takes a 4096-key tile by ticket, counts its digits,
+// publishes them per digit, looks back per digit (thread d walks digit d) for
+// the count of equal digits in earlier tiles, and scatters its keys in input
+// order (ranks within the tile come from __match_any_sync peers plus per-warp
+// digit counts), so equal digits keep their order — LSD stability.
+//
+// Descriptor words carry a per-launch tag and the state arrays are cleared
+// once per sort / scan call, so no per-pass reset is needed.
 #include "internal.cuh"
 
 namespace bm {
 
 constexpr unsigned FM = 0xffffffffu;
-constexpr int SCAN_NT = 512, SCAN_IPT = 8, SCAN_TILE = SCAN_NT * SCAN_IPT;
+
+// ------------------------------------------------------------------ scan
+constexpr int SC_NT = 512, SC_IPT = 8, SC_TILE = SC_NT * SC_IPT;
+constexpr uint32_t ST_AGG = 1u, ST_INC = 2u;
 
 __device__ __forceinline__ int64_t warp_incl_scan(int64_t v, int lane) {
 #pragma unroll
@@ -46,58 +60,78 @@ __device__ __forceinline__ int64_t block_excl_scan(int64_t v, int64_t* total) {
   return r;
 }
 
-__global__ void __launch_bounds__(SCAN_NT) k_scan_partial(const int64_t* __restrict__ in,
-                                                         int64_t n, int64_t* __restrict__ part) {
-  const int64_t base = (int64_t)blockIdx.x * SCAN_TILE + (int64_t)threadIdx.x * SCAN_IPT;
-  int64_t s = 0;
-#pragma unroll
-  for (int k = 0; k < SCAN_IPT; ++k)
-    if (base + k < n) s += in[base + k];
-  int64_t tot;
-  block_excl_scan<SCAN_NT>(s, &tot);
-  if (threadIdx.x == 0) part[blockIdx.x] = tot;
-}
+struct ScanState {       // per tile: flag word (tag << 2 | ST_*), aggregate, inclusive prefix
+  uint32_t* flag;
+  int64_t* agg;
+  int64_t* inc;
+  int32_t* ticket;
+};
 
-__global__ void __launch_bounds__(1024) k_scan_top(int64_t* __restrict__ part, int64_t nb,
-                                                   int64_t* __restrict__ total) {
-  __shared__ int64_t carry;
-  if (threadIdx.x == 0) carry = 0;
+__global__ void __launch_bounds__(SC_NT) k_scan_lb(const int64_t* __restrict__ in, int64_t n,
+                                                  int64_t* __restrict__ out,
+                                                  int64_t* __restrict__ total, ScanState st,
+                                                  uint32_t tag) {
+  __shared__ int s_tile;
+  __shared__ int64_t s_excl;
+  if (threadIdx.x == 0) s_tile = atomicAdd(st.ticket, 1);
   __syncthreads();
-  for (int64_t b = 0; b < nb; b += 1024) {
-    const int64_t i = b + threadIdx.x;
-    const int64_t v = i < nb ? part[i] : 0;
-    int64_t tot;
-    const int64_t ex = block_excl_scan<1024>(v, &tot);
-    if (i < nb) part[i] = carry + ex;
-    __syncthreads();
-    if (threadIdx.x == 0) carry += tot;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0 && total) *total = carry;
-}
-
-__global__ void __launch_bounds__(SCAN_NT) k_scan_down(const int64_t* __restrict__ in, int64_t n,
-                                                      const int64_t* __restrict__ part,
-                                                      int64_t* __restrict__ out) {
-  const int64_t base = (int64_t)blockIdx.x * SCAN_TILE + (int64_t)threadIdx.x * SCAN_IPT;
-  int64_t v[SCAN_IPT];
-  int64_t s = 0;
+  const int64_t tile = s_tile;
+  const int64_t base = tile * SC_TILE + (int64_t)threadIdx.x * SC_IPT;
+  int64_t v[SC_IPT];
+  int64_t sum = 0;
 #pragma unroll
-  for (int k = 0; k < SCAN_IPT; ++k) {
+  for (int k = 0; k < SC_IPT; ++k) {
     v[k] = base + k < n ? in[base + k] : 0;
-    s += v[k];
+    sum += v[k];
   }
-  int64_t ex = block_excl_scan<SCAN_NT>(s, nullptr) + part[blockIdx.x];
+  int64_t agg;
+  int64_t ex = block_excl_scan<SC_NT>(sum, &agg);
+  if (threadIdx.x == 0) {
+    volatile uint32_t* fl = st.flag;
+    volatile int64_t* va = st.agg;
+    volatile int64_t* vi = st.inc;
+    int64_t excl = 0;
+    if (tile == 0) {
+      vi[0] = agg;
+      __threadfence();
+      fl[0] = (tag << 2) | ST_INC;
+    } else {
+      va[tile] = agg;
+      __threadfence();
+      fl[tile] = (tag << 2) | ST_AGG;
+      for (int64_t j = tile - 1; j >= 0; --j) {
+        uint32_t f;
+        do {
+          f = fl[j];
+        } while ((f >> 2) != tag);
+        __threadfence();
+        if ((f & 3u) == ST_INC) {
+          excl += vi[j];
+          break;
+        }
+        excl += va[j];
+      }
+      vi[tile] = excl + agg;
+      __threadfence();
+      fl[tile] = (tag << 2) | ST_INC;
+    }
+    s_excl = excl;
+    if ((tile + 1) * SC_TILE >= n && total) *total = excl + agg;
+  }
+  __syncthreads();
+  ex += s_excl;
 #pragma unroll
-  for (int k = 0; k < SCAN_IPT; ++k) {
+  for (int k = 0; k < SC_IPT; ++k) {
     if (base + k < n) out[base + k] = ex;
     ex += v[k];
   }
 }
 
+static int64_t scan_tiles(int64_t n) { return (n + SC_TILE - 1) / SC_TILE; }
+
 size_t scan_temp_bytes(int64_t n) {
-  int64_t nb = (n + SCAN_TILE - 1) / SCAN_TILE;
-  return (size_t)(nb + 1) * sizeof(int64_t);
+  const int64_t t = scan_tiles(n) + 1;
+  return (size_t)t * (4 + 8 + 8) + 64;
 }
 
 cudaError_t exclusive_scan_i64(const int64_t* in, int64_t* out, int64_t n, void* temp,
@@ -106,63 +140,126 @@ cudaError_t exclusive_scan_i64(const int64_t* in, int64_t* out, int64_t n, void*
     if (total_dev) return cudaMemsetAsync(total_dev, 0, sizeof(int64_t), s);
     return cudaSuccess;
   }
-  int64_t nb = (n + SCAN_TILE - 1) / SCAN_TILE;
-  int64_t* part = (int64_t*)temp;
-  k_scan_partial<<<(unsigned)nb, SCAN_NT, 0, s>>>(in, n, part);
-  k_scan_top<<<1, 1024, 0, s>>>(part, nb, total_dev);
-  k_scan_down<<<(unsigned)nb, SCAN_NT, 0, s>>>(in, n, part, out);
-  *launches += 3;
+  const int64_t t = scan_tiles(n);
+  ScanState st;
+  st.agg = (int64_t*)temp;
+  st.inc = st.agg + (t + 1);
+  st.flag = (uint32_t*)(st.inc + (t + 1));
+  st.ticket = (int32_t*)(st.flag + (t + 1));
+  cudaError_t e = cudaMemsetAsync(st.flag, 0, sizeof(uint32_t) * (t + 2), s);
+  if (e != cudaSuccess) return e;
+  k_scan_lb<<<(unsigned)t, SC_NT, 0, s>>>(in, n, out, total_dev, st, 1u);
+  ++*launches;
   return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ radix sort
 constexpr int RS_NT = 256, RS_ROUNDS = 16, RS_TILE = RS_NT * RS_ROUNDS, RS_BINS = 256;
+constexpr int RS_MAXP = 8;   // 64 bits / 8
+
+struct RsPasses {
+  int np;
+  int shift[RS_MAXP];
+  int bits[RS_MAXP];
+};
 
 __global__ void __launch_bounds__(RS_NT) k_rs_hist(const unsigned long long* __restrict__ keys,
-                                                  int64_t n, int shift, int bits,
-                                                  int64_t* __restrict__ hist, int64_t nblk) {
-  __shared__ int h[RS_BINS];
-  h[threadIdx.x] = 0;
+                                                  int64_t n, RsPasses P,
+                                                  unsigned long long* __restrict__ hist) {
+  __shared__ unsigned h[RS_MAXP][RS_BINS];
+  for (int p = 0; p < P.np; ++p) h[p][threadIdx.x] = 0u;
   __syncthreads();
-  const unsigned mask = (1u << bits) - 1u;
-  const int64_t t0 = (int64_t)blockIdx.x * RS_TILE;
-#pragma unroll 4
-  for (int r = 0; r < RS_ROUNDS; ++r) {
-    const int64_t i = t0 + r * RS_NT + threadIdx.x;
-    if (i < n) atomicAdd(&h[(unsigned)(keys[i] >> shift) & mask], 1);
+  for (int64_t i = (int64_t)blockIdx.x * RS_NT + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * RS_NT) {
+    const unsigned long long k = keys[i];
+    for (int p = 0; p < P.np; ++p)
+      atomicAdd(&h[p][(unsigned)(k >> P.shift[p]) & ((1u << P.bits[p]) - 1u)], 1u);
   }
   __syncthreads();
-  hist[(int64_t)threadIdx.x * nblk + blockIdx.x] = h[threadIdx.x];
+  for (int p = 0; p < P.np; ++p)
+    if (h[p][threadIdx.x]) atomicAdd(&hist[p * RS_BINS + threadIdx.x], (unsigned long long)h[p][threadIdx.x]);
+}
+
+// digit offsets: off[p][d] = number of keys with a smaller digit in pass p
+__global__ void __launch_bounds__(RS_BINS) k_rs_offsets(const unsigned long long* __restrict__ hist,
+                                                       int np, int64_t* __restrict__ off) {
+  for (int p = 0; p < np; ++p) {
+    int64_t tot;
+    const int64_t ex = block_excl_scan<RS_BINS>((int64_t)hist[p * RS_BINS + threadIdx.x], &tot);
+    off[p * RS_BINS + threadIdx.x] = ex;
+  }
+}
+
+__device__ __forceinline__ unsigned long long rs_pack(uint32_t tag, uint32_t flag, uint32_t v) {
+  return ((unsigned long long)tag << 34) | ((unsigned long long)flag << 32) | v;
 }
 
 __global__ void __launch_bounds__(RS_NT) k_rs_scatter(const unsigned long long* __restrict__ in,
                                                      unsigned long long* __restrict__ out,
                                                      int64_t n, int shift, int bits,
                                                      const int64_t* __restrict__ off,
-                                                     int64_t nblk) {
+                                                     unsigned long long* state, int32_t* ticket,
+                                                     uint32_t tag) {
+  __shared__ int s_tile;
+  __shared__ unsigned s_hist[RS_BINS];
   __shared__ int64_t run[RS_BINS];
   __shared__ int wcnt[RS_NT / 32][RS_BINS];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  if (tid == 0) s_tile = atomicAdd(ticket, 1);
+  s_hist[tid] = 0u;
+  __syncthreads();
+  const int64_t tile = s_tile;
+  const int64_t t0 = tile * RS_TILE;
   const unsigned mask = (1u << bits) - 1u;
-  run[tid] = off[(int64_t)tid * nblk + blockIdx.x];
-  const int64_t t0 = (int64_t)blockIdx.x * RS_TILE;
+  // keys of this tile, round r holds items t0 + r*NT + tid
+  unsigned long long key[RS_ROUNDS];
+  int dig[RS_ROUNDS];
+#pragma unroll
   for (int r = 0; r < RS_ROUNDS; ++r) {
     const int64_t i = t0 + r * RS_NT + tid;
+    key[r] = i < n ? in[i] : 0ull;
+    dig[r] = i < n ? (int)((unsigned)(key[r] >> shift) & mask) : RS_BINS + lane;  // invalid: unique
+    const unsigned peers = __match_any_sync(FM, dig[r]);
+    if (i < n && __popc(peers & ((1u << lane) - 1u)) == 0) atomicAdd(&s_hist[dig[r]], __popc(peers));
+  }
+  __syncthreads();
+  // publish this tile's count of digit tid, look back for earlier tiles' counts
+  {
+    volatile unsigned long long* st = state;
+    const unsigned c = s_hist[tid];
+    int64_t excl = 0;
+    if (tile == 0) {
+      st[tid] = rs_pack(tag, ST_INC, c);
+    } else {
+      st[tile * RS_BINS + tid] = rs_pack(tag, ST_AGG, c);
+      for (int64_t j = tile - 1; j >= 0; --j) {
+        unsigned long long v;
+        do {
+          v = st[j * RS_BINS + tid];
+        } while ((uint32_t)(v >> 34) != tag || ((v >> 32) & 3ull) == 0ull);
+        excl += (uint32_t)v;
+        if (((v >> 32) & 3ull) == ST_INC) break;
+      }
+      st[tile * RS_BINS + tid] = rs_pack(tag, ST_INC, (uint32_t)(excl + c));
+    }
+    run[tid] = off[tid] + excl;
+  }
+  __syncthreads();
+  for (int r = 0; r < RS_ROUNDS; ++r) {
     if (t0 + r * RS_NT >= n) break;  // uniform across the CTA
+    const int64_t i = t0 + r * RS_NT + tid;
     const bool valid = i < n;
-    const unsigned long long key = valid ? in[i] : 0ull;
-    const int dig = valid ? (int)((unsigned)(key >> shift) & mask) : (RS_BINS + lane);
-    const unsigned peers = __match_any_sync(FM, dig);
+    const unsigned peers = __match_any_sync(FM, dig[r]);
     const int intra = __popc(peers & ((1u << lane) - 1u));
 #pragma unroll
     for (int ww = 0; ww < RS_NT / 32; ++ww) wcnt[ww][tid] = 0;
     __syncthreads();
-    if (valid && intra == 0) wcnt[w][dig] = __popc(peers);
+    if (valid && intra == 0) wcnt[w][dig[r]] = __popc(peers);
     __syncthreads();
     if (valid) {
-      int64_t rank = run[dig] + intra;
-      for (int ww = 0; ww < w; ++ww) rank += wcnt[ww][dig];
-      out[rank] = key;
+      int64_t rank = run[dig[r]] + intra;
+      for (int ww = 0; ww < w; ++ww) rank += wcnt[ww][dig[r]];
+      out[rank] = key[r];
     }
     __syncthreads();
     int add = 0;
@@ -173,34 +270,51 @@ __global__ void __launch_bounds__(RS_NT) k_rs_scatter(const unsigned long long* 
   }
 }
 
+static int64_t rs_tiles(int64_t n) { return (n + RS_TILE - 1) / RS_TILE; }
+
 size_t radix_temp_bytes(int64_t n) {
-  int64_t nblk = (n + RS_TILE - 1) / RS_TILE;
-  if (nblk < 1) nblk = 1;
-  size_t hist = (size_t)nblk * RS_BINS * sizeof(int64_t);
-  return 2 * hist + scan_temp_bytes(nblk * RS_BINS) + 256;
+  const int64_t t = rs_tiles(n) > 0 ? rs_tiles(n) : 1;
+  return (size_t)RS_MAXP * RS_BINS * (8 + 8)      // hist, off
+         + 64 * sizeof(int32_t)                     // tickets
+         + (size_t)t * RS_BINS * 8 + 256;           // look-back descriptors
 }
 
 cudaError_t radix_sort_u64(unsigned long long** keys, unsigned long long** alt, int64_t n,
-                           int lo_bit, int hi_bit, void* temp, cudaStream_t s,
+                           const BitRange* ranges, int nranges, void* temp, cudaStream_t s,
                            int64_t* launches) {
-  if (n <= 1 || hi_bit <= lo_bit) return cudaSuccess;
-  int64_t nblk = (n + RS_TILE - 1) / RS_TILE;
-  int64_t* hist = (int64_t*)temp;
-  int64_t* off = hist + nblk * RS_BINS;
-  void* stemp = (void*)(off + nblk * RS_BINS);
-  for (int sh = lo_bit; sh < hi_bit; sh += 8) {
-    int bits = hi_bit - sh < 8 ? hi_bit - sh : 8;
-    k_rs_hist<<<(unsigned)nblk, RS_NT, 0, s>>>(*keys, n, sh, bits, hist, nblk);
-    ++*launches;
-    cudaError_t e = exclusive_scan_i64(hist, off, nblk * RS_BINS, stemp, nullptr, s, launches);
-    if (e != cudaSuccess) return e;
-    k_rs_scatter<<<(unsigned)nblk, RS_NT, 0, s>>>(*keys, *alt, n, sh, bits, off, nblk);
+  if (n <= 1) return cudaSuccess;
+  RsPasses P{};
+  for (int r = 0; r < nranges; ++r)
+    for (int sh = ranges[r].lo; sh < ranges[r].hi; sh += 8) {
+      if (P.np == RS_MAXP) return cudaErrorInvalidValue;
+      P.shift[P.np] = sh;
+      P.bits[P.np] = ranges[r].hi - sh < 8 ? ranges[r].hi - sh : 8;
+      ++P.np;
+    }
+  if (P.np == 0) return cudaSuccess;
+  const int64_t t = rs_tiles(n);
+  unsigned long long* hist = (unsigned long long*)temp;
+  int64_t* off = (int64_t*)(hist + RS_MAXP * RS_BINS);
+  int32_t* tickets = (int32_t*)(off + RS_MAXP * RS_BINS);
+  unsigned long long* state = (unsigned long long*)(tickets + 64);
+  cudaError_t e = cudaMemsetAsync(hist, 0, sizeof(unsigned long long) * RS_MAXP * RS_BINS, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(tickets, 0, 64 * sizeof(int32_t), s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(state, 0, sizeof(unsigned long long) * t * RS_BINS, s);
+  if (e != cudaSuccess) return e;
+  int64_t hg = t < 148 * 4 ? t : 148 * 4;
+  k_rs_hist<<<(unsigned)hg, RS_NT, 0, s>>>(*keys, n, P, hist);
+  k_rs_offsets<<<1, RS_BINS, 0, s>>>(hist, P.np, off);
+  *launches += 2;
+  for (int p = 0; p < P.np; ++p) {
+    k_rs_scatter<<<(unsigned)t, RS_NT, 0, s>>>(*keys, *alt, n, P.shift[p], P.bits[p],
+                                               off + p * RS_BINS, state, tickets + p,
+                                               (uint32_t)(p + 1));
     ++*launches;
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    unsigned long long* t = *keys;
+    unsigned long long* tmp = *keys;
     *keys = *alt;
-    *alt = t;
+    *alt = tmp;
   }
   return cudaSuccess;
 }

@@ -65,6 +65,11 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, ui
       "l"(tm), "r"(x), "r"(y), "r"(su32(bar))
       : "memory");
 }
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* tm, int x, int y) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(tm),
+               "r"(x), "r"(y)
+               : "memory");
+}
 __device__ __forceinline__ void fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
@@ -136,16 +141,20 @@ struct Smem {
   static constexpr int A_BYTES = RA * KATOMS * A_ATOM;
   static constexpr int B_STAGE = BN * 128;
   static constexpr int B_BYTES = STAGES * B_STAGE;
-  static constexpr int KEYCAP = 1024, BANDCAP = 1024;
+  static constexpr int EPI_WARPS = 8;                     // two epilogue warpgroups
+  static constexpr int KW = 128, BW = 128;                // staging slots per epilogue warp
   static constexpr int BAR_OFF = A_BYTES + B_BYTES;
   static constexpr int NBARS = 2 * STAGES + 2 + 4;
-  static constexpr int BUF_OFF = BAR_OFF + NBARS * 8 + 16;
-  static constexpr int TOTAL = BUF_OFF + (KEYCAP + BANDCAP) * 8 + 1024;  // + align slack
+  static constexpr int CNT_OFF = BAR_OFF + NBARS * 8;     // tmem slot + per-warp counts
+  static constexpr int BUF_OFF = CNT_OFF + 128;
+  static constexpr int TOTAL = BUF_OFF + EPI_WARPS * (KW + BW) * 8 + 1024;  // + align slack
 };
 
 // ------------------------------------------------------------------ kernel
+constexpr int TC_THREADS = 384;   // warps 0-3 roles, 4-11 epilogue
+
 template <int KIND, int RA, int BN, int KATOMS, int STAGES, int MODE>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(TC_THREADS, 1)
     k_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
          TcArgs args) {
   using S = Smem<RA, BN, KATOMS, STAGES>;
@@ -166,11 +175,11 @@ __global__ void __launch_bounds__(256, 1)
   uint64_t* a_empty = a_full + 1;
   uint64_t* t_full = a_full + 2;   // [2]
   uint64_t* t_empty = a_full + 4;  // [2]
-  uint32_t* tmem_slot = (uint32_t*)(bars + S::NBARS);
-  uint32_t* kcount = tmem_slot + 1;
-  uint32_t* bcount = tmem_slot + 2;
-  unsigned long long* kbuf = (unsigned long long*)(sm + S::BUF_OFF);
-  unsigned long long* bbuf = kbuf + S::KEYCAP;
+  uint32_t* tmem_slot = (uint32_t*)(sm + S::CNT_OFF);
+  uint32_t* kcount = tmem_slot + 1;                  // [EPI_WARPS]
+  uint32_t* bcount = kcount + S::EPI_WARPS;          // [EPI_WARPS]
+  unsigned long long* kbuf = (unsigned long long*)(sm + S::BUF_OFF);   // [EPI_WARPS][KW]
+  unsigned long long* bbuf = kbuf + S::EPI_WARPS * S::KW;            // [EPI_WARPS][BW]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -182,10 +191,12 @@ __global__ void __launch_bounds__(256, 1)
     mbar_init(a_empty, 1);
     mbar_init(&t_full[0], 1);
     mbar_init(&t_full[1], 1);
-    mbar_init(&t_empty[0], 4);
+    mbar_init(&t_empty[0], 4);   // the 4 warps of the group that drains buffer 0
     mbar_init(&t_empty[1], 4);
-    *kcount = 0;
-    *bcount = 0;
+    for (int w = 0; w < S::EPI_WARPS; ++w) {
+      kcount[w] = 0;
+      bcount[w] = 0;
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0 && lane == 0) {
@@ -204,9 +215,16 @@ __global__ void __launch_bounds__(256, 1)
   fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  const int64_t n_tiles = args.n_tiles;           // BN-wide landmark tiles
-  const int64_t tiles_per_chunk = args.tiles_per_chunk;
-  const int64_t n_chunks = (n_tiles + tiles_per_chunk - 1) / tiles_per_chunk;
+  // Work units = (block of RA*128 point rows, chunk of BN-wide landmark tiles),
+  // enough units to balance the grid; the column count may live on the device
+  // (fused greedy tile), so every role derives the same schedule here.
+  const int64_t n_cols = args.l_count_dev ? (int64_t)*args.l_count_dev : args.L;
+  const int64_t lpos0 = args.l_count_dev ? (int64_t)*args.l_total_dev - n_cols : 0;
+  const int64_t n_tiles = (n_cols + BN - 1) / BN;
+  int64_t n_chunks = (4 * (int64_t)gridDim.x + args.n_mblk - 1) / args.n_mblk;
+  n_chunks = max((int64_t)1, min(n_chunks, n_tiles));
+  const int64_t tiles_per_chunk = n_tiles > 0 ? (n_tiles + n_chunks - 1) / n_chunks : 1;
+  n_chunks = n_tiles > 0 ? (n_tiles + tiles_per_chunk - 1) / tiles_per_chunk : 0;
   const int64_t n_units = args.n_mblk * n_chunks;
 
   if (warp == 0) {
@@ -228,6 +246,13 @@ __global__ void __launch_bounds__(256, 1)
           for (int ka = 0; ka < KATOMS; ++ka)
             tma_load_2d(sA + (r * KATOMS + ka) * S::A_ATOM, &tmA, a_full, ka * ATOM_ELEMS,
                         (int)(mb * RA * 128 + r * 128));
+        // warm L2 with the next unit's point block while this one computes
+        const int64_t un = u + gridDim.x;
+        if (un < n_units && un / n_chunks != mb) {
+          for (int r = 0; r < RA; ++r)
+            for (int ka = 0; ka < KATOMS; ++ka)
+              tma_prefetch_2d(&tmA, ka * ATOM_ELEMS, (int)((un / n_chunks) * RA * 128 + r * 128));
+        }
         for (int64_t t = t0; t < t1; ++t) {
           for (int ka = 0; ka < KATOMS; ++ka) {
             mbar_wait(&empty[stage], phase ^ 1u);
@@ -288,10 +313,54 @@ __global__ void __launch_bounds__(256, 1)
       }
     }
   } else if (warp >= 4) {
-    // ---------------- epilogue (warps 4..7 -> TMEM lane quarters 0..3)
-    const int q = warp & 3;
-    uint32_t use[2] = {0u, 0u};
-    int buf = 0;
+    // ---------------- epilogue: warps 4-7 drain TMEM buffer 0, warps 8-11
+    // buffer 1 (tiles alternate buffers), warp w reads TMEM lanes 32*(w%4)..
+    const int ew = warp - 4, grp = ew >> 2, q = warp & 3;
+    unsigned long long* kb = kbuf + ew * S::KW;
+    unsigned long long* bb = bbuf + ew * S::BW;
+    uint32_t* kc = kcount + ew;
+    uint32_t* bc = bcount + ew;
+    // flush this warp's staged keys / band pairs to global (warp-collective)
+    auto flush = [&](void) {
+      __syncwarp();
+      const uint32_t kn = min(*kc, (uint32_t)S::KW), bn = min(*bc, (uint32_t)S::BW);
+      unsigned long long g0 = 0, g1 = 0;
+      if (lane == 0) {
+        if (kn) g0 = atomicAdd(args.key_count, (unsigned long long)kn);
+        if (bn) g1 = atomicAdd(args.band_count, (unsigned long long)bn);
+      }
+      g0 = __shfl_sync(FULLM, g0, 0);
+      g1 = __shfl_sync(FULLM, g1, 0);
+      for (uint32_t i = lane; i < kn; i += 32)
+        if ((int64_t)(g0 + i) < args.key_cap) args.keys[g0 + i] = kb[i];
+      for (uint32_t i = lane; i < bn; i += 32)
+        if ((int64_t)(g1 + i) < args.band_cap) args.band[g1 + i] = bb[i];
+      __syncwarp();
+      if (lane == 0) {
+        *kc = 0;
+        *bc = 0;
+      }
+      __syncwarp();
+    };
+    // append one pair (cls 1: in -> key; cls 2: band -> queue); beyond the
+    // staging capacity it goes straight to global memory
+    auto append = [&](int cls, unsigned long long key) {
+      uint32_t* cnt = cls == 1 ? kc : bc;
+      unsigned long long* buf_s = cls == 1 ? kb : bb;
+      const uint32_t cap = cls == 1 ? S::KW : S::BW;
+      const uint32_t k = atomicAdd(cnt, 1u);
+      if (k < cap) {
+        buf_s[k] = key;
+      } else {
+        unsigned long long* gcnt = cls == 1 ? args.key_count : args.band_count;
+        unsigned long long* gbuf = cls == 1 ? args.keys : args.band;
+        const int64_t gcap = cls == 1 ? args.key_cap : args.band_cap;
+        const unsigned long long g = atomicAdd(gcnt, 1ull);
+        if ((int64_t)g < gcap) gbuf[g] = key;
+      }
+    };
+    uint32_t phase = 0;
+    int64_t tcount = 0;   // tiles seen, in the MMA issuer's order (buffer = tcount & 1)
     for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
       const int64_t mb = u / n_chunks, ch = u % n_chunks;
       const int64_t t0 = ch * tiles_per_chunk, t1 = min(n_tiles, t0 + tiles_per_chunk);
@@ -308,9 +377,11 @@ __global__ void __launch_bounds__(256, 1)
           rint[r] = args.row_r[prow[r]];
         }
       }
-      for (int64_t t = t0; t < t1; ++t) {
-        mbar_wait(&t_full[buf], use[buf] & 1u);
-        ++use[buf];
+      for (int64_t t = t0; t < t1; ++t, ++tcount) {
+        const int buf = (int)(tcount & 1);
+        if (buf != grp) continue;
+        mbar_wait(&t_full[buf], phase);
+        phase ^= 1u;
         fence_after();
 #pragma unroll
         for (int r = 0; r < RA; ++r) {
@@ -325,10 +396,11 @@ __global__ void __launch_bounds__(256, 1)
               if (prow[r] < args.n) {
 #pragma unroll
                 for (int i = 0; i < 32; ++i)
-                  if (j0 + i < args.L) args.gram[prow[r] * args.L + j0 + i] = v[i];
+                  if (j0 + i < n_cols) args.gram[prow[r] * n_cols + j0 + i] = v[i];
               }
               continue;
             }
+            // fast path: one compare per 32 pairs decides "all out"
             bool surv;
             if constexpr (KIND == TC_TF32) {
               const float4* cb = reinterpret_cast<const float4*>(args.col_b + j0);
@@ -356,71 +428,45 @@ __global__ void __launch_bounds__(256, 1)
               surv = m > rint[r];
             }
             if (__any_sync(FULLM, surv)) {
-              // rare path: classify the surviving columns of this lane
+              // rare path: column masks of candidates (not certainly out) and
+              // certain-in pairs, then one append per set bit
+              uint32_t cand = 0u, inm = 0u;
               if (surv) {
 #pragma unroll
                 for (int i = 0; i < 32; ++i) {
-                  const int64_t j = j0 + i;
-                  int cls = 0;  // 0 out, 1 in, 2 band
                   if constexpr (KIND == TC_TF32) {
                     const float a = __uint_as_float(v[i]);
-                    if (a - args.col_b[j] > rlo[r]) cls = (a - args.col_a[j] > rhi[r]) ? 1 : 2;
+                    cand |= (a - __ldg(args.col_b + j0 + i) > rlo[r] ? 1u : 0u) << i;
+                    inm |= (a - __ldg(args.col_a + j0 + i) > rhi[r] ? 1u : 0u) << i;
                   } else {
-                    cls = (2 * (int)v[i] - args.col_c[j] > rint[r]) ? 1 : 0;
-                  }
-                  if (cls == 0) continue;
-                  const unsigned long long key =
-                      cls == 1 ? (((unsigned long long)prow[r] << args.lbits) |
-                                  (unsigned long long)j)
-                               : (((unsigned long long)prow[r] << 32) | (unsigned long long)j);
-                  uint32_t* cnt = cls == 1 ? kcount : bcount;
-                  unsigned long long* buf_s = cls == 1 ? kbuf : bbuf;
-                  const uint32_t cap = cls == 1 ? S::KEYCAP : S::BANDCAP;
-                  const uint32_t k = atomicAdd(cnt, 1u);
-                  if (k < cap) {
-                    buf_s[k] = key;
-                  } else {
-                    unsigned long long* gcnt = cls == 1 ? args.key_count : args.band_count;
-                    unsigned long long* gbuf = cls == 1 ? args.keys : args.band;
-                    const int64_t gcap = cls == 1 ? args.key_cap : args.band_cap;
-                    const unsigned long long g = atomicAdd(gcnt, 1ull);
-                    if ((int64_t)g < gcap) gbuf[g] = key;
+                    cand |= (2 * (int)v[i] - __ldg(args.col_c + j0 + i) > rint[r] ? 1u : 0u) << i;
                   }
                 }
+                if constexpr (KIND != TC_TF32) inm = cand;
               }
+              while (cand) {
+                const int i = __ffs(cand) - 1;
+                cand &= cand - 1u;
+                const int64_t j = j0 + i;
+                if ((inm >> i) & 1u) {
+                  if (args.covered) args.covered[prow[r]] = 1;
+                  append(1, ((unsigned long long)prow[r] << args.lbits) |
+                                (unsigned long long)(lpos0 + j));
+                } else {
+                  append(2, ((unsigned long long)prow[r] << 32) | (unsigned long long)j);
+                }
+              }
+              __syncwarp();
+              if (*kc > S::KW / 2 || *bc > S::BW / 2) flush();
             }
           }
         }
         fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&t_empty[buf]);
-        buf ^= 1;
-        // flush the shared staging buffers when half full (epilogue warps only)
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        const uint32_t kc = *kcount, bc = *bcount;
-        const bool last = (t + 1 == t1) && (u + gridDim.x >= n_units);
-        if (kc > S::KEYCAP / 2 || bc > S::BANDCAP / 2 || last) {
-          __shared__ unsigned long long gbase[2];
-          const int et = threadIdx.x - 128;
-          const uint32_t kn = min(kc, (uint32_t)S::KEYCAP), bn = min(bc, (uint32_t)S::BANDCAP);
-          if (et == 0) {
-            gbase[0] = kn ? atomicAdd(args.key_count, (unsigned long long)kn) : 0ull;
-            gbase[1] = bn ? atomicAdd(args.band_count, (unsigned long long)bn) : 0ull;
-          }
-          asm volatile("bar.sync 1, 128;" ::: "memory");
-          for (uint32_t i = et; i < kn; i += 128)
-            if ((int64_t)(gbase[0] + i) < args.key_cap) args.keys[gbase[0] + i] = kbuf[i];
-          for (uint32_t i = et; i < bn; i += 128)
-            if ((int64_t)(gbase[1] + i) < args.band_cap) args.band[gbase[1] + i] = bbuf[i];
-          asm volatile("bar.sync 1, 128;" ::: "memory");
-          if (et == 0) {
-            *kcount = 0;
-            *bcount = 0;
-          }
-        }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
       }
     }
+    flush();
   }
   fence_before();
   __syncthreads();
@@ -478,17 +524,17 @@ static cudaError_t launch_cfg(const TcPlan& P, TcArgs a, cudaStream_t s) {
   auto kern = k_tc<KIND, RA, BN, KATOMS, STAGES, MODE>;
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::TOTAL);
   if (e != cudaSuccess) return e;
-  a.n_tiles = P.l_rows / BN;
   a.n_mblk = (P.n_rows + RA * 128 - 1) / (RA * 128);
-  // work units: (m-block, chunk of landmark tiles); enough units to balance 148 SMs
-  int64_t chunks = (4 * P.num_sms + a.n_mblk - 1) / a.n_mblk;
-  if (chunks < 1) chunks = 1;
-  if (chunks > a.n_tiles) chunks = a.n_tiles;
-  a.tiles_per_chunk = (a.n_tiles + chunks - 1) / chunks;
-  chunks = (a.n_tiles + a.tiles_per_chunk - 1) / a.tiles_per_chunk;
-  int64_t units = a.n_mblk * chunks;
-  int grid = (int)(units < P.num_sms ? units : P.num_sms);
-  kern<<<grid, 256, S::TOTAL, s>>>(tA, tB, a);
+  // persistent grid: one CTA per SM (the schedule is derived on the device)
+  int64_t grid = P.num_sms;
+  if (!a.l_count_dev) {
+    const int64_t n_tiles = (a.L + BN - 1) / BN;
+    int64_t chunks = (4 * grid + a.n_mblk - 1) / a.n_mblk;
+    chunks = chunks < 1 ? 1 : (chunks > n_tiles ? n_tiles : chunks);
+    if (a.n_mblk * chunks < grid) grid = a.n_mblk * chunks;
+  }
+  if (grid < 1) grid = 1;
+  kern<<<(unsigned)grid, TC_THREADS, S::TOTAL, s>>>(tA, tB, a);
   return cudaGetLastError();
 }
 
@@ -675,6 +721,124 @@ __global__ void k_tc_recheck(const unsigned long long* __restrict__ band, int64_
       if ((int64_t)k < key_cap) keys[k] = ((unsigned long long)p << lbits) | (unsigned long long)j;
     }
   }
+}
+
+// Fused greedy tile: landmark operand rows + column constants for the tile's
+// new landmarks (count on the device); columns >= count are inert.
+__global__ void k_tc_tile_lm(const uint8_t* __restrict__ xop, int64_t row_bytes,
+                             const int32_t* __restrict__ new_lm,
+                             const int32_t* __restrict__ l_count_dev, int kind,
+                             const void* __restrict__ nrm, double C2, uint8_t* __restrict__ lop,
+                             float* __restrict__ ca, float* __restrict__ cb,
+                             int32_t* __restrict__ cc) {
+  const int64_t j = blockIdx.x;
+  const int64_t cnt = *l_count_dev;
+  const bool live = j < cnt;
+  const int32_t pt = live ? new_lm[j] : 0;
+  const uint4* src = reinterpret_cast<const uint4*>(xop + (int64_t)pt * row_bytes);
+  uint4* dst = reinterpret_cast<uint4*>(lop + j * row_bytes);
+  for (int64_t i = threadIdx.x; i < row_bytes / 16; i += blockDim.x)
+    dst[i] = live ? src[i] : make_uint4(0, 0, 0, 0);
+  if (threadIdx.x == 0) {
+    if (kind == TC_TF32) {
+      if (live) {
+        const double nl = ((const double*)nrm)[pt];
+        ca[j] = __double2float_ru(0.5 * nl + C2 * nl);
+        cb[j] = __double2float_rd(0.5 * nl - C2 * nl);
+      } else {
+        ca[j] = INFINITY;
+        cb[j] = INFINITY;
+      }
+    } else {
+      cc[j] = live ? ((const int32_t*)nrm)[pt] : (1 << 30);
+    }
+  }
+}
+
+cudaError_t launch_tc_tile_landmarks(const TcPlan& P, const void* nrm, const int32_t* new_lm,
+                                     const int32_t* l_count_dev, double C2, TcArgs& a,
+                                     cudaStream_t s, int64_t* launches) {
+  ++*launches;
+  k_tc_tile_lm<<<(unsigned)P.l_rows, 64, 0, s>>>(
+      (const uint8_t*)P.xop, P.row_bytes, new_lm, l_count_dev, P.kind, nrm, C2,
+      (uint8_t*)P.lop, (float*)a.col_a, (float*)a.col_b, (int32_t*)a.col_c);
+  return cudaGetLastError();
+}
+
+// B' for a fused greedy tile: grid-stride over the device-side band count;
+// in-ball pairs join the keys and mark coverage.
+__global__ void k_tc_recheck_tile(const unsigned long long* __restrict__ band,
+                                  const unsigned long long* __restrict__ band_count,
+                                  int64_t band_cap, const float* __restrict__ X, int xstride,
+                                  int d, const int32_t* __restrict__ lm,
+                                  const int32_t* __restrict__ l_count_dev,
+                                  const int32_t* __restrict__ l_total_dev, double eps,
+                                  double eps2, double tie_rel, unsigned long long* keys,
+                                  unsigned long long* key_count, int64_t key_cap,
+                                  uint8_t* covered, int64_t* ties, int64_t tie_cap,
+                                  DevStats* stats) {
+  const int64_t nb = min((int64_t)*band_count, band_cap);
+  const int64_t lpos0 = (int64_t)*l_total_dev - (int64_t)*l_count_dev;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < nb; base += stride) {
+    const int64_t i = base + threadIdx.x;
+    bool in = false;
+    int64_t p = 0, j = 0;
+    if (i < nb) {
+      p = (int64_t)(band[i] >> 32);
+      j = (int64_t)(band[i] & 0xffffffffull);
+      const int64_t q = lm[j];
+      const float* x = X + p * (int64_t)xstride;
+      const float* y = X + q * (int64_t)xstride;
+      double sacc = 0.0;
+      for (int k = 0; k < d; ++k) {
+        double t = __dsub_rn((double)x[k], (double)y[k]);
+        sacc = __dadd_rn(sacc, __dmul_rn(t, t));
+      }
+      in = sacc < eps2;
+      const double dist = __dsqrt_rn(sacc);
+      if (fabs(dist - eps) <= tie_rel * eps) {
+        unsigned long long k = atomicAdd(&stats->near_ties, 1ull);
+        if ((int64_t)k < tie_cap && ties) {
+          ties[3 * k] = p;
+          ties[3 * k + 1] = q;
+          ties[3 * k + 2] = in ? 1 : 0;
+        }
+      }
+      if (in) covered[p] = 1;
+    }
+    const unsigned m = __ballot_sync(FULLM, in);
+    if (m) {
+      const int lane = threadIdx.x & 31;
+      unsigned long long b = 0;
+      if (lane == 0) b = atomicAdd(key_count, (unsigned long long)__popc(m));
+      b = __shfl_sync(FULLM, b, 0);
+      if (in) {
+        const unsigned long long k = b + __popc(m & ((1u << lane) - 1u));
+        if ((int64_t)k < key_cap) keys[k] = ((unsigned long long)p << 32) | (unsigned long long)(lpos0 + j);
+      }
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    atomicAdd(&stats->band_pairs, (unsigned long long)nb);
+    if ((int64_t)*band_count > band_cap) stats->overflow = 1;
+  }
+}
+
+cudaError_t launch_tc_recheck_tile(const unsigned long long* band,
+                                   const unsigned long long* band_count, int64_t band_cap,
+                                   const float* X, int xstride, int d, const int32_t* lm,
+                                   const int32_t* l_count_dev, const int32_t* l_total_dev,
+                                   const Thresh& th, unsigned long long* keys,
+                                   unsigned long long* key_count, int64_t key_cap,
+                                   uint8_t* covered, int64_t* ties, int64_t tie_cap,
+                                   DevStats* stats, int num_sms, cudaStream_t s,
+                                   int64_t* launches) {
+  ++*launches;
+  k_tc_recheck_tile<<<(unsigned)(2 * num_sms), 256, 0, s>>>(
+      band, band_count, band_cap, X, xstride, d, lm, l_count_dev, l_total_dev, th.eps, th.eps2,
+      th.tie_rel, keys, key_count, key_cap, covered, ties, tie_cap, stats);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_tc_prep(const void* X, int dtype, int64_t n, int d, const TcPlan& P,

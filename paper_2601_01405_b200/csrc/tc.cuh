@@ -26,10 +26,12 @@ struct TcPlan {
 };
 
 struct TcArgs {
-  int64_t n, L;
-  int64_t n_tiles, n_mblk, tiles_per_chunk;  // filled by the launcher
+  int64_t n, L;                              // L: landmark columns (host value)
+  const int32_t* l_count_dev;                // if non-null: columns = *l_count_dev (fused tile)
+  const int32_t* l_total_dev;                // fused tile: position base = *l_total_dev - columns
+  int64_t n_mblk;                            // filled by the launcher
   int ksteps;                                // 32-byte K steps to issue
-  int lbits;
+  int lbits;                                 // key = point << lbits | landmark position
   // per-row / per-column constants
   const float* row_lo;
   const float* row_hi;
@@ -45,6 +47,7 @@ struct TcArgs {
   unsigned long long* band_count;
   int64_t band_cap;
   uint32_t* gram;      // debug: raw accumulators [n][L]
+  uint8_t* covered;    // fused greedy: covered[p] = 1 for every in-ball pair (may be null)
 };
 
 int tc_bn_for(int kind, int katoms);
@@ -58,6 +61,23 @@ cudaError_t launch_tc_rows(const TcPlan& P, const void* nrm, int64_t n, double C
                            int64_t* launches);
 cudaError_t launch_tc_landmarks(const TcPlan& P, const void* nrm, const int32_t* lm, int64_t L,
                                 double C2, TcArgs& a, cudaStream_t s, int64_t* launches);
+// Fused greedy tile: gather the *l_count_dev new landmarks' operand rows into
+// P.lop (rows up to P.l_rows zero-filled) and their column constants.
+cudaError_t launch_tc_tile_landmarks(const TcPlan& P, const void* nrm, const int32_t* new_lm,
+                                     const int32_t* l_count_dev, double C2, TcArgs& a,
+                                     cudaStream_t s, int64_t* launches);
+// Band recheck with a device-side pair count (persistent grid-stride), for the
+// fused greedy tile: band keys are (p << 32 | tile column), lm = the tile's
+// landmark point indices, positions = *l_total_dev - *l_count_dev + column.
+cudaError_t launch_tc_recheck_tile(const unsigned long long* band,
+                                   const unsigned long long* band_count, int64_t band_cap,
+                                   const float* X, int xstride, int d, const int32_t* lm,
+                                   const int32_t* l_count_dev, const int32_t* l_total_dev,
+                                   const Thresh& th, unsigned long long* keys,
+                                   unsigned long long* key_count, int64_t key_cap,
+                                   uint8_t* covered, int64_t* ties, int64_t tie_cap,
+                                   DevStats* stats, int num_sms, cudaStream_t s,
+                                   int64_t* launches);
 cudaError_t launch_tc(const TcPlan& P, const TcArgs& a, cudaStream_t s, int64_t* launches);
 cudaError_t launch_tc_recheck(const unsigned long long* band, int64_t nb, const float* X,
                               int xstride, int d, const int32_t* lm, const Thresh& th, int lbits,
