@@ -213,6 +213,14 @@ bm_status bm_debug_resolve_tile(const uint32_t *adj, int32_t nc, uint8_t *lm_out
 bm_status bm_debug_tc_gram(const void *points, bm_dtype dtype, int64_t n, int32_t d,
                            const int32_t *lm, int64_t L, uint32_t *out, void *stream);
 
+/* Timing probe of the tcgen05 contraction (step B) for fp32 data with d <= 64:
+ * n points (DEVICE pointer, row-major) against the first L of them, with an
+ * epilogue that classifies (mode 0: the membership epilogue, every pair out),
+ * only reads the accumulators (mode 2) or releases them unread (mode 3).
+ * *ms_out (HOST) receives the mean launch time over `iters` launches. */
+bm_status bm_debug_tc_probe(const float *points, int64_t n, int32_t d, int64_t L, int32_t mode,
+                            int32_t iters, float *ms_out, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -26,7 +26,8 @@ STEPS = ("prep", "greedy", "member", "csr", "edges", "total", "member_kernel")
 
 EXPORTED = ("bm_cover_build", "bm_cover_build_ex", "bm_cover_build_host", "bm_free",
             "bm_last_error", "bm_version", "bm_trim_memory", "bm_debug_radix_sort_u64",
-            "bm_debug_exclusive_scan_i64", "bm_debug_resolve_tile", "bm_debug_tc_gram")
+            "bm_debug_exclusive_scan_i64", "bm_debug_resolve_tile", "bm_debug_tc_gram",
+            "bm_debug_tc_probe")
 
 
 class BMError(RuntimeError):
@@ -95,6 +96,8 @@ def load() -> ctypes.CDLL:
     lib.bm_debug_resolve_tile.restype = i32
     lib.bm_debug_tc_gram.argtypes = [vp, i32, i64, i32, vp, i64, vp, vp]
     lib.bm_debug_tc_gram.restype = i32
+    lib.bm_debug_tc_probe.argtypes = [vp, i64, i32, i64, i32, i32, ctypes.POINTER(ctypes.c_float), vp]
+    lib.bm_debug_tc_probe.restype = i32
     _lib = lib
     return lib
 
@@ -332,3 +335,16 @@ def tc_gram(points, landmarks):
 def trim_memory():
     """Return the library's cached device memory (its stream-ordered pool) to the system."""
     _check(load().bm_trim_memory())
+
+
+def tc_probe(points, L: int, mode: int, iters: int = 10) -> float:
+    """Mean launch time (ms) of the tcgen05 contraction with a probe epilogue
+    (diagnostic entry point bm_debug_tc_probe)."""
+    import torch
+    assert points.is_cuda and points.dtype == torch.float32 and points.is_contiguous()
+    ms = ctypes.c_float(0.0)
+    n, d = points.shape
+    _check(load().bm_debug_tc_probe(ctypes.c_void_p(points.data_ptr()), n, d, int(L), int(mode),
+                                    int(iters), ctypes.byref(ms),
+                                    ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    return float(ms.value)

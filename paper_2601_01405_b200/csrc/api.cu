@@ -198,11 +198,14 @@ int64_t initial_key_cap(int64_t n) {
 // |x||l|, c1 = operand rounding to tf32 (2u_t + u_t^2) + fp32 accumulation
 // (4 K 2^-23, safety 2); the epilogue's roundings add 2^-22; |x||l| <=
 // (n_p + n_l)/2, and 1.25 is a further safety factor.
+// The column constant cb_j (|cb_j| <= n_l/2) is folded into the MMA as three
+// more exact products, adding c3 |cb_j| with c3 = 4 (K+3) 2^-23 (1.001).
 double tc_band_c2(int ksteps) {
   const double ut = ldexp(1.0, -11);
-  const double K = 8.0 * ksteps;
+  const double K = 8.0 * ksteps + 3.0;
   const double c1 = 2.0 * ut + ut * ut + 4.0 * K * ldexp(1.0, -23) * (1.0 + ut) * (1.0 + ut);
-  return 1.25 * 0.5 * (c1 + ldexp(1.0, -22));
+  const double c3 = 4.0 * K * ldexp(1.0, -23) * 1.001;
+  return 1.25 * 0.5 * (c1 + c3 + ldexp(1.0, -22));
 }
 
 __global__ void k_iota(int32_t* a, int64_t n) {
@@ -227,6 +230,18 @@ struct Timer {
     if (on) cudaEventRecord(ev[i], s);
   }
 };
+
+// tf32 column-constant fold operands: B constants [l_rows][8] and the A ones tile.
+bm_status alloc_fold(Pool& pool, bm::tc::TcPlan& P, bm::tc::TcArgs& ta, cudaStream_t s,
+                     int64_t* launches) {
+  float *colk = nullptr, *ones = nullptr;
+  TRY(pool.alloc(&colk, (size_t)P.l_rows * 8));
+  TRY(pool.alloc(&ones, (size_t)128 * 8));
+  CK(bm::tc::launch_tc_ones(ones, s, launches));
+  ta.colk = colk;
+  P.ones = ones;
+  return BM_OK;
+}
 
 // Step B over all n points x all L landmarks in one pass (used only when the
 // fused loop's key buffer overflowed: M is then known exactly and `keys` has
@@ -262,6 +277,7 @@ bm_status membership_full(Pool& pool, int kind, const bm::PairArgs& base, bm::tc
       ta.row_hi = rhi;
       ta.col_a = ca;
       ta.col_b = cb;
+      TRY(alloc_fold(pool, P, ta, s, launches));
       tau = 1.0000005e-6 * th.eps2 + th.eps2 * ldexp(1.0, -21);
     } else {
       int32_t *rr, *cc;
@@ -490,6 +506,7 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
       ta.row_hi = rhi;
       ta.col_a = ca;
       ta.col_b = cb;
+      TRY(alloc_fold(pool, P, ta, s, &launches));
       C2 = tc_band_c2(ta.ksteps);
       tau = 1.0000005e-6 * th.eps2 + th.eps2 * ldexp(1.0, -21);
       band_cap = o.band_cap > 0 ? (int64_t)o.band_cap : (n * 4 > (1 << 22) ? n * 4 : (1 << 22));
@@ -938,10 +955,89 @@ bm_status bm_debug_tc_gram(const void* points, bm_dtype dtype, int64_t n, int32_
   ta.col_a = fa;
   ta.col_b = fb;
   ta.col_c = (const int32_t*)fa;
+  TRY(alloc_fold(pool, P, ta, s, &launches));
   CK(tc::launch_tc_landmarks(P, nrm, lm, L, 0.0, ta, s, &launches));
   ta.gram = out;
   CK(tc::launch_tc(P, ta, s, &launches));
   CK(cudaStreamSynchronize(s));
+  return BM_OK;
+}
+
+bm_status bm_debug_tc_probe(const float* points, int64_t n, int32_t d, int64_t L, int32_t mode,
+                            int32_t iters, float* ms_out, void* stream) {
+  using namespace bm;
+  if (!points || !ms_out || n < 1 || d < 1 || L < 1 || L > n || iters < 1)
+    return set_err(BM_EINVAL, "bad arguments");
+  cudaStream_t s = (cudaStream_t)stream;
+  tc::TcPlan P{};
+  P.kind = tc::TC_TF32;
+  P.row_bytes = (((int64_t)d * 4 + 15) / 16) * 16;
+  P.k_elems = P.row_bytes / 4;
+  P.katoms = (int)((P.row_bytes + 127) / 128);
+  if (P.katoms > 2) return set_err(BM_EUNSUPPORTED, "probe: d <= 64 only");
+  Pool pool(s);
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&P.num_sms, cudaDevAttrMultiProcessorCount, dev));
+  uint8_t* xop = nullptr;
+  double* nrm = nullptr;
+  DevStats* stats = nullptr;
+  int32_t* lm = nullptr;
+  TRY(pool.alloc(&xop, (size_t)n * P.row_bytes));
+  TRY(pool.alloc(&nrm, (size_t)n));
+  TRY(pool.alloc(&stats, 1));
+  TRY(pool.alloc(&lm, (size_t)L));
+  CK(cudaMemsetAsync(stats, 0, sizeof(DevStats), s));
+  P.xop = xop;
+  P.n_rows = n;
+  int64_t launches = 0;
+  CK(tc::launch_tc_prep(points, BM_F32, n, d, P, nrm, stats, s, &launches));
+  k_iota<<<(unsigned)((L + 255) / 256), 256, 0, s>>>(lm, L);
+  const int BN = tc::tc_bn_for(P.kind, P.katoms), RB = tc::tc_rows_for(P.kind, P.katoms);
+  P.l_rows = ((L + BN - 1) / BN) * BN;
+  P.n_pad = ((n + RB - 1) / RB) * RB;
+  TRY(pool.alloc((uint8_t**)&P.lop, (size_t)P.l_rows * P.row_bytes));
+  tc::TcArgs ta{};
+  ta.n = n;
+  ta.L = L;
+  ta.ksteps = (int)(((int64_t)d * 4 + 31) / 32);
+  ta.lbits = 32;
+  float *rlo, *rhi, *ca, *cb;
+  TRY(pool.alloc(&rlo, (size_t)P.n_pad));
+  TRY(pool.alloc(&rhi, (size_t)P.n_pad));
+  TRY(pool.alloc(&ca, (size_t)P.l_rows));
+  TRY(pool.alloc(&cb, (size_t)P.l_rows));
+  ta.row_lo = rlo;
+  ta.row_hi = rhi;
+  ta.col_a = ca;
+  ta.col_b = cb;
+  TRY(alloc_fold(pool, P, ta, s, &launches));
+  // eps tiny: every pair is certainly out, the epilogue takes its fast path only
+  CK(tc::launch_tc_rows(P, nrm, n, tc_band_c2(ta.ksteps), 1e-30, 0.0, 0, ta, s, &launches));
+  CK(tc::launch_tc_landmarks(P, nrm, lm, L, tc_band_c2(ta.ksteps), ta, s, &launches));
+  unsigned long long *keys = nullptr, *kc = nullptr;
+  TRY(pool.alloc(&keys, 1024));
+  TRY(pool.alloc(&kc, 2));
+  CK(cudaMemsetAsync(kc, 0, 16, s));
+  ta.keys = keys;
+  ta.key_count = kc;
+  ta.key_cap = 1024;
+  ta.band = keys;
+  ta.band_count = kc + 1;
+  ta.band_cap = 1024;
+  CK(tc::launch_tc_probe(P, ta, mode, s));   // warm-up
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0, s));
+  for (int i = 0; i < iters; ++i) CK(tc::launch_tc_probe(P, ta, mode, s));
+  CK(cudaEventRecord(e1, s));
+  CK(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  *ms_out = ms / iters;
   return BM_OK;
 }
 

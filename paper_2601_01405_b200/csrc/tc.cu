@@ -32,6 +32,40 @@ namespace tc {
 
 constexpr unsigned FULLM = 0xffffffffu;
 
+// Column constants of landmark j: cb_j =
+// round_down(n_l/2 - C2 n_l) folded into the MMA as the exact tf32 split
+// -cb = -(hi + mid + lo); d_j = round_up(n_l/2 + C2 n_l - cb_j) for the in-test.
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t t;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(t) : "f"(x));
+  return __uint_as_float(t);
+}
+__device__ __forceinline__ void tc_col_consts(double nl, double C2, int64_t j, float* ca,
+                                              float* cb, float* colk) {
+  const float c = __double2float_rd(0.5 * nl - C2 * nl);
+  const float hi = tf32_rna(c);
+  const float r1 = c - hi;              // exact
+  const float mid = tf32_rna(r1);
+  const float lo = r1 - mid;            // exact, <= 3 significant bits
+  cb[j] = c;
+  ca[j] = __double2float_ru(0.5 * nl + C2 * nl - (double)c);
+  float* k = colk + j * 8;
+  k[0] = -hi;
+  k[1] = -mid;
+  k[2] = -lo;
+#pragma unroll
+  for (int i = 3; i < 8; ++i) k[i] = 0.f;
+}
+__device__ __forceinline__ void tc_col_inert(int64_t j, float* ca, float* cb, float* colk) {
+  // padding column: acc' = 0 - 1e30 never exceeds a row threshold
+  cb[j] = INFINITY;
+  ca[j] = INFINITY;
+  float* k = colk + j * 8;
+  k[0] = -1e30f;
+#pragma unroll
+  for (int i = 1; i < 8; ++i) k[i] = 0.f;
+}
+
 __device__ __forceinline__ uint32_t su32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
@@ -63,6 +97,15 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, ui
       "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%2, %3}], [%4];" ::"r"(su32(dst)),
       "l"(tm), "r"(x), "r"(y), "r"(su32(bar))
+      : "memory");
+}
+// 1-D bulk copy global -> shared, completion counted on an mbarrier
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes,
+                                          uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(su32(dst)),
+      "l"(src), "r"(bytes), "r"(su32(bar))
       : "memory");
 }
 __device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* tm, int x, int y) {
@@ -98,6 +141,34 @@ __device__ __forceinline__ void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t
         : "memory");
   }
 }
+// tcgen05.ld without the wait; the registers are valid only after tmem_wait(v)
+__device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, "
+      "%28, %29, %30, %31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+        "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
+        "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+        "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
+        "=r"(v[31])
+      : "r"(taddr)
+      : "memory");
+}
+// tcgen05.wait::ld, with v as in/out operands so no use of v moves above it
+__device__ __forceinline__ void tmem_wait(uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.wait::ld.sync.aligned;"
+      : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]),
+        "+r"(v[7]), "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]), "+r"(v[12]),
+        "+r"(v[13]), "+r"(v[14]), "+r"(v[15]), "+r"(v[16]), "+r"(v[17]), "+r"(v[18]),
+        "+r"(v[19]), "+r"(v[20]), "+r"(v[21]), "+r"(v[22]), "+r"(v[23]), "+r"(v[24]),
+        "+r"(v[25]), "+r"(v[26]), "+r"(v[27]), "+r"(v[28]), "+r"(v[29]), "+r"(v[30]),
+        "+r"(v[31])
+      :
+      : "memory");
+}
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
@@ -125,6 +196,18 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
   return d;
 }
 
+// Shared-memory matrix descriptor: K-major, 32-byte swizzle (one 8-element
+// tf32 K step per row), 8-row groups 256 B apart.
+__device__ __forceinline__ uint64_t sdesc32(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)1u << 16;
+  d |= (uint64_t)(256u >> 4) << 32;
+  d |= (uint64_t)1u << 46;
+  d |= (uint64_t)6u << 61;
+  return d;
+}
+
 template <int KIND>
 constexpr uint32_t make_idesc(int M, int N) {
   // c_format [4,6): 1 = F32, 2 = S32; a/b format [7,10)/[10,13): TF32 = 2,
@@ -135,16 +218,23 @@ constexpr uint32_t make_idesc(int M, int N) {
          ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
-template <int RA, int BN, int KATOMS, int STAGES>
+template <int RA, int BN, int KATOMS, int STAGES, int ABUF, bool FOLD>
 struct Smem {
   static constexpr int A_ATOM = 128 * 128;                 // 128 rows x 128 B
-  static constexpr int A_BYTES = RA * KATOMS * A_ATOM;
+  static constexpr int A_BYTES = RA * KATOMS * A_ATOM;     // one A buffer
   static constexpr int B_STAGE = BN * 128;
   static constexpr int B_BYTES = STAGES * B_STAGE;
   static constexpr int EPI_WARPS = 8;                     // two epilogue warpgroups
-  static constexpr int KW = 128, BW = 128;                // staging slots per epilogue warp
-  static constexpr int BAR_OFF = A_BYTES + B_BYTES;
-  static constexpr int NBARS = 2 * STAGES + 2 + 4;
+  static constexpr int KW = FOLD ? 64 : (KATOMS > 4 ? 96 : 128);  // staging slots per warp
+  static constexpr int BW = KW;
+  static constexpr int NBUF = 512 / (RA * BN);              // TMEM accumulator buffers
+  // fold tiles (tf32): A ones [128 rows x 32 B], B constants [2 slots][BN rows x 32 B]
+  static constexpr int AK_OFF = ABUF * A_BYTES + B_BYTES;
+  static constexpr int BK_SLOT = BN * 32;
+  static constexpr int COL_OFF = AK_OFF + (FOLD ? 128 * 32 + 2 * BK_SLOT : 0);
+  static constexpr int COL_BYTES = BN * 4;                 // int8: per-buffer column constants
+  static constexpr int BAR_OFF = COL_OFF + (FOLD ? 0 : NBUF * COL_BYTES);
+  static constexpr int NBARS = 2 * STAGES + 2 * ABUF + 3 * NBUF + 5;
   static constexpr int CNT_OFF = BAR_OFF + NBARS * 8;     // tmem slot + per-warp counts
   static constexpr int BUF_OFF = CNT_OFF + 128;
   static constexpr int TOTAL = BUF_OFF + EPI_WARPS * (KW + BW) * 8 + 1024;  // + align slack
@@ -153,28 +243,42 @@ struct Smem {
 // ------------------------------------------------------------------ kernel
 constexpr int TC_THREADS = 384;   // warps 0-3 roles, 4-11 epilogue
 
-template <int KIND, int RA, int BN, int KATOMS, int STAGES, int MODE>
+template <int KIND, int RA, int BN, int KATOMS, int STAGES, int ABUF, int MODE>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     k_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+         const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmO,
          TcArgs args) {
-  using S = Smem<RA, BN, KATOMS, STAGES>;
+  // tf32: the column constant is folded into the contraction by one extra K=8
+  // MMA per tile (ones x {-cb_hi, -cb_mid, -cb_lo}), so the epilogue's test is
+  // a plain max over the accumulators
+  constexpr bool FOLD = KIND == TC_TF32 && MODE != TC_MODE_GRAM;
+  using S = Smem<RA, BN, KATOMS, STAGES, ABUF, FOLD>;
   constexpr int BUFCOLS = RA * BN;
-  static_assert(2 * BUFCOLS <= 512, "TMEM: two accumulator buffers must fit 512 columns");
+  constexpr int NBUF = 512 / BUFCOLS;   // TMEM accumulator buffers (2 at BN=256, 4 at BN=128)
+  static_assert(NBUF >= 2 && NBUF * BUFCOLS <= 512, "TMEM: accumulator buffers must fit 512 columns");
   static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "BN");
+  static_assert(RA == 1, "one 128-row block per unit (N = BN MMAs, A double-buffered)");
   constexpr int ATOM_ELEMS = KIND == TC_TF32 ? 32 : 128;
   constexpr uint32_t IDESC = make_idesc<KIND>(128, BN);
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint8_t* sA = sm;
-  uint8_t* sB = sm + S::A_BYTES;
+  uint8_t* sA = sm;                                  // [ABUF][RA][KATOMS] atoms
+  uint8_t* sB = sm + ABUF * S::A_BYTES;
   uint64_t* bars = (uint64_t*)(sm + S::BAR_OFF);
   uint64_t* full = bars;
   uint64_t* empty = bars + STAGES;
-  uint64_t* a_full = bars + 2 * STAGES;
-  uint64_t* a_empty = a_full + 1;
-  uint64_t* t_full = a_full + 2;   // [2]
-  uint64_t* t_empty = a_full + 4;  // [2]
+  uint64_t* a_full = bars + 2 * STAGES;             // [ABUF]
+  uint64_t* a_empty = a_full + ABUF;                // [ABUF]
+  uint64_t* t_full = a_empty + ABUF;                // [NBUF]
+  uint64_t* t_empty = t_full + NBUF;                // [NBUF]
+  uint64_t* c_full = t_empty + NBUF;                // [NBUF] column constants of TMEM buffer b
+  uint64_t* bk_full = c_full + NBUF;                // [2] fold: B constant slots
+  uint64_t* bk_empty = bk_full + 2;                 // [2]
+  uint64_t* ak_full = bk_empty + 2;                 // fold: A ones tile
+  float* scol = (float*)(sm + S::COL_OFF);          // [NBUF][BN] (int8)
+  uint8_t* sAK = sm + S::AK_OFF;                    // fold: [128][32 B]
+  uint8_t* sBK = sAK + 128 * 32;                    // fold: [2][BN][32 B]
   uint32_t* tmem_slot = (uint32_t*)(sm + S::CNT_OFF);
   uint32_t* kcount = tmem_slot + 1;                  // [EPI_WARPS]
   uint32_t* bcount = kcount + S::EPI_WARPS;          // [EPI_WARPS]
@@ -187,12 +291,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(a_full, 1);
-    mbar_init(a_empty, 1);
-    mbar_init(&t_full[0], 1);
-    mbar_init(&t_full[1], 1);
-    mbar_init(&t_empty[0], 4);   // the 4 warps of the group that drains buffer 0
-    mbar_init(&t_empty[1], 4);
+    for (int b = 0; b < ABUF; ++b) {
+      mbar_init(&a_full[b], 1);
+      mbar_init(&a_empty[b], 1);
+    }
+    for (int b = 0; b < NBUF; ++b) {
+      mbar_init(&t_full[b], 1);
+      mbar_init(&t_empty[b], 4);   // the 4 warps of the group that drains buffer b
+      mbar_init(&c_full[b], 1);
+    }
+    mbar_init(&bk_full[0], 1);
+    mbar_init(&bk_full[1], 1);
+    mbar_init(&bk_empty[0], 1);
+    mbar_init(&bk_empty[1], 1);
+    mbar_init(ak_full, 1);
     for (int w = 0; w < S::EPI_WARPS; ++w) {
       kcount[w] = 0;
       bcount[w] = 0;
@@ -202,6 +314,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+    if constexpr (FOLD) asm volatile("prefetch.tensormap [%0];" ::"l"(&tmK) : "memory");
   }
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -231,20 +344,27 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     if (lane == 0) {
       // ---------------- TMA producer
       int stage = 0;
-      uint32_t phase = 0, a_ph = 0;
-      bool first = true;
-      for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
+      uint32_t phase = 0, a_ph = 0;   // a_ph bit b: parity of A buffer b's next release
+      uint32_t bk_ph = 0;             // fold: bit b = parity of B constant slot b's release
+      int64_t tk = 0;                 // tiles issued by this CTA
+      int64_t ui = 0;                 // units issued by this CTA
+      if constexpr (FOLD) {
+        mbar_expect_tx(ak_full, 128u * 32u);
+        tma_load_2d(sAK, &tmO, ak_full, 0, 0);
+      }
+      for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x, ++ui) {
         const int64_t mb = u / n_chunks, ch = u % n_chunks;
         const int64_t t0 = ch * tiles_per_chunk, t1 = min(n_tiles, t0 + tiles_per_chunk);
-        if (!first) {
-          mbar_wait(a_empty, a_ph);
-          a_ph ^= 1u;
+        const int ab = (int)(ui % ABUF);
+        if (ui >= ABUF) {             // wait until the MMAs of unit ui - ABUF released it
+          mbar_wait(&a_empty[ab], (a_ph >> ab) & 1u);
+          a_ph ^= 1u << ab;
         }
-        first = false;
-        mbar_expect_tx(a_full, (uint32_t)S::A_BYTES);
+        uint8_t* sAb = sA + ab * S::A_BYTES;
+        mbar_expect_tx(&a_full[ab], (uint32_t)S::A_BYTES);
         for (int r = 0; r < RA; ++r)
           for (int ka = 0; ka < KATOMS; ++ka)
-            tma_load_2d(sA + (r * KATOMS + ka) * S::A_ATOM, &tmA, a_full, ka * ATOM_ELEMS,
+            tma_load_2d(sAb + (r * KATOMS + ka) * S::A_ATOM, &tmA, &a_full[ab], ka * ATOM_ELEMS,
                         (int)(mb * RA * 128 + r * 128));
         // warm L2 with the next unit's point block while this one computes
         const int64_t un = u + gridDim.x;
@@ -264,6 +384,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               phase ^= 1u;
             }
           }
+          if constexpr (FOLD) {   // the tile's column constants, two slots
+            const int sl = (int)(tk & 1);
+            if (tk >= 2) {
+              mbar_wait(&bk_empty[sl], (bk_ph >> sl) & 1u);
+              bk_ph ^= 1u << sl;
+            }
+            mbar_expect_tx(&bk_full[sl], (uint32_t)S::BK_SLOT);
+            tma_load_2d(sBK + sl * S::BK_SLOT, &tmK, &bk_full[sl], 0, (int)(t * BN));
+          }
+          ++tk;
         }
       }
     }
@@ -272,18 +402,29 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       // ---------------- MMA issuer
       int stage = 0;
       uint32_t phase = 0, a_ph = 0;
-      uint32_t use[2] = {0u, 0u};
+      uint32_t use[NBUF] = {};
       int buf = 0;
       const int ksteps = args.ksteps;  // 32-byte K steps actually needed
-      for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
+      int64_t ui = 0;
+      int64_t tk = 0;                  // tiles issued (fold: B constant slot = tk & 1)
+      if constexpr (FOLD) mbar_wait(ak_full, 0u);
+      for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x, ++ui) {
         const int64_t ch = u % n_chunks;
         const int64_t t0 = ch * tiles_per_chunk, t1 = min(n_tiles, t0 + tiles_per_chunk);
-        mbar_wait(a_full, a_ph);
-        a_ph ^= 1u;
+        const int ab = (int)(ui % ABUF);
+        mbar_wait(&a_full[ab], (a_ph >> ab) & 1u);
+        a_ph ^= 1u << ab;
         fence_after();
+        const uint8_t* sAb = sA + ab * S::A_BYTES;
         for (int64_t t = t0; t < t1; ++t) {
           mbar_wait(&t_empty[buf], (use[buf] & 1u) ^ 1u);
           fence_after();
+          // int8: the tile's per-column constants (col_c) into this buffer's slot
+          if constexpr (MODE == TC_MODE_MEMBER && !FOLD) {
+            mbar_expect_tx(&c_full[buf], (uint32_t)S::COL_BYTES);
+            bulk_load(scol + buf * BN, (const void*)(args.col_c + t * BN),
+                      (uint32_t)S::COL_BYTES, &c_full[buf]);
+          }
           const uint32_t dcol = tmem + (uint32_t)(buf * BUFCOLS);
           for (int ka = 0; ka < KATOMS; ++ka) {
             mbar_wait(&full[stage], phase);
@@ -291,7 +432,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             const uint32_t bbase = su32(sB + stage * S::B_STAGE);
 #pragma unroll
             for (int r = 0; r < RA; ++r) {
-              const uint32_t abase = su32(sA + (r * KATOMS + ka) * S::A_ATOM);
+              const uint32_t abase = su32(sAb + (r * KATOMS + ka) * S::A_ATOM);
 #pragma unroll
               for (int ks = 0; ks < 4; ++ks) {
                 if (ka * 4 + ks < ksteps)
@@ -305,11 +446,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               phase ^= 1u;
             }
           }
+          if constexpr (FOLD) {   // acc' = x.l - cb_j: ones x {-cb_hi, -cb_mid, -cb_lo}
+            const int sl = (int)(tk & 1);
+            mbar_wait(&bk_full[sl], (uint32_t)((tk >> 1) & 1));
+            fence_after();
+            mma<KIND>(dcol, sdesc32(su32(sAK)), sdesc32(su32(sBK + sl * S::BK_SLOT)), IDESC, 1u);
+            mma_commit(&bk_empty[sl]);
+          }
+          ++tk;
           mma_commit(&t_full[buf]);
           ++use[buf];
-          buf ^= 1;
+          buf = buf + 1 == NBUF ? 0 : buf + 1;
         }
-        mma_commit(a_empty);
+        mma_commit(&a_empty[ab]);
       }
     }
   } else if (warp >= 4) {
@@ -359,8 +508,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         if ((int64_t)g < gcap) gbuf[g] = key;
       }
     };
-    uint32_t phase = 0;
-    int64_t tcount = 0;   // tiles seen, in the MMA issuer's order (buffer = tcount & 1)
+    uint32_t phase = 0;   // bit b: parity of the next completion of buffer b
+    int64_t tcount = 0;   // tiles seen, in the MMA issuer's order (buffer = tcount % NBUF)
     for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
       const int64_t mb = u / n_chunks, ch = u % n_chunks;
       const int64_t t0 = ch * tiles_per_chunk, t1 = min(n_tiles, t0 + tiles_per_chunk);
@@ -378,54 +527,69 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
       }
       for (int64_t t = t0; t < t1; ++t, ++tcount) {
-        const int buf = (int)(tcount & 1);
-        if (buf != grp) continue;
-        mbar_wait(&t_full[buf], phase);
-        phase ^= 1u;
+        if ((int)(tcount & 1) != grp) continue;      // the two groups alternate tiles
+        const int buf = (int)(tcount % NBUF);
+        const uint32_t ph = (phase >> buf) & 1u;    // this group's parity for buffer buf
+        mbar_wait(&t_full[buf], ph);
+        if constexpr (MODE == TC_MODE_MEMBER && !FOLD) mbar_wait(&c_full[buf], ph);
+        phase ^= 1u << buf;
         fence_after();
-#pragma unroll
-        for (int r = 0; r < RA; ++r) {
-#pragma unroll 1
-          for (int cc = 0; cc < BN / 32; ++cc) {
-            uint32_t v[32];
-            const uint32_t taddr =
-                tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * BUFCOLS + r * BN + cc * 32);
-            tmem_ld32(taddr, v);
+        const float* colb = scol + buf * BN;   // tile's col_b (tf32) / col_c (int8) in smem
+        // TMEM -> registers 32 columns at a time, the next chunk's load in
+        // flight while this one is classified (va / vb ping-pong)
+        const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * BUFCOLS);
+        constexpr int NCH = RA * (BN / 32);
+        uint32_t va[32], vb[32];
+        if constexpr (MODE != TC_MODE_PROBE_NOLD) {
+          tmem_ld32_nowait(trow, va);
+          tmem_wait(va);
+        }
+        auto chunk = [&](int c, uint32_t (&v)[32]) {
+          const int r = RA == 1 ? 0 : c / (BN / 32), cc = RA == 1 ? c : c % (BN / 32);
+          {
             const int64_t j0 = t * BN + cc * 32;
+            if constexpr (MODE == TC_MODE_PROBE_LDONLY) {
+              uint32_t x = 0u;
+#pragma unroll
+              for (int i = 0; i < 32; ++i) x ^= v[i];
+              if (x == 0x9e3779b9u && prow[r] < 0) args.keys[0] = x;   // keeps the loads live
+              return;
+            }
             if constexpr (MODE == TC_MODE_GRAM) {
               if (prow[r] < args.n) {
 #pragma unroll
                 for (int i = 0; i < 32; ++i)
                   if (j0 + i < n_cols) args.gram[prow[r] * n_cols + j0 + i] = v[i];
               }
-              continue;
+              return;
             }
             // fast path: one compare per 32 pairs decides "all out"
             bool surv;
             if constexpr (KIND == TC_TF32) {
-              const float4* cb = reinterpret_cast<const float4*>(args.col_b + j0);
-              float m = -INFINITY;
+              // acc' = x.l - cb_j straight from the MMA: max over 32 columns
+              float m[4];
 #pragma unroll
-              for (int i4 = 0; i4 < 8; ++i4) {
-                const float4 b = __ldg(cb + i4);
-                m = fmaxf(m, __uint_as_float(v[4 * i4 + 0]) - b.x);
-                m = fmaxf(m, __uint_as_float(v[4 * i4 + 1]) - b.y);
-                m = fmaxf(m, __uint_as_float(v[4 * i4 + 2]) - b.z);
-                m = fmaxf(m, __uint_as_float(v[4 * i4 + 3]) - b.w);
+              for (int k = 0; k < 4; ++k) m[k] = __uint_as_float(v[k]);
+#pragma unroll
+              for (int i = 4; i < 32; i += 8) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                  m[k] = fmaxf(m[k], fmaxf(__uint_as_float(v[i + 2 * k]),
+                                           __uint_as_float(v[i + 2 * k + 1])));
               }
-              surv = m > rlo[r];
+              surv = fmaxf(fmaxf(m[0], m[1]), fmaxf(m[2], m[3])) > rlo[r];
             } else {
-              const int4* cc4 = reinterpret_cast<const int4*>(args.col_c + j0);
-              int m = INT_MIN;
+              const int4* cc4 = reinterpret_cast<const int4*>(colb + cc * 32);
+              int m[4] = {INT_MIN, INT_MIN, INT_MIN, INT_MIN};
 #pragma unroll
               for (int i4 = 0; i4 < 8; ++i4) {
-                const int4 c = __ldg(cc4 + i4);
-                m = max(m, 2 * (int)v[4 * i4 + 0] - c.x);
-                m = max(m, 2 * (int)v[4 * i4 + 1] - c.y);
-                m = max(m, 2 * (int)v[4 * i4 + 2] - c.z);
-                m = max(m, 2 * (int)v[4 * i4 + 3] - c.w);
+                const int4 c = cc4[i4];
+                m[0] = max(m[0], 2 * (int)v[4 * i4 + 0] - c.x);
+                m[1] = max(m[1], 2 * (int)v[4 * i4 + 1] - c.y);
+                m[2] = max(m[2], 2 * (int)v[4 * i4 + 2] - c.z);
+                m[3] = max(m[3], 2 * (int)v[4 * i4 + 3] - c.w);
               }
-              surv = m > rint[r];
+              surv = max(max(m[0], m[1]), max(m[2], m[3])) > rint[r];
             }
             if (__any_sync(FULLM, surv)) {
               // rare path: column masks of candidates (not certainly out) and
@@ -436,7 +600,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 for (int i = 0; i < 32; ++i) {
                   if constexpr (KIND == TC_TF32) {
                     const float a = __uint_as_float(v[i]);
-                    cand |= (a - __ldg(args.col_b + j0 + i) > rlo[r] ? 1u : 0u) << i;
+                    cand |= (a > rlo[r] ? 1u : 0u) << i;
                     inm |= (a - __ldg(args.col_a + j0 + i) > rhi[r] ? 1u : 0u) << i;
                   } else {
                     cand |= (2 * (int)v[i] - __ldg(args.col_c + j0 + i) > rint[r] ? 1u : 0u) << i;
@@ -458,6 +622,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               }
               __syncwarp();
               if (*kc > S::KW / 2 || *bc > S::BW / 2) flush();
+            }
+          }
+        };
+        if constexpr (MODE != TC_MODE_PROBE_NOLD) {
+#pragma unroll 1
+          for (int c = 0; c < NCH; c += 2) {
+            if (c + 1 < NCH) tmem_ld32_nowait(trow + (uint32_t)(((c + 1) / (BN / 32)) * BN + ((c + 1) % (BN / 32)) * 32), vb);
+            chunk(c, va);
+            if (c + 1 < NCH) {
+              tmem_wait(vb);
+              if (c + 2 < NCH) tmem_ld32_nowait(trow + (uint32_t)(((c + 2) / (BN / 32)) * BN + ((c + 2) % (BN / 32)) * 32), va);
+              chunk(c + 1, vb);
+              if (c + 2 < NCH) tmem_wait(va);
             }
           }
         }
@@ -513,15 +690,41 @@ static cudaError_t make_tmap(CUtensorMap* tm, const void* base, int kind, int64_
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
-template <int KIND, int RA, int BN, int KATOMS, int STAGES, int MODE>
+// fp32 [rows][8] tile map, box 8 x box_rows, 32-byte swizzle (fold operands)
+static cudaError_t make_tmap8(CUtensorMap* tm, const void* base, int64_t rows, int box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return cudaErrorNotSupported;
+  cuuint64_t dims[2] = {8, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {32};
+  cuuint32_t box[2] = {8, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+template <int KIND, int RA, int BN, int KATOMS, int STAGES, int ABUF, int MODE>
 static cudaError_t launch_cfg(const TcPlan& P, TcArgs a, cudaStream_t s) {
-  using S = Smem<RA, BN, KATOMS, STAGES>;
-  CUtensorMap tA, tB;
+  constexpr bool FOLD = KIND == TC_TF32 && MODE != TC_MODE_GRAM;
+  using S = Smem<RA, BN, KATOMS, STAGES, ABUF, FOLD>;
+  static_assert(S::TOTAL <= 232448, "shared memory");
+  CUtensorMap tA, tB, tK, tO;
   cudaError_t e = make_tmap(&tA, P.xop, KIND, P.k_elems, P.n_rows, P.row_bytes, 128);
   if (e != cudaSuccess) return e;
   e = make_tmap(&tB, P.lop, KIND, P.k_elems, P.l_rows, P.row_bytes, BN);
   if (e != cudaSuccess) return e;
-  auto kern = k_tc<KIND, RA, BN, KATOMS, STAGES, MODE>;
+  if (FOLD) {
+    if (!a.colk || !P.ones) return cudaErrorInvalidValue;
+    e = make_tmap8(&tK, a.colk, P.l_rows, BN);
+    if (e != cudaSuccess) return e;
+    e = make_tmap8(&tO, P.ones, 128, 128);
+    if (e != cudaSuccess) return e;
+  } else {
+    tK = tB;
+    tO = tB;
+  }
+  auto kern = k_tc<KIND, RA, BN, KATOMS, STAGES, ABUF, MODE>;
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::TOTAL);
   if (e != cudaSuccess) return e;
   a.n_mblk = (P.n_rows + RA * 128 - 1) / (RA * 128);
@@ -534,41 +737,55 @@ static cudaError_t launch_cfg(const TcPlan& P, TcArgs a, cudaStream_t s) {
     if (a.n_mblk * chunks < grid) grid = a.n_mblk * chunks;
   }
   if (grid < 1) grid = 1;
-  kern<<<(unsigned)grid, TC_THREADS, S::TOTAL, s>>>(tA, tB, a);
+  kern<<<(unsigned)grid, TC_THREADS, S::TOTAL, s>>>(tA, tB, tK, tO, a);
   return cudaGetLastError();
 }
 
-// Configuration table:
-//   tf32, K <= 64 floats (2 atoms): A-stationary 512 rows (RA=4), BN=64, 8 stages
-//   tf32, K <= 128 floats:          RA=2, BN=64
-//   int8, K <= 896 bytes (7 atoms): RA=1, BN=256, 3 stages
+// Configuration table: every configuration
+// issues M=128 x N=256 MMAs (N=64 MMAs measured ~3x slower per flop on B200);
+// a unit = 128 point rows (A, double-buffered when it fits) against a chunk
+// of 256-wide landmark tiles streamed one 128-byte K atom per stage.
+//   K <= 256 bytes (tf32 d <= 64, int8 d <= 256): 4 stages, 2 A buffers
+//   K <= 512 bytes (tf32 d <= 128):               4 stages, 1 A buffer
+//   K <= 896 bytes (int8 d <= 896):               3 stages, 1 A buffer
 template <int MODE>
 static cudaError_t dispatch(const TcPlan& P, const TcArgs& a, cudaStream_t s) {
   if (P.kind == TC_TF32) {
-    if (P.katoms <= 2) return launch_cfg<TC_TF32, 4, 64, 2, 8, MODE>(P, a, s);
-    if (P.katoms <= 4) return launch_cfg<TC_TF32, 2, 64, 4, 8, MODE>(P, a, s);
+    if (P.katoms <= 2) return launch_cfg<TC_TF32, 1, 256, 2, 4, 2, MODE>(P, a, s);
+    if (P.katoms <= 4) return launch_cfg<TC_TF32, 1, 256, 4, 4, 1, MODE>(P, a, s);
     return cudaErrorNotSupported;
   }
   if (P.kind == TC_U8) {
-    if (P.katoms <= 2) return launch_cfg<TC_U8, 4, 64, 2, 8, MODE>(P, a, s);
-    if (P.katoms <= 7) return launch_cfg<TC_U8, 1, 256, 7, 3, MODE>(P, a, s);
+    if (P.katoms <= 2) return launch_cfg<TC_U8, 1, 256, 2, 4, 2, MODE>(P, a, s);
+    if (P.katoms <= 7) return launch_cfg<TC_U8, 1, 256, 7, 3, 1, MODE>(P, a, s);
     return cudaErrorNotSupported;
   }
-  if (P.katoms <= 2) return launch_cfg<TC_S8, 4, 64, 2, 8, MODE>(P, a, s);
-  if (P.katoms <= 7) return launch_cfg<TC_S8, 1, 256, 7, 3, MODE>(P, a, s);
+  if (P.katoms <= 2) return launch_cfg<TC_S8, 1, 256, 2, 4, 2, MODE>(P, a, s);
+  if (P.katoms <= 7) return launch_cfg<TC_S8, 1, 256, 7, 3, 1, MODE>(P, a, s);
   return cudaErrorNotSupported;
 }
 
-int tc_bn_for(int kind, int katoms) {
-  if (kind == TC_TF32) return 64;
-  return katoms <= 2 ? 64 : 256;
-}
-int tc_rows_for(int kind, int katoms) {
-  if (kind == TC_TF32) return katoms <= 2 ? 512 : 256;
-  return katoms <= 2 ? 512 : 128;
-}
+int tc_bn_for(int kind, int katoms) { return 256; }
+int tc_rows_for(int kind, int katoms) { return 128; }
 bool tc_supported(int kind, int katoms) {
   return kind == TC_TF32 ? katoms <= 4 : katoms <= 7;
+}
+
+// mode: TC_MODE_MEMBER / TC_MODE_PROBE_LDONLY / TC_MODE_PROBE_NOLD on the
+// production configuration for tf32 with K <= 64
+template <int BN, int ST>
+static cudaError_t probe_cfg(const TcPlan& P, const TcArgs& a, int mode, cudaStream_t s) {
+  if (mode == TC_MODE_PROBE_LDONLY)
+    return launch_cfg<TC_TF32, 1, BN, 2, ST, 2, TC_MODE_PROBE_LDONLY>(P, a, s);
+  if (mode == TC_MODE_PROBE_NOLD)
+    return launch_cfg<TC_TF32, 1, BN, 2, ST, 2, TC_MODE_PROBE_NOLD>(P, a, s);
+  return launch_cfg<TC_TF32, 1, BN, 2, ST, 2, TC_MODE_MEMBER>(P, a, s);
+}
+// mode + 16 * cfg: cfg 0 = N=256 tiles (2 TMEM buffers), cfg 1 = N=128 (4 buffers)
+cudaError_t launch_tc_probe(const TcPlan& P, const TcArgs& a, int mode, cudaStream_t s) {
+  if (P.kind != TC_TF32 || P.katoms > 2) return cudaErrorNotSupported;
+  if ((mode >> 4) == 1) return probe_cfg<128, 8>(P, a, mode & 15, s);
+  return probe_cfg<256, 4>(P, a, mode & 15, s);
 }
 
 cudaError_t launch_tc(const TcPlan& P, const TcArgs& a, cudaStream_t s, int64_t* launches) {
@@ -656,17 +873,11 @@ __global__ void k_tc_gather_lm(const uint8_t* __restrict__ xop, int64_t row_byte
 
 __global__ void k_tc_cols_f32(const double* __restrict__ nrm, const int32_t* __restrict__ lm,
                               int64_t L, int64_t l_pad, double C2, float* __restrict__ ca,
-                              float* __restrict__ cb) {
+                              float* __restrict__ cb, float* __restrict__ colk) {
   int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= l_pad) return;
-  if (j >= L) {
-    ca[j] = INFINITY;
-    cb[j] = INFINITY;
-    return;
-  }
-  const double nl = nrm[lm[j]];
-  ca[j] = __double2float_ru(0.5 * nl + C2 * nl);
-  cb[j] = __double2float_rd(0.5 * nl - C2 * nl);
+  if (j >= L) tc_col_inert(j, ca, cb, colk);
+  else tc_col_consts(nrm[lm[j]], C2, j, ca, cb, colk);
 }
 
 __global__ void k_tc_cols_int(const int32_t* __restrict__ nrm, const int32_t* __restrict__ lm,
@@ -730,7 +941,7 @@ __global__ void k_tc_tile_lm(const uint8_t* __restrict__ xop, int64_t row_bytes,
                              const int32_t* __restrict__ l_count_dev, int kind,
                              const void* __restrict__ nrm, double C2, uint8_t* __restrict__ lop,
                              float* __restrict__ ca, float* __restrict__ cb,
-                             int32_t* __restrict__ cc) {
+                             float* __restrict__ colk, int32_t* __restrict__ cc) {
   const int64_t j = blockIdx.x;
   const int64_t cnt = *l_count_dev;
   const bool live = j < cnt;
@@ -741,14 +952,8 @@ __global__ void k_tc_tile_lm(const uint8_t* __restrict__ xop, int64_t row_bytes,
     dst[i] = live ? src[i] : make_uint4(0, 0, 0, 0);
   if (threadIdx.x == 0) {
     if (kind == TC_TF32) {
-      if (live) {
-        const double nl = ((const double*)nrm)[pt];
-        ca[j] = __double2float_ru(0.5 * nl + C2 * nl);
-        cb[j] = __double2float_rd(0.5 * nl - C2 * nl);
-      } else {
-        ca[j] = INFINITY;
-        cb[j] = INFINITY;
-      }
+      if (live) tc_col_consts(((const double*)nrm)[pt], C2, j, ca, cb, colk);
+      else tc_col_inert(j, ca, cb, colk);
     } else {
       cc[j] = live ? ((const int32_t*)nrm)[pt] : (1 << 30);
     }
@@ -761,7 +966,7 @@ cudaError_t launch_tc_tile_landmarks(const TcPlan& P, const void* nrm, const int
   ++*launches;
   k_tc_tile_lm<<<(unsigned)P.l_rows, 64, 0, s>>>(
       (const uint8_t*)P.xop, P.row_bytes, new_lm, l_count_dev, P.kind, nrm, C2,
-      (uint8_t*)P.lop, (float*)a.col_a, (float*)a.col_b, (int32_t*)a.col_c);
+      (uint8_t*)P.lop, (float*)a.col_a, (float*)a.col_b, (float*)a.colk, (int32_t*)a.col_c);
   return cudaGetLastError();
 }
 
@@ -841,6 +1046,16 @@ cudaError_t launch_tc_recheck_tile(const unsigned long long* band,
   return cudaGetLastError();
 }
 
+__global__ void k_tc_ones(float* o) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < 128 * 8) o[i] = (i & 7) < 3 ? 1.f : 0.f;
+}
+cudaError_t launch_tc_ones(float* ones, cudaStream_t s, int64_t* launches) {
+  ++*launches;
+  k_tc_ones<<<4, 256, 0, s>>>(ones);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_tc_prep(const void* X, int dtype, int64_t n, int d, const TcPlan& P,
                            void* nrm, DevStats* stats, cudaStream_t s, int64_t* launches) {
   ++*launches;
@@ -875,7 +1090,7 @@ cudaError_t launch_tc_landmarks(const TcPlan& P, const void* nrm, const int32_t*
   const unsigned g = (unsigned)((P.l_rows + 255) / 256);
   if (P.kind == TC_TF32)
     k_tc_cols_f32<<<g, 256, 0, s>>>((const double*)nrm, lm, L, P.l_rows, C2,
-                                    (float*)a.col_a, (float*)a.col_b);
+                                    (float*)a.col_a, (float*)a.col_b, (float*)a.colk);
   else
     k_tc_cols_int<<<g, 256, 0, s>>>((const int32_t*)nrm, lm, L, P.l_rows, (int32_t*)a.col_c);
   return cudaGetLastError();

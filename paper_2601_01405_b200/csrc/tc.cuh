@@ -9,7 +9,12 @@ namespace bm {
 namespace tc {
 
 enum TcKind : int { TC_TF32 = 0, TC_U8 = 1, TC_S8 = 2 };
-enum TcMode : int { TC_MODE_MEMBER = 0, TC_MODE_GRAM = 1 };
+enum TcMode : int {
+  TC_MODE_MEMBER = 0,
+  TC_MODE_GRAM = 1,
+  TC_MODE_PROBE_LDONLY = 2,   // diagnostics: epilogue reads TMEM, no classification
+  TC_MODE_PROBE_NOLD = 3      // diagnostics: epilogue releases buffers without reading
+};
 
 // Operand geometry (host side).
 struct TcPlan {
@@ -23,6 +28,7 @@ struct TcPlan {
   int64_t k_elems;     // row_bytes / element size
   int katoms;          // ceil(row_bytes / 128)
   int num_sms;
+  const float* ones;   // tf32: [128][8] constant A tile {1,1,1,0,0,0,0,0} (column-constant fold)
 };
 
 struct TcArgs {
@@ -36,8 +42,10 @@ struct TcArgs {
   const float* row_lo;
   const float* row_hi;
   const int32_t* row_r;
-  const float* col_a;
-  const float* col_b;
+  const float* col_a;    // tf32: in-test offset d_j (acc' - d_j > row_hi proves "in")
+  const float* col_b;    // tf32: column constant cb_j folded into the MMA (diagnostics)
+  const float* colk;     // tf32: [l_rows][8] {-cb_hi, -cb_mid, -cb_lo, 0...}: B operand of
+                         //       the fold MMA, so the accumulator is acc' = x.l - cb_j
   const int32_t* col_c;
   // outputs
   unsigned long long* keys;
@@ -54,6 +62,8 @@ int tc_bn_for(int kind, int katoms);
 int tc_rows_for(int kind, int katoms);
 bool tc_supported(int kind, int katoms);
 
+// fill the [128][8] constant A tile of the column-constant fold ({1,1,1,0,...})
+cudaError_t launch_tc_ones(float* ones, cudaStream_t s, int64_t* launches);
 cudaError_t launch_tc_prep(const void* X, int dtype, int64_t n, int d, const TcPlan& P,
                            void* nrm, DevStats* stats, cudaStream_t s, int64_t* launches);
 cudaError_t launch_tc_rows(const TcPlan& P, const void* nrm, int64_t n, double C2, double eps2,
@@ -79,6 +89,8 @@ cudaError_t launch_tc_recheck_tile(const unsigned long long* band,
                                    DevStats* stats, int num_sms, cudaStream_t s,
                                    int64_t* launches);
 cudaError_t launch_tc(const TcPlan& P, const TcArgs& a, cudaStream_t s, int64_t* launches);
+// diagnostics: the contraction with a probe epilogue (TC_MODE_PROBE_*), tf32 K <= 64 only
+cudaError_t launch_tc_probe(const TcPlan& P, const TcArgs& a, int mode, cudaStream_t s);
 cudaError_t launch_tc_recheck(const unsigned long long* band, int64_t nb, const float* X,
                               int xstride, int d, const int32_t* lm, const Thresh& th, int lbits,
                               unsigned long long* keys, unsigned long long* key_count,
