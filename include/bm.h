@@ -90,8 +90,8 @@ typedef struct bm_options {
   int64_t near_tie_cap;  /* max near-tie pairs stored (0 = default 65536); all are counted      */
   int32_t key_cap;       /* initial membership key capacity (0 = default 16 n); a smaller M
                             fits, a larger one costs one exact-capacity recount             */
-  int32_t band_cap;      /* tensor path: per-tile fp64 band queue capacity (0 = default);
-                            an overflow re-runs the build on the CUDA-core path             */
+  int32_t band_cap;      /* ignored (kept for layout): band pairs are re-decided in fp64
+                            inside the contraction kernels, no queue is needed              */
   int32_t reserved[6];
 } bm_options;
 

@@ -231,6 +231,21 @@ struct Timer {
   }
 };
 
+// B' inside the contraction's epilogue: rows to re-decide band pairs from.
+void set_recheck(bm::tc::TcArgs& ta, const void* xrows, int xstride, int d, const bm::Thresh& th,
+                 const int32_t* lm_idx, int64_t* ties, int64_t tie_cap, bm::DevStats* stats) {
+  ta.xrows = (const float*)xrows;
+  ta.xstride = xstride;
+  ta.d = d;
+  ta.eps = th.eps;
+  ta.eps2 = th.eps2;
+  ta.tie_rel = th.tie_rel;
+  ta.lm_idx = lm_idx;
+  ta.ties = ties;
+  ta.tie_cap = tie_cap;
+  ta.stats = stats;
+}
+
 // tf32 column-constant fold operands: B constants [l_rows][8] and the A ones tile.
 bm_status alloc_fold(Pool& pool, bm::tc::TcPlan& P, bm::tc::TcArgs& ta, cudaStream_t s,
                      int64_t* launches) {
@@ -288,35 +303,11 @@ bm_status membership_full(Pool& pool, int kind, const bm::PairArgs& base, bm::tc
     }
     CK(tc::launch_tc_rows(P, tc_nrm, n, C2, th.eps2, tau, th.lo_i, ta, s, launches));
     CK(tc::launch_tc_landmarks(P, tc_nrm, lm, L, C2, ta, s, launches));
-    int64_t band_cap = n * 4 > (1 << 22) ? n * 4 : (1 << 22);
-    unsigned long long* bcount = nullptr;
-    TRY(pool.alloc(&bcount, 1));
-    for (int attempt = 0; attempt < 2; ++attempt) {
-      unsigned long long* band = nullptr;
-      TRY(pool.alloc(&band, (size_t)band_cap));
-      CK(cudaMemsetAsync(bcount, 0, sizeof(unsigned long long), s));
-      CK(cudaMemsetAsync(&stats->key_count, 0, sizeof(unsigned long long), s));
-      ta.keys = keys;
-      ta.key_count = &stats->key_count;
-      ta.key_cap = key_cap;
-      ta.band = band;
-      ta.band_count = bcount;
-      ta.band_cap = band_cap;
-      CK(tc::launch_tc(P, ta, s, launches));
-      unsigned long long hb = 0;
-      CK(cudaMemcpyAsync(&hb, bcount, sizeof hb, cudaMemcpyDeviceToHost, s));
-      CK(cudaStreamSynchronize(s));
-      if ((int64_t)hb <= band_cap) {
-        CK(tc::launch_tc_recheck(band, (int64_t)hb, (const float*)base.xrows, 2 * nu, d, lm, th,
-                                 32, keys, &stats->key_count, key_cap, ties_dev, tie_cap, stats,
-                                 s, launches));
-        pool.free_now(band);
-        break;
-      }
-      pool.free_now(band);
-      band_cap = (int64_t)hb;
-      if (attempt == 1) return set_err(BM_ENOMEM, "band queue kept overflowing");
-    }
+    ta.keys = keys;
+    ta.key_count = &stats->key_count;
+    ta.key_cap = key_cap;
+    set_recheck(ta, base.xrows, 2 * nu, d, th, lm, ties_dev, tie_cap, stats);
+    CK(tc::launch_tc(P, ta, s, launches));
     pool.free_now((void*)P.lop);
   } else {
     PairArgs m = base;
@@ -477,10 +468,8 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
   base.th = th;
   base.stats = stats;
 
-  // tensor path: tile landmark operand [T_pad][row_bytes], column constants, band queue
+  // tensor path: tile landmark operand [T_pad][row_bytes], column constants
   tc::TcArgs ta{};
-  unsigned long long *band = nullptr, *bcount = nullptr;
-  int64_t band_cap = 0;
   double C2 = 0.0;
   if (use_tc) {
     const int BN = tc::tc_bn_for(P.kind, P.katoms);
@@ -509,10 +498,6 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
       TRY(alloc_fold(pool, P, ta, s, &launches));
       C2 = tc_band_c2(ta.ksteps);
       tau = 1.0000005e-6 * th.eps2 + th.eps2 * ldexp(1.0, -21);
-      band_cap = o.band_cap > 0 ? (int64_t)o.band_cap : (n * 4 > (1 << 22) ? n * 4 : (1 << 22));
-      TRY(pool.alloc(&band, (size_t)band_cap));
-      TRY(pool.alloc(&bcount, 1));
-      CK(cudaMemsetAsync(bcount, 0, sizeof(unsigned long long), s));
     } else {
       int32_t *rr, *cc;
       TRY(pool.alloc(&rr, (size_t)P.n_pad));
@@ -524,9 +509,7 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
     ta.keys = keys;
     ta.key_count = &stats->key_count;
     ta.key_cap = key_cap;
-    ta.band = band;
-    ta.band_count = bcount;
-    ta.band_cap = band_cap;
+    set_recheck(ta, rows, 2 * nu, d, th, new_lm, ties_dev, tie_cap, stats);
   }
   tm.mark(1);
 
@@ -571,18 +554,13 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
       CK(launch_pairs(kind, MODE_ADJ, a, T, s, &launches));
       // A3: in-order resolve, append landmarks (resets the tile's counters)
       CK(launch_resolve(adj, adj_words, uncb[cur], cnt + cur, T, lm, cnt + 2, new_lm, cnt + 3,
-                        stats, cnt + 4, bcount, s, &launches));
+                        stats, cnt + 4, nullptr, s, &launches));
       // B (+A4 marks): membership of every point in the new balls
       if (use_tc) {
         CK(tc::launch_tc_tile_landmarks(P, tc_nrm, new_lm, cnt + 3, C2, ta, s, &launches));
         CK(mark_member());
         CK(tc::launch_tc(P, ta, s, &launches));
         CK(mark_member());
-        if (P.kind == tc::TC_TF32)
-          CK(tc::launch_tc_recheck_tile(band, bcount, band_cap, (const float*)rows, 2 * nu, d,
-                                        new_lm, cnt + 3, cnt + 2, th, keys, &stats->key_count,
-                                        key_cap, covered, ties_dev, tie_cap, stats, P.num_sms, s,
-                                        &launches));
       } else {
         PairArgs m = base;
         m.qidx = nullptr;
@@ -627,18 +605,10 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
   CK(cudaMemcpyAsync(&hL, cnt + 2, sizeof hL, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   const int64_t L = hL;
-  if (hs.overflow) {
-    // a tile's band queue overflowed (adversarial input): redo on the CUDA-core
-    // path, whose band is re-decided inline and cannot overflow
-    bm_options o2 = o;
-    o2.path = BM_PATH_CUDA_CORE;
-    return build_impl(points, dtype, n, d, metric, eps, s, &o2, host_in, out);
-  }
   pool.free_now(unc0);
   pool.free_now(unc1);
   pool.free_now(covered);
   pool.free_now(cstate);
-  if (band) pool.free_now(band);
 
   // ---- B fallback: the key buffer overflowed; recompute the membership alone
   // with the exact capacity (the greedy's coverage decisions were unaffected)
@@ -1022,9 +992,7 @@ bm_status bm_debug_tc_probe(const float* points, int64_t n, int32_t d, int64_t L
   ta.keys = keys;
   ta.key_count = kc;
   ta.key_cap = 1024;
-  ta.band = keys;
-  ta.band_count = kc + 1;
-  ta.band_cap = 1024;
+  set_recheck(ta, points, d, d, make_thresh(K_L2F, d, 1e-15), lm, nullptr, 0, stats);
   CK(tc::launch_tc_probe(P, ta, mode, s));   // warm-up
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
@@ -1048,9 +1016,15 @@ bm_status bm_debug_resolve_tile(const uint32_t* adj, int32_t nc, uint8_t* lm_out
   const int words = (nc + 31) / 32;
   uint32_t* dadj = nullptr;
   uint8_t* dlm = nullptr;
-  TRY(pool.alloc(&dadj, (size_t)nc * words));
+  // the library's layout is word-major: word v of candidate a at [v * 32 words + a]
+  const int T = 32 * words;
+  std::vector<uint32_t> wm((size_t)words * T, 0u);
+  for (int a = 0; a < nc; ++a)
+    for (int v = 0; v < words; ++v) wm[(size_t)v * T + a] = adj[(size_t)a * words + v];
+  TRY(pool.alloc(&dadj, (size_t)words * T));
   TRY(pool.alloc(&dlm, (size_t)nc));
-  CK(cudaMemcpyAsync(dadj, adj, sizeof(uint32_t) * nc * words, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(dadj, wm.data(), sizeof(uint32_t) * words * T, cudaMemcpyHostToDevice, s));
+  CK(cudaStreamSynchronize(s));
   int64_t launches = 0;
   CK(bm::launch_resolve_debug(dadj, words, nc, dlm, s, &launches));
   CK(cudaMemcpyAsync(lm_out, dlm, nc, cudaMemcpyDeviceToHost, s));

@@ -33,8 +33,10 @@ __device__ __forceinline__ uint32_t resolve_tile_core(const uint32_t* __restrict
   const bool valid = a < nc;
   uint32_t wv[32];
 #pragma unroll
-  for (int v = 0; v < 32; ++v) wv[v] = (valid && v < w) ? adj[(int64_t)a * adj_words + v] : 0u;
-  uint32_t inrow = valid ? (adj[(int64_t)a * adj_words + w] & ((1u << lane) - 1u)) : 0u;
+  // word-major adjacency: word v of candidate a at adj[v * T + a] (coalesced per warp)
+  const int T = adj_words * 32;
+  for (int v = 0; v < 32; ++v) wv[v] = (valid && v < w) ? adj[(int64_t)v * T + a] : 0u;
+  uint32_t inrow = valid ? (adj[(int64_t)w * T + a] & ((1u << lane) - 1u)) : 0u;
   bool conflict = false;
 #pragma unroll
   for (int v = 0; v < 32; ++v) {
@@ -76,6 +78,8 @@ __global__ void __launch_bounds__(1024) k_resolve(const uint32_t* __restrict__ a
   __shared__ volatile int ready[32];
   __shared__ int wpre[33];
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  pdl_wait();
+  pdl_trigger();   // a single CTA
   const int n_unc = *n_unc_dev;
   const int nc = min(T, n_unc);
   if (tid == 0) {
@@ -128,9 +132,8 @@ cudaError_t launch_resolve(const uint32_t* adj, int adj_words, const int32_t* un
                            int32_t* new_lm, int32_t* dL_dev, DevStats* stats, int32_t* ticket,
                            unsigned long long* band_count, cudaStream_t s, int64_t* launches) {
   ++*launches;
-  k_resolve<<<1, 1024, 0, s>>>(adj, adj_words, unc, n_unc, T, lm_out, L_dev, new_lm, dL_dev,
-                               stats, ticket, band_count);
-  return cudaGetLastError();
+  return launch_pdl(k_resolve, dim3(1), dim3(1024), 0, s, adj, adj_words, unc, n_unc, T, lm_out,
+                    L_dev, new_lm, dL_dev, stats, ticket, band_count);
 }
 
 __global__ void __launch_bounds__(1024) k_resolve_debug(const uint32_t* __restrict__ adj,
@@ -177,6 +180,7 @@ __global__ void __launch_bounds__(CP_NT) k_compact(const uint8_t* __restrict__ c
   __shared__ int s_wcnt[CP_ROUNDS][CP_NT / 32];
   __shared__ int s_excl;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  pdl_wait();   // (multi-wave, ticketed: the next kernel launches as CTAs exit)
   if (tid == 0) s_bid = atomicAdd(ticket, 1);
   __syncthreads();
   const int bid = s_bid;
@@ -255,9 +259,8 @@ cudaError_t launch_compact_unc(const uint8_t* covered, const int32_t* unc, const
                                int64_t n, cudaStream_t s, int64_t* launches) {
   const int64_t nblk = (n + CP_TILE - 1) / CP_TILE;
   ++*launches;
-  k_compact<<<(unsigned)(nblk > 0 ? nblk : 1), CP_NT, 0, s>>>(covered, unc, n_unc, T, unc_next,
-                                                               n_unc_next, state, ticket, tag);
-  return cudaGetLastError();
+  return launch_pdl(k_compact, dim3((unsigned)(nblk > 0 ? nblk : 1)), dim3(CP_NT), 0, s, covered,
+                    unc, n_unc, T, unc_next, n_unc_next, state, ticket, tag);
 }
 
 }  // namespace bm

@@ -17,6 +17,34 @@
 
 namespace bm {
 
+// ------------------------------------------------- programmatic dependent launch
+// Kernels of the dependent chains (greedy tile loop, sorts, CSR, edges) are
+// launched with programmatic stream serialization: the next kernel's launch
+// overlaps the current one's tail, and every such kernel begins with
+// pdl_wait() (griddepcontrol.wait: full completion and memory visibility of
+// the previous grid) before touching its inputs.  pdl_trigger() lets the next
+// kernel start launching.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, ((KArgs)args)...);
+}
+
 // ---------------------------------------------------------------- kinds
 enum Kind : int { K_L2F = 0, K_L1F = 1, K_COSF = 2, K_L2I = 3, K_L1I = 4 };
 
@@ -66,7 +94,8 @@ struct PairArgs {
   const int32_t* l_total_dev; // if non-null: lpos0 = *l_total_dev - (l_end - l_begin)
                               // (fused greedy tile: the new landmarks are the last ones)
   // outputs
-  uint32_t* adj; int adj_words;                 // MODE_ADJ
+  uint32_t* adj; int adj_words;                 // MODE_ADJ: word v of candidate a at
+                                                //   adj[v * (32 * adj_words) + a]
   uint8_t* covered;                             // MODE_MEMBER: covered[p] = 1 for in-ball pairs
   unsigned long long* keys; int64_t key_cap; int lbits;   // MODE_MEMBER: (p << lbits) | j
   int64_t* ties; int64_t tie_cap;               // MODE_MEMBER near-tie triples (host-mapped)

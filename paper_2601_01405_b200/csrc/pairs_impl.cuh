@@ -248,7 +248,7 @@ __device__ __forceinline__ void pairs_block(const PairArgs& A, uint2* sl, int32_
     const int64_t wcol = l0 / 32;
 #pragma unroll
     for (int r = 0; r < R; ++r)
-      if (act[r]) A.adj[qi[r] * (int64_t)A.adj_words + wcol] = word[r];
+      if (act[r]) A.adj[wcol * (int64_t)A.adj_words * 32 + qi[r]] = word[r];   // word-major
   }
 }
 
@@ -275,6 +275,8 @@ __global__ void __launch_bounds__(256) k_pairs(PairArgs A) {
   extern __shared__ uint2 sl[];          // [LC][nu]
   __shared__ int32_t sln[LC];
   __shared__ int32_t slp[LC];
+  pdl_wait();
+  pdl_trigger();   // one wave (ADJ) or persistent (MEMBER)
   // device-resident counts act as caps on the host bounds: actual = min(host, *dev)
   int64_t q_end = A.q_end_dev ? min(A.q_end, (int64_t)*A.q_end_dev) : A.q_end;
   int64_t q_begin = A.q_begin_dev ? min(A.q_begin, (int64_t)*A.q_begin_dev) : A.q_begin;
@@ -338,8 +340,7 @@ cudaError_t launch_pairs_nu(const PairArgs& a, int64_t q_rows_max, cudaStream_t 
     if (gx < 1) gx = 1;
   }
   if (gx > 0x7fffffffLL || gy > 65535) return cudaErrorInvalidConfiguration;
-  kern<<<dim3((unsigned)gx, (unsigned)gy), NT, smem, s>>>(a);
-  return cudaGetLastError();
+  return launch_pdl(kern, dim3((unsigned)gx, (unsigned)gy), dim3(NT), smem, s, a);
 }
 
 template <int KIND, int NU>

@@ -73,6 +73,7 @@ __global__ void __launch_bounds__(SC_NT) k_scan_lb(const int64_t* __restrict__ i
                                                   uint32_t tag) {
   __shared__ int s_tile;
   __shared__ int64_t s_excl;
+  pdl_wait();   // (multi-wave, ticketed: the next kernel launches as CTAs exit)
   if (threadIdx.x == 0) s_tile = atomicAdd(st.ticket, 1);
   __syncthreads();
   const int64_t tile = s_tile;
@@ -148,9 +149,9 @@ cudaError_t exclusive_scan_i64(const int64_t* in, int64_t* out, int64_t n, void*
   st.ticket = (int32_t*)(st.flag + (t + 1));
   cudaError_t e = cudaMemsetAsync(st.flag, 0, sizeof(uint32_t) * (t + 2), s);
   if (e != cudaSuccess) return e;
-  k_scan_lb<<<(unsigned)t, SC_NT, 0, s>>>(in, n, out, total_dev, st, 1u);
   ++*launches;
-  return cudaGetLastError();
+  return launch_pdl(k_scan_lb, dim3((unsigned)t), dim3(SC_NT), 0, s, in, n, out, total_dev, st,
+                    1u);
 }
 
 // ------------------------------------------------------------------ radix sort
@@ -167,6 +168,8 @@ __global__ void __launch_bounds__(RS_NT) k_rs_hist(const unsigned long long* __r
                                                   int64_t n, RsPasses P,
                                                   unsigned long long* __restrict__ hist) {
   __shared__ unsigned h[RS_MAXP][RS_BINS];
+  pdl_wait();
+  pdl_trigger();   // one wave
   for (int p = 0; p < P.np; ++p) h[p][threadIdx.x] = 0u;
   __syncthreads();
   for (int64_t i = (int64_t)blockIdx.x * RS_NT + threadIdx.x; i < n;
@@ -183,6 +186,8 @@ __global__ void __launch_bounds__(RS_NT) k_rs_hist(const unsigned long long* __r
 // digit offsets: off[p][d] = number of keys with a smaller digit in pass p
 __global__ void __launch_bounds__(RS_BINS) k_rs_offsets(const unsigned long long* __restrict__ hist,
                                                        int np, int64_t* __restrict__ off) {
+  pdl_wait();
+  pdl_trigger();
   for (int p = 0; p < np; ++p) {
     int64_t tot;
     const int64_t ex = block_excl_scan<RS_BINS>((int64_t)hist[p * RS_BINS + threadIdx.x], &tot);
@@ -205,6 +210,7 @@ __global__ void __launch_bounds__(RS_NT) k_rs_scatter(const unsigned long long* 
   __shared__ int64_t run[RS_BINS];
   __shared__ int wcnt[RS_NT / 32][RS_BINS];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  pdl_wait();   // (multi-wave, ticketed: the next kernel launches as CTAs exit)
   if (tid == 0) s_tile = atomicAdd(ticket, 1);
   s_hist[tid] = 0u;
   __syncthreads();
@@ -302,15 +308,15 @@ cudaError_t radix_sort_u64(unsigned long long** keys, unsigned long long** alt, 
   if (e == cudaSuccess) e = cudaMemsetAsync(state, 0, sizeof(unsigned long long) * t * RS_BINS, s);
   if (e != cudaSuccess) return e;
   int64_t hg = t < 148 * 4 ? t : 148 * 4;
-  k_rs_hist<<<(unsigned)hg, RS_NT, 0, s>>>(*keys, n, P, hist);
-  k_rs_offsets<<<1, RS_BINS, 0, s>>>(hist, P.np, off);
+  e = launch_pdl(k_rs_hist, dim3((unsigned)hg), dim3(RS_NT), 0, s, *keys, n, P, hist);
+  if (e == cudaSuccess) e = launch_pdl(k_rs_offsets, dim3(1), dim3(RS_BINS), 0, s, hist, P.np, off);
+  if (e != cudaSuccess) return e;
   *launches += 2;
   for (int p = 0; p < P.np; ++p) {
-    k_rs_scatter<<<(unsigned)t, RS_NT, 0, s>>>(*keys, *alt, n, P.shift[p], P.bits[p],
-                                               off + p * RS_BINS, state, tickets + p,
-                                               (uint32_t)(p + 1));
+    e = launch_pdl(k_rs_scatter, dim3((unsigned)t), dim3(RS_NT), 0, s, *keys, *alt, n, P.shift[p],
+                   P.bits[p], (const int64_t*)(off + p * RS_BINS), state, tickets + p,
+                   (uint32_t)(p + 1));
     ++*launches;
-    e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     unsigned long long* tmp = *keys;
     *keys = *alt;

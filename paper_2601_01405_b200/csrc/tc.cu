@@ -327,6 +327,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   __syncthreads();
   fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();   // everything above overlaps the previous kernel's tail
 
   // Work units = (block of RA*128 point rows, chunk of BN-wide landmark tiles),
   // enough units to balance the grid; the column count may live on the device
@@ -470,20 +471,48 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     uint32_t* kc = kcount + ew;
     uint32_t* bc = bcount + ew;
     // flush this warp's staged keys / band pairs to global (warp-collective)
+    // B': one band pair (p << 32 | tile column) re-decided with the oracle's
+    // fp64 formula (ascending coordinates, no contraction); an in-ball pair
+    // becomes a key at once (per-lane, so callable from divergent code)
+    auto recheck = [&](unsigned long long bk) {
+      const int64_t p = (int64_t)(bk >> 32), j = (int64_t)(bk & 0xffffffffull);
+      const int64_t qp = args.lm_idx[j];
+      const float* x = args.xrows + p * (int64_t)args.xstride;
+      const float* y = args.xrows + qp * (int64_t)args.xstride;
+      double sacc = 0.0;
+      for (int k = 0; k < args.d; ++k) {
+        const double t = __dsub_rn((double)x[k], (double)y[k]);
+        sacc = __dadd_rn(sacc, __dmul_rn(t, t));
+      }
+      const bool in = sacc < args.eps2;
+      const double dist = __dsqrt_rn(sacc);
+      if (fabs(dist - args.eps) <= args.tie_rel * args.eps) {
+        const unsigned long long k = atomicAdd(&args.stats->near_ties, 1ull);
+        if ((int64_t)k < args.tie_cap && args.ties) {
+          args.ties[3 * k] = p;
+          args.ties[3 * k + 1] = qp;
+          args.ties[3 * k + 2] = in ? 1 : 0;
+        }
+      }
+      if (in) {
+        if (args.covered) args.covered[p] = 1;
+        const unsigned long long g = atomicAdd(args.key_count, 1ull);
+        if ((int64_t)g < args.key_cap)
+          args.keys[g] = ((unsigned long long)p << args.lbits) | (unsigned long long)(lpos0 + j);
+      }
+    };
     auto flush = [&](void) {
       __syncwarp();
       const uint32_t kn = min(*kc, (uint32_t)S::KW), bn = min(*bc, (uint32_t)S::BW);
-      unsigned long long g0 = 0, g1 = 0;
+      unsigned long long g0 = 0;
       if (lane == 0) {
         if (kn) g0 = atomicAdd(args.key_count, (unsigned long long)kn);
-        if (bn) g1 = atomicAdd(args.band_count, (unsigned long long)bn);
+        if (bn) atomicAdd(&args.stats->band_pairs, (unsigned long long)bn);
       }
       g0 = __shfl_sync(FULLM, g0, 0);
-      g1 = __shfl_sync(FULLM, g1, 0);
       for (uint32_t i = lane; i < kn; i += 32)
         if ((int64_t)(g0 + i) < args.key_cap) args.keys[g0 + i] = kb[i];
-      for (uint32_t i = lane; i < bn; i += 32)
-        if ((int64_t)(g1 + i) < args.band_cap) args.band[g1 + i] = bb[i];
+      for (uint32_t i = lane; i < bn; i += 32) recheck(bb[i]);
       __syncwarp();
       if (lane == 0) {
         *kc = 0;
@@ -491,8 +520,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
       __syncwarp();
     };
-    // append one pair (cls 1: in -> key; cls 2: band -> queue); beyond the
-    // staging capacity it goes straight to global memory
+    // append one pair (cls 1: in -> key; cls 2: band -> staged for the
+    // recheck); beyond the staging capacity it is handled at once
     auto append = [&](int cls, unsigned long long key) {
       uint32_t* cnt = cls == 1 ? kc : bc;
       unsigned long long* buf_s = cls == 1 ? kb : bb;
@@ -500,12 +529,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const uint32_t k = atomicAdd(cnt, 1u);
       if (k < cap) {
         buf_s[k] = key;
+      } else if (cls == 1) {
+        const unsigned long long g = atomicAdd(args.key_count, 1ull);
+        if ((int64_t)g < args.key_cap) args.keys[g] = key;
       } else {
-        unsigned long long* gcnt = cls == 1 ? args.key_count : args.band_count;
-        unsigned long long* gbuf = cls == 1 ? args.keys : args.band;
-        const int64_t gcap = cls == 1 ? args.key_cap : args.band_cap;
-        const unsigned long long g = atomicAdd(gcnt, 1ull);
-        if ((int64_t)g < gcap) gbuf[g] = key;
+        atomicAdd(&args.stats->band_pairs, 1ull);
+        recheck(key);
       }
     };
     uint32_t phase = 0;   // bit b: parity of the next completion of buffer b
@@ -737,8 +766,8 @@ static cudaError_t launch_cfg(const TcPlan& P, TcArgs a, cudaStream_t s) {
     if (a.n_mblk * chunks < grid) grid = a.n_mblk * chunks;
   }
   if (grid < 1) grid = 1;
-  kern<<<(unsigned)grid, TC_THREADS, S::TOTAL, s>>>(tA, tB, tK, tO, a);
-  return cudaGetLastError();
+  return launch_pdl(kern, dim3((unsigned)grid), dim3(TC_THREADS), (size_t)S::TOTAL, s, tA, tB,
+                    tK, tO, a);
 }
 
 // Configuration table: every configuration
@@ -887,53 +916,6 @@ __global__ void k_tc_cols_int(const int32_t* __restrict__ nrm, const int32_t* __
   cc[j] = j < L ? nrm[lm[j]] : (1 << 30);
 }
 
-// B': exact fp64 decision for every queued band pair (p << 32 | j), the
-// oracle's formula operation for operation; in-ball pairs join the keys.
-__global__ void k_tc_recheck(const unsigned long long* __restrict__ band, int64_t nb,
-                             const float* __restrict__ X, int xstride, int d,
-                             const int32_t* __restrict__ lm,
-                             double eps, double eps2, double tie_rel, int lbits,
-                             unsigned long long* keys, unsigned long long* key_count,
-                             int64_t key_cap, int64_t* ties, int64_t tie_cap,
-                             DevStats* stats) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  bool in = false;
-  int64_t p = 0, j = 0;
-  if (i < nb) {
-    p = (int64_t)(band[i] >> 32);
-    j = (int64_t)(band[i] & 0xffffffffull);
-    const int64_t q = lm[j];
-    const float* x = X + p * (int64_t)xstride;
-    const float* y = X + q * (int64_t)xstride;
-    double s = 0.0;
-    for (int k = 0; k < d; ++k) {
-      double t = __dsub_rn((double)x[k], (double)y[k]);
-      s = __dadd_rn(s, __dmul_rn(t, t));
-    }
-    in = s < eps2;
-    const double dist = __dsqrt_rn(s);
-    if (fabs(dist - eps) <= tie_rel * eps) {
-      unsigned long long k = atomicAdd(&stats->near_ties, 1ull);
-      if ((int64_t)k < tie_cap && ties) {
-        ties[3 * k] = p;
-        ties[3 * k + 1] = q;
-        ties[3 * k + 2] = in ? 1 : 0;
-      }
-    }
-  }
-  const unsigned m = __ballot_sync(FULLM, in);
-  if (m) {
-    const int lane = threadIdx.x & 31;
-    unsigned long long base = 0;
-    if (lane == 0) base = atomicAdd(key_count, (unsigned long long)__popc(m));
-    base = __shfl_sync(FULLM, base, 0);
-    if (in) {
-      const unsigned long long k = base + __popc(m & ((1u << lane) - 1u));
-      if ((int64_t)k < key_cap) keys[k] = ((unsigned long long)p << lbits) | (unsigned long long)j;
-    }
-  }
-}
-
 // Fused greedy tile: landmark operand rows + column constants for the tile's
 // new landmarks (count on the device); columns >= count are inert.
 __global__ void k_tc_tile_lm(const uint8_t* __restrict__ xop, int64_t row_bytes,
@@ -942,6 +924,8 @@ __global__ void k_tc_tile_lm(const uint8_t* __restrict__ xop, int64_t row_bytes,
                              const void* __restrict__ nrm, double C2, uint8_t* __restrict__ lop,
                              float* __restrict__ ca, float* __restrict__ cb,
                              float* __restrict__ colk, int32_t* __restrict__ cc) {
+  pdl_wait();
+  pdl_trigger();   // one wave
   const int64_t j = blockIdx.x;
   const int64_t cnt = *l_count_dev;
   const bool live = j < cnt;
@@ -964,87 +948,12 @@ cudaError_t launch_tc_tile_landmarks(const TcPlan& P, const void* nrm, const int
                                      const int32_t* l_count_dev, double C2, TcArgs& a,
                                      cudaStream_t s, int64_t* launches) {
   ++*launches;
-  k_tc_tile_lm<<<(unsigned)P.l_rows, 64, 0, s>>>(
-      (const uint8_t*)P.xop, P.row_bytes, new_lm, l_count_dev, P.kind, nrm, C2,
-      (uint8_t*)P.lop, (float*)a.col_a, (float*)a.col_b, (float*)a.colk, (int32_t*)a.col_c);
-  return cudaGetLastError();
+  return launch_pdl(k_tc_tile_lm, dim3((unsigned)P.l_rows), dim3(64), 0, s,
+                    (const uint8_t*)P.xop, P.row_bytes, new_lm, l_count_dev, P.kind, nrm, C2,
+                    (uint8_t*)P.lop, (float*)a.col_a, (float*)a.col_b, (float*)a.colk,
+                    (int32_t*)a.col_c);
 }
 
-// B' for a fused greedy tile: grid-stride over the device-side band count;
-// in-ball pairs join the keys and mark coverage.
-__global__ void k_tc_recheck_tile(const unsigned long long* __restrict__ band,
-                                  const unsigned long long* __restrict__ band_count,
-                                  int64_t band_cap, const float* __restrict__ X, int xstride,
-                                  int d, const int32_t* __restrict__ lm,
-                                  const int32_t* __restrict__ l_count_dev,
-                                  const int32_t* __restrict__ l_total_dev, double eps,
-                                  double eps2, double tie_rel, unsigned long long* keys,
-                                  unsigned long long* key_count, int64_t key_cap,
-                                  uint8_t* covered, int64_t* ties, int64_t tie_cap,
-                                  DevStats* stats) {
-  const int64_t nb = min((int64_t)*band_count, band_cap);
-  const int64_t lpos0 = (int64_t)*l_total_dev - (int64_t)*l_count_dev;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < nb; base += stride) {
-    const int64_t i = base + threadIdx.x;
-    bool in = false;
-    int64_t p = 0, j = 0;
-    if (i < nb) {
-      p = (int64_t)(band[i] >> 32);
-      j = (int64_t)(band[i] & 0xffffffffull);
-      const int64_t q = lm[j];
-      const float* x = X + p * (int64_t)xstride;
-      const float* y = X + q * (int64_t)xstride;
-      double sacc = 0.0;
-      for (int k = 0; k < d; ++k) {
-        double t = __dsub_rn((double)x[k], (double)y[k]);
-        sacc = __dadd_rn(sacc, __dmul_rn(t, t));
-      }
-      in = sacc < eps2;
-      const double dist = __dsqrt_rn(sacc);
-      if (fabs(dist - eps) <= tie_rel * eps) {
-        unsigned long long k = atomicAdd(&stats->near_ties, 1ull);
-        if ((int64_t)k < tie_cap && ties) {
-          ties[3 * k] = p;
-          ties[3 * k + 1] = q;
-          ties[3 * k + 2] = in ? 1 : 0;
-        }
-      }
-      if (in) covered[p] = 1;
-    }
-    const unsigned m = __ballot_sync(FULLM, in);
-    if (m) {
-      const int lane = threadIdx.x & 31;
-      unsigned long long b = 0;
-      if (lane == 0) b = atomicAdd(key_count, (unsigned long long)__popc(m));
-      b = __shfl_sync(FULLM, b, 0);
-      if (in) {
-        const unsigned long long k = b + __popc(m & ((1u << lane) - 1u));
-        if ((int64_t)k < key_cap) keys[k] = ((unsigned long long)p << 32) | (unsigned long long)(lpos0 + j);
-      }
-    }
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    atomicAdd(&stats->band_pairs, (unsigned long long)nb);
-    if ((int64_t)*band_count > band_cap) stats->overflow = 1;
-  }
-}
-
-cudaError_t launch_tc_recheck_tile(const unsigned long long* band,
-                                   const unsigned long long* band_count, int64_t band_cap,
-                                   const float* X, int xstride, int d, const int32_t* lm,
-                                   const int32_t* l_count_dev, const int32_t* l_total_dev,
-                                   const Thresh& th, unsigned long long* keys,
-                                   unsigned long long* key_count, int64_t key_cap,
-                                   uint8_t* covered, int64_t* ties, int64_t tie_cap,
-                                   DevStats* stats, int num_sms, cudaStream_t s,
-                                   int64_t* launches) {
-  ++*launches;
-  k_tc_recheck_tile<<<(unsigned)(2 * num_sms), 256, 0, s>>>(
-      band, band_count, band_cap, X, xstride, d, lm, l_count_dev, l_total_dev, th.eps, th.eps2,
-      th.tie_rel, keys, key_count, key_cap, covered, ties, tie_cap, stats);
-  return cudaGetLastError();
-}
 
 __global__ void k_tc_ones(float* o) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1096,18 +1005,6 @@ cudaError_t launch_tc_landmarks(const TcPlan& P, const void* nrm, const int32_t*
   return cudaGetLastError();
 }
 
-cudaError_t launch_tc_recheck(const unsigned long long* band, int64_t nb, const float* X,
-                              int xstride, int d, const int32_t* lm, const Thresh& th, int lbits,
-                              unsigned long long* keys, unsigned long long* key_count,
-                              int64_t key_cap, int64_t* ties, int64_t tie_cap, DevStats* stats,
-                              cudaStream_t s, int64_t* launches) {
-  if (nb <= 0) return cudaSuccess;
-  ++*launches;
-  k_tc_recheck<<<(unsigned)((nb + 255) / 256), 256, 0, s>>>(
-      band, nb, X, xstride, d, lm, th.eps, th.eps2, th.tie_rel, lbits, keys, key_count, key_cap, ties,
-      tie_cap, stats);
-  return cudaGetLastError();
-}
 
 }  // namespace tc
 }  // namespace bm

@@ -51,9 +51,16 @@ struct TcArgs {
   unsigned long long* keys;
   unsigned long long* key_count;
   int64_t key_cap;
-  unsigned long long* band;
-  unsigned long long* band_count;
-  int64_t band_cap;
+  // B' (tf32): band pairs are re-decided inside the epilogue with the oracle's
+  // fp64 formula on the original fp32 rows
+  const float* xrows;  // [rows][xstride] fp32 coordinates (first d used)
+  int xstride;
+  int d;
+  double eps, eps2, tie_rel;
+  const int32_t* lm_idx;   // landmark column -> point index
+  int64_t* ties;           // near-tie triples (point, landmark point, decision)
+  int64_t tie_cap;
+  DevStats* stats;         // band_pairs / near_ties counters
   uint32_t* gram;      // debug: raw accumulators [n][L]
   uint8_t* covered;    // fused greedy: covered[p] = 1 for every in-ball pair (may be null)
 };
@@ -76,26 +83,9 @@ cudaError_t launch_tc_landmarks(const TcPlan& P, const void* nrm, const int32_t*
 cudaError_t launch_tc_tile_landmarks(const TcPlan& P, const void* nrm, const int32_t* new_lm,
                                      const int32_t* l_count_dev, double C2, TcArgs& a,
                                      cudaStream_t s, int64_t* launches);
-// Band recheck with a device-side pair count (persistent grid-stride), for the
-// fused greedy tile: band keys are (p << 32 | tile column), lm = the tile's
-// landmark point indices, positions = *l_total_dev - *l_count_dev + column.
-cudaError_t launch_tc_recheck_tile(const unsigned long long* band,
-                                   const unsigned long long* band_count, int64_t band_cap,
-                                   const float* X, int xstride, int d, const int32_t* lm,
-                                   const int32_t* l_count_dev, const int32_t* l_total_dev,
-                                   const Thresh& th, unsigned long long* keys,
-                                   unsigned long long* key_count, int64_t key_cap,
-                                   uint8_t* covered, int64_t* ties, int64_t tie_cap,
-                                   DevStats* stats, int num_sms, cudaStream_t s,
-                                   int64_t* launches);
 cudaError_t launch_tc(const TcPlan& P, const TcArgs& a, cudaStream_t s, int64_t* launches);
 // diagnostics: the contraction with a probe epilogue (TC_MODE_PROBE_*), tf32 K <= 64 only
 cudaError_t launch_tc_probe(const TcPlan& P, const TcArgs& a, int mode, cudaStream_t s);
-cudaError_t launch_tc_recheck(const unsigned long long* band, int64_t nb, const float* X,
-                              int xstride, int d, const int32_t* lm, const Thresh& th, int lbits,
-                              unsigned long long* keys, unsigned long long* key_count,
-                              int64_t key_cap, int64_t* ties, int64_t tie_cap, DevStats* stats,
-                              cudaStream_t s, int64_t* launches);
 
 }  // namespace tc
 }  // namespace bm
