@@ -294,6 +294,9 @@ def run_ours(args):
     clocks = sampler.stop()
     step_ms = [a.elapsed_time(b) for a, b in ev]
     ms = sum(step_ms) / len(step_ms)
+    ss = sorted(step_ms)
+    step_stats = {"min": round(ss[0], 4), "median": round(ss[len(ss) // 2], 4),
+                  "max": round(ss[-1], 4)}
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -350,6 +353,7 @@ def run_ours(args):
                            last.path_used], "l2": "flushed (256 MiB write) before each step",
                        "parallelism": "replicas" if world > 1 else "single"},
             "cover_ms": round(ms, 4),
+            "step_ms_stats": step_stats,
             "breakdown_ms": breakdown,
             "greedy": {"tiles": int(last.n_greedy_tiles), "evals": int(last.n_greedy_evals),
                        "band_pairs": int(last.n_band_pairs), "near_ties": int(last.n_near_ties)},

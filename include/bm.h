@@ -76,7 +76,7 @@ enum {
 
 /* Execution path for the membership / coverage contraction. */
 typedef enum bm_path {
-  BM_PATH_AUTO = 0,     /* tensor cores for L2 with d >= 32, CUDA cores otherwise */
+  BM_PATH_AUTO = 0,     /* tensor cores for L2 with d >= 32 or n >= 32768, else CUDA cores */
   BM_PATH_CUDA_CORE = 1,
   BM_PATH_TENSOR = 2    /* tcgen05 (L2 only; falls back to BM_EUNSUPPORTED otherwise) */
 } bm_path;

@@ -381,8 +381,12 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
     P.k_elems = P.row_bytes / esz;
     P.katoms = (int)((P.row_bytes + 127) / 128);
   }
+  // AUTO: tensor cores for Euclidean when the rows are wide or numerous
+  // enough to fill the 128 x 256 tiles (measured: C2, d = 10, n = 1e5, is
+  // faster on tcgen05; C1, n = 2e3, on CUDA cores)
   bool use_tc = metric == BM_L2 && tc::tc_supported(P.kind, P.katoms) &&
-                (o.path == BM_PATH_TENSOR || (o.path == BM_PATH_AUTO && d >= 32));
+                (o.path == BM_PATH_TENSOR ||
+                 (o.path == BM_PATH_AUTO && (d >= 32 || n >= 32768)));
   if (o.path == BM_PATH_TENSOR && !use_tc)
     return set_err(BM_EUNSUPPORTED, "tensor-core path supports L2 with d*elem <= %d bytes",
                    dtype == BM_F32 ? 512 : 896);
@@ -656,48 +660,67 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
   pool.free_now(rtemp);
   tm.mark(4);
 
-  // ---- D1-D3 edges
-  int64_t *pcnt = nullptr, *poff = nullptr, *ptot = nullptr;
-  void* stemp = nullptr;
-  TRY(pool.alloc(&pcnt, (size_t)n));
-  TRY(pool.alloc(&poff, (size_t)n));
-  TRY(pool.alloc(&ptot, 2));
-  TRY(pool.alloc((uint8_t**)&stemp, scan_temp_bytes(n)));
-  CK(launch_pair_counts(pt_ptr, n, pcnt, s, &launches));
-  CK(exclusive_scan_i64(pcnt, poff, n, stemp, ptot, s, &launches));
+  // ---- D1-D3 edges (edges.cu)
   int64_t NP = 0;  // P = sum_p C(t_p, 2) witnessed pairs
-  CK(cudaMemcpyAsync(&NP, ptot, sizeof NP, cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
   int64_t E = 0;
   int32_t* edges = nullptr;
-  if (NP > 0) {
-    unsigned long long *ek = nullptr, *ea = nullptr;
-    int64_t *flags = nullptr, *pos = nullptr;
-    void *et = nullptr, *ft = nullptr;
-    TRY(pool.alloc(&ek, (size_t)NP));
-    TRY(pool.alloc(&ea, (size_t)NP));
-    TRY(pool.alloc((uint8_t**)&et, radix_temp_bytes(NP)));
-    CK(launch_pair_emit(pt_ptr, pt_lm, n, poff, lbits, ek, s, &launches));
-    const BitRange er[1] = {{0, 2 * lbits}};
-    CK(radix_sort_u64(&ek, &ea, NP, er, 1, et, s, &launches));
-    TRY(pool.alloc(&flags, (size_t)NP));
-    TRY(pool.alloc(&pos, (size_t)NP));
-    TRY(pool.alloc((uint8_t**)&ft, scan_temp_bytes(NP)));
-    CK(launch_unique_flags(ek, NP, flags, s, &launches));
-    CK(exclusive_scan_i64(flags, pos, NP, ft, ptot + 1, s, &launches));
-    CK(cudaMemcpyAsync(&E, ptot + 1, sizeof E, cudaMemcpyDeviceToHost, s));
+  int64_t* ptot = nullptr;
+  TRY(pool.alloc(&ptot, 2));
+  if (L >= 2 && L <= kEdgeBitmapMaxL) {
+    // L x L bit matrix: no pair buffer, no sort; one host sync for (P, E)
+    uint32_t* bits = nullptr;
+    void* etemp = nullptr;
+    const int64_t cap = L * (L - 1) / 2;
+    TRY(pool.alloc(&bits, (size_t)edge_bitmap_words(L)));
+    TRY(pool.alloc((uint8_t**)&etemp, edge_lb_temp_bytes(edge_bitmap_words(L))));
+    TRY(pool.alloc(&edges, (size_t)(2 * cap)));
+    CK(launch_edge_bits(pt_ptr, pt_lm, n, L, bits, (unsigned long long*)ptot, s, &launches));
+    CK(launch_bits_compact(bits, L, edges, cap, ptot + 1, etemp, s, &launches));
+    int64_t h2[2];
+    CK(cudaMemcpyAsync(h2, ptot, sizeof h2, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    TRY(pool.alloc(&edges, (size_t)(2 * E > 0 ? 2 * E : 1)));
-    CK(launch_unique_scatter(ek, NP, pos, lbits, edges, s, &launches));
-    pool.free_now(ek);
-    pool.free_now(ea);
-    pool.free_now(flags);
-    pool.free_now(pos);
-    pool.free_now(et);
-    pool.free_now(ft);
-  } else {
-    TRY(pool.alloc(&edges, 1));
+    NP = h2[0];
+    E = h2[1];
+    pool.free_now(bits);
+    pool.free_now(etemp);
+  } else if (L >= 2) {
+    int64_t *pcnt = nullptr, *poff = nullptr;
+    void* stemp = nullptr;
+    TRY(pool.alloc(&pcnt, (size_t)n));
+    TRY(pool.alloc(&poff, (size_t)n));
+    TRY(pool.alloc((uint8_t**)&stemp, scan_temp_bytes(n)));
+    CK(launch_pair_counts(pt_ptr, n, pcnt, s, &launches));
+    CK(exclusive_scan_i64(pcnt, poff, n, stemp, ptot, s, &launches));
+    CK(cudaMemcpyAsync(&NP, ptot, sizeof NP, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (NP > 0) {
+      unsigned long long *ek = nullptr, *ea = nullptr;
+      int32_t* etmp = nullptr;
+      void *et = nullptr, *ct = nullptr;
+      TRY(pool.alloc(&ek, (size_t)NP));
+      TRY(pool.alloc(&ea, (size_t)NP));
+      TRY(pool.alloc((uint8_t**)&et, radix_temp_bytes(NP)));
+      CK(launch_pair_emit(pt_ptr, pt_lm, n, poff, lbits, ek, s, &launches));
+      const BitRange er[1] = {{0, 2 * lbits}};
+      CK(radix_sort_u64(&ek, &ea, NP, er, 1, et, s, &launches));
+      pool.free_now(et);
+      etmp = (int32_t*)ea;   // the sort's spare buffer holds 2 NP int32
+      TRY(pool.alloc((uint8_t**)&ct, edge_lb_temp_bytes(NP)));
+      CK(launch_unique_compact(ek, NP, lbits, etmp, ptot + 1, ct, s, &launches));
+      CK(cudaMemcpyAsync(&E, ptot + 1, sizeof E, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      TRY(pool.alloc(&edges, (size_t)(2 * E > 0 ? 2 * E : 1)));
+      if (E > 0)
+        CK(cudaMemcpyAsync(edges, etmp, sizeof(int32_t) * 2 * E, cudaMemcpyDeviceToDevice, s));
+      pool.free_now(ek);
+      pool.free_now(ea);
+      pool.free_now(ct);
+    }
+    pool.free_now(pcnt);
+    pool.free_now(poff);
+    pool.free_now(stemp);
   }
+  if (!edges) TRY(pool.alloc(&edges, 1));
   int32_t* landmarks = nullptr;
   TRY(pool.alloc(&landmarks, (size_t)(L > 0 ? L : 1)));
   CK(launch_copy_i32(lm, landmarks, L, s, &launches));

@@ -1,0 +1,238 @@
+// edges.cu — steps D1-D3 (the nerve's 1-skeleton, Def 2.2 / PAPER.md:84-92):
+// landmarks i < j are joined iff some data point lies in both balls, i.e. iff
+// (i, j) is a pair of some point's ascending landmark row pt_lm[p] (the
+// "∩ X ≠ ∅" witness).
+//
+// Two device paths, both producing edges[E][2] in lexicographic order:
+//   bitmap (L <= BM_EDGE_BITMAP_MAX_L): every witnessed pair sets bit (i, j)
+//     of an L x L bit matrix (atomicOr), and one look-back compaction walks
+//     the words in row-major order writing (i, j) for every set bit — no sort;
+//   keys (large L): pair keys i << lbits | j are radix sorted (sort.cu) and
+//     one look-back compaction keeps the first of each run of equal keys.
+#include "internal.cuh"
+
+namespace bm {
+
+constexpr unsigned FME = 0xffffffffu;
+constexpr unsigned long long LB_AGG = 1ull, LB_INC = 2ull;
+
+__device__ __forceinline__ unsigned long long lb_pack(uint32_t tag, unsigned long long flag,
+                                                      uint32_t v) {
+  return ((unsigned long long)tag << 34) | (flag << 32) | (unsigned long long)v;
+}
+
+// Decoupled look-back (thread 0 of the CTA): publish this tile's aggregate,
+// return the sum of all earlier tiles' aggregates, publish the inclusive prefix.
+__device__ __forceinline__ uint32_t lookback_excl(unsigned long long* state, int64_t tile,
+                                                  uint32_t tag, uint32_t agg) {
+  volatile unsigned long long* st = state;
+  if (tile == 0) {
+    st[0] = lb_pack(tag, LB_INC, agg);
+    return 0u;
+  }
+  st[tile] = lb_pack(tag, LB_AGG, agg);
+  uint32_t excl = 0u;
+  for (int64_t j = tile - 1; j >= 0; --j) {
+    unsigned long long v;
+    do {
+      v = st[j];
+    } while ((uint32_t)(v >> 34) != tag || ((v >> 32) & 3ull) == 0ull);
+    excl += (uint32_t)v;
+    if (((v >> 32) & 3ull) == LB_INC) break;
+  }
+  st[tile] = lb_pack(tag, LB_INC, excl + agg);
+  return excl;
+}
+
+// ---------------------------------------------------------------- bitmap path
+// One warp per point: set bit (i, j) for every pair a < c of its row.
+__global__ void k_edge_bits(const int64_t* __restrict__ pt_ptr, const int32_t* __restrict__ pt_lm,
+                            int64_t n, int W, uint32_t* __restrict__ bits,
+                            unsigned long long* __restrict__ npairs) {
+  pdl_wait();
+  const int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (p >= n) return;
+  const int64_t b = pt_ptr[p], t = pt_ptr[p + 1] - b;
+  if (t < 2) return;
+  if (lane == 0) atomicAdd(npairs, (unsigned long long)(t * (t - 1) / 2));
+  for (int64_t a = 0; a + 1 < t; ++a) {
+    const int64_t i = pt_lm[b + a];
+    uint32_t* row = bits + i * (int64_t)W;
+    for (int64_t c = a + 1 + lane; c < t; c += 32) {
+      const int32_t j = pt_lm[b + c];
+      atomicOr(row + (j >> 5), 1u << (j & 31));
+    }
+  }
+}
+
+// Row-major walk of the bit matrix: CTA tile = 256 threads x 4 consecutive
+// words each; edges written in (i, j) order.
+constexpr int EB_NT = 256, EB_WPT = 4, EB_TILE = EB_NT * EB_WPT;
+
+__global__ void __launch_bounds__(EB_NT) k_bits_compact(const uint32_t* __restrict__ bits,
+                                                       int64_t nwords, int W,
+                                                       int32_t* __restrict__ edges,
+                                                       int64_t cap, int64_t* __restrict__ total,
+                                                       unsigned long long* state,
+                                                       int32_t* ticket, uint32_t tag) {
+  __shared__ int s_tile;
+  __shared__ uint32_t s_warp[EB_NT / 32];
+  __shared__ uint32_t s_excl;
+  pdl_wait();
+  if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1);
+  __syncthreads();
+  const int64_t tile = s_tile;
+  const int64_t w0 = tile * EB_TILE + (int64_t)threadIdx.x * EB_WPT;
+  uint32_t wv[EB_WPT];
+  uint32_t cnt = 0;
+#pragma unroll
+  for (int k = 0; k < EB_WPT; ++k) {
+    wv[k] = w0 + k < nwords ? bits[w0 + k] : 0u;
+    cnt += __popc(wv[k]);
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(FME, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) s_warp[w] = incl;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t agg = 0;
+    for (int k = 0; k < EB_NT / 32; ++k) agg += s_warp[k];
+    const uint32_t ex = lookback_excl(state, tile, tag, agg);
+    s_excl = ex;
+    if ((tile + 1) * EB_TILE >= nwords) *total = (int64_t)ex + agg;
+  }
+  __syncthreads();
+  int64_t pos = s_excl + incl - cnt;
+  for (int k = 0; k < w; ++k) pos += s_warp[k];
+#pragma unroll
+  for (int k = 0; k < EB_WPT; ++k) {
+    uint32_t v = wv[k];
+    const int64_t word = w0 + k;
+    const int32_t i = (int32_t)(word / W);
+    const int32_t jb = (int32_t)(word % W) * 32;
+    while (v) {
+      const int b = __ffs(v) - 1;
+      v &= v - 1u;
+      if (pos < cap) {
+        edges[2 * pos] = i;
+        edges[2 * pos + 1] = jb + b;
+      }
+      ++pos;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- keys path
+// Sorted keys i << lbits | j: keep the first of every run, in order.
+constexpr int UQ_NT = 256, UQ_IPT = 8, UQ_TILE = UQ_NT * UQ_IPT;
+
+__global__ void __launch_bounds__(UQ_NT) k_unique_compact(const unsigned long long* __restrict__ keys,
+                                                         int64_t m, int lbits,
+                                                         int32_t* __restrict__ edges,
+                                                         int64_t* __restrict__ total,
+                                                         unsigned long long* state,
+                                                         int32_t* ticket, uint32_t tag) {
+  __shared__ int s_tile;
+  __shared__ uint32_t s_warp[UQ_NT / 32];
+  __shared__ uint32_t s_excl;
+  pdl_wait();
+  if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1);
+  __syncthreads();
+  const int64_t tile = s_tile;
+  const int64_t i0 = tile * UQ_TILE + (int64_t)threadIdx.x * UQ_IPT;
+  unsigned long long kv[UQ_IPT];
+  uint32_t keep = 0u, cnt = 0u;
+#pragma unroll
+  for (int k = 0; k < UQ_IPT; ++k) {
+    const int64_t i = i0 + k;
+    kv[k] = i < m ? keys[i] : 0ull;
+    const bool f = i < m && (i == 0 || kv[k] != (k > 0 ? kv[k - 1] : keys[i - 1]));
+    keep |= (f ? 1u : 0u) << k;
+    cnt += f ? 1u : 0u;
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(FME, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) s_warp[w] = incl;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t agg = 0;
+    for (int k = 0; k < UQ_NT / 32; ++k) agg += s_warp[k];
+    const uint32_t ex = lookback_excl(state, tile, tag, agg);
+    s_excl = ex;
+    if ((tile + 1) * UQ_TILE >= m) *total = (int64_t)ex + agg;
+  }
+  __syncthreads();
+  int64_t pos = s_excl + incl - cnt;
+  for (int k = 0; k < w; ++k) pos += s_warp[k];
+  const unsigned long long lm = (1ull << lbits) - 1ull;
+#pragma unroll
+  for (int k = 0; k < UQ_IPT; ++k) {
+    if ((keep >> k) & 1u) {
+      edges[2 * pos] = (int32_t)(kv[k] >> lbits);
+      edges[2 * pos + 1] = (int32_t)(kv[k] & lm);
+      ++pos;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- host side
+int64_t edge_bitmap_words(int64_t L) { return L * ((L + 31) / 32); }
+
+size_t edge_lb_temp_bytes(int64_t items) {
+  const int64_t t = (items + 1023) / 1024 + 2;
+  return (size_t)t * 8 + 64;
+}
+
+cudaError_t launch_edge_bits(const int64_t* pt_ptr, const int32_t* pt_lm, int64_t n, int64_t L,
+                             uint32_t* bits, unsigned long long* npairs, cudaStream_t s,
+                             int64_t* launches) {
+  const int W = (int)((L + 31) / 32);
+  cudaError_t e = cudaMemsetAsync(bits, 0, sizeof(uint32_t) * edge_bitmap_words(L), s);
+  if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(npairs, 0, sizeof(unsigned long long), s);
+  if (e != cudaSuccess) return e;
+  ++*launches;
+  int64_t g = (n * 32 + 255) / 256;
+  return launch_pdl(k_edge_bits, dim3((unsigned)(g > 0 ? g : 1)), dim3(256), 0, s, pt_ptr, pt_lm,
+                    n, W, bits, npairs);
+}
+
+cudaError_t launch_bits_compact(const uint32_t* bits, int64_t L, int32_t* edges, int64_t cap,
+                                int64_t* total, void* temp, cudaStream_t s, int64_t* launches) {
+  const int W = (int)((L + 31) / 32);
+  const int64_t nwords = edge_bitmap_words(L);
+  const int64_t t = (nwords + EB_TILE - 1) / EB_TILE;
+  int32_t* ticket = (int32_t*)temp;
+  unsigned long long* state = (unsigned long long*)((char*)temp + 64);
+  cudaError_t e = cudaMemsetAsync(temp, 0, 64 + sizeof(unsigned long long) * (t + 1), s);
+  if (e != cudaSuccess) return e;
+  ++*launches;
+  return launch_pdl(k_bits_compact, dim3((unsigned)(t > 0 ? t : 1)), dim3(EB_NT), 0, s, bits,
+                    nwords, W, edges, cap, total, state, ticket, 1u);
+}
+
+cudaError_t launch_unique_compact(const unsigned long long* keys, int64_t m, int lbits,
+                                  int32_t* edges, int64_t* total, void* temp, cudaStream_t s,
+                                  int64_t* launches) {
+  const int64_t t = (m + UQ_TILE - 1) / UQ_TILE;
+  int32_t* ticket = (int32_t*)temp;
+  unsigned long long* state = (unsigned long long*)((char*)temp + 64);
+  cudaError_t e = cudaMemsetAsync(temp, 0, 64 + sizeof(unsigned long long) * (t + 1), s);
+  if (e != cudaSuccess) return e;
+  ++*launches;
+  return launch_pdl(k_unique_compact, dim3((unsigned)(t > 0 ? t : 1)), dim3(UQ_NT), 0, s, keys,
+                    m, lbits, edges, total, state, ticket, 1u);
+}
+
+}  // namespace bm

@@ -165,6 +165,18 @@ cudaError_t launch_unique_flags(const unsigned long long* keys, int64_t m, int64
 cudaError_t launch_unique_scatter(const unsigned long long* keys, int64_t m,
                                   const int64_t* pos, int lbits, int32_t* edges,
                                   cudaStream_t s, int64_t* launches);
+// edges.cu: bitmap path for L <= kEdgeBitmapMaxL, keys path (sort + unique) above
+constexpr int64_t kEdgeBitmapMaxL = 4096;
+int64_t edge_bitmap_words(int64_t L);
+size_t edge_lb_temp_bytes(int64_t items);
+cudaError_t launch_edge_bits(const int64_t* pt_ptr, const int32_t* pt_lm, int64_t n, int64_t L,
+                             uint32_t* bits, unsigned long long* npairs, cudaStream_t s,
+                             int64_t* launches);
+cudaError_t launch_bits_compact(const uint32_t* bits, int64_t L, int32_t* edges, int64_t cap,
+                                int64_t* total, void* temp, cudaStream_t s, int64_t* launches);
+cudaError_t launch_unique_compact(const unsigned long long* keys, int64_t m, int lbits,
+                                  int32_t* edges, int64_t* total, void* temp, cudaStream_t s,
+                                  int64_t* launches);
 cudaError_t launch_copy_i32(const int32_t* src, int32_t* dst, int64_t n, cudaStream_t s,
                             int64_t* launches);
 

@@ -11,7 +11,7 @@
 // Radix sort ("onesweep" structure): 8-bit digits over a list of bit ranges.
 // (1) one histogram kernel reads the keys once and counts every pass's
 // digits; (2) one CTA turns them into global digit offsets; (3) one scatter
-// kernel per pass: a CTA takes a 4096-key tile by ticket, counts its digits,
+// kernel per pass: a CTA takes a 1024- or 4096-key tile by ticket, counts its digits,
 // publishes them per digit, looks back per digit (thread d walks digit d) for
 // the count of equal digits in earlier tiles, and scatters its keys in input
 // order (ranks within the tile come from __match_any_sync peers plus per-warp
@@ -155,8 +155,12 @@ cudaError_t exclusive_scan_i64(const int64_t* in, int64_t* out, int64_t n, void*
 }
 
 // ------------------------------------------------------------------ radix sort
-constexpr int RS_NT = 256, RS_ROUNDS = 16, RS_TILE = RS_NT * RS_ROUNDS, RS_BINS = 256;
+// Tiles of RS_NT x ROUNDS keys: 1024 for inputs below 2^22 keys (more CTAs,
+// shorter per-CTA chains), 4096 above (fewer look-back descriptors).
+constexpr int RS_NT = 256, RS_BINS = 256;
 constexpr int RS_MAXP = 8;   // 64 bits / 8
+constexpr int64_t RS_SMALL = (int64_t)1 << 22;
+static inline int rs_rounds(int64_t n) { return n < RS_SMALL ? 4 : 16; }
 
 struct RsPasses {
   int np;
@@ -199,6 +203,7 @@ __device__ __forceinline__ unsigned long long rs_pack(uint32_t tag, uint32_t fla
   return ((unsigned long long)tag << 34) | ((unsigned long long)flag << 32) | v;
 }
 
+template <int RS_ROUNDS>
 __global__ void __launch_bounds__(RS_NT) k_rs_scatter(const unsigned long long* __restrict__ in,
                                                      unsigned long long* __restrict__ out,
                                                      int64_t n, int shift, int bits,
@@ -214,6 +219,7 @@ __global__ void __launch_bounds__(RS_NT) k_rs_scatter(const unsigned long long* 
   if (tid == 0) s_tile = atomicAdd(ticket, 1);
   s_hist[tid] = 0u;
   __syncthreads();
+  constexpr int RS_TILE = RS_NT * RS_ROUNDS;
   const int64_t tile = s_tile;
   const int64_t t0 = tile * RS_TILE;
   const unsigned mask = (1u << bits) - 1u;
@@ -276,11 +282,16 @@ __global__ void __launch_bounds__(RS_NT) k_rs_scatter(const unsigned long long* 
   }
 }
 
-static int64_t rs_tiles(int64_t n) { return (n + RS_TILE - 1) / RS_TILE; }
+static int64_t rs_tiles(int64_t n) {
+  const int64_t tile = (int64_t)RS_NT * rs_rounds(n);
+  return (n + tile - 1) / tile;
+}
 
+// temp layout: off [MAXP][BINS] | hist [MAXP][BINS] | tickets [64] | state [tiles][BINS]
+// (hist .. state is one contiguous region cleared by one memset)
 size_t radix_temp_bytes(int64_t n) {
   const int64_t t = rs_tiles(n) > 0 ? rs_tiles(n) : 1;
-  return (size_t)RS_MAXP * RS_BINS * (8 + 8)      // hist, off
+  return (size_t)RS_MAXP * RS_BINS * (8 + 8)      // off, hist
          + 64 * sizeof(int32_t)                     // tickets
          + (size_t)t * RS_BINS * 8 + 256;           // look-back descriptors
 }
@@ -299,13 +310,15 @@ cudaError_t radix_sort_u64(unsigned long long** keys, unsigned long long** alt, 
     }
   if (P.np == 0) return cudaSuccess;
   const int64_t t = rs_tiles(n);
-  unsigned long long* hist = (unsigned long long*)temp;
-  int64_t* off = (int64_t*)(hist + RS_MAXP * RS_BINS);
-  int32_t* tickets = (int32_t*)(off + RS_MAXP * RS_BINS);
+  int64_t* off = (int64_t*)temp;
+  unsigned long long* hist = (unsigned long long*)(off + RS_MAXP * RS_BINS);
+  int32_t* tickets = (int32_t*)(hist + RS_MAXP * RS_BINS);
   unsigned long long* state = (unsigned long long*)(tickets + 64);
-  cudaError_t e = cudaMemsetAsync(hist, 0, sizeof(unsigned long long) * RS_MAXP * RS_BINS, s);
-  if (e == cudaSuccess) e = cudaMemsetAsync(tickets, 0, 64 * sizeof(int32_t), s);
-  if (e == cudaSuccess) e = cudaMemsetAsync(state, 0, sizeof(unsigned long long) * t * RS_BINS, s);
+  cudaError_t e = cudaMemsetAsync(hist, 0,
+                                  sizeof(unsigned long long) * RS_MAXP * RS_BINS +
+                                      64 * sizeof(int32_t) +
+                                      sizeof(unsigned long long) * t * RS_BINS,
+                                  s);
   if (e != cudaSuccess) return e;
   int64_t hg = t < 148 * 4 ? t : 148 * 4;
   e = launch_pdl(k_rs_hist, dim3((unsigned)hg), dim3(RS_NT), 0, s, *keys, n, P, hist);
@@ -313,9 +326,14 @@ cudaError_t radix_sort_u64(unsigned long long** keys, unsigned long long** alt, 
   if (e != cudaSuccess) return e;
   *launches += 2;
   for (int p = 0; p < P.np; ++p) {
-    e = launch_pdl(k_rs_scatter, dim3((unsigned)t), dim3(RS_NT), 0, s, *keys, *alt, n, P.shift[p],
-                   P.bits[p], (const int64_t*)(off + p * RS_BINS), state, tickets + p,
-                   (uint32_t)(p + 1));
+    if (rs_rounds(n) == 4)
+      e = launch_pdl(k_rs_scatter<4>, dim3((unsigned)t), dim3(RS_NT), 0, s, *keys, *alt, n,
+                     P.shift[p], P.bits[p], (const int64_t*)(off + p * RS_BINS), state,
+                     tickets + p, (uint32_t)(p + 1));
+    else
+      e = launch_pdl(k_rs_scatter<16>, dim3((unsigned)t), dim3(RS_NT), 0, s, *keys, *alt, n,
+                     P.shift[p], P.bits[p], (const int64_t*)(off + p * RS_BINS), state,
+                     tickets + p, (uint32_t)(p + 1));
     ++*launches;
     if (e != cudaSuccess) return e;
     unsigned long long* tmp = *keys;
