@@ -9,12 +9,15 @@
 // M (membership count), P (pair count) and E (edge count).
 #include <math.h>
 #include <stdarg.h>
+#include <time.h>
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
 
+#include <map>
 #include <mutex>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "internal.cuh"
@@ -44,55 +47,108 @@ bm_status set_err(bm_status st, const char* fmt, ...) {
     }                                                                                 \
   } while (0)
 
-// The library's own stream-ordered memory pool per device: freed blocks stay
-// reserved for the next call (release threshold = unlimited) instead of
-// being unmapped at every synchronisation; bm_trim_memory() returns them.
-std::mutex g_pool_mu;
-cudaMemPool_t g_pools[64] = {};
-
-cudaMemPool_t device_pool() {
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
-  std::lock_guard<std::mutex> lk(g_pool_mu);
-  if (!g_pools[dev]) {
-    cudaMemPoolProps pr{};
-    pr.allocType = cudaMemAllocationTypePinned;
-    pr.handleTypes = cudaMemHandleTypeNone;
-    pr.location.type = cudaMemLocationTypeDevice;
-    pr.location.id = dev;
-    cudaMemPool_t mp = nullptr;
-    if (cudaMemPoolCreate(&mp, &pr) != cudaSuccess) {
-      cudaGetLastError();
-      return nullptr;
+// Device memory: a library-owned block cache.  Blocks are carved by
+// cudaMalloc in size classes (8 per octave above 1 MiB, powers of two below,
+// <= 12.5% slack) and, once released, kept on a free list of the (device,
+// stream) they were last used on: a later allocation on the same stream reuses
+// them with no synchronisation (stream order makes the reuse safe).  The CUDA
+// stream-ordered pool was measured to stall the host for 100-600 ms in
+// cudaMallocFromPoolAsync on this platform even with an unlimited release
+// threshold; the cache has no such path.  bm_trim_memory() returns cached
+// blocks to the system.
+struct BlockCache {
+  struct Key {
+    int dev;
+    cudaStream_t s;
+    size_t cls;
+    bool operator<(const Key& o) const {
+      if (dev != o.dev) return dev < o.dev;
+      if (s != o.s) return (uintptr_t)s < (uintptr_t)o.s;
+      return cls < o.cls;
     }
-    uint64_t thr = UINT64_MAX;
-    cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &thr);
-    g_pools[dev] = mp;
-  }
-  return g_pools[dev];
-}
+  };
+  std::mutex mu;
+  std::map<Key, std::vector<void*>> free_;
+  std::unordered_map<void*, std::pair<int, size_t>> live_;   // ptr -> (device, class)
 
-// Stream-ordered allocations owned by one build call.
+  static size_t size_class(size_t b) {
+    if (b <= 256) return 256;
+    if (b <= ((size_t)1 << 20)) {
+      size_t c = 256;
+      while (c < b) c <<= 1;
+      return c;
+    }
+    int lg = 63 - __builtin_clzll((unsigned long long)b);
+    const size_t step = (size_t)1 << (lg - 3);
+    return (b + step - 1) / step * step;
+  }
+  cudaError_t alloc(void** p, size_t bytes, cudaStream_t s) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const size_t cls = size_class(bytes);
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      auto it = free_.find(Key{dev, s, cls});
+      if (it != free_.end() && !it->second.empty()) {
+        *p = it->second.back();
+        it->second.pop_back();
+        live_[*p] = {dev, cls};
+        return cudaSuccess;
+      }
+    }
+    e = cudaMalloc(p, cls);
+    if (e == cudaErrorMemoryAllocation) {   // give cached blocks back, retry once
+      cudaGetLastError();
+      trim();
+      e = cudaMalloc(p, cls);
+    }
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lk(mu);
+    live_[*p] = {dev, cls};
+    return cudaSuccess;
+  }
+  void release(void* p, cudaStream_t s) {
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = live_.find(p);
+    if (it == live_.end()) return;
+    free_[Key{it->second.first, s, it->second.second}].push_back(p);
+    live_.erase(it);
+  }
+  void trim() {
+    std::map<Key, std::vector<void*>> victims;
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      victims.swap(free_);
+    }
+    if (victims.empty()) return;
+    cudaDeviceSynchronize();   // blocks may still be in use by queued work
+    for (auto& kv : victims)
+      for (void* q : kv.second) cudaFree(q);
+  }
+};
+BlockCache g_cache;
+
+// Allocations owned by one build call (stream-ordered on the call's stream).
 struct Pool {
   cudaStream_t s;
-  cudaMemPool_t mp;
   std::vector<void*> ptrs;
-  explicit Pool(cudaStream_t st) : s(st), mp(device_pool()) {}
+  explicit Pool(cudaStream_t st) : s(st) {}
   ~Pool() {
     for (void* p : ptrs)
-      if (p) cudaFreeAsync(p, s);
+      if (p) g_cache.release(p, s);
   }
   template <class T>
   bm_status alloc(T** out, size_t count) {
     void* p = nullptr;
-    size_t bytes = count * sizeof(T);
-    if (bytes < 256) bytes = 256;
-    cudaError_t e = mp ? cudaMallocFromPoolAsync(&p, bytes, mp, s) : cudaMallocAsync(&p, bytes, s);
+    const size_t bytes = count * sizeof(T);
+    cudaError_t e = g_cache.alloc(&p, bytes, s);
     if (e != cudaSuccess) {
       cudaGetLastError();
       *out = nullptr;
       return set_err(e == cudaErrorMemoryAllocation ? BM_ENOMEM : BM_ECUDA,
-                     "cudaMallocAsync(%zu bytes): %s", bytes, cudaGetErrorString(e));
+                     "device allocation (%zu bytes): %s", bytes, cudaGetErrorString(e));
     }
     ptrs.push_back(p);
     *out = (T*)p;
@@ -106,7 +162,7 @@ struct Pool {
   void free_now(void* p) {
     for (auto& q : ptrs)
       if (q == p) {
-        cudaFreeAsync(q, s);
+        g_cache.release(q, s);
         q = nullptr;
       }
   }
@@ -212,6 +268,36 @@ __global__ void k_iota(int32_t* a, int64_t n) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) a[i] = (int32_t)i;
 }
+
+// BM_TRACE=1: synchronise and print the host time of every traced sub-step
+// (diagnostics only; off by default).
+struct Trace {
+  bool on;
+  cudaStream_t s;
+  double t0;
+  static double now() {
+    struct timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return ts.tv_sec * 1e3 + ts.tv_nsec * 1e-6;
+  }
+  int level;
+  explicit Trace(cudaStream_t st)
+      : on(getenv("BM_TRACE") != nullptr && atoi(getenv("BM_TRACE")) == 1), s(st), t0(now()),
+        level(getenv("BM_TRACE") ? atoi(getenv("BM_TRACE")) : 0) {}
+  void operator()(const char* what) {
+    if (level == 3) {   // host timestamps only (no synchronisation)
+      const double t = now();
+      fprintf(stderr, "[bm trace host] %-28s %9.3f ms\n", what, t - t0);
+      t0 = t;
+      return;
+    }
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    const double t = now();
+    fprintf(stderr, "[bm trace] %-28s %9.3f ms\n", what, t - t0);
+    t0 = t;
+  }
+};
 
 struct Timer {
   bool on;
@@ -394,6 +480,7 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
   int64_t launches = 0;
   Pool pool(s);
   Timer tm(o.timing != 0, s);
+  Trace tr(s);
   tm.mark(0);
 
   // ---- A0 prep
@@ -409,12 +496,15 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
   uint2* xhat = nullptr;
   int32_t* inorm = nullptr;
   DevStats* stats = nullptr;
+  tr("prep: start");
   TRY(pool.alloc(&rows, (size_t)n * nu));
   if (kind == K_COSF) TRY(pool.alloc(&xhat, (size_t)n * nu));
   if (kind == K_L2I) TRY(pool.alloc(&inorm, (size_t)n));
   TRY(pool.alloc(&stats, 1));
   CK(cudaMemsetAsync(stats, 0, sizeof(DevStats), s));
+  tr("prep: allocs");
   CK(launch_prep(dpoints, dtype, n, d, kind, nu, rows, xhat, inorm, stats, s, &launches));
+  tr("prep: launch");
   void* tc_nrm = nullptr;
   if (use_tc) {
     uint8_t* xop = nullptr;
@@ -429,6 +519,7 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
     CK(tc::launch_tc_prep(dpoints, dtype, n, d, P, tc_nrm, stats, s, &launches));
   }
   if (host_in) pool.free_now((void*)dpoints);
+  tr("prep");
 
   // ---- buffers of the fused greedy + membership loop
   const int64_t nL_max = n;  // L <= n
@@ -516,6 +607,7 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
     set_recheck(ta, rows, 2 * nu, d, th, new_lm, ties_dev, tie_cap, stats);
   }
   tm.mark(1);
+  tr("greedy buffers");
 
   // ---- A1-A4 + B: blocked greedy, each tile's membership pass over all points
   // (SURVEY §3 (iii) variant: total membership work is exactly n * L).
@@ -602,6 +694,7 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
     if (batch < 64) batch *= 2;
   }
   tm.mark(2);
+  tr("greedy+membership loop");
 
   DevStats hs{};
   CK(cudaMemcpyAsync(&hs, stats, sizeof hs, cudaMemcpyDeviceToHost, s));
@@ -649,7 +742,9 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
   const unsigned long long lo32 = 0xffffffffull;
   const BitRange pm[2] = {{0, lbits}, {32, 32 + pbits}};
   const BitRange lmaj[1] = {{0, lbits}};
+  tr("csr alloc");
   CK(radix_sort_u64(&keys, &alt, M, pm, 2, rtemp, s, &launches));
+  tr("csr sort point-major");
   CK(launch_unpack_low(keys, M, lo32, pt_lm, s, &launches));
   CK(launch_segment_ptr(keys, M, 32, lo32, n, pt_ptr, s, &launches));
   CK(radix_sort_u64(&keys, &alt, M, lmaj, 1, rtemp, s, &launches));
@@ -659,6 +754,7 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
   pool.free_now(alt);
   pool.free_now(rtemp);
   tm.mark(4);
+  tr("csr rest");
 
   // ---- D1-D3 edges (edges.cu)
   int64_t NP = 0;  // P = sum_p C(t_p, 2) witnessed pairs
@@ -675,6 +771,7 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
     TRY(pool.alloc((uint8_t**)&etemp, edge_lb_temp_bytes(edge_bitmap_words(L))));
     TRY(pool.alloc(&edges, (size_t)(2 * cap)));
     CK(launch_edge_bits(pt_ptr, pt_lm, n, L, bits, (unsigned long long*)ptot, s, &launches));
+    tr("edges: bits");
     CK(launch_bits_compact(bits, L, edges, cap, ptot + 1, etemp, s, &launches));
     int64_t h2[2];
     CK(cudaMemcpyAsync(h2, ptot, sizeof h2, cudaMemcpyDeviceToHost, s));
@@ -693,6 +790,7 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
     CK(exclusive_scan_i64(pcnt, poff, n, stemp, ptot, s, &launches));
     CK(cudaMemcpyAsync(&NP, ptot, sizeof NP, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    tr("edges count");
     if (NP > 0) {
       unsigned long long *ek = nullptr, *ea = nullptr;
       int32_t* etmp = nullptr;
@@ -700,31 +798,43 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
       TRY(pool.alloc(&ek, (size_t)NP));
       TRY(pool.alloc(&ea, (size_t)NP));
       TRY(pool.alloc((uint8_t**)&et, radix_temp_bytes(NP)));
+      tr("edges alloc");
       CK(launch_pair_emit(pt_ptr, pt_lm, n, poff, lbits, ek, s, &launches));
+      tr("edges emit");
       const BitRange er[1] = {{0, 2 * lbits}};
       CK(radix_sort_u64(&ek, &ea, NP, er, 1, et, s, &launches));
+      tr("edges sort");
       pool.free_now(et);
       etmp = (int32_t*)ea;   // the sort's spare buffer holds 2 NP int32
       TRY(pool.alloc((uint8_t**)&ct, edge_lb_temp_bytes(NP)));
       CK(launch_unique_compact(ek, NP, lbits, etmp, ptot + 1, ct, s, &launches));
+      tr("edges: compact launched");
       CK(cudaMemcpyAsync(&E, ptot + 1, sizeof E, cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
+      tr("edges: E readback");
       TRY(pool.alloc(&edges, (size_t)(2 * E > 0 ? 2 * E : 1)));
+      tr("edges: alloc exact");
       if (E > 0)
         CK(cudaMemcpyAsync(edges, etmp, sizeof(int32_t) * 2 * E, cudaMemcpyDeviceToDevice, s));
+      tr("edges: copy");
       pool.free_now(ek);
+      tr("edges: free ek");
       pool.free_now(ea);
+      tr("edges: free ea");
       pool.free_now(ct);
     }
     pool.free_now(pcnt);
     pool.free_now(poff);
     pool.free_now(stemp);
+    tr("edges: frees");
   }
   if (!edges) TRY(pool.alloc(&edges, 1));
   int32_t* landmarks = nullptr;
   TRY(pool.alloc(&landmarks, (size_t)(L > 0 ? L : 1)));
+  tr("landmarks alloc");
   CK(launch_copy_i32(lm, landmarks, L, s, &launches));
   tm.mark(5);
+  tr("edges rest");
 
   // ---- results
   CK(cudaMemcpyAsync(&hs, stats, sizeof hs, cudaMemcpyDeviceToHost, s));
@@ -854,7 +964,7 @@ void bm_free(bm_cover* c) {
     cudaStream_t s = pv ? pv->stream : nullptr;
     for (void* p : {(void*)c->landmarks, (void*)c->ball_ptr, (void*)c->ball_idx,
                     (void*)c->pt_ptr, (void*)c->pt_lm, (void*)c->edges})
-      if (p) cudaFreeAsync(p, s);
+      g_cache.release(p, s);
   }
   free(c->near_tie_pairs);
   free(pv);
@@ -864,8 +974,7 @@ void bm_free(bm_cover* c) {
 const char* bm_last_error(void) { return g_err.c_str(); }
 
 bm_status bm_trim_memory(void) {
-  cudaMemPool_t mp = device_pool();
-  if (mp) CK(cudaMemPoolTrimTo(mp, 0));
+  g_cache.trim();
   return BM_OK;
 }
 

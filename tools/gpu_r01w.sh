@@ -1,0 +1,1 @@
+./tools/ubench/pool 0; echo ---; ./tools/ubench/pool 1
