@@ -145,18 +145,25 @@ def roofline_tensor(w, L, kernel_ms, n, peaks, step_ms):
 
 
 def roofline_alu(w, L, kernel_ms, n, peaks):
-    """Dominant kernel = the membership pass (step B).  CUDA-core path:
-    bound 'alu' — algorithmic FP32/INT lane-instructions per pair (DESIGN.md
-    §Roofline): L2 f32 direct 2d (sub + fma), L1 f32 2d (sub + abs-add),
-    cosine d (fma), int L2 ceil(d/4) dp4a, int L1 2*ceil(d/4).  Peak = 148 SMs x
-    128 lanes x sm_max clock (lane-instr/s)."""
+    """Dominant kernel = the membership pass (step B) on CUDA cores: bound
+    'alu', algorithmic lane-instructions per pair against the issue rate of the
+    unit doing the work (DESIGN.md §7 "Rooflines"):
+      L1 f32 (8-bit SAD prefilter, d <= 64): ceil(d/4) VABSDIFF4 per pair, peak
+        148 SM x 64 lanes x clock (half-rate instruction, measured 18.5 T/s);
+      L2 f32 direct 2d (sub + fma), cosine d (fma), L1 f32 without the
+        prefilter 2d, int L2 ceil(d/4) dp4a, int L1 2 ceil(d/4): peak
+        148 SM x 128 lanes x clock (full-rate FP32/INT issue)."""
     d = w.d
-    per_pair = {("f32", "l2"): 2 * d, ("f32", "l1"): 2 * d, ("f32", "cos"): d,
-                ("i8", "l2"): math.ceil(d / 4), ("u8", "l2"): math.ceil(d / 4),
-                ("i8", "l1"): 2 * math.ceil(d / 4), ("u8", "l1"): 2 * math.ceil(d / 4)}[
-        (w.dtype, w.metric)]
     clk = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
-    peak = 148 * 128 * clk / 1e12
+    if (w.dtype, w.metric) == ("f32", "l1") and d <= 64:
+        per_pair, lanes, what = math.ceil(d / 4), 64, "VABSDIFF4 (half rate)"
+    else:
+        per_pair = {("f32", "l2"): 2 * d, ("f32", "l1"): 2 * d, ("f32", "cos"): d,
+                    ("i8", "l2"): math.ceil(d / 4), ("u8", "l2"): math.ceil(d / 4),
+                    ("i8", "l1"): 2 * math.ceil(d / 4), ("u8", "l1"): 2 * math.ceil(d / 4)}[
+            (w.dtype, w.metric)]
+        lanes, what = 128, "FP32/INT issue"
+    peak = 148 * lanes * clk / 1e12
     ops = float(n) * L * per_pair
     achieved = ops / (kernel_ms * 1e-3) / 1e12 if kernel_ms > 0 else 0.0
     traffic = _traffic(w)
@@ -165,7 +172,7 @@ def roofline_alu(w, L, kernel_ms, n, peaks):
             "peak": round(peak, 4), "unit": "Tinst/s", "frac": round(achieved / peak, 4),
             "traffic": traffic, "ops_per_pair": per_pair,
             "kernel_ms": round(kernel_ms, 5),
-            "peak_basis": "148 SM x 128 lanes x sm_max_mhz (DESIGN.md §Roofline)"}
+            "peak_basis": f"148 SM x {lanes} lanes x sm_max_mhz, {what} (DESIGN.md §7)"}
 
 
 def cpu_baseline(w, X, budget_s: float):

@@ -92,8 +92,12 @@ typedef struct bm_options {
                             fits, a larger one costs one exact-capacity recount             */
   int32_t band_cap;      /* ignored (kept for layout): band pairs are re-decided in fp64
                             inside the contraction kernels, no queue is needed              */
-  int32_t reserved[6];
+  int32_t flags;         /* BM_FLAG_* (diagnostics)                                           */
+  int32_t reserved[5];
 } bm_options;
+
+/* bm_options.flags */
+#define BM_FLAG_NO_L1_PREFILTER 1   /* L1: score every pair in fp32 (no 8-bit SAD prefilter) */
 
 /*
  * Result of one cover construction.  All arrays are owned by the library and

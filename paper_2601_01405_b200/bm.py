@@ -22,6 +22,7 @@ STATUS_NAMES = {0: "BM_OK", 1: "BM_EINVAL", 2: "BM_EUNSUPPORTED", 3: "BM_ENOMEM"
 METRIC = {"l2": 0, "l1": 1, "cos": 2, "cosine": 2}
 DTYPE = {"f32": 0, "i8": 1, "u8": 2}
 PATH = {"auto": 0, "cuda_core": 1, "tensor": 2}
+FLAG_NO_L1_PREFILTER = 1
 STEPS = ("prep", "greedy", "member", "csr", "edges", "total", "member_kernel")
 
 EXPORTED = ("bm_cover_build", "bm_cover_build_ex", "bm_cover_build_host", "bm_free",
@@ -40,7 +41,8 @@ class _Options(ctypes.Structure):
     _fields_ = [("struct_size", ctypes.c_int32), ("tile", ctypes.c_int32),
                 ("path", ctypes.c_int32), ("timing", ctypes.c_int32),
                 ("near_tie_cap", ctypes.c_int64), ("key_cap", ctypes.c_int32),
-                ("band_cap", ctypes.c_int32), ("reserved", ctypes.c_int32 * 6)]
+                ("band_cap", ctypes.c_int32), ("flags", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 5)]
 
 
 class _Cover(ctypes.Structure):
@@ -108,7 +110,7 @@ def _check(rc: int):
 
 
 def _options(tile=0, path="auto", timing=False, near_tie_cap=0, key_cap=0,
-             band_cap=0) -> _Options:
+             band_cap=0, flags=0) -> _Options:
     o = _Options()
     o.struct_size = ctypes.sizeof(_Options)
     o.tile = int(tile)
@@ -117,6 +119,7 @@ def _options(tile=0, path="auto", timing=False, near_tie_cap=0, key_cap=0,
     o.near_tie_cap = int(near_tie_cap)
     o.key_cap = int(key_cap)
     o.band_cap = int(band_cap)
+    o.flags = int(flags)
     return o
 
 
@@ -227,7 +230,7 @@ def _dtype_of(t) -> str:
 
 def cover_build(points, metric: str, eps: float, stream=None, tile: int = 0,
                 path: str = "auto", timing: bool = False, near_tie_cap: int = 0,
-                key_cap: int = 0, band_cap: int = 0) -> Cover:
+                key_cap: int = 0, band_cap: int = 0, flags: int = 0) -> Cover:
     """bm_cover_build_ex on a CUDA torch tensor [n, d] (row-major, contiguous)."""
     import torch
     if not (isinstance(points, torch.Tensor) and points.is_cuda):
@@ -240,7 +243,7 @@ def cover_build(points, metric: str, eps: float, stream=None, tile: int = 0,
         stream = torch.cuda.current_stream(points.device)
     sp = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
     out = ctypes.POINTER(_Cover)()
-    o = _options(tile, path, timing, near_tie_cap, key_cap, band_cap)
+    o = _options(tile, path, timing, near_tie_cap, key_cap, band_cap, flags)
     lib = load()
     with torch.cuda.device(points.device):
         rc = lib.bm_cover_build_ex(ctypes.c_void_p(points.data_ptr()), DTYPE[_dtype_of(points)],
@@ -252,7 +255,7 @@ def cover_build(points, metric: str, eps: float, stream=None, tile: int = 0,
 
 def cover_build_host(points: np.ndarray, metric: str, eps: float, stream=None, tile: int = 0,
                      path: str = "auto", timing: bool = False, near_tie_cap: int = 0,
-                     key_cap: int = 0, band_cap: int = 0) -> Cover:
+                     key_cap: int = 0, band_cap: int = 0, flags: int = 0) -> Cover:
     """bm_cover_build_host on a host buffer (numpy array or CPU torch tensor,
     ideally pinned): copies in, builds, copies every result back to host."""
     import torch
@@ -270,7 +273,7 @@ def cover_build_host(points: np.ndarray, metric: str, eps: float, stream=None, t
         stream = torch.cuda.current_stream()
     sp = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
     out = ctypes.POINTER(_Cover)()
-    o = _options(tile, path, timing, near_tie_cap, key_cap, band_cap)
+    o = _options(tile, path, timing, near_tie_cap, key_cap, band_cap, flags)
     rc = load().bm_cover_build_host(ctypes.c_void_p(ptr), DTYPE[dt], n, d, METRIC[metric],
                                     float(eps), ctypes.c_void_p(sp), ctypes.byref(o),
                                     ctypes.byref(out))

@@ -203,6 +203,7 @@ bm::Thresh make_thresh(int kind, int d, double eps) {
   t.eps = eps;
   t.eps2 = eps * eps;
   t.tie_rel = tie;
+  t.cosine = kind == bm::K_COSF ? 1 : 0;
   if (kind == bm::K_L2F) {
     // |s - D| <= (d+3) u D (difference rounding, squaring, fp32 accumulation),
     // near tie |d-eps| <= 1e-6 eps  <=>  |D - eps^2| <= 2.000001e-6 eps^2
@@ -256,6 +257,16 @@ int64_t initial_key_cap(int64_t n) {
 // (n_p + n_l)/2, and 1.25 is a further safety factor.
 // The column constant cb_j (|cb_j| <= n_l/2) is folded into the MMA as three
 // more exact products, adding c3 |cb_j| with c3 = 4 (K+3) 2^-23 (1.001).
+// Cosine on tensor cores: |acc - x.y/(|x||y|)| <= c1 (operands x/|x| within
+// 2u of the exact unit vectors per coordinate, then rounded to tf32), plus
+// 8u for the fp32 normalisation and 2^-20 slack.
+double tc_cos_margin(int ksteps) {
+  const double ut = ldexp(1.0, -11), u = ldexp(1.0, -24);
+  const double K = 8.0 * ksteps + 3.0;
+  const double c1 = 2.0 * ut + ut * ut + 4.0 * K * ldexp(1.0, -23) * (1.0 + ut) * (1.0 + ut);
+  return 1.25 * (c1 * (1.0 + 4.0 * u) * (1.0 + 4.0 * u) + 8.0 * u + ldexp(1.0, -20));
+}
+
 double tc_band_c2(int ksteps) {
   const double ut = ldexp(1.0, -11);
   const double K = 8.0 * ksteps + 3.0;
@@ -327,6 +338,7 @@ void set_recheck(bm::tc::TcArgs& ta, const void* xrows, int xstride, int d, cons
   ta.eps2 = th.eps2;
   ta.tie_rel = th.tie_rel;
   ta.lm_idx = lm_idx;
+  ta.cosine = th.cosine;
   ta.ties = ties;
   ta.tie_cap = tie_cap;
   ta.stats = stats;
@@ -387,7 +399,9 @@ bm_status membership_full(Pool& pool, int kind, const bm::PairArgs& base, bm::tc
       ta.row_r = rr;
       ta.col_c = cc;
     }
-    CK(tc::launch_tc_rows(P, tc_nrm, n, C2, th.eps2, tau, th.lo_i, ta, s, launches));
+    if (P.cosine) CK(tc::launch_tc_rows_cos(P, tc_nrm, n, th.eps, tc_cos_margin(ta.ksteps), ta, s,
+                                            launches));
+    else CK(tc::launch_tc_rows(P, tc_nrm, n, C2, th.eps2, tau, th.lo_i, ta, s, launches));
     CK(tc::launch_tc_landmarks(P, tc_nrm, lm, L, C2, ta, s, launches));
     ta.keys = keys;
     ta.key_count = &stats->key_count;
@@ -457,10 +471,11 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
   if (nu == 0) nu = nu_needed;
   const Thresh th = make_thresh(kind, d, eps);
 
-  // Tensor-core membership contraction (tc.cu): Euclidean only, K up to the
-  // configured atom counts; AUTO picks it for d >= 32.
+  // Tensor-core membership contraction (tc.cu): Euclidean (Gram form) and
+  // cosine (Gram of the normalised rows), K up to the configured atom counts.
   tc::TcPlan P{};
   P.kind = dtype == BM_F32 ? tc::TC_TF32 : (dtype == BM_U8 ? tc::TC_U8 : tc::TC_S8);
+  P.cosine = metric == BM_COSINE ? 1 : 0;
   {
     const int esz = dtype == BM_F32 ? 4 : 1;
     P.row_bytes = (((int64_t)d * esz + 15) / 16) * 16;
@@ -470,11 +485,13 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
   // AUTO: tensor cores for Euclidean when the rows are wide or numerous
   // enough to fill the 128 x 256 tiles (measured: C2, d = 10, n = 1e5, is
   // faster on tcgen05; C1, n = 2e3, on CUDA cores)
-  bool use_tc = metric == BM_L2 && tc::tc_supported(P.kind, P.katoms) &&
+  bool use_tc = (metric == BM_L2 || (metric == BM_COSINE && dtype == BM_F32)) &&
+                tc::tc_supported(P.kind, P.katoms) &&
                 (o.path == BM_PATH_TENSOR ||
                  (o.path == BM_PATH_AUTO && (d >= 32 || n >= 32768)));
   if (o.path == BM_PATH_TENSOR && !use_tc)
-    return set_err(BM_EUNSUPPORTED, "tensor-core path supports L2 with d*elem <= %d bytes",
+    return set_err(BM_EUNSUPPORTED,
+                   "tensor-core path supports L2 and cosine with d*elem <= %d bytes",
                    dtype == BM_F32 ? 512 : 896);
 
   int64_t launches = 0;
@@ -518,6 +535,16 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
     CK(cudaDeviceGetAttribute(&P.num_sms, cudaDevAttrMultiProcessorCount, dev));
     CK(tc::launch_tc_prep(dpoints, dtype, n, d, P, tc_nrm, stats, s, &launches));
   }
+  // L1: 8-bit quantised rows for the membership prefilter (exact decisions unchanged)
+  uint32_t* qrows = nullptr;
+  double* qparam = nullptr;
+  const int nq = kind == K_L1F ? l1q_words(d) : 0;
+  if (nq > 0 && !(o.flags & BM_FLAG_NO_L1_PREFILTER)) {
+    TRY(pool.alloc(&qrows, (size_t)n * nq));
+    TRY(pool.alloc(&qparam, 4));
+    CK(launch_l1_quantize((const float*)dpoints, n, d, nq, qparam, qrows, s, &launches));
+  }
+
   if (host_in) pool.free_now((void*)dpoints);
   tr("prep");
 
@@ -600,7 +627,9 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
       ta.row_r = rr;
       ta.col_c = cc;
     }
-    CK(tc::launch_tc_rows(P, tc_nrm, n, C2, th.eps2, tau, th.lo_i, ta, s, &launches));
+    if (P.cosine) CK(tc::launch_tc_rows_cos(P, tc_nrm, n, th.eps, tc_cos_margin(ta.ksteps), ta, s,
+                                            &launches));
+    else CK(tc::launch_tc_rows(P, tc_nrm, n, C2, th.eps2, tau, th.lo_i, ta, s, &launches));
     ta.keys = keys;
     ta.key_count = &stats->key_count;
     ta.key_cap = key_cap;
@@ -673,6 +702,9 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
         m.ties = ties_dev;
         m.tie_cap = tie_cap;
         m.covered = covered;
+        m.qrows = qrows;
+        m.nq = nq;
+        m.qparam = qparam;
         CK(mark_member());
         CK(launch_pairs(kind, MODE_MEMBER, m, n, s, &launches));
         CK(mark_member());

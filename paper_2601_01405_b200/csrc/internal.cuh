@@ -58,6 +58,7 @@ struct Thresh {
   int32_t lo_i;          // in iff score <= lo_i - 1 (i.e. score < lo_i)
   double eps, eps2;      // fp64 truth: L2 d2 < eps2, L1 s < eps, cos 1-c < eps
   double tie_rel;        // near-tie band (1e-6)
+  int cosine;            // metric is cosine (for kernels shared with L2)
 };
 
 struct Dev;   // per-call device workspace (api.cu)
@@ -97,6 +98,9 @@ struct PairArgs {
   uint32_t* adj; int adj_words;                 // MODE_ADJ: word v of candidate a at
                                                 //   adj[v * (32 * adj_words) + a]
   uint8_t* covered;                             // MODE_MEMBER: covered[p] = 1 for in-ball pairs
+  // L1 prefilter (K_L1F, MODE_MEMBER): 8-bit quantised rows, nq 32-bit words
+  // per row; qparam = {min, max} of all coordinates (device, fp64)
+  const uint32_t* qrows; int nq; const double* qparam;
   unsigned long long* keys; int64_t key_cap; int lbits;   // MODE_MEMBER: (p << lbits) | j
   int64_t* ties; int64_t tie_cap;               // MODE_MEMBER near-tie triples (host-mapped)
   DevStats* stats;
@@ -110,6 +114,12 @@ cudaError_t launch_prep(const void* X, int dtype, int64_t n, int d, int kind, in
 
 cudaError_t launch_pairs(int kind, int mode, const PairArgs& a, int64_t q_rows_max,
                          cudaStream_t s, int64_t* launches);
+
+// L1 prefilter: coordinate range -> qparam[0..1],
+// then 8-bit rows q = rint((x - min) / s), s = (max - min) / 255, nq words per row.
+int l1q_words(int d);   // 0 if the prefilter does not apply (d > 64)
+cudaError_t launch_l1_quantize(const float* X, int64_t n, int d, int nq, double* qparam,
+                               uint32_t* qrows, cudaStream_t s, int64_t* launches);
 
 // A3; also resets the per-tile device counters (*ticket = 0, *band_count = 0).
 cudaError_t launch_resolve(const uint32_t* adj, int adj_words, const int32_t* unc,

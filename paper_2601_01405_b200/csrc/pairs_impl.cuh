@@ -113,19 +113,46 @@ __device__ __forceinline__ int classify(typename KindTraits<KIND>::acc_t acc, in
   }
 }
 
+// L1 prefilter threshold: with q = rint((x - min)/s)
+// every coordinate is within s (1/2 + 1e-6) of min + s q, so
+// L1(x, y) >= s (SAD(q_x, q_y) - d (1 + 2e-6)); SAD >= thr proves
+// L1 >= eps (1 + 1.001e-6): out, and not a near tie.
+__device__ __forceinline__ double l1q_scale(const double* qp) {
+  const double r = qp[1] - qp[0];
+  return r > 0.0 ? r / 255.0 : 1.0;
+}
+__device__ __forceinline__ uint32_t l1q_threshold(const double* qp, double eps, int d) {
+  const double t = ceil(eps * (1.0 + 1.001e-6) / l1q_scale(qp) + d * (1.0 + 2e-6)) + 1.0;
+  return t > 4.0e9 ? 0xffffffffu : (uint32_t)t;
+}
+__device__ __forceinline__ uint32_t vsad4(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("vabsdiff4.u32.u32.u32.add %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
 // NU > 0: query rows live in registers (NU units).  NU == 0 ("wide"): rows of
 // any length; the query row is re-read from global/L1 for every landmark.
+// NQ > 0 (K_L1F, MODE_MEMBER): the 8-bit quantised rows (NQ words) score a
+// sum of absolute differences first; only pairs it cannot prove "out" are
+// scored exactly in fp32 (and, in the band, fp64).
 // One call = one block of NT*R query rows [blk_q0, ..) against landmarks
 // lidx[l0 .. l1) (positions lpos0 + (l - l_begin)).
-template <int KIND, int NU, int R, int MODE, int LC>
+template <int KIND, int NU, int R, int MODE, int LC, int NQ>
 __device__ __forceinline__ void pairs_block(const PairArgs& A, uint2* sl, int32_t* sln,
                                             int32_t* slp, int64_t blk_q0, int64_t q_end,
                                             int64_t l0, int64_t l1, int64_t lpos0) {
   constexpr int NT = 256;
-  constexpr int QU = NU > 0 ? NU : 1;   // register units per query row
+  constexpr bool QF = NQ > 0;
+  constexpr int QU = (NU > 0 && !QF) ? NU : 1;   // register units per query row
   using acc_t = typename KindTraits<KIND>::acc_t;
   const int nu = NU > 0 ? NU : A.nu;
   const int tid = threadIdx.x, lane = tid & 31;
+  // prefilter: quantised landmark rows follow the fp32 rows in shared memory
+  uint32_t* sq = reinterpret_cast<uint32_t*>(sl + LC * nu);
+  uint32_t thrq = 0u;
+  if constexpr (QF) thrq = l1q_threshold(A.qparam, A.th.eps, A.d);
+  uint32_t qq[R][QF ? NQ : 1];
 
   // ---- query rows into registers
   uint2 q[R][QU];
@@ -140,7 +167,12 @@ __device__ __forceinline__ void pairs_block(const PairArgs& A, uint2* sl, int32_
     qp[r] = act[r] ? (A.qidx ? (int64_t)A.qidx[qi[r]] : qi[r]) : 0;
     const uint2* src = A.rows + qp[r] * (int64_t)nu;
 #pragma unroll
-    for (int u = 0; u < QU; ++u) q[r][u] = (act[r] && NU > 0) ? src[u] : make_uint2(0u, 0u);
+    for (int u = 0; u < QU; ++u)
+      q[r][u] = (act[r] && NU > 0 && !QF) ? src[u] : make_uint2(0u, 0u);
+    if constexpr (QF) {
+#pragma unroll
+      for (int w = 0; w < NQ; ++w) qq[r][w] = act[r] ? A.qrows[qp[r] * NQ + w] : 0u;
+    }
     qn[r] = (KIND == K_L2I && act[r]) ? A.inorm[qp[r]] : 0;
   }
 
@@ -161,16 +193,48 @@ __device__ __forceinline__ void pairs_block(const PairArgs& A, uint2* sl, int32_
       slp[t] = pt;
       sln[t] = (KIND == K_L2I) ? A.inorm[pt] : 0;
     }
+    if constexpr (QF) {
+      for (int t = tid; t < nl * NQ; t += NT) {
+        const int jj = t / NQ, w = t - jj * NQ;
+        sq[t] = A.qrows[(int64_t)A.lidx[lb + jj] * NQ + w];
+      }
+    }
     __syncthreads();
 
     for (int jj = 0; jj < nl; ++jj) {
-      uint2 l[QU];
-#pragma unroll
-      for (int u = 0; u < QU; ++u) l[u] = NU > 0 ? sl[jj * nu + u] : make_uint2(0u, 0u);
       int cls[R];
       bool special = false;
+      if constexpr (QF) {
+        // quantised SAD (4 coordinates per instruction); cls 3 = "exact check needed"
+        uint32_t lq[NQ];
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
+        for (int w = 0; w < NQ; ++w) lq[w] = sq[jj * NQ + w];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          uint32_t sad = 0u;
+#pragma unroll
+          for (int w = 0; w < NQ; ++w) sad = vsad4(qq[r][w], lq[w], sad);
+          cls[r] = (act[r] && sad < thrq) ? 3 : 0;
+          special = special || (cls[r] != 0);
+        }
+        if (!__any_sync(FULL, special)) continue;
+        // exact fp32 score of the candidates (rows from global, landmark from smem)
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          if (cls[r] == 3) {
+            acc_t a = 0;
+            const uint2* src = A.rows + qp[r] * (int64_t)nu;
+            for (int u = 0; u < nu; ++u) acc_unit<KIND>(a, __ldg(src + u), sl[jj * nu + u]);
+            cls[r] = classify<KIND>(a, qn[r], sln[jj], A.th);
+          }
+        }
+      }
+      uint2 l[QU];
+#pragma unroll
+      for (int u = 0; u < QU; ++u)
+        l[u] = (NU > 0 && !QF) ? sl[jj * nu + u] : make_uint2(0u, 0u);
+#pragma unroll
+      for (int r = 0; r < R && !QF; ++r) {
         acc_t a = 0;
         if constexpr (NU > 0) {
 #pragma unroll
@@ -269,7 +333,7 @@ __device__ __forceinline__ MemberSched member_sched(int64_t nq, int64_t nl, int 
   return m;
 }
 
-template <int KIND, int NU, int R, int MODE, int LC>
+template <int KIND, int NU, int R, int MODE, int LC, int NQ>
 __global__ void __launch_bounds__(256) k_pairs(PairArgs A) {
   constexpr int NT = 256;
   extern __shared__ uint2 sl[];          // [LC][nu]
@@ -288,7 +352,7 @@ __global__ void __launch_bounds__(256) k_pairs(PairArgs A) {
     const int64_t l1 = min(l_end, l0 + 32);
     if (blk_q0 >= q_end || l0 >= l1) return;
     if (l0 >= min(q_end, blk_q0 + NT * R)) return;   // only b < a is needed
-    pairs_block<KIND, NU, R, MODE, LC>(A, sl, sln, slp, blk_q0, q_end, l0, l1, A.lpos0);
+    pairs_block<KIND, NU, R, MODE, LC, NQ>(A, sl, sln, slp, blk_q0, q_end, l0, l1, A.lpos0);
   } else {
     const int64_t nl = l_end - A.l_begin;
     const int64_t lpos0 = A.l_total_dev ? (int64_t)*A.l_total_dev - nl : A.lpos0;
@@ -298,20 +362,20 @@ __global__ void __launch_bounds__(256) k_pairs(PairArgs A) {
       const int64_t rb = it % m.nrb, ch = it / m.nrb;
       const int64_t l0 = A.l_begin + ch * m.chunk;
       const int64_t l1 = min(l_end, l0 + m.chunk);
-      pairs_block<KIND, NU, R, MODE, LC>(A, sl, sln, slp, q_begin + rb * (NT * R), q_end, l0,
+      pairs_block<KIND, NU, R, MODE, LC, NQ>(A, sl, sln, slp, q_begin + rb * (NT * R), q_end, l0,
                                          l1, lpos0);
       __syncthreads();   // the next item restages the landmark rows
     }
   }
 }
 
-template <int KIND, int NU, int MODE>
+template <int KIND, int NU, int MODE, int NQ = 0>
 cudaError_t launch_pairs_nu(const PairArgs& a, int64_t q_rows_max, cudaStream_t s) {
   constexpr int R = (MODE == MODE_ADJ || NU == 0) ? 1 : (NU <= 8 ? 4 : (NU <= 16 ? 2 : 1));
   constexpr int LC = NU == 0 ? 32 : 64;
   constexpr int NT = 256;
-  size_t smem = (size_t)LC * a.nu * sizeof(uint2);
-  auto kern = k_pairs<KIND, NU, R, MODE, LC>;
+  size_t smem = (size_t)LC * a.nu * sizeof(uint2) + (size_t)LC * NQ * sizeof(uint32_t);
+  auto kern = k_pairs<KIND, NU, R, MODE, LC, NQ>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
@@ -346,6 +410,18 @@ cudaError_t launch_pairs_nu(const PairArgs& a, int64_t q_rows_max, cudaStream_t 
 template <int KIND, int NU>
 cudaError_t launch_pairs_mode(int mode, const PairArgs& a, int64_t q_rows_max, cudaStream_t s) {
   if (mode == MODE_ADJ) return launch_pairs_nu<KIND, NU, MODE_ADJ>(a, q_rows_max, s);
+  if constexpr (KIND == K_L1F && NU > 0 && NU <= 32) {
+    if (a.qrows) {   // quantised prefilter: NQ = words per 8-bit row (power of two)
+      switch (a.nq) {
+        case 1: return launch_pairs_nu<KIND, NU, MODE_MEMBER, 1>(a, q_rows_max, s);
+        case 2: return launch_pairs_nu<KIND, NU, MODE_MEMBER, 2>(a, q_rows_max, s);
+        case 4: return launch_pairs_nu<KIND, NU, MODE_MEMBER, 4>(a, q_rows_max, s);
+        case 8: return launch_pairs_nu<KIND, NU, MODE_MEMBER, 8>(a, q_rows_max, s);
+        case 16: return launch_pairs_nu<KIND, NU, MODE_MEMBER, 16>(a, q_rows_max, s);
+        default: break;
+      }
+    }
+  }
   return launch_pairs_nu<KIND, NU, MODE_MEMBER>(a, q_rows_max, s);
 }
 

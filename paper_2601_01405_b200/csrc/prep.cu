@@ -68,6 +68,83 @@ __global__ void k_prep_int(const uint8_t* __restrict__ X, int64_t n, int d, int 
   if (inorm) inorm[p] = ss;
 }
 
+// ---- L1 prefilter rows
+// float -> int with the same order (for atomicMin / atomicMax)
+__device__ __forceinline__ int f2ord(float f) {
+  const int i = __float_as_int(f);
+  return i >= 0 ? i : i ^ 0x7fffffff;
+}
+__device__ __forceinline__ float ord2f(int i) { return __int_as_float(i >= 0 ? i : i ^ 0x7fffffff); }
+
+__global__ void k_minmax(const float* __restrict__ X, int64_t m, int* __restrict__ mm) {
+  float lo = INFINITY, hi = -INFINITY;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float v = X[i];
+    lo = fminf(lo, v);
+    hi = fmaxf(hi, v);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(&mm[0], f2ord(lo));
+    atomicMax(&mm[1], f2ord(hi));
+  }
+}
+
+// q = rint((x - min) / s), s = (max - min) / 255, 4 coordinates per word, zero padded
+__global__ void k_l1_quantize(const float* __restrict__ X, int64_t n, int d, int nq,
+                              const int* __restrict__ mm, double* __restrict__ qparam,
+                              uint32_t* __restrict__ qrows) {
+  const double mn = (double)ord2f(mm[0]), mx = (double)ord2f(mm[1]);
+  const double sc = mx > mn ? (mx - mn) / 255.0 : 1.0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    qparam[0] = mn;
+    qparam[1] = mx;
+  }
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const float* x = X + p * (int64_t)d;
+  for (int w = 0; w < nq; ++w) {
+    uint32_t word = 0u;
+    for (int k = 0; k < 4; ++k) {
+      const int j = 4 * w + k;
+      uint32_t q = 0u;
+      if (j < d) {
+        double t = rint(((double)x[j] - mn) / sc);
+        t = t < 0.0 ? 0.0 : (t > 255.0 ? 255.0 : t);
+        q = (uint32_t)t;
+      }
+      word |= q << (8 * k);
+    }
+    qrows[p * nq + w] = word;
+  }
+}
+
+int l1q_words(int d) {
+  if (d > 64) return 0;
+  int w = 1;
+  while (4 * w < d) w *= 2;
+  return w;
+}
+
+cudaError_t launch_l1_quantize(const float* X, int64_t n, int d, int nq, double* qparam,
+                               uint32_t* qrows, cudaStream_t s, int64_t* launches) {
+  int* mm = reinterpret_cast<int*>(qparam + 2);   // scratch after the two doubles
+  const int init[2] = {0x7fffffff, (int)0x80000000};
+  cudaError_t e = cudaMemcpyAsync(mm, init, sizeof init, cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return e;
+  const int64_t m = n * (int64_t)d;
+  int64_t g = (m + 255) / 256;
+  if (g > 148 * 8) g = 148 * 8;
+  k_minmax<<<(unsigned)g, 256, 0, s>>>(X, m, mm);
+  k_l1_quantize<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(X, n, d, nq, mm, qparam, qrows);
+  *launches += 2;
+  return cudaGetLastError();
+}
+
 cudaError_t launch_prep(const void* X, int dtype, int64_t n, int d, int kind, int nu,
                         uint2* rows, uint2* xhat, int32_t* inorm, DevStats* stats,
                         cudaStream_t s, int64_t* launches) {

@@ -56,12 +56,24 @@ __device__ __forceinline__ void tc_col_consts(double nl, double C2, int64_t j, f
 #pragma unroll
   for (int i = 3; i < 8; ++i) k[i] = 0.f;
 }
+// cosine columns: no constant (acc = cosine); a zero landmark gets acc' = +1e30
+// and d_j = +inf, so every pair with it is re-decided by the fp64 zero rule
+__device__ __forceinline__ void tc_col_consts_cos(double nl, int64_t j, float* ca, float* cb,
+                                                  float* colk) {
+  const bool zero = nl == 0.0;
+  cb[j] = zero ? -1e30f : 0.f;
+  ca[j] = zero ? INFINITY : 0.f;
+  float* k = colk + j * 8;
+  k[0] = zero ? 1e30f : 0.f;
+#pragma unroll
+  for (int i = 1; i < 8; ++i) k[i] = 0.f;
+}
 __device__ __forceinline__ void tc_col_inert(int64_t j, float* ca, float* cb, float* colk) {
-  // padding column: acc' = 0 - 1e30 never exceeds a row threshold
+  // padding column: acc' = acc - 1e38 never exceeds a row threshold (>= -1e37)
   cb[j] = INFINITY;
   ca[j] = INFINITY;
   float* k = colk + j * 8;
-  k[0] = -1e30f;
+  k[0] = -1e38f;
 #pragma unroll
   for (int i = 1; i < 8; ++i) k[i] = 0.f;
 }
@@ -476,16 +488,33 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // becomes a key at once (per-lane, so callable from divergent code)
     auto recheck = [&](unsigned long long bk) {
       const int64_t p = (int64_t)(bk >> 32), j = (int64_t)(bk & 0xffffffffull);
+      if (j >= n_cols || p >= args.n) return;   // padding rows / columns never qualify
       const int64_t qp = args.lm_idx[j];
       const float* x = args.xrows + p * (int64_t)args.xstride;
       const float* y = args.xrows + qp * (int64_t)args.xstride;
-      double sacc = 0.0;
-      for (int k = 0; k < args.d; ++k) {
-        const double t = __dsub_rn((double)x[k], (double)y[k]);
-        sacc = __dadd_rn(sacc, __dmul_rn(t, t));
+      bool in;
+      double dist;
+      if (args.cosine) {   // 1 - x.y / (|x| |y|), zero-vector rule (A7)
+        double dot = 0.0, xx = 0.0, yy = 0.0;
+        for (int k = 0; k < args.d; ++k) {
+          const double a = (double)x[k], b = (double)y[k];
+          dot = __dadd_rn(dot, __dmul_rn(a, b));
+          xx = __dadd_rn(xx, __dmul_rn(a, a));
+          yy = __dadd_rn(yy, __dmul_rn(b, b));
+        }
+        if (xx == 0.0 && yy == 0.0) dist = 0.0;
+        else if (xx == 0.0 || yy == 0.0) dist = 1.0;
+        else dist = __dsub_rn(1.0, __ddiv_rn(dot, __dmul_rn(__dsqrt_rn(xx), __dsqrt_rn(yy))));
+        in = dist < args.eps;
+      } else {
+        double sacc = 0.0;
+        for (int k = 0; k < args.d; ++k) {
+          const double t = __dsub_rn((double)x[k], (double)y[k]);
+          sacc = __dadd_rn(sacc, __dmul_rn(t, t));
+        }
+        in = sacc < args.eps2;
+        dist = __dsqrt_rn(sacc);
       }
-      const bool in = sacc < args.eps2;
-      const double dist = __dsqrt_rn(sacc);
       if (fabs(dist - args.eps) <= args.tie_rel * args.eps) {
         const unsigned long long k = atomicAdd(&args.stats->near_ties, 1ull);
         if ((int64_t)k < args.tie_cap && args.ties) {
@@ -827,7 +856,7 @@ cudaError_t launch_tc(const TcPlan& P, const TcArgs& a, cudaStream_t s, int64_t*
 // Operand rows: fp32 rounded to tf32 (cvt.rna) or raw int8 bytes, K padded
 // with zeros to row_bytes; norms in fp64 (float) / int32 (int).
 __global__ void k_tc_prep_f32(const float* __restrict__ X, int64_t n, int d, int row_elems,
-                              float* __restrict__ xop, double* __restrict__ nrm,
+                              int cosine, float* __restrict__ xop, double* __restrict__ nrm,
                               DevStats* stats) {
   int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
@@ -835,13 +864,18 @@ __global__ void k_tc_prep_f32(const float* __restrict__ X, int64_t n, int d, int
   float* o = xop + p * (int64_t)row_elems;
   double ss = 0.0;
   bool fin = true;
-  for (int j = 0; j < row_elems; ++j) {
-    float v = j < d ? x[j] : 0.f;
+  for (int j = 0; j < d; ++j) {
+    const float v = x[j];
     fin = fin && isfinite(v);
+    ss = __dadd_rn(ss, __dmul_rn((double)v, (double)v));
+  }
+  // cosine: operand x / |x| (fp64 norm), a zero row stays zero
+  const double sc = cosine ? (ss > 0.0 ? 1.0 / sqrt(ss) : 0.0) : 1.0;
+  for (int j = 0; j < row_elems; ++j) {
+    const float v = j < d ? (cosine ? (float)((double)x[j] * sc) : x[j]) : 0.f;
     uint32_t t;
     asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(t) : "f"(v));
     o[j] = __uint_as_float(t);
-    ss = __dadd_rn(ss, __dmul_rn((double)v, (double)v));
   }
   if (!fin) atomicExch(&stats->nonfinite, 1);
   nrm[p] = ss;
@@ -880,6 +914,35 @@ __global__ void k_tc_rows_f32(const double* __restrict__ nrm, int64_t n, int64_t
   hi[p] = __double2float_ru(g + C2 * np + tau);
 }
 
+__global__ void k_tc_rows_cos(const double* __restrict__ nrm, int64_t n, int64_t n_pad,
+                              double eps, double m, float* __restrict__ lo,
+                              float* __restrict__ hi) {
+  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n_pad) return;
+  if (p >= n) {
+    lo[p] = INFINITY;
+    hi[p] = INFINITY;
+    return;
+  }
+  if (nrm[p] == 0.0) {   // zero vector: every live pair to the fp64 zero rule
+    lo[p] = -1e37f;       // (padding columns sit at -1e38, below it)
+    hi[p] = INFINITY;
+    return;
+  }
+  // out if cos <= 1 - eps - tie - m, in if cos > 1 - eps + tie + m (tie: 1e-6 eps)
+  lo[p] = __double2float_rd(1.0 - eps - 1.0000005e-6 * eps - m);
+  hi[p] = __double2float_ru(1.0 - eps + 1.0000005e-6 * eps + m);
+}
+
+cudaError_t launch_tc_rows_cos(const TcPlan& P, const void* nrm, int64_t n, double eps, double m,
+                               TcArgs& a, cudaStream_t s, int64_t* launches) {
+  ++*launches;
+  const unsigned g = (unsigned)((P.n_pad + 255) / 256);
+  k_tc_rows_cos<<<g, 256, 0, s>>>((const double*)nrm, n, P.n_pad, eps, m, (float*)a.row_lo,
+                                  (float*)a.row_hi);
+  return cudaGetLastError();
+}
+
 __global__ void k_tc_rows_int(const int32_t* __restrict__ nrm, int64_t n, int64_t n_pad,
                               int32_t lo_i, int32_t* __restrict__ r) {
   int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -901,11 +964,13 @@ __global__ void k_tc_gather_lm(const uint8_t* __restrict__ xop, int64_t row_byte
 }
 
 __global__ void k_tc_cols_f32(const double* __restrict__ nrm, const int32_t* __restrict__ lm,
-                              int64_t L, int64_t l_pad, double C2, float* __restrict__ ca,
-                              float* __restrict__ cb, float* __restrict__ colk) {
+                              int64_t L, int64_t l_pad, double C2, int cosine,
+                              float* __restrict__ ca, float* __restrict__ cb,
+                              float* __restrict__ colk) {
   int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= l_pad) return;
   if (j >= L) tc_col_inert(j, ca, cb, colk);
+  else if (cosine) tc_col_consts_cos(nrm[lm[j]], j, ca, cb, colk);
   else tc_col_consts(nrm[lm[j]], C2, j, ca, cb, colk);
 }
 
@@ -920,7 +985,7 @@ __global__ void k_tc_cols_int(const int32_t* __restrict__ nrm, const int32_t* __
 // new landmarks (count on the device); columns >= count are inert.
 __global__ void k_tc_tile_lm(const uint8_t* __restrict__ xop, int64_t row_bytes,
                              const int32_t* __restrict__ new_lm,
-                             const int32_t* __restrict__ l_count_dev, int kind,
+                             const int32_t* __restrict__ l_count_dev, int kind, int cosine,
                              const void* __restrict__ nrm, double C2, uint8_t* __restrict__ lop,
                              float* __restrict__ ca, float* __restrict__ cb,
                              float* __restrict__ colk, int32_t* __restrict__ cc) {
@@ -936,8 +1001,9 @@ __global__ void k_tc_tile_lm(const uint8_t* __restrict__ xop, int64_t row_bytes,
     dst[i] = live ? src[i] : make_uint4(0, 0, 0, 0);
   if (threadIdx.x == 0) {
     if (kind == TC_TF32) {
-      if (live) tc_col_consts(((const double*)nrm)[pt], C2, j, ca, cb, colk);
-      else tc_col_inert(j, ca, cb, colk);
+      if (!live) tc_col_inert(j, ca, cb, colk);
+      else if (cosine) tc_col_consts_cos(((const double*)nrm)[pt], j, ca, cb, colk);
+      else tc_col_consts(((const double*)nrm)[pt], C2, j, ca, cb, colk);
     } else {
       cc[j] = live ? ((const int32_t*)nrm)[pt] : (1 << 30);
     }
@@ -949,7 +1015,8 @@ cudaError_t launch_tc_tile_landmarks(const TcPlan& P, const void* nrm, const int
                                      cudaStream_t s, int64_t* launches) {
   ++*launches;
   return launch_pdl(k_tc_tile_lm, dim3((unsigned)P.l_rows), dim3(64), 0, s,
-                    (const uint8_t*)P.xop, P.row_bytes, new_lm, l_count_dev, P.kind, nrm, C2,
+                    (const uint8_t*)P.xop, P.row_bytes, new_lm, l_count_dev, P.kind, P.cosine,
+                    nrm, C2,
                     (uint8_t*)P.lop, (float*)a.col_a, (float*)a.col_b, (float*)a.colk,
                     (int32_t*)a.col_c);
 }
@@ -970,7 +1037,7 @@ cudaError_t launch_tc_prep(const void* X, int dtype, int64_t n, int d, const TcP
   ++*launches;
   const unsigned g = (unsigned)((n + 255) / 256);
   if (dtype == BM_F32)
-    k_tc_prep_f32<<<g, 256, 0, s>>>((const float*)X, n, d, (int)(P.row_bytes / 4),
+    k_tc_prep_f32<<<g, 256, 0, s>>>((const float*)X, n, d, (int)(P.row_bytes / 4), P.cosine,
                                     (float*)P.xop, (double*)nrm, stats);
   else
     k_tc_prep_int<<<g, 256, 0, s>>>((const uint8_t*)X, n, d, (int)P.row_bytes, dtype == BM_U8,
@@ -998,7 +1065,7 @@ cudaError_t launch_tc_landmarks(const TcPlan& P, const void* nrm, const int32_t*
                                                     P.l_rows, (uint8_t*)P.lop);
   const unsigned g = (unsigned)((P.l_rows + 255) / 256);
   if (P.kind == TC_TF32)
-    k_tc_cols_f32<<<g, 256, 0, s>>>((const double*)nrm, lm, L, P.l_rows, C2,
+    k_tc_cols_f32<<<g, 256, 0, s>>>((const double*)nrm, lm, L, P.l_rows, C2, P.cosine,
                                     (float*)a.col_a, (float*)a.col_b, (float*)a.colk);
   else
     k_tc_cols_int<<<g, 256, 0, s>>>((const int32_t*)nrm, lm, L, P.l_rows, (int32_t*)a.col_c);

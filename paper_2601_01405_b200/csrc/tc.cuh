@@ -29,6 +29,7 @@ struct TcPlan {
   int katoms;          // ceil(row_bytes / 128)
   int num_sms;
   const float* ones;   // tf32: [128][8] constant A tile {1,1,1,0,0,0,0,0} (column-constant fold)
+  int cosine;          // tf32: operands are x / |x| and the contraction scores cosine similarity
 };
 
 struct TcArgs {
@@ -58,6 +59,7 @@ struct TcArgs {
   int d;
   double eps, eps2, tie_rel;
   const int32_t* lm_idx;   // landmark column -> point index
+  int cosine;              // recheck with the cosine formula (else Euclidean)
   int64_t* ties;           // near-tie triples (point, landmark point, decision)
   int64_t tie_cap;
   DevStats* stats;         // band_pairs / near_ties counters
@@ -76,6 +78,9 @@ cudaError_t launch_tc_prep(const void* X, int dtype, int64_t n, int d, const TcP
 cudaError_t launch_tc_rows(const TcPlan& P, const void* nrm, int64_t n, double C2, double eps2,
                            double tau, int32_t lo_i, TcArgs& a, cudaStream_t s,
                            int64_t* launches);
+// cosine: uniform row thresholds around 1 - eps with margin m (zero rows: every pair rechecked)
+cudaError_t launch_tc_rows_cos(const TcPlan& P, const void* nrm, int64_t n, double eps, double m,
+                               TcArgs& a, cudaStream_t s, int64_t* launches);
 cudaError_t launch_tc_landmarks(const TcPlan& P, const void* nrm, const int32_t* lm, int64_t L,
                                 double C2, TcArgs& a, cudaStream_t s, int64_t* launches);
 // Fused greedy tile: gather the *l_count_dev new landmarks' operand rows into

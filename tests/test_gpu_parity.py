@@ -242,3 +242,28 @@ def test_capacity_fallbacks(bm):
     cov = bm.cover_build(t3, w3.metric, w3.eps, path="tensor", key_cap=100)
     assert cov.stats.path_used == 2
     compare(X3, w3.metric, w3.eps, cov, float_path=True)
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_l1_prefilter_equivalence(bm, seed):
+    """The 8-bit SAD prefilter of the L1 membership pass only skips pairs it
+    proves out: results equal the unfiltered fp32 path and the oracle, also
+    for wide coordinate ranges (coarse quantisation), exact-eps distances and
+    d not a multiple of 4."""
+    from paper_2601_01405_b200 import bm as B
+    rng = np.random.default_rng([seed, 77])
+    n, d = 4000, [16, 7, 33][seed]
+    X = rng.random((n, d)).astype(np.float32)
+    if seed == 1:
+        X[::50] *= 1000.0            # a few far outliers: coarse 8-bit scale
+    if seed == 2:
+        X[1::2] = X[0::2][: n // 2]  # duplicates, then shift coordinate 0 by exactly eps
+        X[1::2, 0] += np.float32(0.5)
+    eps = 0.5 if seed == 2 else 0.25 * d / 4
+    t = torch.from_numpy(X).cuda()
+    a = bm.cover_build(t, "l1", eps, tile=256)
+    b = bm.cover_build(t, "l1", eps, tile=256, flags=B.FLAG_NO_L1_PREFILTER)
+    na, nb = a.numpy(), b.numpy()
+    for k in na:
+        assert np.array_equal(na[k], nb[k]), k
+    compare(X, "l1", eps, a, float_path=True)

@@ -89,3 +89,27 @@ def test_tensor_path_random(bm, d, dtype):
         Y[1::2] = Y[0::2][: len(Y[1::2])] + np.float32(eps / math.sqrt(d)) * (1 + 1e-6)
         cov = bm.cover_build(torch.from_numpy(Y).cuda(), "l2", eps, path="tensor")
         compare(Y, "l2", eps, cov, float_path=True)
+
+
+@pytest.mark.parametrize("d", [3, 16, 64, 100])
+def test_tensor_path_cosine(bm, d):
+    """Cosine distance on tcgen05 (Gram of the normalised rows, rigorous band,
+    fp64 recheck with the zero-vector rule): equal to the oracle, with zero
+    rows, duplicate directions and points exactly at eps."""
+    rng = np.random.default_rng(d)
+    n = 3000
+    X = rng.normal(size=(n, d)).astype(np.float32)
+    X[::97] = 0.0                                  # zero vectors (reading A7)
+    X[1::5] = X[0::5][: len(X[1::5])] * np.float32(3.0)   # same direction: distance 0
+    eps = 0.05 if d > 3 else 0.02
+    cov = bm.cover_build(torch.from_numpy(X).cuda(), "cos", eps, path="tensor", tile=256)
+    assert cov.stats.path_used == 2
+    compare(X, "cos", eps, cov, float_path=True)
+
+
+def test_tensor_path_cosine_c5_prefix(bm):
+    w = gen.get("c5_cos")
+    X = gen.generate(w, 60000)
+    cov = bm.cover_build(torch.from_numpy(X).cuda(), w.metric, w.eps, path="tensor")
+    assert cov.stats.path_used == 2
+    compare(X, w.metric, w.eps, cov, float_path=True, tie_rate_limit=True)
