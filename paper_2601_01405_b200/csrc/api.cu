@@ -759,32 +759,46 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
   // sort on the position bits and then the point bits gives the point-major
   // order; a further stable sort on the position bits alone gives the
   // landmark-major order with the points of each ball still ascending.
-  unsigned long long* alt = nullptr;
-  void* rtemp = nullptr;
+  // (n * L <= 2^30: both CSRs from two bit matrices instead, no sort)
   int64_t* pt_ptr = nullptr;
   int32_t* pt_lm = nullptr;
   int64_t* ball_ptr = nullptr;
   int32_t* ball_idx = nullptr;
-  TRY(pool.alloc(&alt, (size_t)(M > 0 ? M : 1)));
-  TRY(pool.alloc((uint8_t**)&rtemp, radix_temp_bytes(M)));
   TRY(pool.alloc(&pt_ptr, (size_t)n + 1));
   TRY(pool.alloc(&pt_lm, (size_t)(M > 0 ? M : 1)));
   TRY(pool.alloc(&ball_ptr, (size_t)L + 1));
   TRY(pool.alloc(&ball_idx, (size_t)(M > 0 ? M : 1)));
-  const unsigned long long lo32 = 0xffffffffull;
-  const BitRange pm[2] = {{0, lbits}, {32, 32 + pbits}};
-  const BitRange lmaj[1] = {{0, lbits}};
-  tr("csr alloc");
-  CK(radix_sort_u64(&keys, &alt, M, pm, 2, rtemp, s, &launches));
-  tr("csr sort point-major");
-  CK(launch_unpack_low(keys, M, lo32, pt_lm, s, &launches));
-  CK(launch_segment_ptr(keys, M, 32, lo32, n, pt_ptr, s, &launches));
-  CK(radix_sort_u64(&keys, &alt, M, lmaj, 1, rtemp, s, &launches));
-  CK(launch_unpack_high(keys, M, ball_idx, s, &launches));
-  CK(launch_segment_ptr(keys, M, 0, lo32, L, ball_ptr, s, &launches));
-  pool.free_now(keys);
-  pool.free_now(alt);
-  pool.free_now(rtemp);
+  if (n * L <= kCsrBitmapMaxBits) {
+    uint32_t* cbits = nullptr;
+    void* ctemp = nullptr;
+    TRY(pool.alloc(&cbits, (size_t)csr_bitmap_words(n, L)));
+    TRY(pool.alloc((uint8_t**)&ctemp, csr_bitmap_temp_bytes(n, L)));
+    tr("csr alloc");
+    CK(csr_from_keys_bitmap(keys, M, n, L, cbits, ctemp, pt_ptr, pt_lm, ball_ptr, ball_idx, s,
+                            &launches));
+    pool.free_now(cbits);
+    pool.free_now(ctemp);
+    pool.free_now(keys);
+  } else {
+    unsigned long long* alt = nullptr;
+    void* rtemp = nullptr;
+    TRY(pool.alloc(&alt, (size_t)(M > 0 ? M : 1)));
+    TRY(pool.alloc((uint8_t**)&rtemp, radix_temp_bytes(M)));
+    const unsigned long long lo32 = 0xffffffffull;
+    const BitRange pm[2] = {{0, lbits}, {32, 32 + pbits}};
+    const BitRange lmaj[1] = {{0, lbits}};
+    tr("csr alloc");
+    CK(radix_sort_u64(&keys, &alt, M, pm, 2, rtemp, s, &launches));
+    tr("csr sort point-major");
+    CK(launch_unpack_low(keys, M, lo32, pt_lm, s, &launches));
+    CK(launch_segment_ptr(keys, M, 32, lo32, n, pt_ptr, s, &launches));
+    CK(radix_sort_u64(&keys, &alt, M, lmaj, 1, rtemp, s, &launches));
+    CK(launch_unpack_high(keys, M, ball_idx, s, &launches));
+    CK(launch_segment_ptr(keys, M, 0, lo32, L, ball_ptr, s, &launches));
+    pool.free_now(keys);
+    pool.free_now(alt);
+    pool.free_now(rtemp);
+  }
   tm.mark(4);
   tr("csr rest");
 

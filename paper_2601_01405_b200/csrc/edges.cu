@@ -45,25 +45,29 @@ __device__ __forceinline__ uint32_t lookback_excl(unsigned long long* state, int
 }
 
 // ---------------------------------------------------------------- bitmap path
-// One warp per point: set bit (i, j) for every pair a < c of its row.
+// One thread per point: set bit (i, j) for every pair a < c of its row
+// (rows are short: t_p ~ 2-40 on the BASELINE configs); the warp adds its C(t,2).
 __global__ void k_edge_bits(const int64_t* __restrict__ pt_ptr, const int32_t* __restrict__ pt_lm,
                             int64_t n, int W, uint32_t* __restrict__ bits,
                             unsigned long long* __restrict__ npairs) {
   pdl_wait();
-  const int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (p >= n) return;
-  const int64_t b = pt_ptr[p], t = pt_ptr[p + 1] - b;
-  if (t < 2) return;
-  if (lane == 0) atomicAdd(npairs, (unsigned long long)(t * (t - 1) / 2));
-  for (int64_t a = 0; a + 1 < t; ++a) {
-    const int64_t i = pt_lm[b + a];
-    uint32_t* row = bits + i * (int64_t)W;
-    for (int64_t c = a + 1 + lane; c < t; c += 32) {
-      const int32_t j = pt_lm[b + c];
-      atomicOr(row + (j >> 5), 1u << (j & 31));
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long mine = 0ull;
+  if (p < n) {
+    const int64_t b = pt_ptr[p], t = pt_ptr[p + 1] - b;
+    if (t >= 2) {
+      mine = (unsigned long long)(t * (t - 1) / 2);
+      for (int64_t a = 0; a + 1 < t; ++a) {
+        uint32_t* row = bits + (int64_t)pt_lm[b + a] * W;
+        for (int64_t c = a + 1; c < t; ++c) {
+          const int32_t j = pt_lm[b + c];
+          atomicOr(row + (j >> 5), 1u << (j & 31));
+        }
+      }
     }
   }
+  for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(FME, mine, o);
+  if ((threadIdx.x & 31) == 0 && mine) atomicAdd(npairs, mine);
 }
 
 // Row-major walk of the bit matrix: CTA tile = 256 threads x 4 consecutive
@@ -186,7 +190,121 @@ __global__ void __launch_bounds__(UQ_NT) k_unique_compact(const unsigned long lo
   }
 }
 
+// ---------------------------------------------------------------- bitmap CSR
+// Step C for moderate n * L: the membership keys (point << 32 | position) set
+// bit (p, j) of a point-major [n][Wp] and bit (j, p) of a landmark-major [L][Wl]
+// bit matrix; one look-back pass per matrix then writes the column index of
+// every set bit in row-major order — i.e. a CSR already sorted both ways.
+__global__ void k_keys_to_bits(const unsigned long long* __restrict__ keys, int64_t m, int Wp,
+                               int Wl, uint32_t* __restrict__ pbits, uint32_t* __restrict__ lbits) {
+  pdl_wait();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long k = keys[i];
+    const int64_t p = (int64_t)(k >> 32), j = (int64_t)(k & 0xffffffffull);
+    atomicOr(pbits + p * Wp + (j >> 5), 1u << (j & 31));
+    atomicOr(lbits + j * Wl + (p >> 5), 1u << (p & 31));
+  }
+}
+
+__global__ void __launch_bounds__(EB_NT) k_bits_csr(const uint32_t* __restrict__ bits, int64_t rows,
+                                                   int W, int64_t* __restrict__ ptr,
+                                                   int32_t* __restrict__ idx,
+                                                   unsigned long long* state, int32_t* ticket,
+                                                   uint32_t tag) {
+  __shared__ int s_tile;
+  __shared__ uint32_t s_warp[EB_NT / 32];
+  __shared__ uint32_t s_excl;
+  pdl_wait();
+  if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1);
+  __syncthreads();
+  const int64_t nwords = rows * (int64_t)W;
+  const int64_t tile = s_tile;
+  const int64_t w0 = tile * EB_TILE + (int64_t)threadIdx.x * EB_WPT;
+  uint32_t wv[EB_WPT];
+  uint32_t cnt = 0;
+#pragma unroll
+  for (int k = 0; k < EB_WPT; ++k) {
+    wv[k] = w0 + k < nwords ? bits[w0 + k] : 0u;
+    cnt += __popc(wv[k]);
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(FME, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) s_warp[w] = incl;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t agg = 0;
+    for (int k = 0; k < EB_NT / 32; ++k) agg += s_warp[k];
+    const uint32_t ex = lookback_excl(state, tile, tag, agg);
+    s_excl = ex;
+    if ((tile + 1) * EB_TILE >= nwords) ptr[rows] = (int64_t)ex + agg;
+  }
+  __syncthreads();
+  int64_t pos = s_excl + incl - cnt;
+  for (int k = 0; k < w; ++k) pos += s_warp[k];
+#pragma unroll
+  for (int k = 0; k < EB_WPT; ++k) {
+    const int64_t word = w0 + k;
+    if (word >= nwords) break;
+    const int64_t row = word / W;
+    const int64_t cb = (word - row * W) * 32;
+    if (cb == 0) ptr[row] = pos;   // first word of a row: its CSR start
+    uint32_t v = wv[k];
+    while (v) {
+      const int b = __ffs(v) - 1;
+      v &= v - 1u;
+      idx[pos++] = (int32_t)(cb + b);
+    }
+  }
+}
+
 // ---------------------------------------------------------------- host side
+int64_t csr_bitmap_words(int64_t n, int64_t L) {
+  return n * ((L + 31) / 32) + L * ((n + 31) / 32);
+}
+
+cudaError_t csr_from_keys_bitmap(const unsigned long long* keys, int64_t m, int64_t n, int64_t L,
+                                 uint32_t* bits, void* temp, int64_t* pt_ptr, int32_t* pt_lm,
+                                 int64_t* ball_ptr, int32_t* ball_idx, cudaStream_t s,
+                                 int64_t* launches) {
+  const int Wp = (int)((L + 31) / 32), Wl = (int)((n + 31) / 32);
+  uint32_t* pb = bits;
+  uint32_t* lb = bits + n * (int64_t)Wp;
+  cudaError_t e = cudaMemsetAsync(bits, 0, sizeof(uint32_t) * csr_bitmap_words(n, L), s);
+  if (e != cudaSuccess) return e;
+  int64_t g = (m + 255) / 256;
+  if (g > 148 * 16) g = 148 * 16;
+  if (g < 1) g = 1;
+  e = launch_pdl(k_keys_to_bits, dim3((unsigned)g), dim3(256), 0, s, keys, m, Wp, Wl, pb, lb);
+  if (e != cudaSuccess) return e;
+  // two look-back passes; state: [ticket x2 | pad][tiles_p + 1][tiles_l + 1]
+  const int64_t tp = (n * (int64_t)Wp + EB_TILE - 1) / EB_TILE;
+  const int64_t tl = (L * (int64_t)Wl + EB_TILE - 1) / EB_TILE;
+  int32_t* tickets = (int32_t*)temp;
+  unsigned long long* sp = (unsigned long long*)((char*)temp + 64);
+  unsigned long long* sl = sp + tp + 1;
+  e = cudaMemsetAsync(temp, 0, 64 + sizeof(unsigned long long) * (tp + tl + 2), s);
+  if (e != cudaSuccess) return e;
+  e = launch_pdl(k_bits_csr, dim3((unsigned)(tp > 0 ? tp : 1)), dim3(EB_NT), 0, s,
+                 (const uint32_t*)pb, n, Wp, pt_ptr, pt_lm, sp, tickets, 1u);
+  if (e != cudaSuccess) return e;
+  e = launch_pdl(k_bits_csr, dim3((unsigned)(tl > 0 ? tl : 1)), dim3(EB_NT), 0, s,
+                 (const uint32_t*)lb, L, Wl, ball_ptr, ball_idx, sl, tickets + 1, 1u);
+  *launches += 3;
+  return e;
+}
+
+size_t csr_bitmap_temp_bytes(int64_t n, int64_t L) {
+  const int64_t Wp = (L + 31) / 32, Wl = (n + 31) / 32;
+  const int64_t tp = (n * Wp + EB_TILE - 1) / EB_TILE, tl = (L * Wl + EB_TILE - 1) / EB_TILE;
+  return 64 + sizeof(unsigned long long) * (size_t)(tp + tl + 2);
+}
+
 int64_t edge_bitmap_words(int64_t L) { return L * ((L + 31) / 32); }
 
 size_t edge_lb_temp_bytes(int64_t items) {
@@ -203,7 +321,7 @@ cudaError_t launch_edge_bits(const int64_t* pt_ptr, const int32_t* pt_lm, int64_
   e = cudaMemsetAsync(npairs, 0, sizeof(unsigned long long), s);
   if (e != cudaSuccess) return e;
   ++*launches;
-  int64_t g = (n * 32 + 255) / 256;
+  int64_t g = (n + 255) / 256;
   return launch_pdl(k_edge_bits, dim3((unsigned)(g > 0 ? g : 1)), dim3(256), 0, s, pt_ptr, pt_lm,
                     n, W, bits, npairs);
 }

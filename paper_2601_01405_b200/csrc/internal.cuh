@@ -175,6 +175,14 @@ cudaError_t launch_unique_flags(const unsigned long long* keys, int64_t m, int64
 cudaError_t launch_unique_scatter(const unsigned long long* keys, int64_t m,
                                   const int64_t* pos, int lbits, int32_t* edges,
                                   cudaStream_t s, int64_t* launches);
+// edges.cu, step C for n * L <= kCsrBitmapMaxBits: both CSRs from bit matrices
+constexpr int64_t kCsrBitmapMaxBits = (int64_t)1 << 30;
+int64_t csr_bitmap_words(int64_t n, int64_t L);
+size_t csr_bitmap_temp_bytes(int64_t n, int64_t L);
+cudaError_t csr_from_keys_bitmap(const unsigned long long* keys, int64_t m, int64_t n, int64_t L,
+                                 uint32_t* bits, void* temp, int64_t* pt_ptr, int32_t* pt_lm,
+                                 int64_t* ball_ptr, int32_t* ball_idx, cudaStream_t s,
+                                 int64_t* launches);
 // edges.cu: bitmap path for L <= kEdgeBitmapMaxL, keys path (sort + unique) above
 constexpr int64_t kEdgeBitmapMaxL = 4096;
 int64_t edge_bitmap_words(int64_t L);

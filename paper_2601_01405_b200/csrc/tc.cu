@@ -244,7 +244,7 @@ struct Smem {
   static constexpr int AK_OFF = ABUF * A_BYTES + B_BYTES;
   static constexpr int BK_SLOT = BN * 32;
   static constexpr int COL_OFF = AK_OFF + (FOLD ? 128 * 32 + 2 * BK_SLOT : 0);
-  static constexpr int COL_BYTES = BN * 4;                 // int8: per-buffer column constants
+  static constexpr int COL_BYTES = BN * 4;   // int8: per-buffer column constants c_j
   static constexpr int BAR_OFF = COL_OFF + (FOLD ? 0 : NBUF * COL_BYTES);
   static constexpr int NBARS = 2 * STAGES + 2 * ABUF + 3 * NBUF + 5;
   static constexpr int CNT_OFF = BAR_OFF + NBARS * 8;     // tmem slot + per-warp counts
@@ -432,13 +432,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         for (int64_t t = t0; t < t1; ++t) {
           mbar_wait(&t_empty[buf], (use[buf] & 1u) ^ 1u);
           fence_after();
-          // int8: the tile's per-column constants (col_c) into this buffer's slot
+          // int8: the tile's per-column constants c_j into this buffer's slot
           if constexpr (MODE == TC_MODE_MEMBER && !FOLD) {
             mbar_expect_tx(&c_full[buf], (uint32_t)S::COL_BYTES);
             bulk_load(scol + buf * BN, (const void*)(args.col_c + t * BN),
                       (uint32_t)S::COL_BYTES, &c_full[buf]);
           }
           const uint32_t dcol = tmem + (uint32_t)(buf * BUFCOLS);
+          // the last tile of a ragged column range issues a narrower MMA
+          // (N rounded up to 32; the padding columns carry inert constants)
+          const int64_t left = n_cols - t * BN;
+          const uint32_t nt = left >= BN ? (uint32_t)BN : (uint32_t)((left + 31) / 32 * 32);
+          const uint32_t idesc = (IDESC & ~(0x3Fu << 17)) | ((nt >> 3) << 17);
           for (int ka = 0; ka < KATOMS; ++ka) {
             mbar_wait(&full[stage], phase);
             fence_after();
@@ -450,7 +455,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               for (int ks = 0; ks < 4; ++ks) {
                 if (ka * 4 + ks < ksteps)
                   mma<KIND>(dcol + (uint32_t)(r * BN), sdesc(abase + ks * 32),
-                            sdesc(bbase + ks * 32), IDESC, (ka | ks) != 0 ? 1u : 0u);
+                            sdesc(bbase + ks * 32), idesc, (ka | ks) != 0 ? 1u : 0u);
               }
             }
             mma_commit(&empty[stage]);
@@ -463,7 +468,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             const int sl = (int)(tk & 1);
             mbar_wait(&bk_full[sl], (uint32_t)((tk >> 1) & 1));
             fence_after();
-            mma<KIND>(dcol, sdesc32(su32(sAK)), sdesc32(su32(sBK + sl * S::BK_SLOT)), IDESC, 1u);
+            mma<KIND>(dcol, sdesc32(su32(sAK)), sdesc32(su32(sBK + sl * S::BK_SLOT)), idesc, 1u);
             mma_commit(&bk_empty[sl]);
           }
           ++tk;
@@ -653,13 +658,25 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               // rare path: column masks of candidates (not certainly out) and
               // certain-in pairs, then one append per set bit
               uint32_t cand = 0u, inm = 0u;
+              float dj[32];   // tf32 in-test offsets of the chunk (warp-uniform loads)
+              if constexpr (KIND == TC_TF32) {
+                const float4* d4 = reinterpret_cast<const float4*>(args.col_a + j0);
+#pragma unroll
+                for (int i4 = 0; i4 < 8; ++i4) {
+                  const float4 q4 = __ldg(d4 + i4);
+                  dj[4 * i4] = q4.x;
+                  dj[4 * i4 + 1] = q4.y;
+                  dj[4 * i4 + 2] = q4.z;
+                  dj[4 * i4 + 3] = q4.w;
+                }
+              }
               if (surv) {
 #pragma unroll
                 for (int i = 0; i < 32; ++i) {
                   if constexpr (KIND == TC_TF32) {
                     const float a = __uint_as_float(v[i]);
                     cand |= (a > rlo[r] ? 1u : 0u) << i;
-                    inm |= (a - __ldg(args.col_a + j0 + i) > rhi[r] ? 1u : 0u) << i;
+                    inm |= (a - dj[i] > rhi[r] ? 1u : 0u) << i;
                   } else {
                     cand |= (2 * (int)v[i] - __ldg(args.col_c + j0 + i) > rint[r] ? 1u : 0u) << i;
                   }
@@ -684,15 +701,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           }
         };
         if constexpr (MODE != TC_MODE_PROBE_NOLD) {
+          // chunks the (possibly narrower) MMA of this tile wrote
+          const int64_t left = n_cols - t * BN;
+          const int nch = RA == 1 && left < BN ? (int)((left + 31) / 32) : NCH;
 #pragma unroll 1
-          for (int c = 0; c < NCH; c += 2) {
-            if (c + 1 < NCH) tmem_ld32_nowait(trow + (uint32_t)(((c + 1) / (BN / 32)) * BN + ((c + 1) % (BN / 32)) * 32), vb);
+          for (int c = 0; c < nch; c += 2) {
+            if (c + 1 < nch) tmem_ld32_nowait(trow + (uint32_t)(((c + 1) / (BN / 32)) * BN + ((c + 1) % (BN / 32)) * 32), vb);
             chunk(c, va);
-            if (c + 1 < NCH) {
+            if (c + 1 < nch) {
               tmem_wait(vb);
-              if (c + 2 < NCH) tmem_ld32_nowait(trow + (uint32_t)(((c + 2) / (BN / 32)) * BN + ((c + 2) % (BN / 32)) * 32), va);
+              if (c + 2 < nch) tmem_ld32_nowait(trow + (uint32_t)(((c + 2) / (BN / 32)) * BN + ((c + 2) % (BN / 32)) * 32), va);
               chunk(c + 1, vb);
-              if (c + 2 < NCH) tmem_wait(va);
+              if (c + 2 < nch) tmem_wait(va);
             }
           }
         }
