@@ -592,7 +592,14 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
 
   // tensor path: tile landmark operand [T_pad][row_bytes], column constants
   tc::TcArgs ta{};
+  // A2 on tensor cores when the CUDA-core adjacency kernel would have to
+  // re-read wide rows from memory (no register-resident width fits, e.g. C4)
+  const bool tc_adj = use_tc && pick_nu(nu_needed) == 0;
+  tc::TcArgs ac{};      // A2 on tensor cores: candidate contraction
+  tc::TcPlan Pc{};
+  tc::RowParams rp{};
   double C2 = 0.0;
+  double tau = 0.0;
   if (use_tc) {
     const int BN = tc::tc_bn_for(P.kind, P.katoms);
     const int RB = tc::tc_rows_for(P.kind, P.katoms);
@@ -606,7 +613,6 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
     ta.l_total_dev = cnt + 2;
     ta.covered = covered;
     TRY(pool.alloc((uint8_t**)&P.lop, (size_t)P.l_rows * P.row_bytes));
-    double tau = 0.0;
     if (P.kind == tc::TC_TF32) {
       float *rlo, *rhi, *ca, *cb;
       TRY(pool.alloc(&rlo, (size_t)P.n_pad));
@@ -634,6 +640,51 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
     ta.key_count = &stats->key_count;
     ta.key_cap = key_cap;
     set_recheck(ta, rows, 2 * nu, d, th, new_lm, ties_dev, tie_cap, stats);
+  }
+  if (tc_adj) {
+    // A2 on tensor cores: the tile's candidates x themselves (adjacency epilogue)
+    rp.tf32 = P.kind == tc::TC_TF32;
+    rp.cosine = P.cosine;
+    rp.C2 = C2;
+    rp.eps = th.eps;
+    rp.eps2 = th.eps2;
+    rp.tau = tau;
+    rp.m = tc_cos_margin(ta.ksteps);
+    rp.lo_i = th.lo_i;
+    const int64_t Tp = ((T + 255) / 256) * 256;
+    Pc = P;
+    Pc.n_rows = Tp;
+    Pc.l_rows = Tp;
+    Pc.n_pad = Tp;
+    uint8_t* cop = nullptr;
+    TRY(pool.alloc(&cop, (size_t)Tp * P.row_bytes));
+    Pc.xop = cop;
+    Pc.lop = cop;
+    ac.n = Tp;
+    ac.L = T;
+    ac.ksteps = ta.ksteps;
+    ac.adj = adj;
+    ac.adj_T = T;
+    if (rp.tf32) {
+      float *rlo, *rhi, *ca, *cb, *colk;
+      TRY(pool.alloc(&rlo, (size_t)Tp));
+      TRY(pool.alloc(&rhi, (size_t)Tp));
+      TRY(pool.alloc(&ca, (size_t)Tp));
+      TRY(pool.alloc(&cb, (size_t)Tp));
+      TRY(pool.alloc(&colk, (size_t)Tp * 8));
+      ac.row_lo = rlo;
+      ac.row_hi = rhi;
+      ac.col_a = ca;
+      ac.col_b = cb;
+      ac.colk = colk;
+    } else {
+      int32_t *rr, *cc;
+      TRY(pool.alloc(&rr, (size_t)Tp));
+      TRY(pool.alloc(&cc, (size_t)Tp));
+      ac.row_r = rr;
+      ac.col_c = cc;
+    }
+    set_recheck(ac, rows, 2 * nu, d, th, nullptr, nullptr, 0, stats);
   }
   tm.mark(1);
   tr("greedy buffers");
@@ -676,7 +727,15 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
       a.l_end_dev = cnt + cur;
       a.adj = adj;
       a.adj_words = adj_words;
-      CK(launch_pairs(kind, MODE_ADJ, a, T, s, &launches));
+      if (tc_adj) {
+        ac.l_count_dev = cnt + cur;
+        ac.lm_idx = uncb[cur];
+        CK(tc::launch_tc_tile_cand(P, Pc, tc_nrm, uncb[cur], cnt + cur, T, C2, rp, ac, s,
+                                   &launches));
+        CK(tc::launch_tc_adj(Pc, ac, s, &launches));
+      } else {
+        CK(launch_pairs(kind, MODE_ADJ, a, T, s, &launches));
+      }
       // A3: in-order resolve, append landmarks (resets the tile's counters)
       CK(launch_resolve(adj, adj_words, uncb[cur], cnt + cur, T, lm, cnt + 2, new_lm, cnt + 3,
                         stats, cnt + 4, nullptr, s, &launches));

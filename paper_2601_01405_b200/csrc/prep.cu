@@ -13,59 +13,59 @@
 
 namespace bm {
 
+// G lanes per row (G = 1..32, a power of two >= the row's float count up to
+// a warp): lanes stride over the row, coalesced for wide rows.
 __global__ void k_prep_f32(const float* __restrict__ X, int64_t n, int d, int nu, int cosine,
-                           uint2* __restrict__ rows, uint2* __restrict__ xhat,
+                           int G, uint2* __restrict__ rows, uint2* __restrict__ xhat,
                            DevStats* stats) {
-  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= n) return;
+  const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t p = gt / G;
+  const int lane = (int)(gt % G);
+  const bool live = p < n;
   const float* x = X + p * (int64_t)d;
-  float2* r = reinterpret_cast<float2*>(rows) + p * (int64_t)nu;
+  float* r = reinterpret_cast<float*>(rows) + p * (int64_t)(2 * nu);
   double ss = 0.0;
   bool finite = true;
-  for (int u = 0; u < nu; ++u) {
-    int j = 2 * u;
-    float a = j < d ? x[j] : 0.f;
-    float b = j + 1 < d ? x[j + 1] : 0.f;
-    finite = finite && isfinite(a) && isfinite(b);
-    r[u] = make_float2(a, b);
+  for (int j = lane; live && j < 2 * nu; j += G) {
+    const float a = j < d ? x[j] : 0.f;
+    finite = finite && isfinite(a);
+    r[j] = a;
     ss = __dadd_rn(ss, __dmul_rn((double)a, (double)a));
-    ss = __dadd_rn(ss, __dmul_rn((double)b, (double)b));
   }
+  for (int o = G / 2; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
   if (!finite) atomicExch(&stats->nonfinite, 1);
-  if (cosine) {
-    float2* h = reinterpret_cast<float2*>(xhat) + p * (int64_t)nu;
-    if (ss == 0.0) {
-      for (int u = 0; u < nu; ++u) h[u] = make_float2(0.f, 0.f);
-      h[0] = make_float2(__int_as_float(0x7fc00000), __int_as_float(0x7fc00000));
-    } else {
-      double inv = 1.0 / sqrt(ss);
-      for (int u = 0; u < nu; ++u) {
-        float2 v = r[u];
-        h[u] = make_float2((float)((double)v.x * inv), (float)((double)v.y * inv));
-      }
+  if (cosine && live) {
+    float* h = reinterpret_cast<float*>(xhat) + p * (int64_t)(2 * nu);
+    const double inv = ss > 0.0 ? 1.0 / sqrt(ss) : 0.0;
+    for (int j = lane; j < 2 * nu; j += G) {
+      const float a = j < d ? x[j] : 0.f;
+      // a zero row gets NaN in unit 0 so every pair with it goes to the fp64 rule
+      h[j] = ss == 0.0 ? (j < 2 ? __int_as_float(0x7fc00000) : 0.f) : (float)((double)a * inv);
     }
   }
 }
 
 __global__ void k_prep_int(const uint8_t* __restrict__ X, int64_t n, int d, int nu, int is_u8,
                            uint2* __restrict__ rows, int32_t* __restrict__ inorm) {
-  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (p >= n) return;
   const uint8_t* x = X + p * (int64_t)d;
-  uint2* r = rows + p * (int64_t)nu;
+  uint32_t* r = reinterpret_cast<uint32_t*>(rows + p * (int64_t)nu);
   int32_t ss = 0;
-  for (int u = 0; u < nu; ++u) {
-    uint32_t w[2] = {0u, 0u};
-    for (int k = 0; k < 8; ++k) {
-      int j = 8 * u + k;
+  for (int w = lane; w < 2 * nu; w += 32) {   // 4 coordinates per 32-bit word
+    uint32_t word = 0u;
+    for (int k = 0; k < 4; ++k) {
+      const int j = 4 * w + k;
       int v = 0;
       if (j < d) v = is_u8 ? (int)x[j] - 128 : (int)(int8_t)x[j];
       ss += v * v;
-      w[k >> 2] |= ((uint32_t)(uint8_t)(int8_t)v) << (8 * (k & 3));
+      word |= ((uint32_t)(uint8_t)(int8_t)v) << (8 * k);
     }
-    r[u] = make_uint2(w[0], w[1]);
+    r[w] = word;
   }
-  if (inorm) inorm[p] = ss;
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  if (inorm && lane == 0) inorm[p] = ss;
 }
 
 // ---- L1 prefilter rows
@@ -149,10 +149,13 @@ cudaError_t launch_prep(const void* X, int dtype, int64_t n, int d, int kind, in
                         uint2* rows, uint2* xhat, int32_t* inorm, DevStats* stats,
                         cudaStream_t s, int64_t* launches) {
   int bs = 256;
-  int64_t g = (n + bs - 1) / bs;
+  int64_t g = (n * 32 + bs - 1) / bs;   // one warp per row
   if (dtype == BM_F32) {
-    k_prep_f32<<<(unsigned)g, bs, 0, s>>>((const float*)X, n, d, nu, kind == K_COSF, rows, xhat,
-                                          stats);
+    int G = 1;
+    while (G < 32 && G < 2 * nu) G *= 2;
+    g = (n * G + bs - 1) / bs;
+    k_prep_f32<<<(unsigned)g, bs, 0, s>>>((const float*)X, n, d, nu, kind == K_COSF, G, rows,
+                                          xhat, stats);
   } else {
     k_prep_int<<<(unsigned)g, bs, 0, s>>>((const uint8_t*)X, n, d, nu, dtype == BM_U8, rows,
                                           inorm);

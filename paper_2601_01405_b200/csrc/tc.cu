@@ -252,6 +252,35 @@ struct Smem {
   static constexpr int TOTAL = BUF_OFF + EPI_WARPS * (KW + BW) * 8 + 1024;  // + align slack
 };
 
+// B': the oracle's fp64 decision for points p, q (ascending coordinates, no
+// contraction; cosine with the zero-vector rule, A6/A7).
+__device__ __noinline__ bool pair_in_fp64(const float* xrows, int xstride, int dd, int cosine,
+                                          double eps, double eps2, int64_t p, int64_t q,
+                                          double* dist) {
+  const float* x = xrows + p * (int64_t)xstride;
+  const float* y = xrows + q * (int64_t)xstride;
+  if (cosine) {
+    double dot = 0.0, xx = 0.0, yy = 0.0;
+    for (int k = 0; k < dd; ++k) {
+      const double a = (double)x[k], b = (double)y[k];
+      dot = __dadd_rn(dot, __dmul_rn(a, b));
+      xx = __dadd_rn(xx, __dmul_rn(a, a));
+      yy = __dadd_rn(yy, __dmul_rn(b, b));
+    }
+    if (xx == 0.0 && yy == 0.0) *dist = 0.0;
+    else if (xx == 0.0 || yy == 0.0) *dist = 1.0;
+    else *dist = __dsub_rn(1.0, __ddiv_rn(dot, __dmul_rn(__dsqrt_rn(xx), __dsqrt_rn(yy))));
+    return *dist < eps;
+  }
+  double sacc = 0.0;
+  for (int k = 0; k < dd; ++k) {
+    const double t = __dsub_rn((double)x[k], (double)y[k]);
+    sacc = __dadd_rn(sacc, __dmul_rn(t, t));
+  }
+  *dist = __dsqrt_rn(sacc);
+  return sacc < eps2;
+}
+
 // ------------------------------------------------------------------ kernel
 constexpr int TC_THREADS = 384;   // warps 0-3 roles, 4-11 epilogue
 
@@ -344,8 +373,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   // Work units = (block of RA*128 point rows, chunk of BN-wide landmark tiles),
   // enough units to balance the grid; the column count may live on the device
   // (fused greedy tile), so every role derives the same schedule here.
-  const int64_t n_cols = args.l_count_dev ? (int64_t)*args.l_count_dev : args.L;
-  const int64_t lpos0 = args.l_count_dev ? (int64_t)*args.l_total_dev - n_cols : 0;
+  const int64_t n_cols =
+      args.l_count_dev ? min((int64_t)*args.l_count_dev, args.L) : args.L;
+  const int64_t lpos0 = args.l_total_dev ? (int64_t)*args.l_total_dev - n_cols : 0;
   const int64_t n_tiles = (n_cols + BN - 1) / BN;
   int64_t n_chunks = (4 * (int64_t)gridDim.x + args.n_mblk - 1) / args.n_mblk;
   n_chunks = max((int64_t)1, min(n_chunks, n_tiles));
@@ -433,7 +463,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           mbar_wait(&t_empty[buf], (use[buf] & 1u) ^ 1u);
           fence_after();
           // int8: the tile's per-column constants c_j into this buffer's slot
-          if constexpr (MODE == TC_MODE_MEMBER && !FOLD) {
+          if constexpr ((MODE == TC_MODE_MEMBER || MODE == TC_MODE_ADJ) && !FOLD) {
             mbar_expect_tx(&c_full[buf], (uint32_t)S::COL_BYTES);
             bulk_load(scol + buf * BN, (const void*)(args.col_c + t * BN),
                       (uint32_t)S::COL_BYTES, &c_full[buf]);
@@ -495,31 +525,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const int64_t p = (int64_t)(bk >> 32), j = (int64_t)(bk & 0xffffffffull);
       if (j >= n_cols || p >= args.n) return;   // padding rows / columns never qualify
       const int64_t qp = args.lm_idx[j];
-      const float* x = args.xrows + p * (int64_t)args.xstride;
-      const float* y = args.xrows + qp * (int64_t)args.xstride;
-      bool in;
       double dist;
-      if (args.cosine) {   // 1 - x.y / (|x| |y|), zero-vector rule (A7)
-        double dot = 0.0, xx = 0.0, yy = 0.0;
-        for (int k = 0; k < args.d; ++k) {
-          const double a = (double)x[k], b = (double)y[k];
-          dot = __dadd_rn(dot, __dmul_rn(a, b));
-          xx = __dadd_rn(xx, __dmul_rn(a, a));
-          yy = __dadd_rn(yy, __dmul_rn(b, b));
-        }
-        if (xx == 0.0 && yy == 0.0) dist = 0.0;
-        else if (xx == 0.0 || yy == 0.0) dist = 1.0;
-        else dist = __dsub_rn(1.0, __ddiv_rn(dot, __dmul_rn(__dsqrt_rn(xx), __dsqrt_rn(yy))));
-        in = dist < args.eps;
-      } else {
-        double sacc = 0.0;
-        for (int k = 0; k < args.d; ++k) {
-          const double t = __dsub_rn((double)x[k], (double)y[k]);
-          sacc = __dadd_rn(sacc, __dmul_rn(t, t));
-        }
-        in = sacc < args.eps2;
-        dist = __dsqrt_rn(sacc);
-      }
+      const bool in = pair_in_fp64(args.xrows, args.xstride, args.d, args.cosine, args.eps,
+                                   args.eps2, p, qp, &dist);
       if (fabs(dist - args.eps) <= args.tie_rel * args.eps) {
         const unsigned long long k = atomicAdd(&args.stats->near_ties, 1ull);
         if ((int64_t)k < args.tie_cap && args.ties) {
@@ -594,7 +602,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const int buf = (int)(tcount % NBUF);
         const uint32_t ph = (phase >> buf) & 1u;    // this group's parity for buffer buf
         mbar_wait(&t_full[buf], ph);
-        if constexpr (MODE == TC_MODE_MEMBER && !FOLD) mbar_wait(&c_full[buf], ph);
+        if constexpr ((MODE == TC_MODE_MEMBER || MODE == TC_MODE_ADJ) && !FOLD)
+          mbar_wait(&c_full[buf], ph);
         phase ^= 1u << buf;
         fence_after();
         const float* colb = scol + buf * BN;   // tile's col_b (tf32) / col_c (int8) in smem
@@ -624,6 +633,57 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 for (int i = 0; i < 32; ++i)
                   if (j0 + i < n_cols) args.gram[prow[r] * n_cols + j0 + i] = v[i];
               }
+              return;
+            }
+            if constexpr (MODE == TC_MODE_ADJ) {
+              // A2: bit i of word j0/32 of candidate a = [cand j0+i adjacent to a],
+              // strictly lower triangle (j < a), rows and columns < nc
+              const int64_t a = prow[r];
+              const uint32_t tri = j0 >= a ? 0u : (j0 + 32 <= a ? FULLM : ((1u << (a - j0)) - 1u));
+              uint32_t mask = 0u;
+              if constexpr (KIND == TC_TF32) {
+                float dj[32];
+                const float4* d4 = reinterpret_cast<const float4*>(args.col_a + j0);
+#pragma unroll
+                for (int i4 = 0; i4 < 8; ++i4) {
+                  const float4 q4 = __ldg(d4 + i4);
+                  dj[4 * i4] = q4.x;
+                  dj[4 * i4 + 1] = q4.y;
+                  dj[4 * i4 + 2] = q4.z;
+                  dj[4 * i4 + 3] = q4.w;
+                }
+                uint32_t cand = 0u;
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                  const float x = __uint_as_float(v[i]);
+                  cand |= (x > rlo[r] ? 1u : 0u) << i;
+                  mask |= (x - dj[i] > rhi[r] ? 1u : 0u) << i;
+                }
+                mask &= tri;
+                uint32_t band = cand & ~mask & tri;
+                if (a < n_cols) {
+                  while (band) {   // B': fp64 decision of the band pairs
+                    const int i = __ffs(band) - 1;
+                    band &= band - 1u;
+                    double dist;
+                    if (pair_in_fp64(args.xrows, args.xstride, args.d, args.cosine, args.eps,
+                                     args.eps2, args.lm_idx[a], args.lm_idx[j0 + i], &dist))
+                      mask |= 1u << i;
+                  }
+                }
+              } else {
+                const int4* cc4 = reinterpret_cast<const int4*>(colb + cc * 32);
+#pragma unroll
+                for (int i4 = 0; i4 < 8; ++i4) {
+                  const int4 c = cc4[i4];
+                  mask |= (2 * (int)v[4 * i4 + 0] - c.x > rint[r] ? 1u : 0u) << (4 * i4);
+                  mask |= (2 * (int)v[4 * i4 + 1] - c.y > rint[r] ? 1u : 0u) << (4 * i4 + 1);
+                  mask |= (2 * (int)v[4 * i4 + 2] - c.z > rint[r] ? 1u : 0u) << (4 * i4 + 2);
+                  mask |= (2 * (int)v[4 * i4 + 3] - c.w > rint[r] ? 1u : 0u) << (4 * i4 + 3);
+                }
+                mask &= tri;
+              }
+              if (a < n_cols) args.adj[(j0 >> 5) * (int64_t)args.adj_T + a] = mask;
               return;
             }
             // fast path: one compare per 32 pairs decides "all out"
@@ -866,6 +926,11 @@ cudaError_t launch_tc_probe(const TcPlan& P, const TcArgs& a, int mode, cudaStre
   return probe_cfg<256, 4>(P, a, mode & 15, s);
 }
 
+cudaError_t launch_tc_adj(const TcPlan& Pc, const TcArgs& ac, cudaStream_t s, int64_t* launches) {
+  ++*launches;
+  return dispatch<TC_MODE_ADJ>(Pc, ac, s);
+}
+
 cudaError_t launch_tc(const TcPlan& P, const TcArgs& a, cudaStream_t s, int64_t* launches) {
   ++*launches;
   if (a.gram) return dispatch<TC_MODE_GRAM>(P, a, s);
@@ -875,46 +940,53 @@ cudaError_t launch_tc(const TcPlan& P, const TcArgs& a, cudaStream_t s, int64_t*
 // ------------------------------------------------------------ prep kernels
 // Operand rows: fp32 rounded to tf32 (cvt.rna) or raw int8 bytes, K padded
 // with zeros to row_bytes; norms in fp64 (float) / int32 (int).
+// G lanes per row (power of two up to a warp), lanes stride over the row
 __global__ void k_tc_prep_f32(const float* __restrict__ X, int64_t n, int d, int row_elems,
-                              int cosine, float* __restrict__ xop, double* __restrict__ nrm,
-                              DevStats* stats) {
-  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= n) return;
+                              int cosine, int G, float* __restrict__ xop,
+                              double* __restrict__ nrm, DevStats* stats) {
+  const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t p = gt / G;
+  const int lane = (int)(gt % G);
+  const bool live = p < n;
   const float* x = X + p * (int64_t)d;
   float* o = xop + p * (int64_t)row_elems;
   double ss = 0.0;
   bool fin = true;
-  for (int j = 0; j < d; ++j) {
+  for (int j = lane; live && j < d; j += G) {
     const float v = x[j];
     fin = fin && isfinite(v);
     ss = __dadd_rn(ss, __dmul_rn((double)v, (double)v));
   }
+  for (int k = G / 2; k > 0; k >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, k);
+  if (!live) return;
   // cosine: operand x / |x| (fp64 norm), a zero row stays zero
   const double sc = cosine ? (ss > 0.0 ? 1.0 / sqrt(ss) : 0.0) : 1.0;
-  for (int j = 0; j < row_elems; ++j) {
+  for (int j = lane; j < row_elems; j += G) {
     const float v = j < d ? (cosine ? (float)((double)x[j] * sc) : x[j]) : 0.f;
     uint32_t t;
     asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(t) : "f"(v));
     o[j] = __uint_as_float(t);
   }
   if (!fin) atomicExch(&stats->nonfinite, 1);
-  nrm[p] = ss;
+  if (lane == 0) nrm[p] = ss;
 }
 
 __global__ void k_tc_prep_int(const uint8_t* __restrict__ X, int64_t n, int d, int row_bytes,
                               int is_u8, uint8_t* __restrict__ xop, int32_t* __restrict__ nrm) {
-  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (p >= n) return;
   const uint8_t* x = X + p * (int64_t)d;
   uint8_t* o = xop + p * (int64_t)row_bytes;
   int32_t ss = 0;
-  for (int j = 0; j < row_bytes; ++j) {
-    uint8_t v = j < d ? x[j] : 0;
+  for (int j = lane; j < row_bytes; j += 32) {
+    const uint8_t v = j < d ? x[j] : 0;
     o[j] = v;
-    int iv = is_u8 ? (int)v : (int)(int8_t)v;
+    const int iv = is_u8 ? (int)v : (int)(int8_t)v;
     ss += iv * iv;
   }
-  nrm[p] = ss;
+  for (int k = 16; k > 0; k >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, k);
+  if (lane == 0) nrm[p] = ss;
 }
 
 // per-row constants; rows >= n get +inf / INT_MAX
@@ -1042,6 +1114,78 @@ cudaError_t launch_tc_tile_landmarks(const TcPlan& P, const void* nrm, const int
 }
 
 
+// per-row thresholds of one row (norm nrm of its point), DESIGN.md 7.2
+__device__ __forceinline__ void tc_row_consts(const RowParams& rp, const void* nrm, int64_t pt,
+                                              bool live, int64_t j, float* lo, float* hi,
+                                              int32_t* rr) {
+  if (!rp.tf32) {
+    rr[j] = live ? ((const int32_t*)nrm)[pt] - rp.lo_i : INT_MAX;
+    return;
+  }
+  if (!live) {
+    lo[j] = INFINITY;
+    hi[j] = INFINITY;
+    return;
+  }
+  const double np = ((const double*)nrm)[pt];
+  if (rp.cosine) {
+    if (np == 0.0) {
+      lo[j] = -1e37f;
+      hi[j] = INFINITY;
+    } else {
+      lo[j] = __double2float_rd(1.0 - rp.eps - 1.0000005e-6 * rp.eps - rp.m);
+      hi[j] = __double2float_ru(1.0 - rp.eps + 1.0000005e-6 * rp.eps + rp.m);
+    }
+    return;
+  }
+  const double g = 0.5 * (np - rp.eps2);
+  lo[j] = __double2float_rd(g - rp.C2 * np - rp.tau);
+  hi[j] = __double2float_ru(g + rp.C2 * np + rp.tau);
+}
+
+// A2 on tensor cores: candidate j of the tile = unc[j] (j < nc): operand row,
+// row thresholds and column constants; rows / columns >= nc are inert.
+__global__ void k_tc_tile_cand(const uint8_t* __restrict__ xop, int64_t row_bytes,
+                               const int32_t* __restrict__ unc,
+                               const int32_t* __restrict__ n_unc_dev, int T, RowParams rp,
+                               const void* __restrict__ nrm, double C2,
+                               uint8_t* __restrict__ cop, float* __restrict__ rlo,
+                               float* __restrict__ rhi, int32_t* __restrict__ rr,
+                               float* __restrict__ ca, float* __restrict__ cb,
+                               float* __restrict__ colk, int32_t* __restrict__ cc) {
+  pdl_wait();
+  pdl_trigger();   // one wave
+  const int64_t j = blockIdx.x;
+  const int64_t nc = min((int64_t)T, (int64_t)*n_unc_dev);
+  const bool live = j < nc;
+  const int32_t pt = live ? unc[j] : 0;
+  const uint4* src = reinterpret_cast<const uint4*>(xop + (int64_t)pt * row_bytes);
+  uint4* dst = reinterpret_cast<uint4*>(cop + j * row_bytes);
+  for (int64_t i = threadIdx.x; i < row_bytes / 16; i += blockDim.x)
+    dst[i] = live ? src[i] : make_uint4(0, 0, 0, 0);
+  if (threadIdx.x == 0) {
+    tc_row_consts(rp, nrm, pt, live, j, rlo, rhi, rr);
+    if (rp.tf32) {
+      if (!live) tc_col_inert(j, ca, cb, colk);
+      else if (rp.cosine) tc_col_consts_cos(((const double*)nrm)[pt], j, ca, cb, colk);
+      else tc_col_consts(((const double*)nrm)[pt], C2, j, ca, cb, colk);
+    } else {
+      cc[j] = live ? ((const int32_t*)nrm)[pt] : (1 << 30);
+    }
+  }
+}
+
+cudaError_t launch_tc_tile_cand(const TcPlan& P, const TcPlan& Pc, const void* nrm,
+                                const int32_t* unc, const int32_t* n_unc_dev, int T, double C2,
+                                const RowParams& rp, TcArgs& ac, cudaStream_t s,
+                                int64_t* launches) {
+  ++*launches;
+  return launch_pdl(k_tc_tile_cand, dim3((unsigned)Pc.l_rows), dim3(64), 0, s,
+                    (const uint8_t*)P.xop, P.row_bytes, unc, n_unc_dev, T, rp, nrm, C2,
+                    (uint8_t*)Pc.lop, (float*)ac.row_lo, (float*)ac.row_hi, (int32_t*)ac.row_r,
+                    (float*)ac.col_a, (float*)ac.col_b, (float*)ac.colk, (int32_t*)ac.col_c);
+}
+
 __global__ void k_tc_ones(float* o) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < 128 * 8) o[i] = (i & 7) < 3 ? 1.f : 0.f;
@@ -1055,10 +1199,13 @@ cudaError_t launch_tc_ones(float* ones, cudaStream_t s, int64_t* launches) {
 cudaError_t launch_tc_prep(const void* X, int dtype, int64_t n, int d, const TcPlan& P,
                            void* nrm, DevStats* stats, cudaStream_t s, int64_t* launches) {
   ++*launches;
-  const unsigned g = (unsigned)((n + 255) / 256);
+  const unsigned g = (unsigned)((n * 32 + 255) / 256);   // one warp per row
+  int G = 1;
+  while (G < 32 && G < (int)(P.row_bytes / 4)) G *= 2;
   if (dtype == BM_F32)
-    k_tc_prep_f32<<<g, 256, 0, s>>>((const float*)X, n, d, (int)(P.row_bytes / 4), P.cosine,
-                                    (float*)P.xop, (double*)nrm, stats);
+    k_tc_prep_f32<<<(unsigned)((n * G + 255) / 256), 256, 0, s>>>(
+        (const float*)X, n, d, (int)(P.row_bytes / 4), P.cosine, G, (float*)P.xop,
+        (double*)nrm, stats);
   else
     k_tc_prep_int<<<g, 256, 0, s>>>((const uint8_t*)X, n, d, (int)P.row_bytes, dtype == BM_U8,
                                     (uint8_t*)P.xop, (int32_t*)nrm);

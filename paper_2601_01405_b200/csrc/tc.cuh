@@ -13,7 +13,16 @@ enum TcMode : int {
   TC_MODE_MEMBER = 0,
   TC_MODE_GRAM = 1,
   TC_MODE_PROBE_LDONLY = 2,   // diagnostics: epilogue reads TMEM, no classification
-  TC_MODE_PROBE_NOLD = 3      // diagnostics: epilogue releases buffers without reading
+  TC_MODE_PROBE_NOLD = 3,     // diagnostics: epilogue releases buffers without reading
+  TC_MODE_ADJ = 4             // A2: candidate x candidate adjacency bits of a greedy tile
+};
+
+// Per-row thresholds of the contraction, shared by the point
+// rows and the greedy tile's candidate rows.
+struct RowParams {
+  int tf32, cosine;
+  double C2, eps, eps2, tau, m;
+  int32_t lo_i;
 };
 
 // Operand geometry (host side).
@@ -64,6 +73,8 @@ struct TcArgs {
   int64_t tie_cap;
   DevStats* stats;         // band_pairs / near_ties counters
   uint32_t* gram;      // debug: raw accumulators [n][L]
+  uint32_t* adj;       // TC_MODE_ADJ: word-major adjacency, word v of candidate a at adj[v*adj_T + a]
+  int adj_T;
   uint8_t* covered;    // fused greedy: covered[p] = 1 for every in-ball pair (may be null)
 };
 
@@ -89,6 +100,14 @@ cudaError_t launch_tc_tile_landmarks(const TcPlan& P, const void* nrm, const int
                                      const int32_t* l_count_dev, double C2, TcArgs& a,
                                      cudaStream_t s, int64_t* launches);
 cudaError_t launch_tc(const TcPlan& P, const TcArgs& a, cudaStream_t s, int64_t* launches);
+// A2 on tensor cores: gather the tile's candidates (first min(T, *n_unc) of unc)
+// into Pc.xop (= Pc.lop) with their row and column constants, then one
+// contraction candidates x candidates with the adjacency epilogue.
+cudaError_t launch_tc_tile_cand(const TcPlan& P, const TcPlan& Pc, const void* nrm,
+                                const int32_t* unc, const int32_t* n_unc_dev, int T, double C2,
+                                const RowParams& rp, TcArgs& ac, cudaStream_t s,
+                                int64_t* launches);
+cudaError_t launch_tc_adj(const TcPlan& Pc, const TcArgs& ac, cudaStream_t s, int64_t* launches);
 // diagnostics: the contraction with a probe epilogue (TC_MODE_PROBE_*), tf32 K <= 64 only
 cudaError_t launch_tc_probe(const TcPlan& P, const TcArgs& a, int mode, cudaStream_t s);
 
