@@ -150,8 +150,13 @@ __device__ __forceinline__ void pairs_block(const PairArgs& A, uint2* sl, int32_
   const int tid = threadIdx.x, lane = tid & 31;
   // prefilter: quantised landmark rows follow the fp32 rows in shared memory
   uint32_t* sq = reinterpret_cast<uint32_t*>(sl + LC * nu);
-  uint32_t thrq = 0u;
-  if constexpr (QF) thrq = l1q_threshold(A.qparam, A.th.eps, A.d);
+  // bias 2^15 - thr (thr > 2^15: the filter cannot prove anything, bias 0
+  // makes every pair a candidate: SADs stay below 2^14 for d <= 64)
+  uint32_t qbase = 0u;
+  if constexpr (QF) {
+    const uint32_t thrq = l1q_threshold(A.qparam, A.th.eps, A.d);
+    qbase = thrq <= 0x8000u ? 0x8000u - thrq : 0u;
+  }
   uint32_t qq[R][QF ? NQ : 1];
 
   // ---- query rows into registers
@@ -201,20 +206,42 @@ __device__ __forceinline__ void pairs_block(const PairArgs& A, uint2* sl, int32_
     }
     __syncthreads();
 
-    for (int jj = 0; jj < nl; ++jj) {
+    // the prefilter screens UG landmarks at a time (one vote per group)
+    constexpr int UG = QF ? 4 : 1;
+    for (int jg = 0; jg < nl; jg += UG) {
+    uint32_t gsad[UG][R];
+    if constexpr (QF) {
+      // quantised SAD (4 coordinates per instruction), accumulated on top of
+      // 2^15 - thr: bit 15 of the sum is clear iff SAD < thr, so one AND over
+      // the group tells whether any pair needs the exact check (cls 3)
+      uint32_t all_out = 0xffffffffu;
+#pragma unroll
+      for (int u = 0; u < UG; ++u) {
+        const int jq = min(jg + u, nl - 1);   // tail: repeat the last landmark
+        uint32_t lq[NQ];
+#pragma unroll
+        for (int w = 0; w < NQ; ++w) lq[w] = sq[jq * NQ + w];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          uint32_t acc = qbase;
+#pragma unroll
+          for (int w = 0; w < NQ; ++w) acc = vsad4(qq[r][w], lq[w], acc);
+          gsad[u][r] = acc;
+          all_out &= acc;
+        }
+      }
+      if (__all_sync(FULL, (all_out & 0x8000u) != 0u)) continue;
+    }
+#pragma unroll
+    for (int ug = 0; ug < UG; ++ug) {
+      const int jj = jg + ug;
+      if (jj >= nl) break;
       int cls[R];
       bool special = false;
       if constexpr (QF) {
-        // quantised SAD (4 coordinates per instruction); cls 3 = "exact check needed"
-        uint32_t lq[NQ];
-#pragma unroll
-        for (int w = 0; w < NQ; ++w) lq[w] = sq[jj * NQ + w];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          uint32_t sad = 0u;
-#pragma unroll
-          for (int w = 0; w < NQ; ++w) sad = vsad4(qq[r][w], lq[w], sad);
-          cls[r] = (act[r] && sad < thrq) ? 3 : 0;
+          cls[r] = (act[r] && (gsad[ug][r] & 0x8000u) == 0u) ? 3 : 0;
           special = special || (cls[r] != 0);
         }
         if (!__any_sync(FULL, special)) continue;
@@ -305,6 +332,7 @@ __device__ __forceinline__ void pairs_block(const PairArgs& A, uint2* sl, int32_
           }
         }
       }
+    }
     }
   }
 
