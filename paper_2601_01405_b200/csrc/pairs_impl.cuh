@@ -207,7 +207,7 @@ __device__ __forceinline__ void pairs_block(const PairArgs& A, uint2* sl, int32_
     __syncthreads();
 
     // the prefilter screens UG landmarks at a time (one vote per group)
-    constexpr int UG = QF ? 4 : 1;
+    constexpr int UG = QF ? 8 : 1;
     for (int jg = 0; jg < nl; jg += UG) {
     uint32_t gsad[UG][R];
     if constexpr (QF) {
