@@ -21,29 +21,6 @@ __device__ __forceinline__ unsigned long long lb_pack(uint32_t tag, unsigned lon
   return ((unsigned long long)tag << 34) | (flag << 32) | (unsigned long long)v;
 }
 
-// Decoupled look-back (thread 0 of the CTA): publish this tile's aggregate,
-// return the sum of all earlier tiles' aggregates, publish the inclusive prefix.
-__device__ __forceinline__ uint32_t lookback_excl(unsigned long long* state, int64_t tile,
-                                                  uint32_t tag, uint32_t agg) {
-  volatile unsigned long long* st = state;
-  if (tile == 0) {
-    st[0] = lb_pack(tag, LB_INC, agg);
-    return 0u;
-  }
-  st[tile] = lb_pack(tag, LB_AGG, agg);
-  uint32_t excl = 0u;
-  for (int64_t j = tile - 1; j >= 0; --j) {
-    unsigned long long v;
-    do {
-      v = st[j];
-    } while ((uint32_t)(v >> 34) != tag || ((v >> 32) & 3ull) == 0ull);
-    excl += (uint32_t)v;
-    if (((v >> 32) & 3ull) == LB_INC) break;
-  }
-  st[tile] = lb_pack(tag, LB_INC, excl + agg);
-  return excl;
-}
-
 // ---------------------------------------------------------------- bitmap path
 // One thread per point: set bit (i, j) for every pair a < c of its row
 // (rows are short: t_p ~ 2-40 on the BASELINE configs); the warp adds its C(t,2).
@@ -104,12 +81,14 @@ __global__ void __launch_bounds__(EB_NT) k_bits_compact(const uint32_t* __restri
   }
   if (lane == 31) s_warp[w] = incl;
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {
     uint32_t agg = 0;
     for (int k = 0; k < EB_NT / 32; ++k) agg += s_warp[k];
-    const uint32_t ex = lookback_excl(state, tile, tag, agg);
-    s_excl = ex;
-    if ((tile + 1) * EB_TILE >= nwords) *total = (int64_t)ex + agg;
+    const uint32_t ex = warp_lookback(state, tile, tag, agg);
+    if (threadIdx.x == 0) {
+      s_excl = ex;
+      if ((tile + 1) * EB_TILE >= nwords) *total = (int64_t)ex + agg;
+    }
   }
   __syncthreads();
   int64_t pos = s_excl + incl - cnt;
@@ -169,12 +148,14 @@ __global__ void __launch_bounds__(UQ_NT) k_unique_compact(const unsigned long lo
   }
   if (lane == 31) s_warp[w] = incl;
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {
     uint32_t agg = 0;
     for (int k = 0; k < UQ_NT / 32; ++k) agg += s_warp[k];
-    const uint32_t ex = lookback_excl(state, tile, tag, agg);
-    s_excl = ex;
-    if ((tile + 1) * UQ_TILE >= m) *total = (int64_t)ex + agg;
+    const uint32_t ex = warp_lookback(state, tile, tag, agg);
+    if (threadIdx.x == 0) {
+      s_excl = ex;
+      if ((tile + 1) * UQ_TILE >= m) *total = (int64_t)ex + agg;
+    }
   }
   __syncthreads();
   int64_t pos = s_excl + incl - cnt;
@@ -237,12 +218,14 @@ __global__ void __launch_bounds__(EB_NT) k_bits_csr(const uint32_t* __restrict__
   }
   if (lane == 31) s_warp[w] = incl;
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {
     uint32_t agg = 0;
     for (int k = 0; k < EB_NT / 32; ++k) agg += s_warp[k];
-    const uint32_t ex = lookback_excl(state, tile, tag, agg);
-    s_excl = ex;
-    if ((tile + 1) * EB_TILE >= nwords) ptr[rows] = (int64_t)ex + agg;
+    const uint32_t ex = warp_lookback(state, tile, tag, agg);
+    if (threadIdx.x == 0) {
+      s_excl = ex;
+      if ((tile + 1) * EB_TILE >= nwords) ptr[rows] = (int64_t)ex + agg;
+    }
   }
   __syncthreads();
   int64_t pos = s_excl + incl - cnt;

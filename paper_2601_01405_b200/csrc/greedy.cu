@@ -162,12 +162,6 @@ cudaError_t launch_resolve_debug(const uint32_t* adj, int adj_words, int nc, uin
 // predecessors' published (aggregate | inclusive prefix) words.  Words carry the
 // launch tag, so the state array never needs clearing between tiles.
 constexpr int CP_NT = 256, CP_ROUNDS = 16, CP_TILE = CP_NT * CP_ROUNDS;
-constexpr unsigned long long CP_AGG = 1ull, CP_INC = 2ull;
-
-__device__ __forceinline__ unsigned long long cp_pack(uint32_t tag, unsigned long long flag,
-                                                      uint32_t v) {
-  return ((unsigned long long)tag << 34) | (flag << 32) | (unsigned long long)v;
-}
 
 __global__ void __launch_bounds__(CP_NT) k_compact(const uint8_t* __restrict__ covered,
                                                    const int32_t* __restrict__ unc,
@@ -206,30 +200,13 @@ __global__ void __launch_bounds__(CP_NT) k_compact(const uint8_t* __restrict__ c
   }
   __syncthreads();
   if (tid < 32) {
-    // CTA aggregate, then the look-back (warp 0, lane 0 walks the predecessors)
+    // CTA aggregate, then the warp-wide look-back
     int agg = 0;
     for (int k = lane; k < CP_ROUNDS * (CP_NT / 32); k += 32) agg += (&s_wcnt[0][0])[k];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) agg += __shfl_xor_sync(FULLMASK, agg, o);
+    const int excl = (int)warp_lookback(state, bid, tag, (uint32_t)agg);
     if (lane == 0) {
-      volatile unsigned long long* st = state;
-      int excl = 0;
-      if (bid == 0) {
-        st[0] = cp_pack(tag, CP_INC, (uint32_t)agg);
-      } else {
-        st[bid] = cp_pack(tag, CP_AGG, (uint32_t)agg);
-        __threadfence();
-        for (int j = bid - 1; j >= 0; --j) {
-          unsigned long long v;
-          do {
-            v = st[j];
-          } while ((uint32_t)(v >> 34) != tag || ((v >> 32) & 3ull) == 0ull);
-          excl += (int)(uint32_t)v;
-          if (((v >> 32) & 3ull) == CP_INC) break;
-        }
-        __threadfence();
-        st[bid] = cp_pack(tag, CP_INC, (uint32_t)(excl + agg));
-      }
       s_excl = excl;
       if (i0 + CP_TILE >= m) *n_unc_next = excl + agg;   // the last CTA holds the total
     }

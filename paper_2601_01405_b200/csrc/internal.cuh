@@ -29,6 +29,43 @@ __device__ __forceinline__ void pdl_trigger() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
+// Decoupled look-back over per-tile descriptors (tag << 34 | flag << 32 |
+// 32-bit value; flag 1 = aggregate, 2 = inclusive prefix), run by one full
+// warp: lanes read 32 predecessors at once, the nearest inclusive prefix ends
+// the walk.  Publishes this tile's aggregate first and its inclusive prefix
+// last; returns the exclusive prefix.  Descriptors are never reset: a word
+// with another launch's tag counts as not ready.
+__device__ __forceinline__ uint32_t warp_lookback(unsigned long long* state, int64_t tile,
+                                                  uint32_t tag, uint32_t agg) {
+  volatile unsigned long long* st = state;
+  const int lane = threadIdx.x & 31;
+  const unsigned long long hdr = (unsigned long long)tag << 34;
+  if (tile == 0) {
+    if (lane == 0) st[0] = hdr | (2ull << 32) | agg;
+    return 0u;
+  }
+  if (lane == 0) st[tile] = hdr | (1ull << 32) | agg;
+  uint32_t excl = 0u;
+  for (int64_t base = tile - 1;; base -= 32) {
+    const int64_t j = base - lane;
+    unsigned long long v = 2ull << 32;   // below tile 0: an inclusive prefix of 0
+    if (j >= 0) {
+      do {
+        v = st[j];
+      } while ((uint32_t)(v >> 34) != tag || ((v >> 32) & 3ull) == 0ull);
+    }
+    const unsigned inc = __ballot_sync(0xffffffffu, ((v >> 32) & 3ull) == 2ull);
+    const int first = inc ? __ffs(inc) - 1 : 32;   // nearest predecessor with a prefix
+    uint32_t val = lane <= first ? (uint32_t)v : 0u;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
+    excl += val;
+    if (inc) break;
+  }
+  if (lane == 0) st[tile] = hdr | (2ull << 32) | (uint32_t)(excl + agg);
+  return excl;
+}
+
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
                        cudaStream_t s, Args... args) {

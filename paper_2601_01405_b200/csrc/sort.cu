@@ -203,6 +203,17 @@ __device__ __forceinline__ unsigned long long rs_pack(uint32_t tag, uint32_t fla
   return ((unsigned long long)tag << 34) | ((unsigned long long)flag << 32) | v;
 }
 
+// One pass of the LSD sort over a tile of RS_NT * RS_ROUNDS keys.  Warp w owns
+// the contiguous keys [w * 32 * RS_ROUNDS, (w + 1) * 32 * RS_ROUNDS) of the
+// tile (round r: 32 consecutive keys), so input order = (warp, round, lane):
+//   1. per-warp digit counts with __match_any_sync (no block barriers): each
+//      key's rank among equal digits of its warp = the warp's running count +
+//      its rank among its round's peers;
+//   2. tile histogram -> tile-local digit offsets; per-digit look-back over the
+//      earlier tiles -> the digit's global base;
+//   3. keys are placed in shared memory in (digit, input order) order, then
+//      written out by consecutive threads: each digit's run is a contiguous,
+//      coalesced range of the output.  Equal digits keep their input order.
 template <int RS_ROUNDS>
 __global__ void __launch_bounds__(RS_NT) k_rs_scatter(const unsigned long long* __restrict__ in,
                                                      unsigned long long* __restrict__ out,
@@ -210,40 +221,62 @@ __global__ void __launch_bounds__(RS_NT) k_rs_scatter(const unsigned long long* 
                                                      const int64_t* __restrict__ off,
                                                      unsigned long long* state, int32_t* ticket,
                                                      uint32_t tag) {
+  constexpr int NW = RS_NT / 32, RS_TILE = RS_NT * RS_ROUNDS;
   __shared__ int s_tile;
-  __shared__ unsigned s_hist[RS_BINS];
-  __shared__ int64_t run[RS_BINS];
-  __shared__ int wcnt[RS_NT / 32][RS_BINS];
+  __shared__ int whist[NW][RS_BINS];    // per-warp counts, then per-warp bases
+  __shared__ int tile_off[RS_BINS];
+  __shared__ int64_t gbase[RS_BINS];     // global position of the tile's first key of digit d
+  __shared__ unsigned long long skey[RS_TILE];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   pdl_wait();   // (multi-wave, ticketed: the next kernel launches as CTAs exit)
   if (tid == 0) s_tile = atomicAdd(ticket, 1);
-  s_hist[tid] = 0u;
+#pragma unroll
+  for (int ww = 0; ww < NW; ++ww) whist[ww][tid] = 0;
   __syncthreads();
-  constexpr int RS_TILE = RS_NT * RS_ROUNDS;
   const int64_t tile = s_tile;
   const int64_t t0 = tile * RS_TILE;
+  const int64_t wbeg = t0 + (int64_t)w * 32 * RS_ROUNDS;
   const unsigned mask = (1u << bits) - 1u;
-  // keys of this tile, round r holds items t0 + r*NT + tid
   unsigned long long key[RS_ROUNDS];
   int dig[RS_ROUNDS];
+  int wrank[RS_ROUNDS];   // rank among equal digits within the warp
 #pragma unroll
   for (int r = 0; r < RS_ROUNDS; ++r) {
-    const int64_t i = t0 + r * RS_NT + tid;
-    key[r] = i < n ? in[i] : 0ull;
-    dig[r] = i < n ? (int)((unsigned)(key[r] >> shift) & mask) : RS_BINS + lane;  // invalid: unique
+    const int64_t i = wbeg + r * 32 + lane;
+    const bool valid = i < n;
+    key[r] = valid ? in[i] : 0ull;
+    dig[r] = valid ? (int)((unsigned)(key[r] >> shift) & mask) : -1;
     const unsigned peers = __match_any_sync(FM, dig[r]);
-    if (i < n && __popc(peers & ((1u << lane) - 1u)) == 0) atomicAdd(&s_hist[dig[r]], __popc(peers));
+    const int leader = __ffs(peers) - 1;
+    int before = 0;
+    if (lane == leader && valid) {
+      before = whist[w][dig[r]];
+      whist[w][dig[r]] = before + __popc(peers);
+    }
+    before = __shfl_sync(FM, before, leader);
+    wrank[r] = before + __popc(peers & ((1u << lane) - 1u));
+    __syncwarp();
   }
   __syncthreads();
-  // publish this tile's count of digit tid, look back for earlier tiles' counts
+  // tile histogram of digit tid, tile-local offsets, per-warp bases
+  int c = 0;
+#pragma unroll
+  for (int ww = 0; ww < NW; ++ww) {
+    const int t = whist[ww][tid];
+    whist[ww][tid] = c;   // exclusive prefix over the warps
+    c += t;
+  }
+  int64_t tot;
+  const int64_t toff = block_excl_scan<RS_NT>((int64_t)c, &tot);
+  tile_off[tid] = (int)toff;
+  // publish this tile's count of digit tid, look back over the earlier tiles
   {
     volatile unsigned long long* st = state;
-    const unsigned c = s_hist[tid];
     int64_t excl = 0;
     if (tile == 0) {
-      st[tid] = rs_pack(tag, ST_INC, c);
+      st[tid] = rs_pack(tag, ST_INC, (uint32_t)c);
     } else {
-      st[tile * RS_BINS + tid] = rs_pack(tag, ST_AGG, c);
+      st[tile * RS_BINS + tid] = rs_pack(tag, ST_AGG, (uint32_t)c);
       for (int64_t j = tile - 1; j >= 0; --j) {
         unsigned long long v;
         do {
@@ -254,31 +287,23 @@ __global__ void __launch_bounds__(RS_NT) k_rs_scatter(const unsigned long long* 
       }
       st[tile * RS_BINS + tid] = rs_pack(tag, ST_INC, (uint32_t)(excl + c));
     }
-    run[tid] = off[tid] + excl;
+    gbase[tid] = off[tid] + excl - toff;
   }
   __syncthreads();
+  // keys into shared memory in (digit, input) order
+#pragma unroll
+  for (int r = 0; r < RS_ROUNDS; ++r)
+    if (dig[r] >= 0) skey[tile_off[dig[r]] + whist[w][dig[r]] + wrank[r]] = key[r];
+  __syncthreads();
+  // coalesced write-out: consecutive local positions of one digit are consecutive outputs
+  const int nloc = (int)min((int64_t)RS_TILE, n - t0);
+#pragma unroll
   for (int r = 0; r < RS_ROUNDS; ++r) {
-    if (t0 + r * RS_NT >= n) break;  // uniform across the CTA
-    const int64_t i = t0 + r * RS_NT + tid;
-    const bool valid = i < n;
-    const unsigned peers = __match_any_sync(FM, dig[r]);
-    const int intra = __popc(peers & ((1u << lane) - 1u));
-#pragma unroll
-    for (int ww = 0; ww < RS_NT / 32; ++ww) wcnt[ww][tid] = 0;
-    __syncthreads();
-    if (valid && intra == 0) wcnt[w][dig[r]] = __popc(peers);
-    __syncthreads();
-    if (valid) {
-      int64_t rank = run[dig[r]] + intra;
-      for (int ww = 0; ww < w; ++ww) rank += wcnt[ww][dig[r]];
-      out[rank] = key[r];
+    const int li = r * RS_NT + tid;
+    if (li < nloc) {
+      const unsigned long long k = skey[li];
+      out[gbase[(unsigned)(k >> shift) & mask] + li] = k;
     }
-    __syncthreads();
-    int add = 0;
-#pragma unroll
-    for (int ww = 0; ww < RS_NT / 32; ++ww) add += wcnt[ww][tid];
-    run[tid] += add;
-    __syncthreads();
   }
 }
 

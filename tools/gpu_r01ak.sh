@@ -1,0 +1,4 @@
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/pytest_gpu.log
+CMD="python bench.py --workload c5_l1 --n 4000000 --steps 1 --warmup 3 --no-cpu-baseline"
+timeout 300 $CMD > gpurun_out/plain_c5p.log 2>&1 && \
+timeout 1200 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed --clock-control none --csv --log-file gpurun_out/hbm_c5p.csv $CMD > gpurun_out/ncu_c5hbm.log 2>&1; echo "ncu rc=$?"
