@@ -58,8 +58,21 @@ typedef enum bm_metric { BM_L2 = 0, BM_L1 = 1, BM_COSINE = 2 } bm_metric;
 typedef enum bm_dtype {
   BM_F32 = 0,  /* IEEE binary32 coordinates                                 */
   BM_I8 = 1,   /* int8 coordinates   (exact integer path: L2, L1)          */
-  BM_U8 = 2    /* uint8 coordinates  (exact integer path: L2, L1)          */
+  BM_U8 = 2,   /* uint8 coordinates  (exact integer path: L2, L1)          */
+  BM_I32 = 3   /* int32 values: labels for bm_color (not a coordinate type) */
 } bm_dtype;
+
+/* Coloring aggregators (PAPER.md:125-133, 167, 187 [§2.3]). */
+typedef enum bm_agg {
+  BM_AGG_MEAN = 0,      /* (1/|X_i|) sum f                                        */
+  BM_AGG_MEDIAN = 1,    /* even |X_i|: mean of the two central order statistics  */
+  BM_AGG_TRIMMED = 2,   /* mean after dropping floor(alpha |X_i|) at each end     */
+  BM_AGG_MIN = 3,
+  BM_AGG_MAX = 4,
+  BM_AGG_MODE = 5,      /* most frequent value, ties -> smallest value            */
+  BM_AGG_VARIANCE = 6,  /* population variance                                    */
+  BM_AGG_RANGE = 7      /* max - min                                              */
+} bm_agg;
 
 /* Per-step device timings, indices into bm_cover.step_ms. */
 enum {
@@ -174,6 +187,35 @@ bm_status bm_cover_build_ex(const void *points, bm_dtype dtype, int64_t n, int32
 bm_status bm_cover_build_host(const void *host_points, bm_dtype dtype, int64_t n, int32_t d,
                               bm_metric metric, double eps, void *stream,
                               const bm_options *opts, bm_cover **out);
+
+/*
+ * bm_color — colour every landmark of a cover (PAPER.md:125-133 [§2.3]):
+ * out[j] = agg of values over the ball X_j = X ∩ B(l_j, eps) (landmark-major
+ * CSR of `c`).
+ *   c       a DEVICE cover (from bm_cover_build / _ex) on the current device.
+ *   values  DEVICE pointer to n values f(x_p): BM_F32 (finite) or BM_I32 (labels).
+ *   agg     bm_agg; alpha in [0, 0.5) for BM_AGG_TRIMMED (ignored otherwise).
+ *   out     DEVICE pointer to L doubles (labels are returned as exact doubles).
+ * Ordered on `stream`; returns after the work is queued and checked.
+ * Errors: BM_EINVAL (NULL pointer, host cover, bad alpha), BM_EUNSUPPORTED
+ * (value type / aggregator), BM_ENOMEM, BM_ECUDA.
+ */
+bm_status bm_color(const bm_cover *c, const void *values, bm_dtype vtype, bm_agg agg,
+                   double alpha, double *out, void *stream);
+
+/*
+ * bm_skeleton — the k-simplices of the nerve (Def 2.2): the
+ * sets of k+1 landmark positions whose balls share a data point, each
+ * ascending, in lexicographic order.  k >= 1 (k = 1 gives the edge list).
+ *   out       DEVICE pointer to capacity*(k+1) int32 (may be NULL with capacity 0);
+ *             receives the first min(count, capacity) simplices.
+ *   count     HOST, receives the number of k-simplices.
+ *   max_emit  cap on the witnessed (k+1)-subsets enumerated (sum_p C(t_p, k+1));
+ *             0 = default 2^31.  Exceeding it returns BM_EOVERFLOW.
+ * Requires (k+1) * bits(L-1) <= 64 (BM_EUNSUPPORTED otherwise).  Synchronous.
+ */
+bm_status bm_skeleton(const bm_cover *c, int32_t k, int32_t *out, int64_t capacity,
+                      int64_t *count, int64_t max_emit, void *stream);
 
 /* Release a cover and every array it owns.  NULL-safe. */
 void bm_free(bm_cover *c);

@@ -20,7 +20,9 @@ BM_OK, BM_EINVAL, BM_EUNSUPPORTED, BM_ENOMEM, BM_ECUDA, BM_EOVERFLOW = range(6)
 STATUS_NAMES = {0: "BM_OK", 1: "BM_EINVAL", 2: "BM_EUNSUPPORTED", 3: "BM_ENOMEM",
                 4: "BM_ECUDA", 5: "BM_EOVERFLOW"}
 METRIC = {"l2": 0, "l1": 1, "cos": 2, "cosine": 2}
-DTYPE = {"f32": 0, "i8": 1, "u8": 2}
+DTYPE = {"f32": 0, "i8": 1, "u8": 2, "i32": 3}
+AGG = {"mean": 0, "median": 1, "trimmed": 2, "min": 3, "max": 4, "mode": 5, "variance": 6,
+       "range": 7}
 PATH = {"auto": 0, "cuda_core": 1, "tensor": 2}
 FLAG_NO_L1_PREFILTER = 1
 STEPS = ("prep", "greedy", "member", "csr", "edges", "total", "member_kernel")
@@ -28,7 +30,7 @@ STEPS = ("prep", "greedy", "member", "csr", "edges", "total", "member_kernel")
 EXPORTED = ("bm_cover_build", "bm_cover_build_ex", "bm_cover_build_host", "bm_free",
             "bm_last_error", "bm_version", "bm_trim_memory", "bm_debug_radix_sort_u64",
             "bm_debug_exclusive_scan_i64", "bm_debug_resolve_tile", "bm_debug_tc_gram",
-            "bm_debug_tc_probe")
+            "bm_debug_tc_probe", "bm_color", "bm_skeleton")
 
 
 class BMError(RuntimeError):
@@ -90,6 +92,11 @@ def load() -> ctypes.CDLL:
     lib.bm_last_error.restype = ctypes.c_char_p
     lib.bm_version.restype = i32
     lib.bm_trim_memory.restype = i32
+    lib.bm_color.argtypes = [ctypes.POINTER(_Cover), vp, i32, i32, dbl, vp, vp]
+    lib.bm_color.restype = i32
+    lib.bm_skeleton.argtypes = [ctypes.POINTER(_Cover), i32, vp, i64, ctypes.POINTER(i64), i64,
+                                vp]
+    lib.bm_skeleton.restype = i32
     lib.bm_debug_radix_sort_u64.argtypes = [vp, i64, i32, vp]
     lib.bm_debug_radix_sort_u64.restype = i32
     lib.bm_debug_exclusive_scan_i64.argtypes = [vp, vp, i64, ctypes.POINTER(i64), vp]
@@ -351,3 +358,34 @@ def tc_probe(points, L: int, mode: int, iters: int = 10) -> float:
                                     int(iters), ctypes.byref(ms),
                                     ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
     return float(ms.value)
+
+
+def color(cov: "Cover", values, agg: str = "mean", alpha: float = 0.1):
+    """bm_color: colour every landmark of a device cover.
+    values: CUDA tensor [n] float32 (function values) or int32 (labels).
+    Returns a CUDA float64 tensor [L]."""
+    import torch
+    if cov.on_host:
+        raise ValueError("bm_color needs a device cover")
+    if not (isinstance(values, torch.Tensor) and values.is_cuda) or values.numel() != cov.n:
+        raise ValueError("values must be a CUDA tensor with one entry per point")
+    vt = {torch.float32: DTYPE["f32"], torch.int32: DTYPE["i32"]}[values.dtype]
+    values = values.contiguous()
+    out = torch.empty(cov.L, dtype=torch.float64, device=values.device)
+    _check(load().bm_color(cov._ptr, ctypes.c_void_p(values.data_ptr()), vt, AGG[agg],
+                           float(alpha), ctypes.c_void_p(out.data_ptr()),
+                           ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    return out
+
+
+def skeleton(cov: "Cover", k: int = 2, max_emit: int = 0):
+    """bm_skeleton: the k-simplices of the nerve as a CUDA int32 tensor [count, k+1]."""
+    import torch
+    cnt = ctypes.c_int64(0)
+    lib = load()
+    sp = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    _check(lib.bm_skeleton(cov._ptr, int(k), None, 0, ctypes.byref(cnt), int(max_emit), sp))
+    out = torch.empty((max(cnt.value, 1), k + 1), dtype=torch.int32, device="cuda")
+    _check(lib.bm_skeleton(cov._ptr, int(k), ctypes.c_void_p(out.data_ptr()), cnt.value,
+                           ctypes.byref(cnt), int(max_emit), sp))
+    return out[: cnt.value]

@@ -1078,6 +1078,92 @@ void bm_free(bm_cover* c) {
 
 const char* bm_last_error(void) { return g_err.c_str(); }
 
+bm_status bm_color(const bm_cover* c, const void* values, bm_dtype vtype, bm_agg agg,
+                   double alpha, double* out, void* stream) {
+  using namespace bm;
+  if (!c || !values || !out) return set_err(BM_EINVAL, "NULL argument");
+  if (c->on_host) return set_err(BM_EINVAL, "bm_color needs a device cover");
+  if (vtype != BM_F32 && vtype != BM_I32)
+    return set_err(BM_EUNSUPPORTED, "values must be BM_F32 or BM_I32");
+  if ((int)agg < 0 || (int)agg > BM_AGG_RANGE) return set_err(BM_EUNSUPPORTED, "unknown aggregator");
+  if (agg == BM_AGG_TRIMMED && !(alpha >= 0.0 && alpha < 0.5))
+    return set_err(BM_EINVAL, "trimmed mean needs 0 <= alpha < 0.5");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t L = c->n_landmarks, M = c->n_members;
+  const int is_int = vtype == BM_I32;
+  if (L == 0) return BM_OK;
+  if (agg == BM_AGG_MEDIAN || agg == BM_AGG_TRIMMED || agg == BM_AGG_MODE) {
+    Pool pool(s);
+    unsigned long long *keys = nullptr, *alt = nullptr;
+    void* rt = nullptr;
+    TRY(pool.alloc(&keys, (size_t)(M > 0 ? M : 1)));
+    TRY(pool.alloc(&alt, (size_t)(M > 0 ? M : 1)));
+    TRY(pool.alloc((uint8_t**)&rt, radix_temp_bytes(M)));
+    CK(launch_color_keys(c->ball_ptr, c->ball_idx, L, values, is_int, keys, s));
+    const BitRange r[2] = {{0, 32}, {32, 32 + bits_for(L > 1 ? L - 1 : 1)}};
+    int64_t launches = 0;
+    CK(radix_sort_u64(&keys, &alt, M, r, 2, rt, s, &launches));
+    CK(launch_color_order(c->ball_ptr, L, keys, is_int, (int)agg, alpha, out, s));
+  } else {
+    CK(launch_color_reduce(c->ball_ptr, c->ball_idx, L, values, is_int, (int)agg, out, s));
+  }
+  CK(cudaGetLastError());
+  return BM_OK;
+}
+
+bm_status bm_skeleton(const bm_cover* c, int32_t k, int32_t* out, int64_t capacity,
+                      int64_t* count, int64_t max_emit, void* stream) {
+  using namespace bm;
+  if (!c || !count || (capacity > 0 && !out)) return set_err(BM_EINVAL, "NULL argument");
+  if (c->on_host) return set_err(BM_EINVAL, "bm_skeleton needs a device cover");
+  if (k < 1 || k > 7) return set_err(BM_EUNSUPPORTED, "k must be in [1, 7]");
+  const int64_t L = c->n_landmarks, n = c->n;
+  const int r = k + 1;
+  const int lbits = bits_for(L > 1 ? L - 1 : 1);
+  if ((int64_t)r * lbits > 64) return set_err(BM_EUNSUPPORTED, "(k+1) * bits(L-1) exceeds 64");
+  if (max_emit <= 0) max_emit = (int64_t)1 << 31;
+  cudaStream_t s = (cudaStream_t)stream;
+  *count = 0;
+  Pool pool(s);
+  int64_t *cnt = nullptr, *off = nullptr, *tot = nullptr;
+  void* st = nullptr;
+  TRY(pool.alloc(&cnt, (size_t)n));
+  TRY(pool.alloc(&off, (size_t)n));
+  TRY(pool.alloc(&tot, 2));
+  TRY(pool.alloc((uint8_t**)&st, scan_temp_bytes(n)));
+  int64_t launches = 0;
+  CK(launch_simplex_counts(c->pt_ptr, n, r, cnt, s));
+  CK(exclusive_scan_i64(cnt, off, n, st, tot, s, &launches));
+  int64_t NP = 0;
+  CK(cudaMemcpyAsync(&NP, tot, sizeof NP, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (NP > max_emit)
+    return set_err(BM_EOVERFLOW, "%lld witnessed subsets exceed max_emit", (long long)NP);
+  if (NP == 0) return BM_OK;
+  unsigned long long *keys = nullptr, *alt = nullptr;
+  void *rt = nullptr, *ut = nullptr;
+  int32_t* tmp = nullptr;
+  TRY(pool.alloc(&keys, (size_t)NP));
+  TRY(pool.alloc(&alt, (size_t)NP));
+  TRY(pool.alloc((uint8_t**)&rt, radix_temp_bytes(NP)));
+  CK(launch_simplex_emit(c->pt_ptr, c->pt_lm, n, r, lbits, off, keys, s));
+  const BitRange br[1] = {{0, r * lbits}};
+  CK(radix_sort_u64(&keys, &alt, NP, br, 1, rt, s, &launches));
+  TRY(pool.alloc(&tmp, (size_t)NP * r));
+  TRY(pool.alloc((uint8_t**)&ut, simplex_unique_temp_bytes(NP)));
+  CK(launch_simplex_unique(keys, NP, r, lbits, tmp, NP, tot + 1, ut, s));
+  int64_t E = 0;
+  CK(cudaMemcpyAsync(&E, tot + 1, sizeof E, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  *count = E;
+  const int64_t ncopy = E < capacity ? E : capacity;
+  if (ncopy > 0) {
+    CK(cudaMemcpyAsync(out, tmp, sizeof(int32_t) * r * ncopy, cudaMemcpyDeviceToDevice, s));
+    CK(cudaStreamSynchronize(s));
+  }
+  return BM_OK;
+}
+
 bm_status bm_trim_memory(void) {
   g_cache.trim();
   return BM_OK;

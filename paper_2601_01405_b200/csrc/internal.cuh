@@ -212,6 +212,26 @@ cudaError_t launch_unique_flags(const unsigned long long* keys, int64_t m, int64
 cudaError_t launch_unique_scatter(const unsigned long long* keys, int64_t m,
                                   const int64_t* pos, int lbits, int32_t* edges,
                                   cudaStream_t s, int64_t* launches);
+// color.cu (NEXT-1)
+cudaError_t launch_color_reduce(const int64_t* ball_ptr, const int32_t* ball_idx, int64_t L,
+                                const void* values, int is_int, int agg, double* out,
+                                cudaStream_t s);
+cudaError_t launch_color_keys(const int64_t* ball_ptr, const int32_t* ball_idx, int64_t L,
+                              const void* values, int is_int, unsigned long long* keys,
+                              cudaStream_t s);
+cudaError_t launch_color_order(const int64_t* ball_ptr, int64_t L, const unsigned long long* keys,
+                               int is_int, int agg, double alpha, double* out, cudaStream_t s);
+// skeleton.cu (NEXT-3)
+cudaError_t launch_simplex_counts(const int64_t* pt_ptr, int64_t n, int r, int64_t* cnt,
+                                  cudaStream_t s);
+cudaError_t launch_simplex_emit(const int64_t* pt_ptr, const int32_t* pt_lm, int64_t n, int r,
+                                int lbits, const int64_t* off, unsigned long long* keys,
+                                cudaStream_t s);
+size_t simplex_unique_temp_bytes(int64_t m);
+cudaError_t launch_simplex_unique(const unsigned long long* keys, int64_t m, int r, int lbits,
+                                  int32_t* out, int64_t cap, int64_t* total, void* temp,
+                                  cudaStream_t s);
+
 // edges.cu, step C for n * L <= kCsrBitmapMaxBits: both CSRs from bit matrices
 constexpr int64_t kCsrBitmapMaxBits = (int64_t)1 << 30;
 int64_t csr_bitmap_words(int64_t n, int64_t L);
