@@ -183,9 +183,59 @@ int oracle_set_threads(int t) {
  * failure.  ov_p / ov_q / ov_val: n_ov override triples (point p, landmark
  * point q, decision) — may be NULL when n_ov == 0.
  */
+/*
+ * Farthest point sampling eps-net (§2.2), NEXT-2 in SURVEY
+ * §8(f): start from x_0 = `start`; repeatedly take x* = argmax_x min_{l in L}
+ * d(x, l) (ties: lowest index, reading F2) and add it while that maximum is
+ * >= eps (reading F1: the paper's step 4 says "> eps", which would leave a
+ * point at distance exactly eps uncovered by the open balls; SPEC S:311 takes
+ * ">=").  d is oracle_distance (for L2 the fp64 squared distance, compared
+ * with eps*eps).  Writes the selection order into seq (capacity n), returns L.
+ */
+int64_t oracle_fps(const void *X, int dtype, int64_t n, int d, int metric, double eps,
+                   int64_t start, int64_t *seq) {
+  if (!X || n < 1 || d < 1 || start < 0 || start >= n || !seq) return -1;
+  const double thr = metric == OR_L2 ? eps * eps : eps;
+  double *mind = (double *)malloc(sizeof(double) * (size_t)n);
+  if (!mind) return -1;
+  int64_t L = 0;
+  int64_t cur = start;                       /* step 1: initial landmark x_0 */
+  for (int64_t p = 0; p < n; ++p) mind[p] = INFINITY;
+  for (;;) {
+    seq[L++] = cur;                          /* add x* to L */
+#pragma omp parallel for schedule(static)
+    for (int64_t p = 0; p < n; ++p) {        /* min over the landmark set */
+      double v = oracle_distance(X, dtype, d, metric, p, cur);
+      if (v < mind[p]) mind[p] = v;
+    }
+    int64_t best = 0;                        /* step 3: argmax, lowest index on ties */
+    for (int64_t p = 1; p < n; ++p)
+      if (mind[p] > mind[best]) best = p;
+    if (!(mind[best] >= thr)) break;         /* step 4 (reading F1), step 5 */
+    cur = best;
+  }
+  free(mind);
+  return L;
+}
+
+int oracle_cover_given(const void *X, int dtype, int64_t n, int d, int metric, double eps,
+                       const int64_t *given, int64_t n_given, const int64_t *ov_p,
+                       const int64_t *ov_q, const int8_t *ov_val, int64_t n_ov,
+                       oracle_cover_t *out);
+
 int oracle_cover(const void *X, int dtype, int64_t n, int d, int metric, double eps,
                  const int64_t *ov_p, const int64_t *ov_q, const int8_t *ov_val, int64_t n_ov,
                  oracle_cover_t *out) {
+  return oracle_cover_given(X, dtype, n, d, metric, eps, NULL, 0, ov_p, ov_q, ov_val, n_ov, out);
+}
+
+/* The cover of a landmark set: the greedy's (given == NULL) or a given
+ * ascending list (e.g. the FPS landmarks, sorted) — one linear range query per
+ * landmark either way. */
+int oracle_cover_given(const void *X, int dtype, int64_t n, int d, int metric, double eps,
+                       const int64_t *given, int64_t n_given, const int64_t *ov_p,
+                       const int64_t *ov_q, const int8_t *ov_val, int64_t n_ov,
+                       oracle_cover_t *out) {
   memset(out, 0, sizeof(*out));
   if (!X || n < 1 || d < 1 || !(eps > 0.0) || !isfinite(eps)) return 1;
   if (dtype < 0 || dtype > 2 || metric < 0 || metric > 2) return 1;
@@ -209,8 +259,9 @@ int oracle_cover(const void *X, int dtype, int64_t n, int d, int metric, double 
   bptr[0] = 0;
 
   /* 1+2: greedy eps-net with one linear range query per landmark */
-  for (int64_t i = 0; i < n; ++i) {
-    if (covered[i]) continue;                 /* "Select an uncovered point x" */
+  for (int64_t gi = 0; gi < (given ? n_given : n); ++gi) {
+    const int64_t i = given ? given[gi] : gi;
+    if (!given && covered[i]) continue;       /* "Select an uncovered point x" */
     if (L == cap_l) {                         /* "Add x to N"                  */
       cap_l *= 2;
       int64_t *a = (int64_t *)realloc(lm, sizeof(int64_t) * cap_l);

@@ -65,6 +65,11 @@ def _load():
         lib.oracle_pair_inball.argtypes = [vp, i32, i32, i32, dbl, vp, vp, i64, vp]
         lib.oracle_distance.argtypes = [vp, i32, i32, i32, i64, i64]
         lib.oracle_distance.restype = dbl
+        lib.oracle_cover_given.argtypes = [vp, i32, i64, i32, i32, dbl, vp, i64, vp, vp, vp,
+                                           i64, ctypes.POINTER(_Cover)]
+        lib.oracle_cover_given.restype = i32
+        lib.oracle_fps.argtypes = [vp, i32, i64, i32, i32, dbl, i64, vp]
+        lib.oracle_fps.restype = i64
         lib.oracle_set_threads.argtypes = [i32]
         lib.oracle_set_threads.restype = i32
         _lib = lib
@@ -107,10 +112,26 @@ def _arr(ptr, n):
     return np.ctypeslib.as_array(ptr, shape=(n,)).copy()
 
 
-def cover(X: np.ndarray, metric: str, eps: float, overrides=None) -> OracleCover:
+def fps(X: np.ndarray, metric: str, eps: float, start: int = 0) -> np.ndarray:
+    """Farthest point sampling eps-net (readings F1-F2 in
+    bm_oracle.c): the landmark indices in selection order."""
+    X = np.ascontiguousarray(X)
+    dt = NP_TO_DTYPE[X.dtype]
+    n, d = X.shape
+    seq = np.zeros(n, dtype=np.int64)
+    L = _load().oracle_fps(X.ctypes.data, DTYPE_CODE[dt], n, d, METRIC_CODE[metric], float(eps),
+                           int(start), seq.ctypes.data)
+    if L < 0:
+        raise ValueError("oracle_fps: invalid input")
+    return seq[:L].copy()
+
+
+def cover(X: np.ndarray, metric: str, eps: float, overrides=None, landmarks=None) -> OracleCover:
     """Greedy eps-net + ball membership + 1-skeleton (see bm_oracle.c header).
 
-    overrides: optional iterable of (p, q, bool) — point p, landmark point q."""
+    overrides: optional iterable of (p, q, bool) — point p, landmark point q.
+    landmarks: optional ascending landmark list (e.g. sorted FPS landmarks)
+    whose cover is built instead of the greedy's."""
     X = np.ascontiguousarray(X)
     if X.ndim != 2:
         raise ValueError("X must be 2-D")
@@ -128,8 +149,14 @@ def cover(X: np.ndarray, metric: str, eps: float, overrides=None) -> OracleCover
     else:
         args = (None, None, None, 0)
     c = _Cover()
-    rc = lib.oracle_cover(X.ctypes.data if n else None, DTYPE_CODE[dt], n, d,
-                          METRIC_CODE[metric], float(eps), *args, ctypes.byref(c))
+    if landmarks is not None:
+        g = np.ascontiguousarray(np.asarray(landmarks, dtype=np.int64))
+        rc = lib.oracle_cover_given(X.ctypes.data if n else None, DTYPE_CODE[dt], n, d,
+                                    METRIC_CODE[metric], float(eps), g.ctypes.data, len(g),
+                                    *args, ctypes.byref(c))
+    else:
+        rc = lib.oracle_cover(X.ctypes.data if n else None, DTYPE_CODE[dt], n, d,
+                              METRIC_CODE[metric], float(eps), *args, ctypes.byref(c))
     if rc == 1:
         raise ValueError("oracle_cover: invalid input")
     if rc != 0:

@@ -143,3 +143,64 @@ def test_c1_skeleton_counts_consistent():
     rows = [set(c.pt_lm[c.pt_ptr[p]:c.pt_ptr[p + 1]].tolist()) for p in range(len(Xp))]
     for tri in t[:200]:
         assert any(set(tri.tolist()) <= r for r in rows)
+
+
+# ---------------------------------------------------------------- FPS (NEXT-2)
+def test_fps_spec_example():
+    """1-D {0,1,2,3}, eps 1.5, start 0 -> (0, 3)."""
+    pts = np.array([[0.0], [1.0], [2.0], [3.0]], dtype=np.float32)
+    assert O.fps(pts, "l2", 1.5).tolist() == [0, 3]
+
+
+def test_fps_hand_collinear():
+    """0..6 unit spacing, eps 2.5: 0, then 6 (distance 6), then 3 (distance 3);
+    the remaining max-min distance is 1 < 2.5."""
+    pts = np.arange(7, dtype=np.float32).reshape(-1, 1)
+    assert O.fps(pts, "l2", 2.5).tolist() == [0, 6, 3]
+    assert O.fps(pts, "l1", 2.5).tolist() == [0, 6, 3]
+
+
+def test_fps_ge_reading():
+    """Reading F1: a point at exactly eps from the landmarks is added
+    (with the paper's literal '>' it would stay uncovered by the open ball)."""
+    pts = np.array([[0.0], [1.5]], dtype=np.float32)
+    assert O.fps(pts, "l2", 1.5).tolist() == [0, 1]
+    c = O.cover(pts, "l2", 1.5, landmarks=[0, 1])
+    assert c.ball_idx.tolist() == [0, 1]                 # each point in its own ball only
+
+
+def _brute_fps_int(Xi, eps):
+    """Independent FPS on integer data: exact int64 squared distances, numpy argmax."""
+    Xl = Xi.astype(np.int64)
+    d2 = ((Xl[:, None, :] - Xl[None, :, :]) ** 2).sum(-1)
+    mind = d2[0].copy()
+    seq = [0]
+    while True:
+        b = int(np.argmax(mind))                   # first maximum = lowest index
+        if not mind[b] >= eps * eps:
+            break
+        seq.append(b)
+        mind = np.minimum(mind, d2[b])
+    return seq
+
+
+@pytest.mark.parametrize("seed", range(5))
+def test_fps_brute_force_and_axioms(seed):
+    rng = np.random.default_rng([seed, 9])
+    Xi = rng.integers(-30, 30, size=(300, 3)).astype(np.int8)
+    eps = float(np.sqrt(150.5))
+    seq = O.fps(Xi, "l2", eps)
+    assert seq.tolist() == _brute_fps_int(Xi, eps)
+    from tests.helpers import brute_distance_matrix
+    for metric, e in (("l2", 0.7), ("l1", 1.1), ("cos", 0.08)):
+        Xf = rng.normal(size=(250, 4)).astype(np.float32)
+        s = O.fps(Xf, metric, e)
+        D = brute_distance_matrix(Xf, metric)
+        assert len(set(s.tolist())) == len(s)
+        assert (D[:, s].min(axis=1) < e).all()                     # coverage (Def 2.1)
+        sub = D[np.ix_(s, s)] + np.eye(len(s)) * 1e9
+        assert (sub >= e - 1e-12).all()                            # separation (Def 2.1)
+        c = O.cover(Xf, metric, e, landmarks=np.sort(s))           # cover of the FPS set
+        for j, lm in enumerate(np.sort(s)):
+            assert c.ball_idx[c.ball_ptr[j]:c.ball_ptr[j + 1]].tolist() == \
+                np.nonzero(D[:, lm] < e)[0].tolist()
