@@ -106,8 +106,17 @@ typedef struct bm_options {
   int32_t band_cap;      /* ignored (kept for layout): band pairs are re-decided in fp64
                             inside the contraction kernels, no queue is needed              */
   int32_t flags;         /* BM_FLAG_* (diagnostics)                                           */
-  int32_t reserved[5];
+  int32_t select;        /* bm_select: landmark selection (default greedy in point order)     */
+  int32_t fps_start;     /* BM_SELECT_FPS: index of the initial landmark x_0 (default 0)      */
+  int32_t reserved[3];
 } bm_options;
+
+/* Landmark selection (PAPER.md:98-119 [§2.2]). */
+typedef enum bm_select {
+  BM_SELECT_GREEDY = 0,  /* greedy eps-net in point order (the north-star path)           */
+  BM_SELECT_FPS = 1      /* farthest point sampling: x* = argmax min d, added while >= eps
+                            (ties: lowest index); landmarks are returned ascending        */
+} bm_select;
 
 /* bm_options.flags */
 #define BM_FLAG_NO_L1_PREFILTER 1   /* L1: score every pair in fp32 (no 8-bit SAD prefilter) */

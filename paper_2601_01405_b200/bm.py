@@ -44,7 +44,8 @@ class _Options(ctypes.Structure):
                 ("path", ctypes.c_int32), ("timing", ctypes.c_int32),
                 ("near_tie_cap", ctypes.c_int64), ("key_cap", ctypes.c_int32),
                 ("band_cap", ctypes.c_int32), ("flags", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 5)]
+                ("select", ctypes.c_int32), ("fps_start", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 3)]
 
 
 class _Cover(ctypes.Structure):
@@ -116,8 +117,11 @@ def _check(rc: int):
         raise BMError(rc, load().bm_last_error().decode())
 
 
+SELECT = {"greedy": 0, "fps": 1}
+
+
 def _options(tile=0, path="auto", timing=False, near_tie_cap=0, key_cap=0,
-             band_cap=0, flags=0) -> _Options:
+             band_cap=0, flags=0, select="greedy", fps_start=0) -> _Options:
     o = _Options()
     o.struct_size = ctypes.sizeof(_Options)
     o.tile = int(tile)
@@ -127,6 +131,8 @@ def _options(tile=0, path="auto", timing=False, near_tie_cap=0, key_cap=0,
     o.key_cap = int(key_cap)
     o.band_cap = int(band_cap)
     o.flags = int(flags)
+    o.select = SELECT[select] if isinstance(select, str) else int(select)
+    o.fps_start = int(fps_start)
     return o
 
 
@@ -237,7 +243,8 @@ def _dtype_of(t) -> str:
 
 def cover_build(points, metric: str, eps: float, stream=None, tile: int = 0,
                 path: str = "auto", timing: bool = False, near_tie_cap: int = 0,
-                key_cap: int = 0, band_cap: int = 0, flags: int = 0) -> Cover:
+                key_cap: int = 0, band_cap: int = 0, flags: int = 0, select: str = "greedy",
+                fps_start: int = 0) -> Cover:
     """bm_cover_build_ex on a CUDA torch tensor [n, d] (row-major, contiguous)."""
     import torch
     if not (isinstance(points, torch.Tensor) and points.is_cuda):
@@ -250,7 +257,8 @@ def cover_build(points, metric: str, eps: float, stream=None, tile: int = 0,
         stream = torch.cuda.current_stream(points.device)
     sp = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
     out = ctypes.POINTER(_Cover)()
-    o = _options(tile, path, timing, near_tie_cap, key_cap, band_cap, flags)
+    o = _options(tile, path, timing, near_tie_cap, key_cap, band_cap, flags, select,
+                 fps_start)
     lib = load()
     with torch.cuda.device(points.device):
         rc = lib.bm_cover_build_ex(ctypes.c_void_p(points.data_ptr()), DTYPE[_dtype_of(points)],
@@ -262,7 +270,8 @@ def cover_build(points, metric: str, eps: float, stream=None, tile: int = 0,
 
 def cover_build_host(points: np.ndarray, metric: str, eps: float, stream=None, tile: int = 0,
                      path: str = "auto", timing: bool = False, near_tie_cap: int = 0,
-                     key_cap: int = 0, band_cap: int = 0, flags: int = 0) -> Cover:
+                     key_cap: int = 0, band_cap: int = 0, flags: int = 0, select: str = "greedy",
+                     fps_start: int = 0) -> Cover:
     """bm_cover_build_host on a host buffer (numpy array or CPU torch tensor,
     ideally pinned): copies in, builds, copies every result back to host."""
     import torch
@@ -280,7 +289,8 @@ def cover_build_host(points: np.ndarray, metric: str, eps: float, stream=None, t
         stream = torch.cuda.current_stream()
     sp = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
     out = ctypes.POINTER(_Cover)()
-    o = _options(tile, path, timing, near_tie_cap, key_cap, band_cap, flags)
+    o = _options(tile, path, timing, near_tie_cap, key_cap, band_cap, flags, select,
+                 fps_start)
     rc = load().bm_cover_build_host(ctypes.c_void_p(ptr), DTYPE[dt], n, d, METRIC[metric],
                                     float(eps), ctypes.c_void_p(sp), ctypes.byref(o),
                                     ctypes.byref(out))

@@ -428,8 +428,7 @@ bm_status membership_full(Pool& pool, int kind, const bm::PairArgs& base, bm::tc
   unsigned long long kc = 0;
   CK(cudaMemcpyAsync(&kc, &stats->key_count, sizeof kc, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
-  if ((int64_t)kc > key_cap) return set_err(BM_ECUDA, "membership recount exceeded its exact size");
-  *M_out = (int64_t)kc;
+  *M_out = (int64_t)kc;   // > key_cap: the keys were dropped, the caller resizes and reruns
   return BM_OK;
 }
 
@@ -462,6 +461,11 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
   if (T < 32 || T > 1024 || (T % 32) != 0)
     return set_err(BM_EINVAL, "tile must be a multiple of 32 in [32, 1024]");
   const int64_t tie_cap = o.near_tie_cap > 0 ? o.near_tie_cap : 65536;
+  if (o.select != BM_SELECT_GREEDY && o.select != BM_SELECT_FPS)
+    return set_err(BM_EINVAL, "unknown landmark selection %d", o.select);
+  const bool fps = o.select == BM_SELECT_FPS;
+  if (fps && (o.fps_start < 0 || o.fps_start >= n))
+    return set_err(BM_EINVAL, "fps_start must be in [0, n) (got %d)", o.fps_start);
 
   const int kind = dtype == BM_F32
                        ? (metric == BM_L2 ? K_L2F : (metric == BM_L1 ? K_L1F : K_COSF))
@@ -712,7 +716,49 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
   int64_t tile = 0;
   int batch = 4;
   int nonfinite_checked = 0;
-  for (;;) {
+  if (fps) {
+    // NEXT-2: farthest point sampling selects the landmarks (fps.cu), then one
+    // membership pass of all points against the ascending landmark list
+    CK(cudaStreamSynchronize(s));
+    int nf = 0;
+    CK(cudaMemcpy(&nf, &stats->nonfinite, sizeof nf, cudaMemcpyDeviceToHost));
+    if (nf) return set_err(BM_EINVAL, "points contain a non-finite coordinate");
+    const int g = fps_grid(d);
+    double *mind = nullptr, *cval = nullptr;
+    int64_t* cidx = nullptr;
+    int32_t* seq = nullptr;
+    TRY(pool.alloc(&mind, (size_t)n));
+    TRY(pool.alloc(&seq, (size_t)n));
+    TRY(pool.alloc(&cval, (size_t)2 * g));
+    TRY(pool.alloc(&cidx, (size_t)2 * g));
+    const double thr = metric == BM_L2 ? eps * eps : eps;
+    CK(launch_fps(rows, nu, d, kind, n, thr, o.fps_start, mind, seq, cnt + 2, cval, cidx, g, s));
+    ++launches;
+    int32_t hl = 0;
+    CK(cudaMemcpyAsync(&hl, cnt + 2, sizeof hl, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    unsigned long long *lk = nullptr, *lalt = nullptr;
+    void* temp = nullptr;
+    TRY(pool.alloc(&lk, (size_t)hl));
+    TRY(pool.alloc(&lalt, (size_t)hl));
+    TRY(pool.alloc((uint8_t**)&temp, radix_temp_bytes(hl)));
+    CK(launch_fps_keys(seq, hl, lk, s, &launches));
+    const BitRange r[1] = {{0, bits_for(n > 1 ? n - 1 : 1)}};
+    CK(radix_sort_u64(&lk, &lalt, hl, r, 1, temp, s, &launches));
+    CK(launch_unpack_low(lk, hl, 0xffffffffull, lm, s, &launches));
+    int64_t Mf = 0;
+    TRY(membership_full(pool, kind, base, P, use_tc, tc_nrm, lm, hl, n, d, dtype, nu, th, C2,
+                        keys, key_cap, ties_dev, tie_cap, stats, s, &launches, &Mf));
+    if (Mf > key_cap) {
+      pool.free_now(keys);
+      key_cap = Mf;
+      TRY(pool.alloc(&keys, (size_t)key_cap));
+      TRY(membership_full(pool, kind, base, P, use_tc, tc_nrm, lm, hl, n, d, dtype, nu, th, C2,
+                          keys, key_cap, ties_dev, tie_cap, stats, s, &launches, &Mf));
+      if (Mf > key_cap) return set_err(BM_ECUDA, "membership recount exceeded its exact size");
+    }
+  }
+  for (; !fps;) {
     for (int b = 0; b < batch; ++b, ++tile) {
       const int cur = (int)(tile & 1), nxt = cur ^ 1;
       // A2: adjacency among the candidates unc[0 .. nc)
@@ -809,6 +855,7 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
     TRY(pool.alloc(&keys, (size_t)key_cap));
     TRY(membership_full(pool, kind, base, P, use_tc, tc_nrm, lm, L, n, d, dtype, nu, th, C2,
                         keys, key_cap, ties_dev, tie_cap, stats, s, &launches, &M));
+    if (M > key_cap) return set_err(BM_ECUDA, "membership recount exceeded its exact size");
     CK(cudaMemcpyAsync(&hs, stats, sizeof hs, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
   }

@@ -19,8 +19,10 @@ def gpu_arrays(cov) -> dict:
 
 
 def compare(X: np.ndarray, metric: str, eps: float, cov, *, float_path: bool,
-            oracle_result=None, tie_rate_limit: bool = False) -> dict:
-    """tie_rate_limit: enforce north_star's "< 1e-6 of the pairs evaluated" —
+            oracle_result=None, tie_rate_limit: bool = False, landmarks=None) -> dict:
+    """landmarks: compare against the oracle's cover of this ascending
+    landmark list (the FPS selection) instead of the greedy's.
+    tie_rate_limit: enforce north_star's "< 1e-6 of the pairs evaluated" —
     a property of the BASELINE workloads, not of arbitrary random test clouds."""
     g = gpu_arrays(cov)
     overrides = []
@@ -34,7 +36,7 @@ def compare(X: np.ndarray, metric: str, eps: float, cov, *, float_path: bool,
         assert cov.stats.n_near_ties == 0
     n = X.shape[0]
     if oracle_result is None or overrides:
-        oracle_result = O.cover(X, metric, eps, overrides=overrides)
+        oracle_result = O.cover(X, metric, eps, overrides=overrides, landmarks=landmarks)
     o = oracle_result
     assert g["landmarks"].tolist() == o.landmarks.tolist(), "landmarks differ"
     assert np.array_equal(g["ball_ptr"], o.ball_ptr), "ball_ptr differs"

@@ -87,3 +87,59 @@ def test_skeleton_overflow_guard(bm):
     cov = bm.cover_build(torch.from_numpy(X_).cuda(), w.metric, w.eps)
     with pytest.raises(B.BMError):
         bm.skeleton(cov, 2, max_emit=10)
+
+
+# ---------------------------------------------------------------- FPS (NEXT-2)
+def _fps_case(bm, X_, metric, eps, start=0, **kw):
+    want = np.sort(O.fps(X_, metric, eps, start))
+    cov = bm.cover_build(torch.from_numpy(np.ascontiguousarray(X_)).cuda(), metric, eps,
+                         select="fps", fps_start=start, **kw)
+    got = cov.numpy()["landmarks"]
+    assert np.array_equal(np.asarray(got, dtype=np.int64), want), "FPS landmark set differs"
+    return compare(X_, metric, eps, cov, float_path=X_.dtype == np.float32, landmarks=want)
+
+
+@pytest.mark.parametrize("metric,eps", [("l2", 0.5), ("l1", 0.9), ("cos", 0.05)])
+@pytest.mark.parametrize("seed", range(3))
+def test_fps_parity_random(bm, metric, eps, seed):
+    rng = np.random.default_rng([seed, 21])
+    X_ = rng.normal(size=(3000 + 77 * seed, 3)).astype(np.float32)
+    _fps_case(bm, X_, metric, eps, start=seed * 11)
+
+
+@pytest.mark.parametrize("dtype,metric,eps", [("i8", "l2", 6.5), ("u8", "l1", 9.0),
+                                              ("i8", "l1", 7.0), ("u8", "l2", 12.0)])
+def test_fps_parity_int(bm, dtype, metric, eps):
+    rng = np.random.default_rng(5)
+    X_ = (rng.integers(-40, 40, size=(4000, 4)).astype(np.int8) if dtype == "i8"
+          else rng.integers(0, 90, size=(4000, 4)).astype(np.uint8))
+    _fps_case(bm, X_, metric, eps)
+
+
+@pytest.mark.parametrize("name,m", [("c1", None), ("c2", 20000)])
+def test_fps_parity_workloads(bm, name, m):
+    w = gen.get(name)
+    X_ = gen.generate(w, m)
+    _fps_case(bm, X_, w.metric, w.eps)
+
+
+@pytest.mark.parametrize("path", ["cuda_core", "tensor"])
+def test_fps_paths_and_ties(bm, path):
+    """Both membership paths; exact-distance ties in the argmax (integer
+    lattice: many points at the same max-min distance, lowest index wins) and
+    a point at exactly eps (reading F1: it becomes a landmark)."""
+    g = np.stack(np.meshgrid(np.arange(12), np.arange(12), np.arange(12)), -1).reshape(-1, 3)
+    X_ = (g * 2).astype(np.float32)
+    _fps_case(bm, X_, "l2", 4.0, path=path)          # distance exactly eps occurs everywhere
+    _fps_case(bm, X_, "l2", 4.0, start=5, path=path)
+
+
+def test_fps_degenerate(bm):
+    one = np.zeros((1, 3), np.float32)
+    assert _fps_case(bm, one, "l2", 1.0)["L"] == 1
+    same = np.ones((500, 2), np.float32)                 # all distances 0: one landmark
+    assert _fps_case(bm, same, "l1", 0.1)["L"] == 1
+    far = np.arange(40, dtype=np.float32).reshape(-1, 1) * 10   # all singletons
+    assert _fps_case(bm, far, "l2", 1.0)["L"] == 40
+    with pytest.raises(Exception):
+        bm.cover_build(torch.from_numpy(far).cuda(), "l2", 1.0, select="fps", fps_start=40)
