@@ -84,6 +84,7 @@ enum {
   BM_STEP_EDGES = 4,    /* D1-D3: pair emission, radix sort, unique               */
   BM_STEP_TOTAL = 5,
   BM_STEP_MEMBER_KERNEL = 6,  /* membership contraction kernels alone, summed over tiles */
+  BM_STEP_SELECT = 7,   /* BM_SELECT_FPS: the farthest point sampling kernel alone    */
   BM_NUM_STEPS = 8
 };
 

@@ -723,7 +723,7 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
     int nf = 0;
     CK(cudaMemcpy(&nf, &stats->nonfinite, sizeof nf, cudaMemcpyDeviceToHost));
     if (nf) return set_err(BM_EINVAL, "points contain a non-finite coordinate");
-    const int g = fps_grid(d);
+    const int g = fps_max_candidates();
     double *mind = nullptr, *cval = nullptr;
     int64_t* cidx = nullptr;
     int32_t* seq = nullptr;
@@ -732,7 +732,10 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
     TRY(pool.alloc(&cval, (size_t)2 * g));
     TRY(pool.alloc(&cidx, (size_t)2 * g));
     const double thr = metric == BM_L2 ? eps * eps : eps;
-    CK(launch_fps(rows, nu, d, kind, n, thr, o.fps_start, mind, seq, cnt + 2, cval, cidx, g, s));
+    tm.mark(6);
+    CK(launch_fps(rows, inorm, nu, d, kind, n, thr, o.fps_start, mind, seq, cnt + 2, cval, cidx,
+                  s));
+    tm.mark(7);
     ++launches;
     int32_t hl = 0;
     CK(cudaMemcpyAsync(&hl, cnt + 2, sizeof hl, cudaMemcpyDeviceToHost, s));
@@ -747,8 +750,10 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
     CK(radix_sort_u64(&lk, &lalt, hl, r, 1, temp, s, &launches));
     CK(launch_unpack_low(lk, hl, 0xffffffffull, lm, s, &launches));
     int64_t Mf = 0;
+    CK(mark_member());
     TRY(membership_full(pool, kind, base, P, use_tc, tc_nrm, lm, hl, n, d, dtype, nu, th, C2,
                         keys, key_cap, ties_dev, tie_cap, stats, s, &launches, &Mf));
+    CK(mark_member());
     if (Mf > key_cap) {
       pool.free_now(keys);
       key_cap = Mf;
@@ -1034,6 +1039,7 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
       km += t;
     }
     c->step_ms[BM_STEP_MEMBER_KERNEL] = km;
+    if (fps) cudaEventElapsedTime(&c->step_ms[BM_STEP_SELECT], tm.ev[6], tm.ev[7]);
   }
   c->n_member_launches = (int64_t)(mev.size() / 2);
   c->n_launches = launches;

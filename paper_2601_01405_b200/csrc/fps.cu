@@ -22,53 +22,77 @@ namespace cg = cooperative_groups;
 namespace bm {
 
 struct FpsArgs {
-  const uint2* rows;   // prepped rows (fp32 bits, or int8 with u8 shifted by -128)
-  int nu, d, kind;     // Kind (K_L2F, K_L1F, K_COSF, K_L2I, K_L1I)
+  const uint2* rows;   // prepped rows: nu 8-byte units (fp32 pairs, or 8 int8 with u8 shifted by -128)
+  const int32_t* inorm;   // K_L2I: sum of squares of the prepped row
+  int nu, nue, d;      // row stride in units; units holding the d coordinates
   int64_t n;
   double thr;          // eps^2 for L2, eps otherwise
   int64_t start;
-  double* mind;        // [n]
+  double* mind;        // [n] running minimum (only when the points do not fit in registers)
   int32_t* seq;        // [n] selection order
   int32_t* L_out;
   double* cval;        // [2][grid] candidate values
   int64_t* cidx;       // [2][grid] candidate indices
 };
 
-__device__ __forceinline__ double fps_dist(const FpsArgs& a, int64_t p, const float* lf,
-                                           const int8_t* li) {
-  if (a.kind == K_L2F || a.kind == K_L1F || a.kind == K_COSF) {
-    const float* x = reinterpret_cast<const float*>(a.rows + p * (int64_t)a.nu);
-    if (a.kind == K_L2F) {
-      double s = 0.0;
-      for (int j = 0; j < a.d; ++j) {
-        const double t = __dsub_rn((double)x[j], (double)lf[j]);
-        s = __dadd_rn(s, __dmul_rn(t, t));
+// d(x_p, l) with l's units in shared memory.  Float kinds: the oracle's fp64
+// formula operation for operation (coordinates ascending, no contraction; the
+// zero padding of the last unit adds an exact +0).  Integer kinds: exact
+// integer arithmetic, so any order gives the oracle's value — L2 as
+// |x|^2 + |l|^2 - 2 x.l with 4-way int8 dot products, L1 as byte SADs
+// (signed bytes re-biased by 0x80, which keeps every difference).
+template <int KIND>
+__device__ __forceinline__ double fps_dist(const FpsArgs& a, int64_t p, const uint2* __restrict__ l,
+                                           int32_t lnorm) {
+  const uint2* x = a.rows + p * (int64_t)a.nu;
+  if constexpr (KIND == K_L2F || KIND == K_L1F) {
+    double s = 0.0;
+    for (int u = 0; u < a.nue; ++u) {
+      const uint2 w = __ldg(x + u), v = l[u];
+      const double t0 = __dsub_rn((double)__uint_as_float(w.x), (double)__uint_as_float(v.x));
+      const double t1 = __dsub_rn((double)__uint_as_float(w.y), (double)__uint_as_float(v.y));
+      if constexpr (KIND == K_L2F) {
+        s = __dadd_rn(s, __dmul_rn(t0, t0));
+        s = __dadd_rn(s, __dmul_rn(t1, t1));
+      } else {
+        s = __dadd_rn(s, fabs(t0));
+        s = __dadd_rn(s, fabs(t1));
       }
-      return s;
     }
-    if (a.kind == K_L1F) {
-      double s = 0.0;
-      for (int j = 0; j < a.d; ++j) s = __dadd_rn(s, fabs(__dsub_rn((double)x[j], (double)lf[j])));
-      return s;
-    }
+    return s;
+  } else if constexpr (KIND == K_COSF) {
     double dot = 0.0, xx = 0.0, yy = 0.0;
-    for (int j = 0; j < a.d; ++j) {
-      const double u = (double)x[j], v = (double)lf[j];
-      dot = __dadd_rn(dot, __dmul_rn(u, v));
-      xx = __dadd_rn(xx, __dmul_rn(u, u));
-      yy = __dadd_rn(yy, __dmul_rn(v, v));
+    for (int u = 0; u < a.nue; ++u) {
+      const uint2 w = __ldg(x + u), v = l[u];
+      const double u0 = (double)__uint_as_float(w.x), v0 = (double)__uint_as_float(v.x);
+      const double u1 = (double)__uint_as_float(w.y), v1 = (double)__uint_as_float(v.y);
+      dot = __dadd_rn(dot, __dmul_rn(u0, v0));
+      xx = __dadd_rn(xx, __dmul_rn(u0, u0));
+      yy = __dadd_rn(yy, __dmul_rn(v0, v0));
+      dot = __dadd_rn(dot, __dmul_rn(u1, v1));
+      xx = __dadd_rn(xx, __dmul_rn(u1, u1));
+      yy = __dadd_rn(yy, __dmul_rn(v1, v1));
     }
     if (xx == 0.0 && yy == 0.0) return 0.0;
     if (xx == 0.0 || yy == 0.0) return 1.0;
     return __dsub_rn(1.0, __ddiv_rn(dot, __dmul_rn(__dsqrt_rn(xx), __dsqrt_rn(yy))));
+  } else if constexpr (KIND == K_L2I) {
+    int dot = 0;
+    for (int u = 0; u < a.nue; ++u) {
+      const uint2 w = __ldg(x + u), v = l[u];
+      dot = __dp4a((int)w.x, (int)v.x, dot);
+      dot = __dp4a((int)w.y, (int)v.y, dot);
+    }
+    return (double)((int64_t)__ldg(a.inorm + p) + lnorm - 2 * (int64_t)dot);
+  } else {
+    unsigned s = 0u;
+    for (int u = 0; u < a.nue; ++u) {
+      const uint2 w = __ldg(x + u), v = l[u];
+      s += __vsadu4(w.x ^ 0x80808080u, v.x ^ 0x80808080u);
+      s += __vsadu4(w.y ^ 0x80808080u, v.y ^ 0x80808080u);
+    }
+    return (double)s;
   }
-  const int8_t* x = reinterpret_cast<const int8_t*>(a.rows + p * (int64_t)a.nu);
-  int64_t s = 0;
-  for (int j = 0; j < a.d; ++j) {
-    const int64_t t = (int64_t)x[j] - (int64_t)li[j];
-    s += a.kind == K_L2I ? t * t : (t < 0 ? -t : t);
-  }
-  return (double)s;
 }
 
 // (value, index) order of the argmax: larger value first, then lower index
@@ -77,37 +101,55 @@ __device__ __forceinline__ bool better(double v, int64_t i, double bv, int64_t b
 }
 
 constexpr int FPS_NT = 256;
+constexpr int FPS_MAX_CAND = 1024;   // grid size bound
 
+// PPT > 0: each thread owns points gt + k * gs (k < PPT) with their running
+// minimum in registers; PPT == 0: any n, running minimum in a.mind.
+template <int KIND, int PPT>
 __global__ void __launch_bounds__(FPS_NT) k_fps(FpsArgs a) {
   cg::grid_group grid = cg::this_grid();
-  extern __shared__ float slm[];   // the current landmark's coordinates (fp32 or int8)
+  extern __shared__ uint2 slm[];   // the current landmark's units
   __shared__ double sv[FPS_NT / 32];
   __shared__ int64_t si[FPS_NT / 32];
   __shared__ int64_t s_next;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int64_t gt = (int64_t)blockIdx.x * FPS_NT + tid, gs = (int64_t)gridDim.x * FPS_NT;
-  const bool is_float = a.kind == K_L2F || a.kind == K_L1F || a.kind == K_COSF;
+  double mr[PPT > 0 ? PPT : 1];
+#pragma unroll
+  for (int k = 0; k < (PPT > 0 ? PPT : 1); ++k) mr[k] = INFINITY;
   int64_t cur = a.start;
   int64_t L = 0;
   for (int step = 0;; ++step) {
     if (blockIdx.x == 0 && tid == 0) a.seq[L] = (int32_t)cur;
     ++L;
-    // the landmark's coordinates
-    for (int j = tid; j < a.d; j += FPS_NT) {
-      if (is_float) slm[j] = reinterpret_cast<const float*>(a.rows + cur * (int64_t)a.nu)[j];
-      else reinterpret_cast<int8_t*>(slm)[j] =
-          reinterpret_cast<const int8_t*>(a.rows + cur * (int64_t)a.nu)[j];
-    }
+    const uint2* lrow = a.rows + cur * (int64_t)a.nu;
+    for (int u = tid; u < a.nue; u += FPS_NT) slm[u] = lrow[u];
+    const int32_t lnorm = KIND == K_L2I ? __ldg(a.inorm + cur) : 0;
     __syncthreads();
     double bv = -INFINITY;
     int64_t bi = a.n;
-    for (int64_t p = gt; p < a.n; p += gs) {
-      const double v = fps_dist(a, p, slm, reinterpret_cast<const int8_t*>(slm));
-      const double m = step == 0 ? v : fmin(a.mind[p], v);
-      a.mind[p] = m;
-      if (better(m, p, bv, bi)) {
-        bv = m;
-        bi = p;
+    if constexpr (PPT > 0) {
+#pragma unroll
+      for (int k = 0; k < PPT; ++k) {
+        const int64_t p = gt + k * gs;
+        if (p < a.n) {
+          const double v = fps_dist<KIND>(a, p, slm, lnorm);
+          if (v < mr[k]) mr[k] = v;
+          if (better(mr[k], p, bv, bi)) {
+            bv = mr[k];
+            bi = p;
+          }
+        }
+      }
+    } else {
+      for (int64_t p = gt; p < a.n; p += gs) {
+        const double v = fps_dist<KIND>(a, p, slm, lnorm);
+        const double m = step == 0 ? v : fmin(a.mind[p], v);
+        a.mind[p] = m;
+        if (better(m, p, bv, bi)) {
+          bv = m;
+          bi = p;
+        }
       }
     }
     for (int o = 16; o > 0; o >>= 1) {
@@ -127,6 +169,7 @@ __global__ void __launch_bounds__(FPS_NT) k_fps(FpsArgs a) {
     if (tid == 0) {
       double v = sv[0];
       int64_t i = si[0];
+#pragma unroll
       for (int k = 1; k < FPS_NT / 32; ++k)
         if (better(sv[k], si[k], v, i)) {
           v = sv[k];
@@ -136,17 +179,26 @@ __global__ void __launch_bounds__(FPS_NT) k_fps(FpsArgs a) {
       a.cidx[buf * gridDim.x + blockIdx.x] = i;
     }
     grid.sync();
-    // every CTA reduces all candidates the same way
+    // every CTA reduces all candidates the same way (loads issued before the compares)
     if (w == 0) {
       double v = -INFINITY;
       int64_t i = a.n;
-      for (int k = lane; k < (int)gridDim.x; k += 32) {
-        const double cv = a.cval[buf * gridDim.x + k];
-        const int64_t ci = a.cidx[buf * gridDim.x + k];
-        if (better(cv, ci, v, i)) {
-          v = cv;
-          i = ci;
+      for (int base = 0; base < (int)gridDim.x; base += 256) {
+        double cv[8];
+        int64_t ci[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          const int k = base + lane + 32 * r;
+          const bool ok = k < (int)gridDim.x;
+          cv[r] = ok ? __ldcg(a.cval + buf * gridDim.x + k) : -INFINITY;
+          ci[r] = ok ? __ldcg(a.cidx + buf * gridDim.x + k) : a.n;
         }
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+          if (better(cv[r], ci[r], v, i)) {
+            v = cv[r];
+            i = ci[r];
+          }
       }
       for (int o = 16; o > 0; o >>= 1) {
         const double ov = __shfl_xor_sync(0xffffffffu, v, o);
@@ -161,19 +213,72 @@ __global__ void __launch_bounds__(FPS_NT) k_fps(FpsArgs a) {
     __syncthreads();
     cur = s_next;
     if (cur < 0) break;
-    __syncthreads();   // slm is rewritten next step
   }
   if (blockIdx.x == 0 && tid == 0) *a.L_out = (int32_t)L;
 }
 
-cudaError_t launch_fps(const uint2* rows, int nu, int d, int kind, int64_t n, double thr,
-                       int64_t start, double* mind, int32_t* seq, int32_t* L_out, double* cval,
-                       int64_t* cidx, int grid, cudaStream_t s) {
-  FpsArgs a{rows, nu, d, kind, n, thr, start, mind, seq, L_out, cval, cidx};
+template <int KIND, int PPT>
+static cudaError_t fps_go(const FpsArgs& a0, int grid, cudaStream_t s) {
+  FpsArgs a = a0;
   void* args[] = {&a};
-  const size_t smem = (size_t)d * sizeof(float);
-  return cudaLaunchCooperativeKernel((void*)k_fps, dim3(grid), dim3(FPS_NT), args, smem, s);
+  const size_t smem = (size_t)a.nue * sizeof(uint2);
+  return cudaLaunchCooperativeKernel((void*)k_fps<KIND, PPT>, dim3(grid), dim3(FPS_NT), args,
+                                     smem, s);
 }
+
+// Grid: CTAs co-resident for every instance of the kind (cooperative launch),
+// at most FPS_MAX_CAND, and no more than one CTA per 256 points (a small
+// problem pays a smaller barrier).
+template <int KIND>
+static int fps_grid_for(int64_t n, int nue) {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const size_t smem = (size_t)nue * sizeof(uint2);
+  const void* fs[] = {(const void*)k_fps<KIND, 0>, (const void*)k_fps<KIND, 1>,
+                      (const void*)k_fps<KIND, 2>, (const void*)k_fps<KIND, 4>,
+                      (const void*)k_fps<KIND, 8>, (const void*)k_fps<KIND, 16>};
+  int per = 1 << 30;
+  for (const void* f : fs) {
+    int q = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&q, f, FPS_NT, smem);
+    per = q < per ? q : per;
+  }
+  if (per < 1) per = 1;
+  int64_t g = (int64_t)sms * per;
+  if (g > FPS_MAX_CAND) g = FPS_MAX_CAND;
+  const int64_t want = (n + FPS_NT - 1) / FPS_NT;
+  if (g > want) g = want;
+  return (int)(g > 0 ? g : 1);
+}
+
+template <int KIND>
+static cudaError_t fps_kind(const FpsArgs& a, cudaStream_t s) {
+  const int grid = fps_grid_for<KIND>(a.n, a.nue);
+  const int64_t per = (a.n + (int64_t)grid * FPS_NT - 1) / ((int64_t)grid * FPS_NT);
+  if (per <= 1) return fps_go<KIND, 1>(a, grid, s);
+  if (per <= 2) return fps_go<KIND, 2>(a, grid, s);
+  if (per <= 4) return fps_go<KIND, 4>(a, grid, s);
+  if (per <= 8) return fps_go<KIND, 8>(a, grid, s);
+  if (per <= 16) return fps_go<KIND, 16>(a, grid, s);
+  return fps_go<KIND, 0>(a, grid, s);
+}
+
+cudaError_t launch_fps(const uint2* rows, const int32_t* inorm, int nu, int d, int kind, int64_t n,
+                       double thr, int64_t start, double* mind, int32_t* seq, int32_t* L_out,
+                       double* cval, int64_t* cidx, cudaStream_t s) {
+  const int nue = (kind == K_L2I || kind == K_L1I) ? (d + 7) / 8 : (d + 1) / 2;
+  FpsArgs a{rows, inorm, nu, nue, d, n, thr, start, mind, seq, L_out, cval, cidx};
+  switch (kind) {
+    case K_L2F: return fps_kind<K_L2F>(a, s);
+    case K_L1F: return fps_kind<K_L1F>(a, s);
+    case K_COSF: return fps_kind<K_COSF>(a, s);
+    case K_L2I: return fps_kind<K_L2I>(a, s);
+    default: return fps_kind<K_L1I>(a, s);
+  }
+}
+
+int fps_max_candidates() { return FPS_MAX_CAND; }
 
 __global__ void k_fps_keys(const int32_t* __restrict__ seq, int64_t L,
                            unsigned long long* __restrict__ keys) {
@@ -187,16 +292,6 @@ cudaError_t launch_fps_keys(const int32_t* seq, int64_t L, unsigned long long* k
   k_fps_keys<<<(unsigned)((L + 255) / 256), 256, 0, s>>>(seq, L, keys);
   ++*launches;
   return cudaGetLastError();
-}
-
-int fps_grid(int d) {
-  int dev = 0, sms = 0, per = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_fps, FPS_NT, (size_t)d * sizeof(float));
-  if (per < 1) per = 1;
-  if (per > 4) per = 4;
-  return sms * per;
 }
 
 }  // namespace bm

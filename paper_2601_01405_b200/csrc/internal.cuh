@@ -213,10 +213,10 @@ cudaError_t launch_unique_scatter(const unsigned long long* keys, int64_t m,
                                   const int64_t* pos, int lbits, int32_t* edges,
                                   cudaStream_t s, int64_t* launches);
 // fps.cu (NEXT-2)
-int fps_grid(int d);
-cudaError_t launch_fps(const uint2* rows, int nu, int d, int kind, int64_t n, double thr,
-                       int64_t start, double* mind, int32_t* seq, int32_t* L_out, double* cval,
-                       int64_t* cidx, int grid, cudaStream_t s);
+int fps_max_candidates();
+cudaError_t launch_fps(const uint2* rows, const int32_t* inorm, int nu, int d, int kind, int64_t n,
+                       double thr, int64_t start, double* mind, int32_t* seq, int32_t* L_out,
+                       double* cval, int64_t* cidx, cudaStream_t s);
 cudaError_t launch_fps_keys(const int32_t* seq, int64_t L, unsigned long long* keys,
                             cudaStream_t s, int64_t* launches);
 
