@@ -18,6 +18,7 @@
 #include <mutex>
 #include <string>
 #include <unordered_map>
+#include <algorithm>
 #include <vector>
 
 #include "internal.cuh"
@@ -267,6 +268,14 @@ double tc_cos_margin(int ksteps) {
   return 1.25 * (c1 * (1.0 + 4.0 * u) * (1.0 + 4.0 * u) + 8.0 * u + ldexp(1.0, -20));
 }
 
+// Tensor-core operand row pitch: whole 128-byte swizzle atoms.  Measured on
+// B200 (tools/tc_probe_c2.py): TMA tiles of 48-byte rows (C2, d = 10) take
+// 3.3x longer than the same tiles of 128-byte rows, and C5 cosine (64-byte
+// rows) drops from 604 to 378 ms with the padded pitch.
+int64_t tc_row_bytes(int d, int esz) {
+  return (((int64_t)d * esz + 127) / 128) * 128;
+}
+
 double tc_band_c2(int ksteps) {
   const double ut = ldexp(1.0, -11);
   const double K = 8.0 * ksteps + 3.0;
@@ -482,7 +491,7 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
   P.cosine = metric == BM_COSINE ? 1 : 0;
   {
     const int esz = dtype == BM_F32 ? 4 : 1;
-    P.row_bytes = (((int64_t)d * esz + 15) / 16) * 16;
+    P.row_bytes = tc_row_bytes(d, esz);
     P.k_elems = P.row_bytes / esz;
     P.katoms = (int)((P.row_bytes + 127) / 128);
   }
@@ -1268,7 +1277,7 @@ bm_status bm_debug_tc_gram(const void* points, bm_dtype dtype, int64_t n, int32_
   tc::TcPlan P{};
   P.kind = dtype == BM_F32 ? tc::TC_TF32 : (dtype == BM_U8 ? tc::TC_U8 : tc::TC_S8);
   const int esz = dtype == BM_F32 ? 4 : 1;
-  P.row_bytes = (((int64_t)d * esz + 15) / 16) * 16;
+  P.row_bytes = tc_row_bytes(d, esz);
   P.k_elems = P.row_bytes / esz;
   P.katoms = (int)((P.row_bytes + 127) / 128);
   if (!tc::tc_supported(P.kind, P.katoms)) return set_err(BM_EUNSUPPORTED, "d too large");
@@ -1317,7 +1326,7 @@ bm_status bm_debug_tc_probe(const float* points, int64_t n, int32_t d, int64_t L
   cudaStream_t s = (cudaStream_t)stream;
   tc::TcPlan P{};
   P.kind = tc::TC_TF32;
-  P.row_bytes = (((int64_t)d * 4 + 15) / 16) * 16;
+  P.row_bytes = tc_row_bytes(d, 4);
   P.k_elems = P.row_bytes / 4;
   P.katoms = (int)((P.row_bytes + 127) / 128);
   if (P.katoms > 2) return set_err(BM_EUNSUPPORTED, "probe: d <= 64 only");
@@ -1382,6 +1391,32 @@ bm_status bm_debug_tc_probe(const float* points, int64_t n, int32_t d, int64_t L
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   *ms_out = ms / iters;
+  if (mode & 256) {   // one traced launch: per-CTA %globaltimer stamps to stderr
+    const int G = P.num_sms;
+    unsigned long long* tr = nullptr;
+    TRY(pool.alloc(&tr, (size_t)G * 16));
+    CK(cudaMemsetAsync(tr, 0, sizeof(unsigned long long) * G * 16, s));
+    ta.trace = tr;
+    CK(tc::launch_tc_probe(P, ta, mode & 255, s));
+    std::vector<unsigned long long> h((size_t)G * 16);
+    CK(cudaMemcpyAsync(h.data(), tr, sizeof(unsigned long long) * G * 16, cudaMemcpyDeviceToHost,
+                       s));
+    CK(cudaStreamSynchronize(s));
+    unsigned long long t0 = ~0ull;
+    for (int b = 0; b < G; ++b) t0 = h[b * 16] && h[b * 16] < t0 ? h[b * 16] : t0;
+    static const char* names[12] = {"start", "prologue", "pdl", "A0 issued", "producer done",
+                                    "A0 landed", "mma done", "epi0 first", "epi1 first",
+                                    "epi0 done", "epi1 done", "end"};
+    for (int k = 0; k < 12; ++k) {
+      std::vector<double> v;
+      for (int b = 0; b < G; ++b)
+        if (h[b * 16 + k]) v.push_back((double)(h[b * 16 + k] - t0) * 1e-3);
+      std::sort(v.begin(), v.end());
+      if (!v.empty())
+        fprintf(stderr, "trace %-14s min %8.2f  med %8.2f  max %8.2f us  (%zu CTAs)\n", names[k],
+                v.front(), v[v.size() / 2], v.back(), v.size());
+    }
+  }
   return BM_OK;
 }
 

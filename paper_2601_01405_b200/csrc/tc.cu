@@ -78,6 +78,17 @@ __device__ __forceinline__ void tc_col_inert(int64_t j, float* ca, float* cb, fl
   for (int i = 1; i < 8; ++i) k[i] = 0.f;
 }
 
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// diagnostics: stamp slot k of this CTA (no-op unless a trace buffer is given)
+#define TC_STAMP(k) \
+  do { \
+    if (args.trace) args.trace[blockIdx.x * 16 + (k)] = gtimer(); \
+  } while (0)
+
 __device__ __forceinline__ uint32_t su32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
@@ -327,6 +338,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   unsigned long long* bbuf = kbuf + S::EPI_WARPS * S::KW;            // [EPI_WARPS][BW]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) TC_STAMP(0);
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
@@ -368,7 +380,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   __syncthreads();
   fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) TC_STAMP(1);
   pdl_wait();   // everything above overlaps the previous kernel's tail
+  if (threadIdx.x == 0) TC_STAMP(2);
 
   // Work units = (block of RA*128 point rows, chunk of BN-wide landmark tiles),
   // enough units to balance the grid; the column count may live on the device
@@ -405,6 +419,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
         uint8_t* sAb = sA + ab * S::A_BYTES;
         mbar_expect_tx(&a_full[ab], (uint32_t)S::A_BYTES);
+        if (ui == 0) TC_STAMP(3);
         for (int r = 0; r < RA; ++r)
           for (int ka = 0; ka < KATOMS; ++ka)
             tma_load_2d(sAb + (r * KATOMS + ka) * S::A_ATOM, &tmA, &a_full[ab], ka * ATOM_ELEMS,
@@ -439,6 +454,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           ++tk;
         }
       }
+      TC_STAMP(4);
     }
   } else if (warp == 1) {
     if (lane == 0) {
@@ -458,6 +474,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         mbar_wait(&a_full[ab], (a_ph >> ab) & 1u);
         a_ph ^= 1u << ab;
         fence_after();
+        if (ui == 0) TC_STAMP(5);
         const uint8_t* sAb = sA + ab * S::A_BYTES;
         for (int64_t t = t0; t < t1; ++t) {
           mbar_wait(&t_empty[buf], (use[buf] & 1u) ^ 1u);
@@ -508,6 +525,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
         mma_commit(&a_empty[ab]);
       }
+      TC_STAMP(6);
     }
   } else if (warp >= 4) {
     // ---------------- epilogue: warps 4-7 drain TMEM buffer 0, warps 8-11
@@ -602,6 +620,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const int buf = (int)(tcount % NBUF);
         const uint32_t ph = (phase >> buf) & 1u;    // this group's parity for buffer buf
         mbar_wait(&t_full[buf], ph);
+        if (tcount < 2 && q == 0 && lane == 0) TC_STAMP(7 + grp);
         if constexpr ((MODE == TC_MODE_MEMBER || MODE == TC_MODE_ADJ) && !FOLD)
           mbar_wait(&c_full[buf], ph);
         phase ^= 1u << buf;
@@ -782,10 +801,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
     }
     flush();
+    if (q == 0 && lane == 0) TC_STAMP(9 + grp);
   }
   fence_before();
   __syncthreads();
   fence_after();
+  if (threadIdx.x == 0) TC_STAMP(11);
   if (warp == 2) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512)
                  : "memory");

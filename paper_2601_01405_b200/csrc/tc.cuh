@@ -76,6 +76,7 @@ struct TcArgs {
   uint32_t* adj;       // TC_MODE_ADJ: word-major adjacency, word v of candidate a at adj[v*adj_T + a]
   int adj_T;
   uint8_t* covered;    // fused greedy: covered[p] = 1 for every in-ball pair (may be null)
+  unsigned long long* trace;   // diagnostics: [grid][16] %globaltimer stamps (null: off)
 };
 
 int tc_bn_for(int kind, int katoms);
