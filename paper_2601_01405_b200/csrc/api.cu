@@ -1416,6 +1416,16 @@ bm_status bm_debug_tc_probe(const float* points, int64_t n, int32_t d, int64_t L
         fprintf(stderr, "trace %-14s min %8.2f  med %8.2f  max %8.2f us  (%zu CTAs)\n", names[k],
                 v.front(), v[v.size() / 2], v.back(), v.size());
     }
+    std::vector<int> ord(G);
+    for (int b = 0; b < G; ++b) ord[b] = b;
+    std::sort(ord.begin(), ord.end(), [&](int x, int y) { return h[x * 16 + 11] > h[y * 16 + 11]; });
+    for (int i = 0; i < 6 && i < G; ++i) {
+      const int b = ord[i];
+      fprintf(stderr, "slow CTA %3d:", b);
+      for (int k = 0; k < 12; ++k)
+        fprintf(stderr, " %6.2f", h[b * 16 + k] ? (double)(h[b * 16 + k] - t0) * 1e-3 : -1.0);
+      fprintf(stderr, "\n");
+    }
   }
   return BM_OK;
 }

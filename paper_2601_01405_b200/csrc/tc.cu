@@ -192,6 +192,17 @@ __device__ __forceinline__ void tmem_wait(uint32_t (&v)[32]) {
       :
       : "memory");
 }
+// compiler-only fence: uses of v cannot move above it (keeps a TMEM load
+// issued before the compute on the other register buffer)
+__device__ __forceinline__ void reg_fence(uint32_t (&v)[32]) {
+  asm volatile(""
+               : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]),
+                 "+r"(v[6]), "+r"(v[7]), "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]),
+                 "+r"(v[12]), "+r"(v[13]), "+r"(v[14]), "+r"(v[15]), "+r"(v[16]), "+r"(v[17]),
+                 "+r"(v[18]), "+r"(v[19]), "+r"(v[20]), "+r"(v[21]), "+r"(v[22]), "+r"(v[23]),
+                 "+r"(v[24]), "+r"(v[25]), "+r"(v[26]), "+r"(v[27]), "+r"(v[28]), "+r"(v[29]),
+                 "+r"(v[30]), "+r"(v[31]));
+}
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
@@ -599,6 +610,24 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     };
     uint32_t phase = 0;   // bit b: parity of the next completion of buffer b
     int64_t tcount = 0;   // tiles seen, in the MMA issuer's order (buffer = tcount % NBUF)
+    // row constants of the next unit are loaded one unit ahead
+    float nlo[RA], nhi[RA];
+    int32_t nint[RA];
+    auto load_rows = [&](int64_t u) {
+      if (u >= n_units) return;
+      const int64_t mbn = u / n_chunks;
+#pragma unroll
+      for (int r = 0; r < RA; ++r) {
+        const int64_t pr = mbn * RA * 128 + r * 128 + q * 32 + lane;
+        if constexpr (KIND == TC_TF32) {
+          nlo[r] = __ldcg(args.row_lo + pr);
+          nhi[r] = __ldcg(args.row_hi + pr);
+        } else {
+          nint[r] = __ldcg(args.row_r + pr);
+        }
+      }
+    };
+    load_rows(blockIdx.x);
     for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
       const int64_t mb = u / n_chunks, ch = u % n_chunks;
       const int64_t t0 = ch * tiles_per_chunk, t1 = min(n_tiles, t0 + tiles_per_chunk);
@@ -609,12 +638,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       for (int r = 0; r < RA; ++r) {
         prow[r] = mb * RA * 128 + r * 128 + q * 32 + lane;   // < n_pad
         if constexpr (KIND == TC_TF32) {
-          rlo[r] = args.row_lo[prow[r]];
-          rhi[r] = args.row_hi[prow[r]];
+          rlo[r] = nlo[r];
+          rhi[r] = nhi[r];
         } else {
-          rint[r] = args.row_r[prow[r]];
+          rint[r] = nint[r];
         }
       }
+      load_rows(u + gridDim.x);
       for (int64_t t = t0; t < t1; ++t, ++tcount) {
         if ((int)(tcount & 1) != grp) continue;      // the two groups alternate tiles
         const int buf = (int)(tcount % NBUF);
@@ -785,11 +815,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           const int nch = RA == 1 && left < BN ? (int)((left + 31) / 32) : NCH;
 #pragma unroll 1
           for (int c = 0; c < nch; c += 2) {
-            if (c + 1 < nch) tmem_ld32_nowait(trow + (uint32_t)(((c + 1) / (BN / 32)) * BN + ((c + 1) % (BN / 32)) * 32), vb);
+            if (c + 1 < nch) {
+              tmem_ld32_nowait(trow + (uint32_t)(((c + 1) / (BN / 32)) * BN + ((c + 1) % (BN / 32)) * 32), vb);
+              reg_fence(va);
+            }
             chunk(c, va);
             if (c + 1 < nch) {
               tmem_wait(vb);
-              if (c + 2 < nch) tmem_ld32_nowait(trow + (uint32_t)(((c + 2) / (BN / 32)) * BN + ((c + 2) % (BN / 32)) * 32), va);
+              if (c + 2 < nch) {
+                tmem_ld32_nowait(trow + (uint32_t)(((c + 2) / (BN / 32)) * BN + ((c + 2) % (BN / 32)) * 32), va);
+                reg_fence(vb);
+              }
               chunk(c + 1, vb);
               if (c + 2 < nch) tmem_wait(va);
             }
@@ -909,16 +945,21 @@ static cudaError_t launch_cfg(const TcPlan& P, TcArgs a, cudaStream_t s) {
 //   K <= 896 bytes (int8 d <= 896):               3 stages, 1 A buffer
 template <int MODE>
 static cudaError_t dispatch(const TcPlan& P, const TcArgs& a, cudaStream_t s) {
+  // one-atom rows get their own instance: a wider template would move (and
+  // TMA-zero-fill) a second, all-padding K atom for every A block and B tile
   if (P.kind == TC_TF32) {
+    if (P.katoms == 1) return launch_cfg<TC_TF32, 1, 256, 1, 4, 2, MODE>(P, a, s);
     if (P.katoms <= 2) return launch_cfg<TC_TF32, 1, 256, 2, 4, 2, MODE>(P, a, s);
     if (P.katoms <= 4) return launch_cfg<TC_TF32, 1, 256, 4, 4, 1, MODE>(P, a, s);
     return cudaErrorNotSupported;
   }
   if (P.kind == TC_U8) {
+    if (P.katoms == 1) return launch_cfg<TC_U8, 1, 256, 1, 4, 2, MODE>(P, a, s);
     if (P.katoms <= 2) return launch_cfg<TC_U8, 1, 256, 2, 4, 2, MODE>(P, a, s);
     if (P.katoms <= 7) return launch_cfg<TC_U8, 1, 256, 7, 3, 1, MODE>(P, a, s);
     return cudaErrorNotSupported;
   }
+  if (P.katoms == 1) return launch_cfg<TC_S8, 1, 256, 1, 4, 2, MODE>(P, a, s);
   if (P.katoms <= 2) return launch_cfg<TC_S8, 1, 256, 2, 4, 2, MODE>(P, a, s);
   if (P.katoms <= 7) return launch_cfg<TC_S8, 1, 256, 7, 3, 1, MODE>(P, a, s);
   return cudaErrorNotSupported;
@@ -932,19 +973,20 @@ bool tc_supported(int kind, int katoms) {
 
 // mode: TC_MODE_MEMBER / TC_MODE_PROBE_LDONLY / TC_MODE_PROBE_NOLD on the
 // production configuration for tf32 with K <= 64
-template <int BN, int ST>
+template <int BN, int ST, int KA>
 static cudaError_t probe_cfg(const TcPlan& P, const TcArgs& a, int mode, cudaStream_t s) {
   if (mode == TC_MODE_PROBE_LDONLY)
-    return launch_cfg<TC_TF32, 1, BN, 2, ST, 2, TC_MODE_PROBE_LDONLY>(P, a, s);
+    return launch_cfg<TC_TF32, 1, BN, KA, ST, 2, TC_MODE_PROBE_LDONLY>(P, a, s);
   if (mode == TC_MODE_PROBE_NOLD)
-    return launch_cfg<TC_TF32, 1, BN, 2, ST, 2, TC_MODE_PROBE_NOLD>(P, a, s);
-  return launch_cfg<TC_TF32, 1, BN, 2, ST, 2, TC_MODE_MEMBER>(P, a, s);
+    return launch_cfg<TC_TF32, 1, BN, KA, ST, 2, TC_MODE_PROBE_NOLD>(P, a, s);
+  return launch_cfg<TC_TF32, 1, BN, KA, ST, 2, TC_MODE_MEMBER>(P, a, s);
 }
 // mode + 16 * cfg: cfg 0 = N=256 tiles (2 TMEM buffers), cfg 1 = N=128 (4 buffers)
 cudaError_t launch_tc_probe(const TcPlan& P, const TcArgs& a, int mode, cudaStream_t s) {
   if (P.kind != TC_TF32 || P.katoms > 2) return cudaErrorNotSupported;
-  if ((mode >> 4) == 1) return probe_cfg<128, 8>(P, a, mode & 15, s);
-  return probe_cfg<256, 4>(P, a, mode & 15, s);
+  if ((mode >> 4) == 1) return probe_cfg<128, 8, 2>(P, a, mode & 15, s);
+  if (P.katoms == 1) return probe_cfg<256, 4, 1>(P, a, mode & 15, s);
+  return probe_cfg<256, 4, 2>(P, a, mode & 15, s);
 }
 
 cudaError_t launch_tc_adj(const TcPlan& Pc, const TcArgs& ac, cudaStream_t s, int64_t* launches) {
