@@ -12,7 +12,8 @@
 //               accumulator buffers of RA x BN columns so the epilogue of tile
 //               t overlaps the MMAs of tile t+1.
 //   warp 2      TMEM allocator.
-//   warps 4-7   epilogue: tcgen05.ld 32 columns at a time, per pair one add and
+//   warps 4-11  epilogue (two warpgroups, one half of each tile's columns each):
+//               tcgen05.ld 32 columns at a time, per pair one add and
 //               one max against a per-row / per-column constant ("out for sure"
 //               test); the rare survivors are classified in / band and staged
 //               in shared memory, flushed to global with one atomic per flush.
@@ -252,7 +253,7 @@ constexpr uint32_t make_idesc(int M, int N) {
          ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
-template <int RA, int BN, int KATOMS, int STAGES, int ABUF, bool FOLD>
+template <int RA, int BN, int KATOMS, int STAGES, int ABUF, bool FOLD, bool BRES = false>
 struct Smem {
   static constexpr int A_ATOM = 128 * 128;                 // 128 rows x 128 B
   static constexpr int A_BYTES = RA * KATOMS * A_ATOM;     // one A buffer
@@ -265,7 +266,8 @@ struct Smem {
   // fold tiles (tf32): A ones [128 rows x 32 B], B constants [2 slots][BN rows x 32 B]
   static constexpr int AK_OFF = ABUF * A_BYTES + B_BYTES;
   static constexpr int BK_SLOT = BN * 32;
-  static constexpr int COL_OFF = AK_OFF + (FOLD ? 128 * 32 + 2 * BK_SLOT : 0);
+  static constexpr int NBK = BRES ? STAGES : 2;            // fold constant slots
+  static constexpr int COL_OFF = AK_OFF + (FOLD ? 128 * 32 + NBK * BK_SLOT : 0);
   static constexpr int COL_BYTES = BN * 4;   // int8: per-buffer column constants c_j
   static constexpr int BAR_OFF = COL_OFF + (FOLD ? 0 : NBUF * COL_BYTES);
   static constexpr int NBARS = 2 * STAGES + 2 * ABUF + 3 * NBUF + 5;
@@ -306,7 +308,12 @@ __device__ __noinline__ bool pair_in_fp64(const float* xrows, int xstride, int d
 // ------------------------------------------------------------------ kernel
 constexpr int TC_THREADS = 384;   // warps 0-3 roles, 4-11 epilogue
 
-template <int KIND, int RA, int BN, int KATOMS, int STAGES, int ABUF, int MODE>
+// BRES (B resident): the launch's whole landmark operand (<= STAGES tiles of
+// one K atom) and its fold constants are loaded once per CTA and stay in
+// shared memory; only the point blocks stream.  Without it every work unit
+// re-reads the same B tiles, and 148 SMs reading the same lines at once is
+// bounded by the L2 slices that hold them (measured: C5 cosine, d = 16).
+template <int KIND, int RA, int BN, int KATOMS, int STAGES, int ABUF, int MODE, bool BRES>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     k_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
          const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmO,
@@ -315,7 +322,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   // MMA per tile (ones x {-cb_hi, -cb_mid, -cb_lo}), so the epilogue's test is
   // a plain max over the accumulators
   constexpr bool FOLD = KIND == TC_TF32 && MODE != TC_MODE_GRAM;
-  using S = Smem<RA, BN, KATOMS, STAGES, ABUF, FOLD>;
+  using S = Smem<RA, BN, KATOMS, STAGES, ABUF, FOLD, BRES>;
+  static_assert(!BRES || KATOMS == 1, "resident B: one K atom per tile");
   constexpr int BUFCOLS = RA * BN;
   constexpr int NBUF = 512 / BUFCOLS;   // TMEM accumulator buffers (2 at BN=256, 4 at BN=128)
   static_assert(NBUF >= 2 && NBUF * BUFCOLS <= 512, "TMEM: accumulator buffers must fit 512 columns");
@@ -361,7 +369,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
     for (int b = 0; b < NBUF; ++b) {
       mbar_init(&t_full[b], 1);
-      mbar_init(&t_empty[b], 4);   // the 4 warps of the group that drains buffer b
+      mbar_init(&t_empty[b], 8);   // all 8 epilogue warps drain every buffer
       mbar_init(&c_full[b], 1);
     }
     mbar_init(&bk_full[0], 1);
@@ -420,6 +428,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         mbar_expect_tx(ak_full, 128u * 32u);
         tma_load_2d(sAK, &tmO, ak_full, 0, 0);
       }
+      if constexpr (BRES) {   // the whole (<= STAGES tiles) landmark operand, once
+        if (blockIdx.x < n_units)
+          for (int64_t t = 0; t < n_tiles; ++t) {
+            mbar_expect_tx(&full[t], (uint32_t)(S::B_STAGE + (FOLD ? S::BK_SLOT : 0)));
+            tma_load_2d(sB + t * S::B_STAGE, &tmB, &full[t], 0, (int)(t * BN));
+            if constexpr (FOLD)
+              tma_load_2d(sBK + t * S::BK_SLOT, &tmK, &full[t], 0, (int)(t * BN));
+          }
+      }
       for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x, ++ui) {
         const int64_t mb = u / n_chunks, ch = u % n_chunks;
         const int64_t t0 = ch * tiles_per_chunk, t1 = min(n_tiles, t0 + tiles_per_chunk);
@@ -442,7 +459,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             for (int ka = 0; ka < KATOMS; ++ka)
               tma_prefetch_2d(&tmA, ka * ATOM_ELEMS, (int)((un / n_chunks) * RA * 128 + r * 128));
         }
-        for (int64_t t = t0; t < t1; ++t) {
+        for (int64_t t = t0; t < t1 && !BRES; ++t) {
           for (int ka = 0; ka < KATOMS; ++ka) {
             mbar_wait(&empty[stage], phase ^ 1u);
             mbar_expect_tx(&full[stage], (uint32_t)S::B_STAGE);
@@ -502,7 +519,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           const int64_t left = n_cols - t * BN;
           const uint32_t nt = left >= BN ? (uint32_t)BN : (uint32_t)((left + 31) / 32 * 32);
           const uint32_t idesc = (IDESC & ~(0x3Fu << 17)) | ((nt >> 3) << 17);
-          for (int ka = 0; ka < KATOMS; ++ka) {
+          if constexpr (BRES) {
+            if (ui == 0) {   // first unit: the resident tile has landed
+              mbar_wait(&full[t], 0u);
+              fence_after();
+            }
+            const uint32_t bbase = su32(sB + t * S::B_STAGE);
+            const uint32_t abase = su32(sAb);
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks)
+              if (ks < ksteps)
+                mma<KIND>(dcol, sdesc(abase + ks * 32), sdesc(bbase + ks * 32), idesc,
+                          ks != 0 ? 1u : 0u);
+            if constexpr (FOLD)
+              mma<KIND>(dcol, sdesc32(su32(sAK)), sdesc32(su32(sBK + t * S::BK_SLOT)), idesc, 1u);
+          }
+          for (int ka = 0; ka < KATOMS && !BRES; ++ka) {
             mbar_wait(&full[stage], phase);
             fence_after();
             const uint32_t bbase = su32(sB + stage * S::B_STAGE);
@@ -522,7 +554,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               phase ^= 1u;
             }
           }
-          if constexpr (FOLD) {   // acc' = x.l - cb_j: ones x {-cb_hi, -cb_mid, -cb_lo}
+          if constexpr (FOLD && !BRES) {   // acc' = x.l - cb_j: ones x {-cb_hi, -cb_mid, -cb_lo}
             const int sl = (int)(tk & 1);
             mbar_wait(&bk_full[sl], (uint32_t)((tk >> 1) & 1));
             fence_after();
@@ -539,8 +571,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       TC_STAMP(6);
     }
   } else if (warp >= 4) {
-    // ---------------- epilogue: warps 4-7 drain TMEM buffer 0, warps 8-11
-    // buffer 1 (tiles alternate buffers), warp w reads TMEM lanes 32*(w%4)..
+    // ---------------- epilogue: warps 4-7 take the first half of every tile's
+    // columns, warps 8-11 the second half; warp w reads TMEM lanes 32*(w%4)..
     const int ew = warp - 4, grp = ew >> 2, q = warp & 3;
     unsigned long long* kb = kbuf + ew * S::KW;
     unsigned long long* bb = bbuf + ew * S::BW;
@@ -646,9 +678,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
       load_rows(u + gridDim.x);
       for (int64_t t = t0; t < t1; ++t, ++tcount) {
-        if ((int)(tcount & 1) != grp) continue;      // the two groups alternate tiles
+        // both groups drain every tile: group g takes its half of the columns
         const int buf = (int)(tcount % NBUF);
-        const uint32_t ph = (phase >> buf) & 1u;    // this group's parity for buffer buf
+        const uint32_t ph = (phase >> buf) & 1u;    // parity of buffer buf's next fill
         mbar_wait(&t_full[buf], ph);
         if (tcount < 2 && q == 0 && lane == 0) TC_STAMP(7 + grp);
         if constexpr ((MODE == TC_MODE_MEMBER || MODE == TC_MODE_ADJ) && !FOLD)
@@ -661,9 +693,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * BUFCOLS);
         constexpr int NCH = RA * (BN / 32);
         uint32_t va[32], vb[32];
+        // chunks the (possibly narrower) MMA of this tile wrote, this group's half
+        const int64_t left = n_cols - t * BN;
+        const int nch = RA == 1 && left < BN ? (int)((left + 31) / 32) : NCH;
+        const int cbeg = grp * (NCH / 2), cend = min(nch, (grp + 1) * (NCH / 2));
+        auto caddr = [&](int c) {
+          return trow + (uint32_t)((c / (BN / 32)) * BN + (c % (BN / 32)) * 32);
+        };
         if constexpr (MODE != TC_MODE_PROBE_NOLD) {
-          tmem_ld32_nowait(trow, va);
-          tmem_wait(va);
+          if (cbeg < cend) {
+            tmem_ld32_nowait(caddr(cbeg), va);
+            tmem_wait(va);
+          }
         }
         auto chunk = [&](int c, uint32_t (&v)[32]) {
           const int r = RA == 1 ? 0 : c / (BN / 32), cc = RA == 1 ? c : c % (BN / 32);
@@ -810,24 +851,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           }
         };
         if constexpr (MODE != TC_MODE_PROBE_NOLD) {
-          // chunks the (possibly narrower) MMA of this tile wrote
-          const int64_t left = n_cols - t * BN;
-          const int nch = RA == 1 && left < BN ? (int)((left + 31) / 32) : NCH;
 #pragma unroll 1
-          for (int c = 0; c < nch; c += 2) {
-            if (c + 1 < nch) {
-              tmem_ld32_nowait(trow + (uint32_t)(((c + 1) / (BN / 32)) * BN + ((c + 1) % (BN / 32)) * 32), vb);
+          for (int c = cbeg; c < cend; c += 2) {
+            if (c + 1 < cend) {
+              tmem_ld32_nowait(caddr(c + 1), vb);
               reg_fence(va);
             }
             chunk(c, va);
-            if (c + 1 < nch) {
+            if (c + 1 < cend) {
               tmem_wait(vb);
-              if (c + 2 < nch) {
-                tmem_ld32_nowait(trow + (uint32_t)(((c + 2) / (BN / 32)) * BN + ((c + 2) % (BN / 32)) * 32), va);
+              if (c + 2 < cend) {
+                tmem_ld32_nowait(caddr(c + 2), va);
                 reg_fence(vb);
               }
               chunk(c + 1, vb);
-              if (c + 2 < nch) tmem_wait(va);
+              if (c + 2 < cend) tmem_wait(va);
             }
           }
         }
@@ -899,10 +937,10 @@ static cudaError_t make_tmap8(CUtensorMap* tm, const void* base, int64_t rows, i
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
-template <int KIND, int RA, int BN, int KATOMS, int STAGES, int ABUF, int MODE>
+template <int KIND, int RA, int BN, int KATOMS, int STAGES, int ABUF, int MODE, bool BRES = false>
 static cudaError_t launch_cfg(const TcPlan& P, TcArgs a, cudaStream_t s) {
   constexpr bool FOLD = KIND == TC_TF32 && MODE != TC_MODE_GRAM;
-  using S = Smem<RA, BN, KATOMS, STAGES, ABUF, FOLD>;
+  using S = Smem<RA, BN, KATOMS, STAGES, ABUF, FOLD, BRES>;
   static_assert(S::TOTAL <= 232448, "shared memory");
   CUtensorMap tA, tB, tK, tO;
   cudaError_t e = make_tmap(&tA, P.xop, KIND, P.k_elems, P.n_rows, P.row_bytes, 128);
@@ -919,7 +957,7 @@ static cudaError_t launch_cfg(const TcPlan& P, TcArgs a, cudaStream_t s) {
     tK = tB;
     tO = tB;
   }
-  auto kern = k_tc<KIND, RA, BN, KATOMS, STAGES, ABUF, MODE>;
+  auto kern = k_tc<KIND, RA, BN, KATOMS, STAGES, ABUF, MODE, BRES>;
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::TOTAL);
   if (e != cudaSuccess) return e;
   a.n_mblk = (P.n_rows + RA * 128 - 1) / (RA * 128);
@@ -943,11 +981,21 @@ static cudaError_t launch_cfg(const TcPlan& P, TcArgs a, cudaStream_t s) {
 //   K <= 256 bytes (tf32 d <= 64, int8 d <= 256): 4 stages, 2 A buffers
 //   K <= 512 bytes (tf32 d <= 128):               4 stages, 1 A buffer
 //   K <= 896 bytes (int8 d <= 896):               3 stages, 1 A buffer
+// resident B applies when every CTA's units share one column chunk (enough
+// point blocks: n_chunks = 1 for any column count) and the launch's columns
+// fit the stage ring (the fused greedy tile: <= 1024 columns)
+static bool bres_ok(const TcPlan& P, const TcArgs& a, int stages) {
+  const int64_t n_mblk = (P.n_rows + 127) / 128;
+  return n_mblk >= 4 * (int64_t)P.num_sms && (a.L + 255) / 256 <= stages;
+}
+
 template <int MODE>
 static cudaError_t dispatch(const TcPlan& P, const TcArgs& a, cudaStream_t s) {
   // one-atom rows get their own instance: a wider template would move (and
   // TMA-zero-fill) a second, all-padding K atom for every A block and B tile
   if (P.kind == TC_TF32) {
+    if (P.katoms == 1 && bres_ok(P, a, 4))
+      return launch_cfg<TC_TF32, 1, 256, 1, 4, 3, MODE, true>(P, a, s);
     if (P.katoms == 1) return launch_cfg<TC_TF32, 1, 256, 1, 4, 2, MODE>(P, a, s);
     if (P.katoms <= 2) return launch_cfg<TC_TF32, 1, 256, 2, 4, 2, MODE>(P, a, s);
     if (P.katoms <= 4) return launch_cfg<TC_TF32, 1, 256, 4, 4, 1, MODE>(P, a, s);
@@ -984,6 +1032,15 @@ static cudaError_t probe_cfg(const TcPlan& P, const TcArgs& a, int mode, cudaStr
 // mode + 16 * cfg: cfg 0 = N=256 tiles (2 TMEM buffers), cfg 1 = N=128 (4 buffers)
 cudaError_t launch_tc_probe(const TcPlan& P, const TcArgs& a, int mode, cudaStream_t s) {
   if (P.kind != TC_TF32 || P.katoms > 2) return cudaErrorNotSupported;
+  if (mode & 32) {
+    if (P.katoms != 1 || !bres_ok(P, a, 4)) return cudaErrorNotSupported;
+    const int m = mode & 15;
+    if (m == TC_MODE_PROBE_LDONLY)
+      return launch_cfg<TC_TF32, 1, 256, 1, 4, 3, TC_MODE_PROBE_LDONLY, true>(P, a, s);
+    if (m == TC_MODE_PROBE_NOLD)
+      return launch_cfg<TC_TF32, 1, 256, 1, 4, 3, TC_MODE_PROBE_NOLD, true>(P, a, s);
+    return launch_cfg<TC_TF32, 1, 256, 1, 4, 3, TC_MODE_MEMBER, true>(P, a, s);
+  }
   if ((mode >> 4) == 1) return probe_cfg<128, 8, 2>(P, a, mode & 15, s);
   if (P.katoms == 1) return probe_cfg<256, 4, 1>(P, a, mode & 15, s);
   return probe_cfg<256, 4, 2>(P, a, mode & 15, s);
