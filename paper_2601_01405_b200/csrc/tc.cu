@@ -204,6 +204,34 @@ __device__ __forceinline__ void reg_fence(uint32_t (&v)[32]) {
                  "+r"(v[24]), "+r"(v[25]), "+r"(v[26]), "+r"(v[27]), "+r"(v[28]), "+r"(v[29]),
                  "+r"(v[30]), "+r"(v[31]));
 }
+// 64 consecutive columns of the warp's 32 TMEM lanes in one load
+__device__ __forceinline__ void tmem_ld64_nowait(uint32_t taddr, uint32_t (&v)[64]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x64.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32, %33, %34, %35, %36, %37, %38, %39, %40, %41, %42, %43, %44, %45, %46, %47, %48, %49, %50, %51, %52, %53, %54, %55, %56, %57, %58, %59, %60, %61, %62, %63}, [%64];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+        "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31]),
+        "=r"(v[32]), "=r"(v[33]), "=r"(v[34]), "=r"(v[35]), "=r"(v[36]), "=r"(v[37]), "=r"(v[38]), "=r"(v[39]),
+        "=r"(v[40]), "=r"(v[41]), "=r"(v[42]), "=r"(v[43]), "=r"(v[44]), "=r"(v[45]), "=r"(v[46]), "=r"(v[47]),
+        "=r"(v[48]), "=r"(v[49]), "=r"(v[50]), "=r"(v[51]), "=r"(v[52]), "=r"(v[53]), "=r"(v[54]), "=r"(v[55]),
+        "=r"(v[56]), "=r"(v[57]), "=r"(v[58]), "=r"(v[59]), "=r"(v[60]), "=r"(v[61]), "=r"(v[62]), "=r"(v[63])
+      : "r"(taddr)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait64(uint32_t (&v)[64]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+      : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7]),
+        "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]), "+r"(v[12]), "+r"(v[13]), "+r"(v[14]), "+r"(v[15]),
+        "+r"(v[16]), "+r"(v[17]), "+r"(v[18]), "+r"(v[19]), "+r"(v[20]), "+r"(v[21]), "+r"(v[22]), "+r"(v[23]),
+        "+r"(v[24]), "+r"(v[25]), "+r"(v[26]), "+r"(v[27]), "+r"(v[28]), "+r"(v[29]), "+r"(v[30]), "+r"(v[31]),
+        "+r"(v[32]), "+r"(v[33]), "+r"(v[34]), "+r"(v[35]), "+r"(v[36]), "+r"(v[37]), "+r"(v[38]), "+r"(v[39]),
+        "+r"(v[40]), "+r"(v[41]), "+r"(v[42]), "+r"(v[43]), "+r"(v[44]), "+r"(v[45]), "+r"(v[46]), "+r"(v[47]),
+        "+r"(v[48]), "+r"(v[49]), "+r"(v[50]), "+r"(v[51]), "+r"(v[52]), "+r"(v[53]), "+r"(v[54]), "+r"(v[55]),
+        "+r"(v[56]), "+r"(v[57]), "+r"(v[58]), "+r"(v[59]), "+r"(v[60]), "+r"(v[61]), "+r"(v[62]), "+r"(v[63])
+      :
+      : "memory");
+}
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
@@ -692,7 +720,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         // flight while this one is classified (va / vb ping-pong)
         const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * BUFCOLS);
         constexpr int NCH = RA * (BN / 32);
-        uint32_t va[32], vb[32];
+        uint32_t vv[64];   // two chunks per TMEM load
         // chunks the (possibly narrower) MMA of this tile wrote, this group's half
         const int64_t left = n_cols - t * BN;
         const int nch = RA == 1 && left < BN ? (int)((left + 31) / 32) : NCH;
@@ -700,12 +728,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         auto caddr = [&](int c) {
           return trow + (uint32_t)((c / (BN / 32)) * BN + (c % (BN / 32)) * 32);
         };
-        if constexpr (MODE != TC_MODE_PROBE_NOLD) {
-          if (cbeg < cend) {
-            tmem_ld32_nowait(caddr(cbeg), va);
-            tmem_wait(va);
-          }
-        }
         auto chunk = [&](int c, uint32_t (&v)[32]) {
           const int r = RA == 1 ? 0 : c / (BN / 32), cc = RA == 1 ? c : c % (BN / 32);
           {
@@ -851,22 +873,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           }
         };
         if constexpr (MODE != TC_MODE_PROBE_NOLD) {
+          // 64 columns per load (a past-the-end half is read and discarded)
 #pragma unroll 1
           for (int c = cbeg; c < cend; c += 2) {
-            if (c + 1 < cend) {
-              tmem_ld32_nowait(caddr(c + 1), vb);
-              reg_fence(va);
-            }
-            chunk(c, va);
-            if (c + 1 < cend) {
-              tmem_wait(vb);
-              if (c + 2 < cend) {
-                tmem_ld32_nowait(caddr(c + 2), va);
-                reg_fence(vb);
-              }
-              chunk(c + 1, vb);
-              if (c + 2 < cend) tmem_wait(va);
-            }
+            tmem_ld64_nowait(caddr(c), vv);
+            tmem_wait64(vv);
+            chunk(c, *reinterpret_cast<uint32_t(*)[32]>(&vv[0]));
+            if (c + 1 < cend) chunk(c + 1, *reinterpret_cast<uint32_t(*)[32]>(&vv[32]));
           }
         }
         fence_before();

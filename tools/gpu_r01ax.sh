@@ -1,5 +1,5 @@
 #!/bin/bash
-# both epilogue groups on every tile (column halves)
+# predicate-chain fast path (TMEM prefetch not held back by register reuse)
 timeout 600 python -m pytest tests/test_gpu_tensor.py tests/test_gpu_parity.py tests/test_gpu_next.py -x -q -m gpu 2>&1 | tail -2
 python tools/tc_probe_c2.py 2>&1 | grep "mode=\(35\|34\|32\|0\):"
 for w in c2 c5_cos c3_e8 c4; do
