@@ -121,6 +121,7 @@ typedef enum bm_select {
 
 /* bm_options.flags */
 #define BM_FLAG_NO_L1_PREFILTER 1   /* L1: score every pair in fp32 (no 8-bit SAD prefilter) */
+#define BM_FLAG_NO_EDGE_TRIANGLE 2  /* L > 4096: build edges by sort + unique, not the bit triangle */
 
 /*
  * Result of one cover construction.  All arrays are owned by the library and

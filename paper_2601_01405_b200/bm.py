@@ -25,6 +25,7 @@ AGG = {"mean": 0, "median": 1, "trimmed": 2, "min": 3, "max": 4, "mode": 5, "var
        "range": 7}
 PATH = {"auto": 0, "cuda_core": 1, "tensor": 2}
 FLAG_NO_L1_PREFILTER = 1
+FLAG_NO_EDGE_TRIANGLE = 2
 STEPS = ("prep", "greedy", "member", "csr", "edges", "total", "member_kernel", "select")
 
 EXPORTED = ("bm_cover_build", "bm_cover_build_ex", "bm_cover_build_host", "bm_free",

@@ -276,6 +276,15 @@ int64_t tc_row_bytes(int d, int esz) {
   return (((int64_t)d * esz + 127) / 128) * 128;
 }
 
+// D: the bit-triangle edge path when it fits min(8 GiB, free / 4) of HBM
+bool use_tri_bitmap(int64_t L, int flags) {
+  if (flags & BM_FLAG_NO_EDGE_TRIANGLE) return false;
+  const double bytes = 4.0 * (double)bm::tri_bitmap_words(L);
+  size_t fr = 0, tot = 0;
+  if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) return false;
+  return bytes <= 8.0 * (1ull << 30) && bytes <= 0.25 * (double)fr;
+}
+
 double tc_band_c2(int ksteps) {
   const double ut = ldexp(1.0, -11);
   const double K = 8.0 * ksteps + 3.0;
@@ -946,6 +955,30 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
     E = h2[1];
     pool.free_now(bits);
     pool.free_now(etemp);
+  } else if (L >= 2 && use_tri_bitmap(L, o.flags)) {
+    // strictly-upper bit triangle: no pair buffer, no sort (edges.cu)
+    uint32_t* bits = nullptr;
+    int64_t *rcnt = nullptr, *roff = nullptr;
+    void* stemp = nullptr;
+    TRY(pool.alloc(&bits, (size_t)tri_bitmap_words(L)));
+    TRY(pool.alloc(&rcnt, (size_t)L));
+    TRY(pool.alloc(&roff, (size_t)L));
+    TRY(pool.alloc((uint8_t**)&stemp, scan_temp_bytes(L)));
+    CK(launch_tri_bits(pt_ptr, pt_lm, n, L, bits, (unsigned long long*)ptot, s, &launches));
+    CK(launch_tri_rowcount(bits, L, rcnt, s, &launches));
+    CK(exclusive_scan_i64(rcnt, roff, L, stemp, ptot + 1, s, &launches));
+    int64_t h2[2];
+    CK(cudaMemcpyAsync(h2, ptot, sizeof h2, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    NP = h2[0];
+    E = h2[1];
+    TRY(pool.alloc(&edges, (size_t)(2 * E > 0 ? 2 * E : 1)));
+    if (E > 0) CK(launch_tri_emit(bits, L, roff, edges, s, &launches));
+    tr("edges: triangle");
+    pool.free_now(bits);
+    pool.free_now(rcnt);
+    pool.free_now(roff);
+    pool.free_now(stemp);
   } else if (L >= 2) {
     int64_t *pcnt = nullptr, *poff = nullptr;
     void* stemp = nullptr;

@@ -336,4 +336,135 @@ cudaError_t launch_unique_compact(const unsigned long long* keys, int64_t m, int
                     m, lbits, edges, total, state, ticket, 1u);
 }
 
+// ------------------------------------------------- triangular bitmap path
+// 4096 < L with the strictly-upper L x L bit triangle affordable (C5: L ~ 1e5
+// to 3e5 -> 1-6 GB of HBM): pair (a, b), a < b, is bit b of row a; row a
+// stores only the words from (a + 1) / 32 on, so the rows need no pair
+// buffer, no sort and no dedupe, and a row-major walk emits the edges already
+// in (a, b) order.  Word offset of row a: a W - sum_{x=1..a} floor(x / 32).
+__host__ __device__ __forceinline__ int64_t tri_offset(int64_t a, int64_t W) {
+  const int64_t q = a >> 5, r = a & 31;
+  return a * W - (32 * q * (q - 1) / 2 + q * (r + 1));
+}
+
+int64_t tri_bitmap_words(int64_t L) { return tri_offset(L, (L + 31) / 32); }
+
+// warp per point (lanes over the partner landmarks), as the keys path's pair
+// emission: a point in many balls does not serialise on one thread
+__global__ void k_tri_bits(const int64_t* __restrict__ pt_ptr, const int32_t* __restrict__ pt_lm,
+                           int64_t n, int64_t W, uint32_t* __restrict__ bits,
+                           unsigned long long* __restrict__ npairs) {
+  pdl_wait();
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  unsigned long long mine = 0ull;
+  for (int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < n; p += nwarps) {
+    const int64_t b = pt_ptr[p], t = pt_ptr[p + 1] - b;
+    if (t < 2) continue;
+    if (lane == 0) mine += (unsigned long long)(t * (t - 1) / 2);
+    for (int64_t i = 0; i + 1 < t; ++i) {
+      const int64_t a = pt_lm[b + i];
+      uint32_t* row = bits + tri_offset(a, W) - ((a + 1) >> 5);
+      for (int64_t c = i + 1 + lane; c < t; c += 32) {
+        const int32_t j = pt_lm[b + c];
+        atomicOr(row + (j >> 5), 1u << (j & 31));
+      }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(FME, mine, o);
+  if (lane == 0 && mine) atomicAdd(npairs, mine);
+}
+
+// warp per row: number of set bits (edges leaving landmark a)
+__global__ void k_tri_rowcount(const uint32_t* __restrict__ bits, int64_t L, int64_t W,
+                               int64_t* __restrict__ cnt) {
+  pdl_wait();
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t a = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; a < L; a += nwarps) {
+    const uint32_t* row = bits + tri_offset(a, W);
+    const int64_t nw = W - ((a + 1) >> 5);
+    int64_t c = 0;
+    for (int64_t k = lane; k < nw; k += 32) c += __popc(__ldcs(row + k));
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(FME, c, o);
+    if (lane == 0) cnt[a] = c;
+  }
+}
+
+// warp per row: edges (a, b) at off[a] onwards, b ascending
+__global__ void k_tri_emit(const uint32_t* __restrict__ bits, int64_t L, int64_t W,
+                           const int64_t* __restrict__ off, int32_t* __restrict__ edges) {
+  pdl_wait();
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t a = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; a < L; a += nwarps) {
+    const int64_t c0 = (a + 1) >> 5;
+    const uint32_t* row = bits + tri_offset(a, W);
+    const int64_t nw = W - c0;
+    int64_t pos = off[a];
+    for (int64_t k0 = 0; k0 < nw; k0 += 32) {
+      const int64_t k = k0 + lane;
+      uint32_t v = k < nw ? __ldcs(row + k) : 0u;
+      const uint32_t c = __popc(v);
+      uint32_t incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(FME, incl, o);
+        if (lane >= o) incl += t;
+      }
+      int64_t q = pos + incl - c;
+      const int32_t jb = (int32_t)((c0 + k) * 32);
+      while (v) {
+        const int bit = __ffs(v) - 1;
+        v &= v - 1u;
+        edges[2 * q] = (int32_t)a;
+        edges[2 * q + 1] = jb + bit;
+        ++q;
+      }
+      pos += __shfl_sync(FME, incl, 31);
+    }
+  }
+}
+
+static int64_t warp_grid(int64_t rows) {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t want = (rows + 7) / 8;   // 8 warps per 256-thread CTA
+  const int64_t cap = (int64_t)sms * 8;
+  return want < cap ? (want > 0 ? want : 1) : cap;
+}
+
+cudaError_t launch_tri_bits(const int64_t* pt_ptr, const int32_t* pt_lm, int64_t n, int64_t L,
+                            uint32_t* bits, unsigned long long* npairs, cudaStream_t s,
+                            int64_t* launches) {
+  const int64_t W = (L + 31) / 32;
+  cudaError_t e = cudaMemsetAsync(bits, 0, sizeof(uint32_t) * tri_bitmap_words(L), s);
+  if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(npairs, 0, sizeof(unsigned long long), s);
+  if (e != cudaSuccess) return e;
+  ++*launches;
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int64_t g = (n + 7) / 8;
+  if (g > (int64_t)sms * 16) g = (int64_t)sms * 16;
+  return launch_pdl(k_tri_bits, dim3((unsigned)(g > 0 ? g : 1)), dim3(256), 0, s, pt_ptr, pt_lm,
+                    n, W, bits, npairs);
+}
+
+cudaError_t launch_tri_rowcount(const uint32_t* bits, int64_t L, int64_t* cnt, cudaStream_t s,
+                                int64_t* launches) {
+  ++*launches;
+  return launch_pdl(k_tri_rowcount, dim3((unsigned)warp_grid(L)), dim3(256), 0, s, bits, L,
+                    (L + 31) / 32, cnt);
+}
+
+cudaError_t launch_tri_emit(const uint32_t* bits, int64_t L, const int64_t* off, int32_t* edges,
+                            cudaStream_t s, int64_t* launches) {
+  ++*launches;
+  return launch_pdl(k_tri_emit, dim3((unsigned)warp_grid(L)), dim3(256), 0, s, bits, L,
+                    (L + 31) / 32, off, edges);
+}
+
 }  // namespace bm

@@ -251,6 +251,15 @@ cudaError_t csr_from_keys_bitmap(const unsigned long long* keys, int64_t m, int6
 // edges.cu: bitmap path for L <= kEdgeBitmapMaxL, keys path (sort + unique) above
 constexpr int64_t kEdgeBitmapMaxL = 4096;
 int64_t edge_bitmap_words(int64_t L);
+// triangular bit matrix for 4096 < L (bytes = 4 * tri_bitmap_words(L))
+int64_t tri_bitmap_words(int64_t L);
+cudaError_t launch_tri_bits(const int64_t* pt_ptr, const int32_t* pt_lm, int64_t n, int64_t L,
+                            uint32_t* bits, unsigned long long* npairs, cudaStream_t s,
+                            int64_t* launches);
+cudaError_t launch_tri_rowcount(const uint32_t* bits, int64_t L, int64_t* cnt, cudaStream_t s,
+                                int64_t* launches);
+cudaError_t launch_tri_emit(const uint32_t* bits, int64_t L, const int64_t* off, int32_t* edges,
+                            cudaStream_t s, int64_t* launches);
 size_t edge_lb_temp_bytes(int64_t items);
 cudaError_t launch_edge_bits(const int64_t* pt_ptr, const int32_t* pt_lm, int64_t n, int64_t L,
                              uint32_t* bits, unsigned long long* npairs, cudaStream_t s,

@@ -267,3 +267,20 @@ def test_l1_prefilter_equivalence(bm, seed):
     for k in na:
         assert np.array_equal(na[k], nb[k]), k
     compare(X, "l1", eps, a, float_path=True)
+
+
+@pytest.mark.parametrize("metric,eps", [("l2", 0.006), ("l1", 0.008), ("cos", 4e-5)])
+def test_edges_triangle_path(bm, metric, eps):
+    """L > 4096: the strictly-upper bit triangle (edges.cu) against the
+    sort + unique keys path and the oracle."""
+    from paper_2601_01405_b200 import bm as B
+    rng = np.random.default_rng(17)
+    X = rng.random((12000, 3 if metric == "cos" else 2)).astype(np.float32)
+    t = torch.from_numpy(X).cuda()
+    a = bm.cover_build(t, metric, eps)
+    b = bm.cover_build(t, metric, eps, flags=B.FLAG_NO_EDGE_TRIANGLE)
+    assert a.L > 4096 and a.E > 100, (a.L, a.E)
+    na, nb = a.numpy(), b.numpy()
+    for k in na:
+        assert np.array_equal(na[k], nb[k]), k
+    compare(X, metric, eps, a, float_path=True)
