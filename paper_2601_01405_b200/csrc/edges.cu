@@ -49,7 +49,7 @@ __global__ void k_edge_bits(const int64_t* __restrict__ pt_ptr, const int32_t* _
 
 // Row-major walk of the bit matrix: CTA tile = 256 threads x 4 consecutive
 // words each; edges written in (i, j) order.
-constexpr int EB_NT = 256, EB_WPT = 4, EB_TILE = EB_NT * EB_WPT;
+constexpr int EB_NT = 256, EB_WPT = 16, EB_TILE = EB_NT * EB_WPT;
 
 __global__ void __launch_bounds__(EB_NT) k_bits_compact(const uint32_t* __restrict__ bits,
                                                        int64_t nwords, int W,
@@ -67,11 +67,21 @@ __global__ void __launch_bounds__(EB_NT) k_bits_compact(const uint32_t* __restri
   const int64_t w0 = tile * EB_TILE + (int64_t)threadIdx.x * EB_WPT;
   uint32_t wv[EB_WPT];
   uint32_t cnt = 0;
+  if (w0 + EB_WPT <= nwords) {   // 16-byte loads (w0 is a multiple of 16 words)
 #pragma unroll
-  for (int k = 0; k < EB_WPT; ++k) {
-    wv[k] = w0 + k < nwords ? bits[w0 + k] : 0u;
-    cnt += __popc(wv[k]);
+    for (int k = 0; k < EB_WPT; k += 4) {
+      const uint4 q = *reinterpret_cast<const uint4*>(bits + w0 + k);
+      wv[k] = q.x;
+      wv[k + 1] = q.y;
+      wv[k + 2] = q.z;
+      wv[k + 3] = q.w;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < EB_WPT; ++k) wv[k] = w0 + k < nwords ? bits[w0 + k] : 0u;
   }
+#pragma unroll
+  for (int k = 0; k < EB_WPT; ++k) cnt += __popc(wv[k]);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   uint32_t incl = cnt;
 #pragma unroll
@@ -204,11 +214,21 @@ __global__ void __launch_bounds__(EB_NT) k_bits_csr(const uint32_t* __restrict__
   const int64_t w0 = tile * EB_TILE + (int64_t)threadIdx.x * EB_WPT;
   uint32_t wv[EB_WPT];
   uint32_t cnt = 0;
+  if (w0 + EB_WPT <= nwords) {   // 16-byte loads (w0 is a multiple of 16 words)
 #pragma unroll
-  for (int k = 0; k < EB_WPT; ++k) {
-    wv[k] = w0 + k < nwords ? bits[w0 + k] : 0u;
-    cnt += __popc(wv[k]);
+    for (int k = 0; k < EB_WPT; k += 4) {
+      const uint4 q = *reinterpret_cast<const uint4*>(bits + w0 + k);
+      wv[k] = q.x;
+      wv[k + 1] = q.y;
+      wv[k + 2] = q.z;
+      wv[k + 3] = q.w;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < EB_WPT; ++k) wv[k] = w0 + k < nwords ? bits[w0 + k] : 0u;
   }
+#pragma unroll
+  for (int k = 0; k < EB_WPT; ++k) cnt += __popc(wv[k]);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   uint32_t incl = cnt;
 #pragma unroll
@@ -247,8 +267,10 @@ __global__ void __launch_bounds__(EB_NT) k_bits_csr(const uint32_t* __restrict__
 }
 
 // ---------------------------------------------------------------- host side
+// the landmark-major matrix starts 16-byte aligned (the compaction loads 4 words at a time)
+static int64_t csr_pm_words(int64_t n, int64_t L) { return (n * ((L + 31) / 32) + 3) & ~int64_t(3); }
 int64_t csr_bitmap_words(int64_t n, int64_t L) {
-  return n * ((L + 31) / 32) + L * ((n + 31) / 32);
+  return csr_pm_words(n, L) + L * ((n + 31) / 32);
 }
 
 cudaError_t csr_from_keys_bitmap(const unsigned long long* keys, int64_t m, int64_t n, int64_t L,
@@ -257,7 +279,7 @@ cudaError_t csr_from_keys_bitmap(const unsigned long long* keys, int64_t m, int6
                                  int64_t* launches) {
   const int Wp = (int)((L + 31) / 32), Wl = (int)((n + 31) / 32);
   uint32_t* pb = bits;
-  uint32_t* lb = bits + n * (int64_t)Wp;
+  uint32_t* lb = bits + csr_pm_words(n, L);
   cudaError_t e = cudaMemsetAsync(bits, 0, sizeof(uint32_t) * csr_bitmap_words(n, L), s);
   if (e != cudaSuccess) return e;
   int64_t g = (m + 255) / 256;

@@ -1,0 +1,8 @@
+#!/bin/bash
+# predicate-chain fast path (TMEM prefetch not held back by register reuse)
+timeout 600 python -m pytest tests -x -q -m gpu 2>&1 | tail -2
+python tools/tc_probe_c2.py 2>&1 | grep "mode=\(35\|34\|32\|0\):"
+for w in c2 c5_cos c3_e8 c4; do
+  timeout 300 python bench.py --workload $w 2>/dev/null | tail -1 > gpurun_out/bc_$w.json
+  python -c "import json;d=json.load(open('gpurun_out/bc_$w.json'));print('$w', round(d['ms_per_step'],4), d['step_ms_stats'], d['roofline']['frac'], d['roofline'].get('kernel_ms'), d['breakdown_ms'])"
+done
