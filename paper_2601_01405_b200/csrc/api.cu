@@ -450,6 +450,22 @@ bm_status membership_full(Pool& pool, int kind, const bm::PairArgs& base, bm::tc
   return BM_OK;
 }
 
+// Pinned host mailbox for the build's small device->host readbacks: a copy
+// into pageable memory blocks the host until the stream reaches it, so two
+// such copies cost two round trips; into pinned memory they are queued and one
+// stream synchronisation covers them all.
+struct Mailbox {
+  int32_t hc[8];        // the greedy loop's counters (n_unc ping-pong, L, dL)
+  bm::DevStats hs;      // statistics at the loop's last check
+  bm::DevStats hs_end;  // statistics at the end of the build
+  int64_t pe[2];        // edges: P (witnessed pairs), E
+};
+static Mailbox* mailbox() {
+  static thread_local Mailbox* mb = nullptr;
+  if (!mb && cudaMallocHost((void**)&mb, sizeof(Mailbox)) != cudaSuccess) mb = nullptr;
+  return mb;
+}
+
 bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, bm_metric metric,
                      double eps, cudaStream_t s, const bm_options* opts, bool host_in,
                      bm_cover** out) {
@@ -517,6 +533,8 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
                    dtype == BM_F32 ? 512 : 896);
 
   int64_t launches = 0;
+  Mailbox* mb = mailbox();
+  if (!mb) return set_err(BM_ENOMEM, "pinned host mailbox allocation failed");
   Pool pool(s);
   Timer tm(o.timing != 0, s);
   Trace tr(s);
@@ -841,26 +859,30 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
       CK(launch_compact_unc(covered, uncb[cur], cnt + cur, T, uncb[nxt], cnt + nxt, cstate,
                             cnt + 4, (uint32_t)(tile + 1), n, s, &launches));
     }
-    int32_t hc[4];
-    CK(cudaMemcpyAsync(hc, cnt, sizeof hc, cudaMemcpyDeviceToHost, s));
+    // one round trip: the counters and the statistics together
+    CK(cudaMemcpyAsync(mb->hc, cnt, sizeof(int32_t) * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&mb->hs, stats, sizeof(DevStats), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     if (!nonfinite_checked) {
-      int nf = 0;
-      CK(cudaMemcpy(&nf, &stats->nonfinite, sizeof nf, cudaMemcpyDeviceToHost));
-      if (nf) return set_err(BM_EINVAL, "points contain a non-finite coordinate");
+      if (mb->hs.nonfinite) return set_err(BM_EINVAL, "points contain a non-finite coordinate");
       nonfinite_checked = 1;
     }
-    if (hc[tile & 1] == 0) break;
+    if (mb->hc[tile & 1] == 0) break;
     if (batch < 64) batch *= 2;
   }
   tm.mark(2);
   tr("greedy+membership loop");
 
   DevStats hs{};
-  CK(cudaMemcpyAsync(&hs, stats, sizeof hs, cudaMemcpyDeviceToHost, s));
   int32_t hL = 0;
-  CK(cudaMemcpyAsync(&hL, cnt + 2, sizeof hL, cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
+  if (fps) {
+    CK(cudaMemcpyAsync(&mb->hs, stats, sizeof(DevStats), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(mb->hc, cnt, sizeof(int32_t) * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+  }
+  // (greedy: the loop's last check read both after all of its work)
+  hs = mb->hs;
+  hL = mb->hc[2];
   const int64_t L = hL;
   pool.free_now(unc0);
   pool.free_now(unc1);
@@ -936,6 +958,7 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
   int64_t E = 0;
   int32_t* edges = nullptr;
   int64_t* ptot = nullptr;
+  bool pe_pending = false;
   TRY(pool.alloc(&ptot, 2));
   if (L >= 2 && L <= kEdgeBitmapMaxL) {
     // L x L bit matrix: no pair buffer, no sort; one host sync for (P, E)
@@ -948,11 +971,9 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
     CK(launch_edge_bits(pt_ptr, pt_lm, n, L, bits, (unsigned long long*)ptot, s, &launches));
     tr("edges: bits");
     CK(launch_bits_compact(bits, L, edges, cap, ptot + 1, etemp, s, &launches));
-    int64_t h2[2];
-    CK(cudaMemcpyAsync(h2, ptot, sizeof h2, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    NP = h2[0];
-    E = h2[1];
+    // (P, E) arrive with the final synchronisation (edges holds the full capacity)
+    CK(cudaMemcpyAsync(mb->pe, ptot, sizeof(int64_t) * 2, cudaMemcpyDeviceToHost, s));
+    pe_pending = true;
     pool.free_now(bits);
     pool.free_now(etemp);
   } else if (L >= 2 && use_tri_bitmap(L, o.flags)) {
@@ -1036,8 +1057,13 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
   tr("edges rest");
 
   // ---- results
-  CK(cudaMemcpyAsync(&hs, stats, sizeof hs, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(&mb->hs_end, stats, sizeof(DevStats), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
+  hs = mb->hs_end;
+  if (pe_pending) {
+    NP = mb->pe[0];
+    E = mb->pe[1];
+  }
   bm_cover* c = (bm_cover*)calloc(1, sizeof(bm_cover));
   Priv* pv = (Priv*)calloc(1, sizeof(Priv));
   if (!c || !pv) {
