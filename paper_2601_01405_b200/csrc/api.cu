@@ -328,6 +328,18 @@ struct Trace {
   }
 };
 
+// Timing events come from a per-thread cache (creating and destroying CUDA
+// events costs host time inside every timed build).
+static cudaEvent_t cached_event(size_t i) {
+  static thread_local std::vector<cudaEvent_t> evs;
+  while (evs.size() <= i) {
+    cudaEvent_t e = nullptr;
+    if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+    evs.push_back(e);
+  }
+  return evs[i];
+}
+
 struct Timer {
   bool on;
   cudaStream_t s;
@@ -335,14 +347,10 @@ struct Timer {
   int n = 0;
   Timer(bool o, cudaStream_t st) : on(o), s(st) {
     if (on)
-      for (auto& e : ev) cudaEventCreate(&e);
-  }
-  ~Timer() {
-    if (on)
-      for (auto& e : ev) cudaEventDestroy(e);
+      for (int i = 0; i < BM_NUM_STEPS; ++i) ev[i] = cached_event((size_t)i);
   }
   void mark(int i) {
-    if (on) cudaEventRecord(ev[i], s);
+    if (on && ev[i]) cudaEventRecord(ev[i], s);
   }
 };
 
@@ -459,6 +467,7 @@ struct Mailbox {
   bm::DevStats hs;      // statistics at the loop's last check
   bm::DevStats hs_end;  // statistics at the end of the build
   int64_t pe[2];        // edges: P (witnessed pairs), E
+  int64_t ties[3 * 1024];   // the first near-tie triples (with the final synchronisation)
 };
 static Mailbox* mailbox() {
   static thread_local Mailbox* mb = nullptr;
@@ -734,18 +743,11 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
   std::vector<cudaEvent_t> mev;   // per-tile membership kernel brackets (timing only)
   auto mark_member = [&](void) -> cudaError_t {
     if (!tm.on) return cudaSuccess;
-    cudaEvent_t e;
-    cudaError_t r = cudaEventCreate(&e);
-    if (r != cudaSuccess) return r;
+    cudaEvent_t e = cached_event(BM_NUM_STEPS + mev.size());
+    if (!e) return cudaErrorMemoryAllocation;
     mev.push_back(e);
     return cudaEventRecord(e, s);
   };
-  struct EvGuard {
-    std::vector<cudaEvent_t>& v;
-    ~EvGuard() {
-      for (auto e : v) cudaEventDestroy(e);
-    }
-  } evguard{mev};
 
   // tiles are issued in batches between host termination checks (a tile after
   // the last one costs a few empty launches; a check costs a round trip)
@@ -1056,8 +1058,10 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
   tm.mark(5);
   tr("edges rest");
 
-  // ---- results
+  // ---- results (the first near ties ride along with the final synchronisation)
   CK(cudaMemcpyAsync(&mb->hs_end, stats, sizeof(DevStats), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(mb->ties, ties_dev, sizeof(int64_t) * 3 * std::min<int64_t>(tie_cap, 1024),
+                     cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   hs = mb->hs_end;
   if (pe_pending) {
@@ -1093,9 +1097,11 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
   c->n_near_ties_stored = nst;
   if (nst > 0) {
     c->near_tie_pairs = (int64_t*)malloc(sizeof(int64_t) * 3 * nst);
-    if (c->near_tie_pairs)
-      CK(cudaMemcpy(c->near_tie_pairs, ties_dev, sizeof(int64_t) * 3 * nst,
-                    cudaMemcpyDeviceToHost));
+    if (c->near_tie_pairs) {
+      if (nst <= 1024) memcpy(c->near_tie_pairs, mb->ties, sizeof(int64_t) * 3 * nst);
+      else CK(cudaMemcpy(c->near_tie_pairs, ties_dev, sizeof(int64_t) * 3 * nst,
+                         cudaMemcpyDeviceToHost));
+    }
   }
   if (tm.on) {
     for (int i = 0; i < 5; ++i) cudaEventElapsedTime(&c->step_ms[i], tm.ev[i], tm.ev[i + 1]);
