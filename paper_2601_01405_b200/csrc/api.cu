@@ -751,6 +751,15 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
 
   // tiles are issued in batches between host termination checks (a tile after
   // the last one costs a few empty launches; a check costs a round trip)
+  // BM_LOOP_PROFILE=1 (diagnostics): per-phase device time of the tile loop
+  // (A2 / A3 / B incl. landmark operands / A4), printed to stderr
+  static const bool loop_prof = getenv("BM_LOOP_PROFILE") != nullptr;
+  std::vector<std::pair<int, cudaEvent_t>> lev;
+  auto loop_mark = [&](int phase) {
+    if (!loop_prof) return;
+    cudaEvent_t e = cached_event(4096 + lev.size());
+    if (e && cudaEventRecord(e, s) == cudaSuccess) lev.emplace_back(phase, e);
+  };
   int64_t tile = 0;
   int batch = 4;
   int nonfinite_checked = 0;
@@ -804,6 +813,7 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
   for (; !fps;) {
     for (int b = 0; b < batch; ++b, ++tile) {
       const int cur = (int)(tile & 1), nxt = cur ^ 1;
+      loop_mark(0);
       // A2: adjacency among the candidates unc[0 .. nc)
       PairArgs a = base;
       a.qidx = uncb[cur];
@@ -825,9 +835,11 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
       } else {
         CK(launch_pairs(kind, MODE_ADJ, a, T, s, &launches));
       }
+      loop_mark(1);
       // A3: in-order resolve, append landmarks (resets the tile's counters)
       CK(launch_resolve(adj, adj_words, uncb[cur], cnt + cur, T, lm, cnt + 2, new_lm, cnt + 3,
                         stats, cnt + 4, nullptr, s, &launches));
+      loop_mark(2);
       // B (+A4 marks): membership of every point in the new balls
       if (use_tc) {
         CK(tc::launch_tc_tile_landmarks(P, tc_nrm, new_lm, cnt + 3, C2, ta, s, &launches));
@@ -857,9 +869,11 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
         CK(launch_pairs(kind, MODE_MEMBER, m, n, s, &launches));
         CK(mark_member());
       }
+      loop_mark(3);
       // A4: keep the still-uncovered points after the tile, in order
       CK(launch_compact_unc(covered, uncb[cur], cnt + cur, T, uncb[nxt], cnt + nxt, cstate,
                             cnt + 4, (uint32_t)(tile + 1), n, s, &launches));
+      loop_mark(4);
     }
     // one round trip: the counters and the statistics together
     CK(cudaMemcpyAsync(mb->hc, cnt, sizeof(int32_t) * 4, cudaMemcpyDeviceToHost, s));
@@ -874,6 +888,17 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
   }
   tm.mark(2);
   tr("greedy+membership loop");
+  if (loop_prof && !lev.empty()) {
+    cudaEventSynchronize(lev.back().second);
+    double acc[5] = {0, 0, 0, 0, 0};
+    for (size_t i = 0; i + 1 < lev.size(); ++i) {
+      float t = 0.f;
+      cudaEventElapsedTime(&t, lev[i].second, lev[i + 1].second);
+      acc[lev[i].first] += t;
+    }
+    fprintf(stderr, "loop profile (ms): tiles %lld  A2 %.4f  A3 %.4f  B %.4f  A4 %.4f  gaps %.4f\n",
+            (long long)tile, acc[0], acc[1], acc[2], acc[3], acc[4]);
+  }
 
   DevStats hs{};
   int32_t hL = 0;
@@ -1513,6 +1538,16 @@ bm_status bm_debug_resolve_tile(const uint32_t* adj, int32_t nc, uint8_t* lm_out
   CK(cudaStreamSynchronize(s));
   int64_t launches = 0;
   CK(bm::launch_resolve_debug(dadj, words, nc, dlm, s, &launches));
+  if (getenv("BM_RESOLVE_BENCH")) {   // diagnostics: device time per resolve launch
+    cudaEvent_t e0 = cached_event(8000), e1 = cached_event(8001);
+    CK(cudaEventRecord(e0, s));
+    for (int i = 0; i < 200; ++i) CK(bm::launch_resolve_debug(dadj, words, nc, dlm, s, &launches));
+    CK(cudaEventRecord(e1, s));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    fprintf(stderr, "resolve nc=%d: %.2f us per launch\n", nc, ms * 1e3f / 200.f);
+  }
   CK(cudaMemcpyAsync(lm_out, dlm, nc, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   return BM_OK;

@@ -19,50 +19,64 @@ namespace bm {
 
 constexpr unsigned FULLMASK = 0xffffffffu;
 
-// One CTA, warp w owns candidates 32w .. 32w+31.  Warp w folds in the landmark
-// words of earlier warps as they become ready (a wavefront through shared
-// memory flags), then resolves its own 32 candidates by a ballot fixed point.
-__device__ __forceinline__ uint32_t resolve_tile_core(const uint32_t* __restrict__ adj,
-                                                      int adj_words, int nc,
-                                                      volatile uint32_t* lmw,
-                                                      volatile int* ready) {
-  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+// The tile's adjacency words are staged in shared memory by the whole CTA
+// (coalesced), then ONE warp resolves the 32 blocks of 32 candidates in order:
+// lane l holds candidate 32w + l of block w; it folds in the landmark words of
+// the earlier blocks (lane v keeps block v's word, read by shuffles), then the
+// block's own 32 candidates are decided by a ballot fixed point.  (Measured:
+// a 32-warp wavefront that handed each block's word to the next warp through
+// shared-memory flags or mbarriers took ~20 us per 1024-candidate tile, almost
+// all of it cross-warp hand-off latency.)
+// sadj: [nb][T] words, T = 32 * adj_words.
+__device__ __forceinline__ void resolve_tile_core(const uint32_t* __restrict__ adj,
+                                                  int adj_words, int nc, volatile uint32_t* lmw,
+                                                  uint32_t* sadj) {
+  const int tid = threadIdx.x, lane = tid & 31;
   const int nb = (nc + 31) >> 5;
-  if (w >= nb) return 0u;
-  const int a = tid;
-  const bool valid = a < nc;
-  uint32_t wv[32];
-#pragma unroll
-  // word-major adjacency: word v of candidate a at adj[v * T + a] (coalesced per warp)
   const int T = adj_words * 32;
-  for (int v = 0; v < 32; ++v) wv[v] = (valid && v < w) ? adj[(int64_t)v * T + a] : 0u;
-  uint32_t inrow = valid ? (adj[(int64_t)w * T + a] & ((1u << lane) - 1u)) : 0u;
-  bool conflict = false;
+  // stage the lower triangle (word v of candidate a is needed for v <= a / 32):
+  // thread a issues its (up to 32) independent loads before any store
+  if (tid < nc) {
+    const int wa = tid >> 5;
+    uint32_t x[32];
 #pragma unroll
-  for (int v = 0; v < 32; ++v) {
-    if (v < w) {
-      while (ready[v] == 0) {
+    for (int v = 0; v < 32; ++v) x[v] = v <= wa ? __ldcg(adj + (int64_t)v * T + tid) : 0u;
+#pragma unroll
+    for (int v = 0; v < 32; ++v)
+      if (v <= wa) sadj[v * T + tid] = x[v];
+  }
+  __syncthreads();
+  if (tid < 32) {
+    for (int w = 0; w < nb; ++w) {
+      const int a = 32 * w + lane;
+      const bool valid = a < nc;
+      // fold in the earlier blocks' landmark words (independent loads, 8 in flight)
+      uint32_t conf = 0u;
+      if (valid) {
+        for (int v0 = 0; v0 < w; v0 += 8) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const int v = v0 + k;
+            if (v < w) conf |= sadj[v * T + a] & lmw[v];
+          }
+        }
       }
-      conflict = conflict || ((wv[v] & lmw[v]) != 0u);
+      const uint32_t inrow = valid ? (sadj[w * T + a] & ((1u << lane) - 1u)) : 0u;
+      unsigned undecided = __ballot_sync(FULLMASK, valid && conf == 0u);
+      unsigned S = 0u;
+      while (undecided) {
+        const bool me = (undecided >> lane) & 1u;
+        const bool is_lm = me && !(inrow & S) && !(inrow & undecided);
+        const bool not_lm = me && (inrow & S);
+        const unsigned ns = __ballot_sync(FULLMASK, is_lm);
+        const unsigned nn = __ballot_sync(FULLMASK, not_lm);
+        S |= ns;
+        undecided &= ~(ns | nn);
+      }
+      if (lane == 0) lmw[w] = S;
+      __syncwarp();
     }
   }
-  unsigned undecided = __ballot_sync(FULLMASK, valid && !conflict);
-  unsigned S = 0u;
-  while (undecided) {
-    const bool me = (undecided >> lane) & 1u;
-    const bool is_lm = me && !(inrow & S) && !(inrow & undecided);
-    const bool not_lm = me && (inrow & S);
-    const unsigned ns = __ballot_sync(FULLMASK, is_lm);
-    const unsigned nn = __ballot_sync(FULLMASK, not_lm);
-    S |= ns;
-    undecided &= ~(ns | nn);
-  }
-  if (lane == 0) {
-    lmw[w] = S;
-    __threadfence_block();
-    ready[w] = 1;
-  }
-  return S;
 }
 
 __global__ void __launch_bounds__(1024) k_resolve(const uint32_t* __restrict__ adj, int adj_words,
@@ -75,8 +89,8 @@ __global__ void __launch_bounds__(1024) k_resolve(const uint32_t* __restrict__ a
                                                   int32_t* __restrict__ ticket,
                                                   unsigned long long* __restrict__ band_count) {
   __shared__ volatile uint32_t lmw[32];
-  __shared__ volatile int ready[32];
   __shared__ int wpre[33];
+  extern __shared__ uint32_t sadj[];
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
   pdl_wait();
   pdl_trigger();   // a single CTA
@@ -90,9 +104,7 @@ __global__ void __launch_bounds__(1024) k_resolve(const uint32_t* __restrict__ a
     if (tid == 0) *dL_dev = 0;
     return;
   }
-  if (tid < 32) ready[tid] = 0;
-  __syncthreads();
-  resolve_tile_core(adj, adj_words, nc, lmw, ready);
+  resolve_tile_core(adj, adj_words, nc, lmw, sadj);
   __syncthreads();
   const int nb = (nc + 31) >> 5;
   if (tid < 32) {
@@ -127,31 +139,44 @@ __global__ void __launch_bounds__(1024) k_resolve(const uint32_t* __restrict__ a
   }
 }
 
+__global__ void __launch_bounds__(1024) k_resolve_debug(const uint32_t* __restrict__ adj,
+                                                        int adj_words, int nc, uint8_t* lm) {
+  __shared__ volatile uint32_t lmw[32];
+  extern __shared__ uint32_t sadj[];
+  const int tid = threadIdx.x;
+  resolve_tile_core(adj, adj_words, nc, lmw, sadj);
+  __syncthreads();
+  if (tid < nc) lm[tid] = (lmw[tid >> 5] >> (tid & 31)) & 1u;
+}
+
 cudaError_t launch_resolve(const uint32_t* adj, int adj_words, const int32_t* unc,
                            const int32_t* n_unc, int T, int32_t* lm_out, int32_t* L_dev,
                            int32_t* new_lm, int32_t* dL_dev, DevStats* stats, int32_t* ticket,
                            unsigned long long* band_count, cudaStream_t s, int64_t* launches) {
   ++*launches;
-  return launch_pdl(k_resolve, dim3(1), dim3(1024), 0, s, adj, adj_words, unc, n_unc, T, lm_out,
-                    L_dev, new_lm, dL_dev, stats, ticket, band_count);
-}
-
-__global__ void __launch_bounds__(1024) k_resolve_debug(const uint32_t* __restrict__ adj,
-                                                        int adj_words, int nc, uint8_t* lm) {
-  __shared__ volatile uint32_t lmw[32];
-  __shared__ volatile int ready[32];
-  const int tid = threadIdx.x;
-  if (tid < 32) ready[tid] = 0;
-  __syncthreads();
-  resolve_tile_core(adj, adj_words, nc, lmw, ready);
-  __syncthreads();
-  if (tid < nc) lm[tid] = (lmw[tid >> 5] >> (tid & 31)) & 1u;
+  const size_t smem = sizeof(uint32_t) * 32 * (size_t)adj_words * adj_words;
+  static bool attr = false;   // (one attribute call per process; T <= 1024)
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_resolve, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(sizeof(uint32_t) * 32 * 32 * 32));
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k_resolve_debug, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(sizeof(uint32_t) * 32 * 32 * 32));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  return launch_pdl(k_resolve, dim3(1), dim3(1024), smem, s, adj, adj_words, unc, n_unc, T,
+                    lm_out, L_dev, new_lm, dL_dev, stats, ticket, band_count);
 }
 
 cudaError_t launch_resolve_debug(const uint32_t* adj, int adj_words, int nc, uint8_t* lm,
                                  cudaStream_t s, int64_t* launches) {
   ++*launches;
-  k_resolve_debug<<<1, 1024, 0, s>>>(adj, adj_words, nc, lm);
+  const size_t smem = sizeof(uint32_t) * 32 * (size_t)adj_words * adj_words;
+  cudaError_t e = cudaFuncSetAttribute(k_resolve_debug, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)(sizeof(uint32_t) * 32 * 32 * 32));
+  if (e != cudaSuccess) return e;
+  k_resolve_debug<<<1, 1024, smem, s>>>(adj, adj_words, nc, lm);
   return cudaGetLastError();
 }
 
