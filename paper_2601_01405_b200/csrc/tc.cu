@@ -301,7 +301,10 @@ struct Smem {
   static constexpr int NBARS = 2 * STAGES + 2 * ABUF + 3 * NBUF + 5;
   static constexpr int CNT_OFF = BAR_OFF + NBARS * 8;     // tmem slot + per-warp counts
   static constexpr int BUF_OFF = CNT_OFF + 128;
-  static constexpr int TOTAL = BUF_OFF + EPI_WARPS * (KW + BW) * 8 + 1024;  // + align slack
+  // resident B (tf32): the launch's in-test offsets d_j, staged once for the rare path
+  static constexpr int DJ_OFF = (BUF_OFF + EPI_WARPS * (KW + BW) * 8 + 15) & ~15;
+  static constexpr int DJ_BYTES = (BRES && FOLD) ? STAGES * BN * 4 : 0;
+  static constexpr int TOTAL = DJ_OFF + DJ_BYTES + 1024;  // + align slack
 };
 
 // B': the oracle's fp64 decision for points p, q (ascending coordinates, no
@@ -602,6 +605,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // ---------------- epilogue: warps 4-7 take the first half of every tile's
     // columns, warps 8-11 the second half; warp w reads TMEM lanes 32*(w%4)..
     const int ew = warp - 4, grp = ew >> 2, q = warp & 3;
+    // resident B: the in-test offsets of all the launch's columns in shared memory
+    float* sdj = reinterpret_cast<float*>(sm + S::DJ_OFF);
+    if constexpr (S::DJ_BYTES > 0) {
+      for (int64_t j = threadIdx.x - 128; j < n_tiles * BN; j += 256) sdj[j] = __ldg(args.col_a + j);
+      asm volatile("bar.sync 1, 256;" ::: "memory");   // the 8 epilogue warps only
+    }
     unsigned long long* kb = kbuf + ew * S::KW;
     unsigned long long* bb = bbuf + ew * S::BW;
     uint32_t* kc = kcount + ew;
@@ -832,10 +841,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               uint32_t cand = 0u, inm = 0u;
               float dj[32];   // tf32 in-test offsets of the chunk (warp-uniform loads)
               if constexpr (KIND == TC_TF32) {
-                const float4* d4 = reinterpret_cast<const float4*>(args.col_a + j0);
+                const float4* d4 = reinterpret_cast<const float4*>(
+                    S::DJ_BYTES > 0 ? (const float*)(sdj + j0) : args.col_a + j0);
 #pragma unroll
                 for (int i4 = 0; i4 < 8; ++i4) {
-                  const float4 q4 = __ldg(d4 + i4);
+                  float4 q4;
+                  if constexpr (S::DJ_BYTES > 0) q4 = d4[i4];   // shared memory
+                  else q4 = __ldg(d4 + i4);
                   dj[4 * i4] = q4.x;
                   dj[4 * i4 + 1] = q4.y;
                   dj[4 * i4 + 2] = q4.z;
