@@ -148,8 +148,10 @@ __device__ __forceinline__ void pairs_block(const PairArgs& A, uint2* sl, int32_
   using acc_t = typename KindTraits<KIND>::acc_t;
   const int nu = NU > 0 ? NU : A.nu;
   const int tid = threadIdx.x, lane = tid & 31;
-  // prefilter: quantised landmark rows follow the fp32 rows in shared memory
-  uint32_t* sq = reinterpret_cast<uint32_t*>(sl + LC * nu);
+  // prefilter: shared memory holds only the quantised landmark rows (the rare
+  // exact check reads the landmark's fp32 row from global memory), so a whole
+  // 1024-landmark tile is staged at once; otherwise the fp32 rows
+  uint32_t* sq = reinterpret_cast<uint32_t*>(sl);
   // bias 2^15 - thr (thr > 2^15: the filter cannot prove anything, bias 0
   // makes every pair a candidate: SADs stay below 2^14 for d <= 64)
   uint32_t qbase = 0u;
@@ -188,7 +190,7 @@ __device__ __forceinline__ void pairs_block(const PairArgs& A, uint2* sl, int32_
   for (int64_t lb = l0; lb < l1; lb += LC) {
     const int nl = (int)min((int64_t)LC, l1 - lb);
     __syncthreads();
-    for (int t = tid; t < nl * nu; t += NT) {
+    for (int t = tid; t < nl * nu && !QF; t += NT) {
       int jj = t / nu, u = t - jj * nu;
       int32_t pt = A.lidx[lb + jj];
       sl[jj * nu + u] = A.rows[(int64_t)pt * nu + u];
@@ -219,8 +221,19 @@ __device__ __forceinline__ void pairs_block(const PairArgs& A, uint2* sl, int32_
       for (int u = 0; u < UG; ++u) {
         const int jq = min(jg + u, nl - 1);   // tail: repeat the last landmark
         uint32_t lq[NQ];
+        if constexpr (NQ % 4 == 0) {   // 16-byte shared loads
 #pragma unroll
-        for (int w = 0; w < NQ; ++w) lq[w] = sq[jq * NQ + w];
+          for (int w = 0; w < NQ; w += 4) {
+            const uint4 v4 = *reinterpret_cast<const uint4*>(sq + jq * NQ + w);
+            lq[w] = v4.x;
+            lq[w + 1] = v4.y;
+            lq[w + 2] = v4.z;
+            lq[w + 3] = v4.w;
+          }
+        } else {
+#pragma unroll
+          for (int w = 0; w < NQ; ++w) lq[w] = sq[jq * NQ + w];
+        }
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           uint32_t acc = qbase;
@@ -251,7 +264,8 @@ __device__ __forceinline__ void pairs_block(const PairArgs& A, uint2* sl, int32_
           if (cls[r] == 3) {
             acc_t a = 0;
             const uint2* src = A.rows + qp[r] * (int64_t)nu;
-            for (int u = 0; u < nu; ++u) acc_unit<KIND>(a, __ldg(src + u), sl[jj * nu + u]);
+            const uint2* lrow = A.rows + (int64_t)slp[jj] * nu;
+            for (int u = 0; u < nu; ++u) acc_unit<KIND>(a, __ldg(src + u), __ldg(lrow + u));
             cls[r] = classify<KIND>(a, qn[r], sln[jj], A.th);
           }
         }
@@ -400,9 +414,10 @@ __global__ void __launch_bounds__(256) k_pairs(PairArgs A) {
 template <int KIND, int NU, int MODE, int NQ = 0>
 cudaError_t launch_pairs_nu(const PairArgs& a, int64_t q_rows_max, cudaStream_t s) {
   constexpr int R = (MODE == MODE_ADJ || NU == 0) ? 1 : (NU <= 8 ? 4 : (NU <= 16 ? 2 : 1));
-  constexpr int LC = NU == 0 ? 32 : 64;
+  // prefilter: a whole 1024-landmark tile of 8-bit rows per staging round
+  constexpr int LC = NQ > 0 ? 1024 : (NU == 0 ? 32 : 64);
   constexpr int NT = 256;
-  size_t smem = (size_t)LC * a.nu * sizeof(uint2) + (size_t)LC * NQ * sizeof(uint32_t);
+  size_t smem = NQ > 0 ? (size_t)LC * NQ * sizeof(uint32_t) : (size_t)LC * a.nu * sizeof(uint2);
   auto kern = k_pairs<KIND, NU, R, MODE, LC, NQ>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
