@@ -194,12 +194,17 @@ __global__ void __launch_bounds__(CP_NT) k_compact(const uint8_t* __restrict__ c
                                                    int32_t* __restrict__ unc_next,
                                                    int32_t* __restrict__ n_unc_next,
                                                    unsigned long long* state,
-                                                   int32_t* ticket, uint32_t tag) {
+                                                   int32_t* ticket, uint32_t tag,
+                                                   int one_wave) {
   __shared__ int s_bid;
   __shared__ int s_wcnt[CP_ROUNDS][CP_NT / 32];
   __shared__ int s_excl;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  pdl_wait();   // (multi-wave, ticketed: the next kernel launches as CTAs exit)
+  pdl_wait();
+  // a grid that fits in one wave lets the next kernel launch early; a
+  // multi-wave grid must not (waiting dependents could hold the SMs its
+  // remaining CTAs need)
+  if (one_wave) pdl_trigger();
   if (tid == 0) s_bid = atomicAdd(ticket, 1);
   __syncthreads();
   const int bid = s_bid;
@@ -261,8 +266,17 @@ cudaError_t launch_compact_unc(const uint8_t* covered, const int32_t* unc, const
                                int64_t n, cudaStream_t s, int64_t* launches) {
   const int64_t nblk = (n + CP_TILE - 1) / CP_TILE;
   ++*launches;
+  static int cap = 0;   // CTAs resident at once
+  if (cap == 0) {
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_compact, CP_NT, 0);
+    cap = sms * (per > 0 ? per : 1);
+  }
+  const int one_wave = nblk <= cap ? 1 : 0;
   return launch_pdl(k_compact, dim3((unsigned)(nblk > 0 ? nblk : 1)), dim3(CP_NT), 0, s, covered,
-                    unc, n_unc, T, unc_next, n_unc_next, state, ticket, tag);
+                    unc, n_unc, T, unc_next, n_unc_next, state, ticket, tag, one_wave);
 }
 
 }  // namespace bm

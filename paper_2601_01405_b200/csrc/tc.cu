@@ -432,6 +432,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const uint32_t tmem = *tmem_slot;
   if (threadIdx.x == 0) TC_STAMP(1);
   pdl_wait();   // everything above overlaps the previous kernel's tail
+  // one persistent wave: the next kernel may be launched now (its CTAs start as
+  // these exit and wait for this grid's completion in their own pdl_wait)
+  pdl_trigger();
   if (threadIdx.x == 0) TC_STAMP(2);
 
   // Work units = (block of RA*128 point rows, chunk of BN-wide landmark tiles),
