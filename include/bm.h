@@ -193,7 +193,8 @@ bm_status bm_cover_build_ex(const void *points, bm_dtype dtype, int64_t n, int32
  * bm_cover_build_host — same computation from a HOST buffer: the points are
  * copied to the device inside the call (pinned host memory gives the best
  * copy rate) and every output array is copied back into library-owned HOST
- * memory (on_host = 1).  Used for end-to-end timing.
+ * memory (on_host = 1): one pinned block per cover, recycled by bm_free and
+ * released by bm_trim_memory.  Used for end-to-end timing.
  */
 bm_status bm_cover_build_host(const void *host_points, bm_dtype dtype, int64_t n, int32_t d,
                               bm_metric metric, double eps, void *stream,

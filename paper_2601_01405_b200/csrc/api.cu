@@ -131,6 +131,47 @@ struct BlockCache {
 };
 BlockCache g_cache;
 
+// Pinned host blocks for the host-buffer API's results (one block per cover,
+// all six arrays carved from it): device->host copies into pinned memory run
+// at full link speed and can be queued behind one synchronisation; pinning
+// fresh pages on every call would cost more than the copies.
+struct PinnedCache {
+  std::mutex mu;
+  std::map<size_t, std::vector<void*>> free_;
+  static size_t size_class(size_t b) { return BlockCache::size_class(b < 4096 ? 4096 : b); }
+  void* get(size_t bytes, size_t* cls_out) {
+    const size_t cls = size_class(bytes);
+    *cls_out = cls;
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      auto it = free_.find(cls);
+      if (it != free_.end() && !it->second.empty()) {
+        void* p = it->second.back();
+        it->second.pop_back();
+        return p;
+      }
+    }
+    void* p = nullptr;
+    if (cudaMallocHost(&p, cls) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    return p;
+  }
+  void put(void* p, size_t cls) {
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(mu);
+    free_[cls].push_back(p);
+  }
+  void trim() {
+    std::lock_guard<std::mutex> lk(mu);
+    for (auto& kv : free_)
+      for (void* p : kv.second) cudaFreeHost(p);
+    free_.clear();
+  }
+};
+PinnedCache g_pinned;
+
 // Allocations owned by one build call (stream-ordered on the call's stream).
 struct Pool {
   cudaStream_t s;
@@ -177,6 +218,8 @@ struct Pool {
 
 struct Priv {
   cudaStream_t stream;
+  void* pinned;        // host-buffer covers: the pinned block holding all arrays
+  size_t pinned_cls;
 };
 
 int bits_for(int64_t v) {  // number of bits to represent 0..v (>= 1)
@@ -1144,20 +1187,33 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
   c->n_launches = launches;
   if (host_in) {
     c->on_host = 1;
-    auto h2 = [&](void* dsrc, size_t bytes) -> void* {
-      void* h = malloc(bytes > 0 ? bytes : 1);
-      if (h && bytes) cudaMemcpy(h, dsrc, bytes, cudaMemcpyDeviceToHost);
-      return h;
-    };
-    c->landmarks = (int32_t*)h2(landmarks, sizeof(int32_t) * L);
-    c->ball_ptr = (int64_t*)h2(ball_ptr, sizeof(int64_t) * (L + 1));
-    c->ball_idx = (int32_t*)h2(ball_idx, sizeof(int32_t) * M);
-    c->pt_ptr = (int64_t*)h2(pt_ptr, sizeof(int64_t) * (n + 1));
-    c->pt_lm = (int32_t*)h2(pt_lm, sizeof(int32_t) * M);
-    c->edges = (int32_t*)h2(edges, sizeof(int32_t) * 2 * E);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess || !c->landmarks || !c->ball_ptr || !c->ball_idx || !c->pt_ptr ||
-        !c->pt_lm || !c->edges) {
+    // all six arrays in one pinned block (256-byte aligned parts), queued
+    // copies, one synchronisation
+    const size_t sz[6] = {sizeof(int32_t) * (size_t)L, sizeof(int64_t) * (size_t)(L + 1),
+                          sizeof(int32_t) * (size_t)M, sizeof(int64_t) * (size_t)(n + 1),
+                          sizeof(int32_t) * (size_t)M, sizeof(int32_t) * 2 * (size_t)E};
+    const void* src[6] = {landmarks, ball_ptr, ball_idx, pt_ptr, pt_lm, edges};
+    size_t off[6], total = 0;
+    for (int i = 0; i < 6; ++i) {
+      off[i] = total;
+      total += (sz[i] + 255) & ~(size_t)255;
+    }
+    uint8_t* blk = (uint8_t*)g_pinned.get(total, &pv->pinned_cls);
+    if (!blk) {
+      bm_free(c);
+      return set_err(BM_ENOMEM, "pinned host allocation for the results failed");
+    }
+    pv->pinned = blk;
+    for (int i = 0; i < 6; ++i)
+      if (sz[i]) CK(cudaMemcpyAsync(blk + off[i], src[i], sz[i], cudaMemcpyDeviceToHost, s));
+    cudaError_t e = cudaStreamSynchronize(s);
+    c->landmarks = (int32_t*)(blk + off[0]);
+    c->ball_ptr = (int64_t*)(blk + off[1]);
+    c->ball_idx = (int32_t*)(blk + off[2]);
+    c->pt_ptr = (int64_t*)(blk + off[3]);
+    c->pt_lm = (int32_t*)(blk + off[4]);
+    c->edges = (int32_t*)(blk + off[5]);
+    if (e != cudaSuccess) {
       bm_free(c);
       return set_err(BM_ECUDA, "device-to-host copy of the results failed");
     }
@@ -1211,12 +1267,16 @@ void bm_free(bm_cover* c) {
   if (!c) return;
   Priv* pv = (Priv*)c->priv;
   if (c->on_host) {
-    free(c->landmarks);
-    free(c->ball_ptr);
-    free(c->ball_idx);
-    free(c->pt_ptr);
-    free(c->pt_lm);
-    free(c->edges);
+    if (pv && pv->pinned) {
+      g_pinned.put(pv->pinned, pv->pinned_cls);
+    } else {
+      free(c->landmarks);
+      free(c->ball_ptr);
+      free(c->ball_idx);
+      free(c->pt_ptr);
+      free(c->pt_lm);
+      free(c->edges);
+    }
   } else {
     cudaStream_t s = pv ? pv->stream : nullptr;
     for (void* p : {(void*)c->landmarks, (void*)c->ball_ptr, (void*)c->ball_idx,
@@ -1318,6 +1378,7 @@ bm_status bm_skeleton(const bm_cover* c, int32_t k, int32_t* out, int64_t capaci
 
 bm_status bm_trim_memory(void) {
   g_cache.trim();
+  g_pinned.trim();
   return BM_OK;
 }
 
