@@ -686,7 +686,9 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
   tc::TcArgs ta{};
   // A2 on tensor cores when the CUDA-core adjacency kernel would have to
   // re-read wide rows from memory (no register-resident width fits, e.g. C4)
-  const bool tc_adj = use_tc && pick_nu(nu_needed) == 0;
+  // (also for d >= 32: measured on C3, d = 64: 9.0 ms of A2 over 572 tiles on
+  // tensor cores vs 12.0 ms on CUDA cores; C2, d = 10, is faster on CUDA cores)
+  const bool tc_adj = use_tc && (pick_nu(nu_needed) == 0 || d >= 32);
   tc::TcArgs ac{};      // A2 on tensor cores: candidate contraction
   tc::TcPlan Pc{};
   tc::RowParams rp{};
