@@ -31,7 +31,7 @@ METRIC = "point-landmark distance evals/sec"
 UNIT = "evals/s"
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
@@ -43,7 +43,7 @@ def parse():
     ap.add_argument("--path", default="auto")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-seconds", type=float, default=15.0)
-    return ap.parse_args()
+    return ap.parse_args(argv)
 
 
 # ----------------------------------------------------------------- clocks
@@ -221,6 +221,24 @@ def cpu_baseline(w, X, budget_s: float):
 
 
 # ----------------------------------------------------------------- arms
+def max_over_ranks(x: float, world: int, device: str = "cuda") -> float:
+    """Max of a per-rank time over all ranks (device timing rule: the job
+    takes as long as its slowest replica).  Gloo on CPU tensors in the tests."""
+    if world <= 1:
+        return float(x)
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def whole_job_value(world: int, pairs_per_replica: float, seconds: float) -> float:
+    """Whole-job throughput: every replica evaluates pairs_per_replica pairs
+    (weak scaling, no data-path collective), the job time is the max over ranks."""
+    return world * pairs_per_replica / seconds
+
+
 def run_reference(args):
     """--impl reference: the CPU oracle arm (rank 0 only)."""
     rank = int(os.environ.get("RANK", "0"))
@@ -345,12 +363,9 @@ def run_ours(args):
     ss = sorted(step_ms)
     step_stats = {"min": round(ss[0], 4), "median": round(ss[len(ss) // 2], 4),
                   "max": round(ss[-1], 4)}
-    if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(ms, world)
     pairs = n * L
-    value = world * pairs / (ms * 1e-3)
+    value = whole_job_value(world, pairs, ms * 1e-3)
 
     # dominant kernel: membership pass, timed by library events on the launch stream
     kern_ms = sorted(s.step_ms["member_kernel"] for s in covs_stats)[len(covs_stats) // 2]
@@ -380,11 +395,7 @@ def run_ours(args):
         e2e_times.append(time.perf_counter() - t0)
         d2h = 4 * hc.L + 8 * (hc.L + 1) + 4 * hc.M + 8 * (n + 1) + 4 * hc.M + 8 * hc.E
         hc.free()
-    e2e_s = sorted(e2e_times)[len(e2e_times) // 2]
-    if world > 1:
-        t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+    e2e_s = max_over_ranks(sorted(e2e_times)[len(e2e_times) // 2], world)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -411,7 +422,7 @@ def run_ours(args):
                        "band_pairs": int(last.n_band_pairs), "near_ties": int(last.n_near_ties)},
             "roofline": roof,
             "cpu_baseline": cpu,
-            "e2e": {"value": world * pairs / e2e_s, "unit": UNIT, "seconds": round(e2e_s, 5),
+            "e2e": {"value": whole_job_value(world, pairs, e2e_s), "unit": UNIT, "seconds": round(e2e_s, 5),
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
             "clocks": clocks,
             "gpu_launches": int(launches)}
