@@ -62,7 +62,8 @@ class ClockSampler:
             self.f = open(self.path, "w")
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f,
+                 "--format=csv,noheader,nounits", "-lms",
+                 os.environ.get("BM_CLOCK_MS", "100")], stdout=self.f,
                 stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
@@ -108,9 +109,9 @@ def load_peaks():
             "sm_max_mhz": 1965.0}, "fallback"
 
 
-def roofline_for(w, L, kernel_ms, n, peaks, path_used, step_ms):
+def roofline_for(w, L, kernel_ms, n, peaks, path_used, step_ms, st=None):
     if path_used == 2:
-        return roofline_tensor(w, L, kernel_ms, n, peaks, step_ms)
+        return roofline_tensor(w, L, kernel_ms, n, peaks, step_ms, st)
     return roofline_alu(w, L, kernel_ms, n, peaks)
 
 
@@ -124,7 +125,7 @@ def _traffic(w):
     return None
 
 
-def roofline_tensor(w, L, kernel_ms, n, peaks, step_ms):
+def roofline_tensor(w, L, kernel_ms, n, peaks, step_ms, st=None):
     """tcgen05 contraction, two ceilings:
       tensor: 2*d algorithmic ops per pair (true d, not the padded K) against
         the measured bf16 peak x the nominal ratio (tf32 0.5, int8 2.0); burst
@@ -139,12 +140,17 @@ def roofline_tensor(w, L, kernel_ms, n, peaks, step_ms):
     bf16 = float(peaks["bf16_tflops_sustained" if sustained else "bf16_tflops"])
     ratio = 0.5 if w.dtype == "f32" else 2.0
     peak = bf16 * ratio
-    ops = 2.0 * w.d * float(n) * L
     ks = kernel_ms * 1e-3
+    # executed work: with the tile-level pruning (cells.cu) only the contracted
+    # 128 x 256 tiles and the 128 x 32 chunks read from TMEM count against the
+    # ceilings; without it (or on paths that do not report) every pair does
+    tiles = getattr(st, "tc_tiles_run", 0) if st is not None else 0
+    chunks = getattr(st, "tc_chunks_run", 0) if st is not None else 0
+    ops = 2.0 * w.d * (tiles * 128.0 * 256.0 if tiles else float(n) * L)
     achieved = ops / ks / 1e12 if kernel_ms > 0 else 0.0
     clk = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
     tmem_peak = 64.0 * 148 * clk / 1e9                      # GB/s
-    tmem_bytes = 4.0 * float(n) * L
+    tmem_bytes = (chunks * 128.0 * 32.0 if chunks else float(n) * L) * 4.0
     tmem_ach = tmem_bytes / ks / 1e9 if kernel_ms > 0 else 0.0
     kern = "k_tc (tcgen05 " + ("tf32" if w.dtype == "f32" else "int8") + ", per-tile)"
     tensor = {"bound": "tensor", "achieved": round(achieved, 3), "peak": round(peak, 3),
@@ -161,7 +167,14 @@ def roofline_tensor(w, L, kernel_ms, n, peaks, step_ms):
     main, other = (tmem, tensor) if tmem["frac"] > tensor["frac"] else (tensor, tmem)
     out = dict(main)
     out.update({"kernel": kern, "traffic": _traffic(w), "kernel_ms": round(kernel_ms, 5),
-                "other": other})
+                "other": other,
+                "work_basis": "executed tiles / TMEM chunks" if tiles else "n x L pairs",
+                "decided_pairs_per_s": round(float(n) * L / ks, 1) if ks > 0 else None})
+    if st is not None and (getattr(st, "tc_tiles_skipped", 0) or getattr(st, "tc_chunks_skipped", 0)):
+        tt = st.tc_tiles_run + st.tc_tiles_skipped
+        cc = st.tc_chunks_run + st.tc_chunks_skipped
+        out["pruned"] = {"tiles_skipped_frac": round(st.tc_tiles_skipped / max(1, tt), 4),
+                         "chunks_skipped_frac": round(st.tc_chunks_skipped / max(1, cc), 4)}
     return out
 
 
@@ -373,7 +386,7 @@ def run_ours(args):
     breakdown = {k: round(sorted(s.step_ms[k] for s in covs_stats)[len(covs_stats) // 2], 4)
                  for k in ("prep", "greedy", "member", "csr", "edges", "member_kernel")}
     peaks, peak_src = load_peaks()
-    roof = roofline_for(w, L, kern_ms, n, peaks, covs_stats[-1].path_used, ms)
+    roof = roofline_for(w, L, kern_ms, n, peaks, covs_stats[-1].path_used, ms, covs_stats[-1])
     roof["peak_source"] = peak_src
     roof["share_of_step"] = round(kern_ms / ms, 4) if ms > 0 else None
     roof["launches_per_step"] = int(kern_launches)

@@ -122,6 +122,8 @@ typedef enum bm_select {
 /* bm_options.flags */
 #define BM_FLAG_NO_L1_PREFILTER 1   /* L1: score every pair in fp32 (no 8-bit SAD prefilter) */
 #define BM_FLAG_NO_EDGE_TRIANGLE 2  /* L > 4096: build edges by sort + unique, not the bit triangle */
+#define BM_FLAG_NO_PRUNE 4          /* tensor path: no tile-level pruning of the membership contraction */
+#define BM_FLAG_FORCE_PRUNE 8       /* tensor path: prune even below the size where it pays (tests) */
 
 /*
  * Result of one cover construction.  All arrays are owned by the library and
@@ -162,6 +164,9 @@ typedef struct bm_cover {
   int32_t path_used;         /* bm_path actually used for the contraction                */
   int32_t tile_used;         /* greedy tile T                                            */
   float step_ms[BM_NUM_STEPS];/* per-step device time (ms) when options.timing = 1       */
+  /* tensor path, fused greedy membership: 128 x 256 tiles contracted / skipped by
+   * the tile-level pruning, 128 x 32 accumulator chunks read from TMEM / skipped */
+  int64_t n_tc_tiles_run, n_tc_tiles_skipped, n_tc_chunks_run, n_tc_chunks_skipped;
   void *priv;                /* library-private                                          */
 } bm_cover;
 

@@ -26,6 +26,8 @@ AGG = {"mean": 0, "median": 1, "trimmed": 2, "min": 3, "max": 4, "mode": 5, "var
 PATH = {"auto": 0, "cuda_core": 1, "tensor": 2}
 FLAG_NO_L1_PREFILTER = 1
 FLAG_NO_EDGE_TRIANGLE = 2
+FLAG_NO_PRUNE = 4
+FLAG_FORCE_PRUNE = 8
 STEPS = ("prep", "greedy", "member", "csr", "edges", "total", "member_kernel", "select")
 
 EXPORTED = ("bm_cover_build", "bm_cover_build_ex", "bm_cover_build_host", "bm_free",
@@ -65,7 +67,10 @@ class _Cover(ctypes.Structure):
                 ("n_greedy_tiles", ctypes.c_int64), ("n_launches", ctypes.c_int64),
                 ("n_member_launches", ctypes.c_int64),
                 ("path_used", ctypes.c_int32), ("tile_used", ctypes.c_int32),
-                ("step_ms", ctypes.c_float * 8), ("priv", ctypes.c_void_p)]
+                ("step_ms", ctypes.c_float * 8),
+                ("n_tc_tiles_run", ctypes.c_int64), ("n_tc_tiles_skipped", ctypes.c_int64),
+                ("n_tc_chunks_run", ctypes.c_int64), ("n_tc_chunks_skipped", ctypes.c_int64),
+                ("priv", ctypes.c_void_p)]
 
 
 _lib = None
@@ -158,6 +163,10 @@ class CoverStats:
     path_used: int
     tile_used: int
     step_ms: dict
+    tc_tiles_run: int = 0
+    tc_tiles_skipped: int = 0
+    tc_chunks_run: int = 0
+    tc_chunks_skipped: int = 0
 
 
 class Cover:
@@ -175,7 +184,9 @@ class Cover:
                                 c.n_near_ties, c.n_greedy_tiles, c.n_launches,
                                 c.n_member_launches, c.path_used,
                                 c.tile_used, {k: float(c.step_ms[i]) for i, k in
-                                              enumerate(STEPS)})
+                                              enumerate(STEPS)},
+                                c.n_tc_tiles_run, c.n_tc_tiles_skipped, c.n_tc_chunks_run,
+                                c.n_tc_chunks_skipped)
         k = c.n_near_ties_stored
         if k > 0:
             self.near_ties = np.ctypeslib.as_array(c.near_tie_pairs, shape=(k, 3)).copy()

@@ -638,6 +638,45 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
   }
 
   if (host_in) pool.free_now((void*)dpoints);
+
+  // ---- tile-level pruning of the tensor-core membership (cells.cu): fp32
+  // Euclidean, large n (the preparation costs ~1 ms at n = 1e6)
+  const bool prune = use_tc && dtype == BM_F32 && metric == BM_L2 && d <= 128 &&
+                     n >= 4 * kPruneCells && !(o.flags & BM_FLAG_NO_PRUNE) &&
+                     (n >= 262144 || (o.flags & BM_FLAG_FORCE_PRUNE));
+  PruneState ps{};
+  tc::TcPlan Pm{};   // the member kernel's plan: A operand in permuted order
+  if (prune) {
+    const int KWd = kPruneCells / 32;
+    const int64_t nblk = (n + 127) / 128;
+    TRY(pool.alloc(&ps.cell, (size_t)n));
+    TRY(pool.alloc(&ps.rank, (size_t)kPruneCells));
+    TRY(pool.alloc(&ps.pdist, (size_t)kPruneCells * kPruneCells));
+    TRY(pool.alloc(&ps.perm, (size_t)n));
+    TRY(pool.alloc(&ps.seg, (size_t)kPruneCells + 1));
+    TRY(pool.alloc(&ps.center, (size_t)kPruneCells * d));
+    TRY(pool.alloc(&ps.radius, (size_t)kPruneCells));
+    TRY(pool.alloc(&ps.near, (size_t)kPruneCells * KWd));
+    TRY(pool.alloc(&ps.bmask, (size_t)nblk * KWd));
+    TRY(pool.alloc(&ps.xop_perm, (size_t)n * P.row_bytes));
+    TRY(pool.alloc(&ps.nrm_perm, (size_t)n));
+    TRY(pool.alloc(&ps.col_pt, 1024));
+    TRY(pool.alloc(&ps.col_pos, 1024));
+    TRY(pool.alloc(&ps.cmask, (size_t)32 * KWd));
+    TRY(pool.alloc(&ps.tmask, (size_t)4 * KWd));
+    TRY(pool.alloc(&ps.act, (size_t)nblk));
+    unsigned long long *pk = nullptr, *pa = nullptr;
+    void* ptemp = nullptr;
+    TRY(pool.alloc(&pk, (size_t)n));
+    TRY(pool.alloc(&pa, (size_t)n));
+    TRY(pool.alloc((uint8_t**)&ptemp, radix_temp_bytes(n)));
+    CK(prune_prepare((const float*)rows, 2 * nu, d, n, eps, (const uint8_t*)P.xop, P.row_bytes,
+                     (const double*)tc_nrm, ps, ptemp, pk, pa, s, &launches));
+    pool.free_now(pk);
+    pool.free_now(pa);
+    pool.free_now(ptemp);
+    tr("prune prepare");
+  }
   tr("prep");
 
   // ---- buffers of the fused greedy + membership loop
@@ -729,11 +768,19 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
     }
     if (P.cosine) CK(tc::launch_tc_rows_cos(P, tc_nrm, n, th.eps, tc_cos_margin(ta.ksteps), ta, s,
                                             &launches));
-    else CK(tc::launch_tc_rows(P, tc_nrm, n, C2, th.eps2, tau, th.lo_i, ta, s, &launches));
+    else CK(tc::launch_tc_rows(P, prune ? (const void*)ps.nrm_perm : tc_nrm, n, C2, th.eps2, tau,
+                               th.lo_i, ta, s, &launches));
     ta.keys = keys;
     ta.key_count = &stats->key_count;
     ta.key_cap = key_cap;
-    set_recheck(ta, rows, 2 * nu, d, th, new_lm, ties_dev, tie_cap, stats);
+    set_recheck(ta, rows, 2 * nu, d, th, prune ? ps.col_pt : new_lm, ties_dev, tie_cap, stats);
+    if (prune) {
+      Pm = P;
+      Pm.xop = ps.xop_perm;
+      ta.row_pt = ps.perm;
+      ta.col_pos = ps.col_pos;
+      ta.act = ps.act;
+    }
   }
   if (tc_adj) {
     // A2 on tensor cores: the tile's candidates x themselves (adjacency epilogue)
@@ -887,9 +934,11 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
       loop_mark(2);
       // B (+A4 marks): membership of every point in the new balls
       if (use_tc) {
-        CK(tc::launch_tc_tile_landmarks(P, tc_nrm, new_lm, cnt + 3, C2, ta, s, &launches));
+        if (prune) CK(launch_tile_sort(new_lm, cnt + 3, ps, n, s, &launches));
+        CK(tc::launch_tc_tile_landmarks(P, tc_nrm, prune ? ps.col_pt : new_lm, cnt + 3, C2, ta, s,
+                                        &launches));
         CK(mark_member());
-        CK(tc::launch_tc(P, ta, s, &launches));
+        CK(tc::launch_tc(prune ? Pm : P, ta, s, &launches));
         CK(mark_member());
       } else {
         PairArgs m = base;
@@ -1161,6 +1210,10 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
   c->n_band_pairs = (int64_t)hs.band_pairs;
   c->n_near_ties = (int64_t)hs.near_ties;
   c->n_greedy_tiles = (int64_t)hs.tiles;
+  c->n_tc_tiles_run = (int64_t)hs.tc_tiles_run;
+  c->n_tc_tiles_skipped = (int64_t)hs.tc_tiles_skip;
+  c->n_tc_chunks_run = (int64_t)hs.tc_chunks_run;
+  c->n_tc_chunks_skipped = (int64_t)hs.tc_chunks_skip;
   c->path_used = use_tc ? BM_PATH_TENSOR : BM_PATH_CUDA_CORE;
   c->tile_used = T;
   const int64_t nst = c->n_near_ties < tie_cap ? c->n_near_ties : tie_cap;

@@ -107,6 +107,10 @@ struct DevStats {
   unsigned long long near_ties;      // near ties found in MODE_MEMBER
   unsigned long long greedy_evals;   // in-tile + coverage evaluations
   unsigned long long tiles;          // greedy tiles with nc > 0
+  unsigned long long tc_tiles_run;   // tensor path: 128 x 256 tiles contracted
+  unsigned long long tc_tiles_skip;  //   ... skipped by the tile-level pruning
+  unsigned long long tc_chunks_run;  //   128 x 32 accumulator chunks read from TMEM
+  unsigned long long tc_chunks_skip; //   ... skipped
   int nonfinite;                     // prep: a NaN/Inf coordinate was seen
   int overflow;                      // fused greedy: a tile's band queue overflowed
 };
@@ -212,6 +216,34 @@ cudaError_t launch_unique_flags(const unsigned long long* keys, int64_t m, int64
 cudaError_t launch_unique_scatter(const unsigned long long* keys, int64_t m,
                                   const int64_t* pos, int lbits, int32_t* edges,
                                   cudaStream_t s, int64_t* launches);
+// cells.cu: tile-level pruning of the tensor-core membership contraction
+constexpr int kPruneCells = 256;
+struct PruneState {
+  int32_t* cell;        // [n] cell of each point
+  int32_t* rank;        // [K] position of each cell in the pivot chain
+  float* pdist;         // [K*K] pivot distances (scratch)
+  int32_t* perm;        // [n] permuted row r -> point
+  int64_t* seg;         // [K+1] rank segments of perm
+  double* center;       // [K*d]
+  double* radius;       // [K] (-1: empty cell)
+  uint32_t* near;       // [K][K/32]
+  uint32_t* bmask;      // [ceil(n/128)][K/32] cells near some row of the block
+  uint8_t* xop_perm;    // [n][row_bytes] the A operand in permuted order
+  double* nrm_perm;     // [n] norms in permuted order
+  int32_t* col_pt;      // [1024] the tile's landmarks sorted by cell rank
+  int32_t* col_pos;     // [1024] their positions in the tile (key positions)
+  uint32_t* cmask;      // [32 chunks][K/32] cells of each 32-column chunk
+  uint32_t* tmask;      // [4 tiles][K/32] cells of each 256-column tile
+  uint32_t* act;        // [ceil(n/128)] per row block: bit 8 t + c = chunk c of tile t may
+                        // hold an in-ball pair (from bmask and cmask, per greedy tile)
+};
+cudaError_t prune_prepare(const float* xrows, int xstride, int d, int64_t n, double eps,
+                          const uint8_t* xop, int64_t row_bytes, const double* nrm, PruneState& ps,
+                          void* sort_temp, unsigned long long* keys, unsigned long long* alt,
+                          cudaStream_t s, int64_t* launches);
+cudaError_t launch_tile_sort(const int32_t* new_lm, const int32_t* dL_dev, const PruneState& ps,
+                             int64_t n, cudaStream_t s, int64_t* launches);
+
 // fps.cu (NEXT-2)
 int fps_max_candidates();
 cudaError_t launch_fps(const uint2* rows, const int32_t* inorm, int nu, int d, int kind, int64_t n,

@@ -449,6 +449,23 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const int64_t tiles_per_chunk = n_tiles > 0 ? (n_tiles + n_chunks - 1) / n_chunks : 1;
   n_chunks = n_tiles > 0 ? (n_tiles + tiles_per_chunk - 1) / tiles_per_chunk : 0;
   const int64_t n_units = args.n_mblk * n_chunks;
+  // pruning: may row block mb hold an in-ball pair with a landmark of tile t?
+  // (every role evaluates the same predicate, so they skip the same tiles)
+  // (ab: the unit's live-chunk word, args.act[mb], or all ones without pruning)
+  // (only the fused greedy tile, <= 4 tiles, is pruned: t < 4 whenever act is set)
+  auto tile_active = [&](uint32_t ab, int64_t t) -> bool {
+    return !args.act || ((ab >> (8 * t)) & 0xffu) != 0u;
+  };
+  // a unit none of whose tiles is live is skipped whole (no A block load)
+  auto unit_active = [&](uint32_t ab, int64_t t0, int64_t t1) -> bool {
+    for (int64_t t = t0; t < t1; ++t)
+      if (tile_active(ab, t)) return true;
+    return false;
+  };
+  // the live-chunk word of unit u (prefetched one unit ahead by every role)
+  auto act_of = [&](int64_t u) -> uint32_t {
+    return (args.act && u < n_units) ? __ldg(args.act + u / n_chunks) : 0xffffffffu;
+  };
 
   if (warp == 0) {
     if (lane == 0) {
@@ -471,9 +488,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               tma_load_2d(sBK + t * S::BK_SLOT, &tmK, &full[t], 0, (int)(t * BN));
           }
       }
-      for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x, ++ui) {
+      uint32_t act_next = act_of(blockIdx.x);
+      for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
         const int64_t mb = u / n_chunks, ch = u % n_chunks;
         const int64_t t0 = ch * tiles_per_chunk, t1 = min(n_tiles, t0 + tiles_per_chunk);
+        const uint32_t uact = act_next;
+        act_next = act_of(u + gridDim.x);
+        if (!unit_active(uact, t0, t1)) continue;
         const int ab = (int)(ui % ABUF);
         if (ui >= ABUF) {             // wait until the MMAs of unit ui - ABUF released it
           mbar_wait(&a_empty[ab], (a_ph >> ab) & 1u);
@@ -494,6 +515,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               tma_prefetch_2d(&tmA, ka * ATOM_ELEMS, (int)((un / n_chunks) * RA * 128 + r * 128));
         }
         for (int64_t t = t0; t < t1 && !BRES; ++t) {
+          if (!tile_active(uact, t)) continue;
           for (int ka = 0; ka < KATOMS; ++ka) {
             mbar_wait(&empty[stage], phase ^ 1u);
             mbar_expect_tx(&full[stage], (uint32_t)S::B_STAGE);
@@ -515,6 +537,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           }
           ++tk;
         }
+        ++ui;
       }
       TC_STAMP(4);
     }
@@ -529,9 +552,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       int64_t ui = 0;
       int64_t tk = 0;                  // tiles issued (fold: B constant slot = tk & 1)
       if constexpr (FOLD) mbar_wait(ak_full, 0u);
-      for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x, ++ui) {
+      uint32_t res_seen = 0u;   // BRES: resident tiles already waited for
+      unsigned long long n_run = 0ull, n_skip = 0ull;
+      uint32_t act_next = act_of(blockIdx.x);
+      for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
         const int64_t ch = u % n_chunks;
         const int64_t t0 = ch * tiles_per_chunk, t1 = min(n_tiles, t0 + tiles_per_chunk);
+        const uint32_t uact = act_next;
+        act_next = act_of(u + gridDim.x);
+        if (!unit_active(uact, t0, t1)) {
+          n_skip += t1 - t0;
+          continue;
+        }
         const int ab = (int)(ui % ABUF);
         mbar_wait(&a_full[ab], (a_ph >> ab) & 1u);
         a_ph ^= 1u << ab;
@@ -539,6 +571,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         if (ui == 0) TC_STAMP(5);
         const uint8_t* sAb = sA + ab * S::A_BYTES;
         for (int64_t t = t0; t < t1; ++t) {
+          if (!tile_active(uact, t)) {
+            ++n_skip;
+            continue;
+          }
+          ++n_run;
           mbar_wait(&t_empty[buf], (use[buf] & 1u) ^ 1u);
           fence_after();
           // int8: the tile's per-column constants c_j into this buffer's slot
@@ -554,9 +591,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           const uint32_t nt = left >= BN ? (uint32_t)BN : (uint32_t)((left + 31) / 32 * 32);
           const uint32_t idesc = (IDESC & ~(0x3Fu << 17)) | ((nt >> 3) << 17);
           if constexpr (BRES) {
-            if (ui == 0) {   // first unit: the resident tile has landed
+            if (!((res_seen >> t) & 1u)) {   // first use: the resident tile has landed
               mbar_wait(&full[t], 0u);
               fence_after();
+              res_seen |= 1u << t;
             }
             const uint32_t bbase = su32(sB + t * S::B_STAGE);
             const uint32_t abase = su32(sAb);
@@ -601,6 +639,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           buf = buf + 1 == NBUF ? 0 : buf + 1;
         }
         mma_commit(&a_empty[ab]);
+        ++ui;
+      }
+      if (MODE == TC_MODE_MEMBER && args.stats) {
+        if (n_run) atomicAdd(&args.stats->tc_tiles_run, n_run);
+        if (n_skip) atomicAdd(&args.stats->tc_tiles_skip, n_skip);
       }
       TC_STAMP(6);
     }
@@ -622,6 +665,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // B': one band pair (p << 32 | tile column) re-decided with the oracle's
     // fp64 formula (ascending coordinates, no contraction); an in-ball pair
     // becomes a key at once (per-lane, so callable from divergent code)
+    // key position of tile column j (sorted columns under pruning)
+    auto kpos = [&](int64_t j) -> int64_t {
+      return args.col_pos ? (int64_t)__ldg(args.col_pos + j) : j;
+    };
     auto recheck = [&](unsigned long long bk) {
       const int64_t p = (int64_t)(bk >> 32), j = (int64_t)(bk & 0xffffffffull);
       if (j >= n_cols || p >= args.n) return;   // padding rows / columns never qualify
@@ -641,7 +688,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         if (args.covered) args.covered[p] = 1;
         const unsigned long long g = atomicAdd(args.key_count, 1ull);
         if ((int64_t)g < args.key_cap)
-          args.keys[g] = ((unsigned long long)p << args.lbits) | (unsigned long long)(lpos0 + j);
+          args.keys[g] = ((unsigned long long)p << args.lbits) |
+                         (unsigned long long)(lpos0 + kpos(j));
       }
     };
     auto flush = [&](void) {
@@ -700,8 +748,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
     };
     load_rows(blockIdx.x);
+    unsigned long long ck_run = 0ull, ck_skip = 0ull;   // chunks of this warp's rows
+    uint32_t act_next = act_of(blockIdx.x);
     for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
       const int64_t mb = u / n_chunks, ch = u % n_chunks;
+      const uint32_t uact = act_next;
+      act_next = act_of(u + gridDim.x);
       const int64_t t0 = ch * tiles_per_chunk, t1 = min(n_tiles, t0 + tiles_per_chunk);
       int64_t prow[RA];
       float rlo[RA], rhi[RA];
@@ -717,7 +769,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
       }
       load_rows(u + gridDim.x);
-      for (int64_t t = t0; t < t1; ++t, ++tcount) {
+      // pruning: original point of each row; the row block's near-cell mask
+      int64_t ppt[RA];
+#pragma unroll
+      for (int r = 0; r < RA; ++r)
+        ppt[r] = (args.row_pt && prow[r] < args.n) ? (int64_t)__ldg(args.row_pt + prow[r]) : prow[r];
+      for (int64_t t = t0; t < t1; ++t) {
+        if (!tile_active(uact, t)) continue;
         // both groups drain every tile: group g takes its half of the columns
         const int buf = (int)(tcount % NBUF);
         const uint32_t ph = (phase >> buf) & 1u;    // parity of buffer buf's next fill
@@ -875,11 +933,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 cand &= cand - 1u;
                 const int64_t j = j0 + i;
                 if ((inm >> i) & 1u) {
-                  if (args.covered) args.covered[prow[r]] = 1;
-                  append(1, ((unsigned long long)prow[r] << args.lbits) |
-                                (unsigned long long)(lpos0 + j));
+                  if (args.covered) args.covered[ppt[r]] = 1;
+                  append(1, ((unsigned long long)ppt[r] << args.lbits) |
+                                (unsigned long long)(lpos0 + kpos(j)));
                 } else {
-                  append(2, ((unsigned long long)prow[r] << 32) | (unsigned long long)j);
+                  append(2, ((unsigned long long)ppt[r] << 32) | (unsigned long long)j);
                 }
               }
               __syncwarp();
@@ -891,6 +949,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           // 64 columns per load (a past-the-end half is read and discarded)
 #pragma unroll 1
           for (int c = cbeg; c < cend; c += 2) {
+            const int nck = c + 1 < cend ? 2 : 1;
+            if (args.act && ((uact >> (8 * t + c)) & (nck == 2 ? 3u : 1u)) == 0u) {
+              ck_skip += nck;
+              continue;   // no landmark of these 64 columns can be near this row block
+            }
+            ck_run += nck;
             tmem_ld64_nowait(caddr(c), vv);
             tmem_wait64(vv);
             chunk(c, *reinterpret_cast<uint32_t(*)[32]>(&vv[0]));
@@ -900,10 +964,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&t_empty[buf]);
+        ++tcount;
       }
     }
     flush();
     if (q == 0 && lane == 0) TC_STAMP(9 + grp);
+    // every chunk is read by the four warps of its group (32 rows each): count
+    // it once, from warp q == 0
+    if (MODE == TC_MODE_MEMBER && args.stats && q == 0 && lane == 0) {
+      if (ck_run) atomicAdd(&args.stats->tc_chunks_run, ck_run);
+      if (ck_skip) atomicAdd(&args.stats->tc_chunks_skip, ck_skip);
+    }
   }
   fence_before();
   __syncthreads();
@@ -1025,6 +1096,10 @@ static cudaError_t dispatch(const TcPlan& P, const TcArgs& a, cudaStream_t s) {
     if (P.katoms == 1 && bres_ok(P, a, 4))
       return launch_cfg<TC_TF32, 1, 256, 1, 4, 3, MODE, true>(P, a, s);
     if (P.katoms == 1) return launch_cfg<TC_TF32, 1, 256, 1, 4, 2, MODE>(P, a, s);
+    // pruned launches run few tiles per point block: the A stream (HBM) is the
+    // bound, so more A buffers in flight at the cost of one B stage
+    if (P.katoms <= 2 && a.act && MODE == TC_MODE_MEMBER)
+      return launch_cfg<TC_TF32, 1, 256, 2, 3, 3, MODE>(P, a, s);
     if (P.katoms <= 2) return launch_cfg<TC_TF32, 1, 256, 2, 4, 2, MODE>(P, a, s);
     if (P.katoms <= 4) return launch_cfg<TC_TF32, 1, 256, 4, 4, 1, MODE>(P, a, s);
     return cudaErrorNotSupported;

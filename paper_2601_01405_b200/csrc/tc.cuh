@@ -77,6 +77,14 @@ struct TcArgs {
   int adj_T;
   uint8_t* covered;    // fused greedy: covered[p] = 1 for every in-ball pair (may be null)
   unsigned long long* trace;   // diagnostics: [grid][16] %globaltimer stamps (null: off)
+  // tile-level pruning (cells.cu; all null when off): A rows are permuted
+  // (row r is point row_pt[r]); columns are the tile's landmarks sorted by
+  // cell (key position lpos0 + col_pos[j]); a 256-column tile / 32-column
+  // chunk whose cell mask meets no cell of the row block's near mask is
+  // skipped (no MMA / no TMEM read)
+  const int32_t* row_pt;
+  const int32_t* col_pos;
+  const uint32_t* act;     // [row block]: bit 8 t + c = chunk c of tile t is live
 };
 
 int tc_bn_for(int kind, int katoms);

@@ -113,3 +113,40 @@ def test_tensor_path_cosine_c5_prefix(bm):
     cov = bm.cover_build(torch.from_numpy(X).cuda(), w.metric, w.eps, path="tensor")
     assert cov.stats.path_used == 2
     compare(X, w.metric, w.eps, cov, float_path=True, tie_rate_limit=True)
+
+
+@pytest.mark.parametrize("name,m", [("c3_e8", 20000), ("c3_e4", 12000), ("c3_e2", 6000),
+                                    ("c2", None)])
+def test_pruned_contraction_parity(bm, name, m):
+    """Tile-level pruning (cells.cu): forced on below its size threshold, the
+    cover equals the unpruned one and the oracle's."""
+    from paper_2601_01405_b200 import bm as B
+    w = gen.get(name)
+    X = gen.generate(w, m)
+    t = torch.from_numpy(X).cuda()
+    a = bm.cover_build(t, w.metric, w.eps, path="tensor", flags=B.FLAG_FORCE_PRUNE)
+    b = bm.cover_build(t, w.metric, w.eps, path="tensor", flags=B.FLAG_NO_PRUNE)
+    na, nb = a.numpy(), b.numpy()
+    for k in na:
+        assert np.array_equal(na[k], nb[k]), k
+    compare(X, w.metric, w.eps, a, float_path=True)
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_pruned_contraction_clusters(bm, seed):
+    """Well-separated clusters (most tiles pruned), points at exactly eps and
+    just inside / outside it across cluster borders."""
+    from paper_2601_01405_b200 import bm as B
+    rng = np.random.default_rng([seed, 77])
+    d, k = 24, 12
+    centres = rng.normal(size=(k, d)) * 20.0
+    X = (centres[rng.integers(0, k, size=9000)] + rng.normal(size=(9000, d))).astype(np.float32)
+    eps = 3.0
+    X[1::97] = X[0::97][: len(X[1::97])] + np.float32(eps / math.sqrt(d))   # |dx| = eps
+    t = torch.from_numpy(X).cuda()
+    a = bm.cover_build(t, "l2", eps, path="tensor", flags=B.FLAG_FORCE_PRUNE, tile=256)
+    b = bm.cover_build(t, "l2", eps, path="tensor", flags=B.FLAG_NO_PRUNE, tile=256)
+    na, nb = a.numpy(), b.numpy()
+    for key in na:
+        assert np.array_equal(na[key], nb[key]), key
+    compare(X, "l2", eps, a, float_path=True)
