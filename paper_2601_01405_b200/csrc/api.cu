@@ -641,7 +641,7 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
 
   // ---- tile-level pruning of the tensor-core membership (cells.cu): fp32
   // Euclidean, large n (the preparation costs ~1 ms at n = 1e6)
-  const bool prune = use_tc && dtype == BM_F32 && metric == BM_L2 && d <= 128 &&
+  const bool prune = use_tc && dtype == BM_F32 && metric == BM_L2 && P.katoms <= 2 &&
                      n >= 4 * kPruneCells && !(o.flags & BM_FLAG_NO_PRUNE) &&
                      (n >= 262144 || (o.flags & BM_FLAG_FORCE_PRUNE));
   PruneState ps{};

@@ -344,7 +344,10 @@ constexpr int TC_THREADS = 384;   // warps 0-3 roles, 4-11 epilogue
 // shared memory; only the point blocks stream.  Without it every work unit
 // re-reads the same B tiles, and 148 SMs reading the same lines at once is
 // bounded by the L2 slices that hold them (measured: C5 cosine, d = 16).
-template <int KIND, int RA, int BN, int KATOMS, int STAGES, int ABUF, int MODE, bool BRES>
+// PR: the launch is pruned (cells.cu; args.act, row_pt, col_pos set) — a
+// separate instance, so the unpruned kernels carry none of its code.
+template <int KIND, int RA, int BN, int KATOMS, int STAGES, int ABUF, int MODE, bool BRES,
+          bool PR>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     k_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
          const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmO,
@@ -449,22 +452,25 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const int64_t tiles_per_chunk = n_tiles > 0 ? (n_tiles + n_chunks - 1) / n_chunks : 1;
   n_chunks = n_tiles > 0 ? (n_tiles + tiles_per_chunk - 1) / tiles_per_chunk : 0;
   const int64_t n_units = args.n_mblk * n_chunks;
-  // pruning: may row block mb hold an in-ball pair with a landmark of tile t?
-  // (every role evaluates the same predicate, so they skip the same tiles)
-  // (ab: the unit's live-chunk word, args.act[mb], or all ones without pruning)
-  // (only the fused greedy tile, <= 4 tiles, is pruned: t < 4 whenever act is set)
+  // pruning: may the unit's row block hold an in-ball pair with a landmark of
+  // tile t?  ab = the unit's live-chunk word args.act[mb]; every role
+  // evaluates the same predicate, so they skip the same tiles.  (Only the
+  // fused greedy tile, <= 4 tiles, is pruned: t < 4.)
   auto tile_active = [&](uint32_t ab, int64_t t) -> bool {
-    return !args.act || ((ab >> (8 * t)) & 0xffu) != 0u;
+    if constexpr (!PR) return true;
+    return ((ab >> (8 * t)) & 0xffu) != 0u;
   };
   // a unit none of whose tiles is live is skipped whole (no A block load)
   auto unit_active = [&](uint32_t ab, int64_t t0, int64_t t1) -> bool {
+    if constexpr (!PR) return true;
     for (int64_t t = t0; t < t1; ++t)
       if (tile_active(ab, t)) return true;
     return false;
   };
   // the live-chunk word of unit u (prefetched one unit ahead by every role)
   auto act_of = [&](int64_t u) -> uint32_t {
-    return (args.act && u < n_units) ? __ldg(args.act + u / n_chunks) : 0xffffffffu;
+    if constexpr (!PR) return 0xffffffffu;
+    return u < n_units ? __ldg(args.act + u / n_chunks) : 0u;
   };
 
   if (warp == 0) {
@@ -667,7 +673,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // becomes a key at once (per-lane, so callable from divergent code)
     // key position of tile column j (sorted columns under pruning)
     auto kpos = [&](int64_t j) -> int64_t {
-      return args.col_pos ? (int64_t)__ldg(args.col_pos + j) : j;
+      if constexpr (PR) return (int64_t)__ldg(args.col_pos + j);
+      return j;
     };
     auto recheck = [&](unsigned long long bk) {
       const int64_t p = (int64_t)(bk >> 32), j = (int64_t)(bk & 0xffffffffull);
@@ -772,8 +779,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       // pruning: original point of each row; the row block's near-cell mask
       int64_t ppt[RA];
 #pragma unroll
-      for (int r = 0; r < RA; ++r)
-        ppt[r] = (args.row_pt && prow[r] < args.n) ? (int64_t)__ldg(args.row_pt + prow[r]) : prow[r];
+      for (int r = 0; r < RA; ++r) {
+        if constexpr (PR) ppt[r] = prow[r] < args.n ? (int64_t)__ldg(args.row_pt + prow[r]) : prow[r];
+        else ppt[r] = prow[r];
+      }
       for (int64_t t = t0; t < t1; ++t) {
         if (!tile_active(uact, t)) continue;
         // both groups drain every tile: group g takes its half of the columns
@@ -949,12 +958,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           // 64 columns per load (a past-the-end half is read and discarded)
 #pragma unroll 1
           for (int c = cbeg; c < cend; c += 2) {
-            const int nck = c + 1 < cend ? 2 : 1;
-            if (args.act && ((uact >> (8 * t + c)) & (nck == 2 ? 3u : 1u)) == 0u) {
-              ck_skip += nck;
-              continue;   // no landmark of these 64 columns can be near this row block
+            if constexpr (PR) {
+              const int nck = c + 1 < cend ? 2 : 1;
+              if (((uact >> (8 * t + c)) & (nck == 2 ? 3u : 1u)) == 0u) {
+                ck_skip += nck;
+                continue;   // no landmark of these 64 columns can be near this row block
+              }
+              ck_run += nck;
             }
-            ck_run += nck;
             tmem_ld64_nowait(caddr(c), vv);
             tmem_wait64(vv);
             chunk(c, *reinterpret_cast<uint32_t(*)[32]>(&vv[0]));
@@ -1036,7 +1047,8 @@ static cudaError_t make_tmap8(CUtensorMap* tm, const void* base, int64_t rows, i
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
-template <int KIND, int RA, int BN, int KATOMS, int STAGES, int ABUF, int MODE, bool BRES = false>
+template <int KIND, int RA, int BN, int KATOMS, int STAGES, int ABUF, int MODE, bool BRES = false,
+          bool PR = false>
 static cudaError_t launch_cfg(const TcPlan& P, TcArgs a, cudaStream_t s) {
   constexpr bool FOLD = KIND == TC_TF32 && MODE != TC_MODE_GRAM;
   using S = Smem<RA, BN, KATOMS, STAGES, ABUF, FOLD, BRES>;
@@ -1056,7 +1068,8 @@ static cudaError_t launch_cfg(const TcPlan& P, TcArgs a, cudaStream_t s) {
     tK = tB;
     tO = tB;
   }
-  auto kern = k_tc<KIND, RA, BN, KATOMS, STAGES, ABUF, MODE, BRES>;
+  if (PR != (a.act != nullptr)) return cudaErrorInvalidValue;   // instance / arguments agree
+  auto kern = k_tc<KIND, RA, BN, KATOMS, STAGES, ABUF, MODE, BRES, PR>;
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::TOTAL);
   if (e != cudaSuccess) return e;
   a.n_mblk = (P.n_rows + RA * 128 - 1) / (RA * 128);
@@ -1093,13 +1106,19 @@ static cudaError_t dispatch(const TcPlan& P, const TcArgs& a, cudaStream_t s) {
   // one-atom rows get their own instance: a wider template would move (and
   // TMA-zero-fill) a second, all-padding K atom for every A block and B tile
   if (P.kind == TC_TF32) {
+    // pruned launches (the fused greedy tile, <= 1024 columns: B stays
+    // resident for one-atom rows); for two atoms the A stream is the bound, so
+    // more A buffers in flight at the cost of one B stage
+    if constexpr (MODE == TC_MODE_MEMBER) {
+      if (a.act && P.katoms == 1)
+        return launch_cfg<TC_TF32, 1, 256, 1, 4, 3, MODE, true, true>(P, a, s);
+      if (a.act && P.katoms <= 2)
+        return launch_cfg<TC_TF32, 1, 256, 2, 3, 3, MODE, false, true>(P, a, s);
+      if (a.act) return cudaErrorNotSupported;
+    }
     if (P.katoms == 1 && bres_ok(P, a, 4))
       return launch_cfg<TC_TF32, 1, 256, 1, 4, 3, MODE, true>(P, a, s);
     if (P.katoms == 1) return launch_cfg<TC_TF32, 1, 256, 1, 4, 2, MODE>(P, a, s);
-    // pruned launches run few tiles per point block: the A stream (HBM) is the
-    // bound, so more A buffers in flight at the cost of one B stage
-    if (P.katoms <= 2 && a.act && MODE == TC_MODE_MEMBER)
-      return launch_cfg<TC_TF32, 1, 256, 2, 3, 3, MODE>(P, a, s);
     if (P.katoms <= 2) return launch_cfg<TC_TF32, 1, 256, 2, 4, 2, MODE>(P, a, s);
     if (P.katoms <= 4) return launch_cfg<TC_TF32, 1, 256, 4, 4, 1, MODE>(P, a, s);
     return cudaErrorNotSupported;
