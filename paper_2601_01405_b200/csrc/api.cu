@@ -780,6 +780,8 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
       ta.row_pt = ps.perm;
       ta.col_pos = ps.col_pos;
       ta.act = ps.act;
+      ta.act_bmask = ps.bmask;
+      ta.act_cmask = ps.cmask;
     }
   }
   if (tc_adj) {
@@ -930,11 +932,13 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
       loop_mark(1);
       // A3: in-order resolve, append landmarks (resets the tile's counters)
       CK(launch_resolve(adj, adj_words, uncb[cur], cnt + cur, T, lm, cnt + 2, new_lm, cnt + 3,
-                        stats, cnt + 4, nullptr, s, &launches));
+                        stats, cnt + 4, nullptr, s, &launches,
+                        prune ? PruneTile{ps.cell, ps.rank, ps.col_pt, ps.col_pos, ps.cmask,
+                                          ps.tmask}
+                              : PruneTile{}));
       loop_mark(2);
       // B (+A4 marks): membership of every point in the new balls
       if (use_tc) {
-        if (prune) CK(launch_tile_sort(new_lm, cnt + 3, ps, n, s, &launches));
         CK(tc::launch_tc_tile_landmarks(P, tc_nrm, prune ? ps.col_pt : new_lm, cnt + 3, C2, ta, s,
                                         &launches));
         CK(mark_member());

@@ -347,30 +347,6 @@ __global__ void __launch_bounds__(1024) k_tile_sort(const int32_t* __restrict__ 
   }
 }
 
-// per row block: which 32-column chunks of this greedy tile may hold an
-// in-ball pair (one word, read once per work unit by every role of k_tc)
-__global__ void k_unit_act(const uint32_t* __restrict__ bmask, const uint32_t* __restrict__ cmask,
-                           int64_t nblk, uint32_t* __restrict__ act) {
-  __shared__ uint32_t scm[32 * KW];
-  pdl_wait();
-  pdl_trigger();   // one wave
-  for (int t = threadIdx.x; t < 32 * KW; t += blockDim.x) scm[t] = cmask[t];
-  __syncthreads();
-  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= nblk) return;
-  uint32_t bm[KW];
-#pragma unroll
-  for (int w = 0; w < KW; ++w) bm[w] = bmask[b * KW + w];
-  uint32_t bits = 0u;
-  for (int c = 0; c < 32; ++c) {
-    uint32_t x = 0u;
-#pragma unroll
-    for (int w = 0; w < KW; ++w) x |= bm[w] & scm[c * KW + w];
-    bits |= (x != 0u ? 1u : 0u) << c;
-  }
-  act[b] = bits;
-}
-
 cudaError_t prune_prepare(const float* xrows, int xstride, int d, int64_t n, double eps,
                           const uint8_t* xop, int64_t row_bytes, const double* nrm, PruneState& ps,
                           void* sort_temp, unsigned long long* keys, unsigned long long* alt,
@@ -441,13 +417,10 @@ cudaError_t prune_prepare(const float* xrows, int xstride, int d, int64_t n, dou
 
 cudaError_t launch_tile_sort(const int32_t* new_lm, const int32_t* dL_dev, const PruneState& ps,
                              int64_t n, cudaStream_t s, int64_t* launches) {
-  *launches += 2;
-  cudaError_t e = launch_pdl(k_tile_sort, dim3(1), dim3(1024), 0, s, new_lm, dL_dev, ps.cell,
-                             ps.rank, ps.col_pt, ps.col_pos, ps.cmask, ps.tmask);
-  if (e != cudaSuccess) return e;
-  const int64_t nblk = (n + 127) / 128;
-  return launch_pdl(k_unit_act, dim3((unsigned)((nblk + 255) / 256)), dim3(256), 0, s,
-                    (const uint32_t*)ps.bmask, (const uint32_t*)ps.cmask, nblk, ps.act);
+  ++*launches;
+  (void)n;   // the live-chunk words are folded by the landmark-operand launch (tc.cu)
+  return launch_pdl(k_tile_sort, dim3(1), dim3(1024), 0, s, new_lm, dL_dev, ps.cell, ps.rank,
+                    ps.col_pt, ps.col_pos, ps.cmask, ps.tmask);
 }
 
 }  // namespace bm

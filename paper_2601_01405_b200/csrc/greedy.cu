@@ -87,9 +87,12 @@ __global__ void __launch_bounds__(1024) k_resolve(const uint32_t* __restrict__ a
                                                   int32_t* __restrict__ new_lm,
                                                   int32_t* __restrict__ dL_dev, DevStats* stats,
                                                   int32_t* __restrict__ ticket,
-                                                  unsigned long long* __restrict__ band_count) {
+                                                  unsigned long long* __restrict__ band_count,
+                                                  PruneTile pt_out) {
   __shared__ volatile uint32_t lmw[32];
   __shared__ int wpre[33];
+  __shared__ uint32_t skey[1024];      // pruning: (cell rank << 16 | position) sort keys
+  __shared__ uint32_t scm[32 * 8];     // pruning: cell masks of the 32-column chunks
   extern __shared__ uint32_t sadj[];
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
   pdl_wait();
@@ -118,6 +121,11 @@ __global__ void __launch_bounds__(1024) k_resolve(const uint32_t* __restrict__ a
     wpre[tid + 1] = incl;
     if (tid == 0) wpre[0] = 0;
   }
+  const bool prune = pt_out.cell != nullptr;
+  if (prune) {
+    skey[tid] = 0xffffffffu;
+    if (tid < 32 * 8) scm[tid] = 0u;
+  }
   __syncthreads();
   const int L0 = *L_dev;
   if (w < nb && tid < nc) {
@@ -127,9 +135,44 @@ __global__ void __launch_bounds__(1024) k_resolve(const uint32_t* __restrict__ a
       const int32_t pt = unc[tid];
       new_lm[pos] = pt;
       lm_out[L0 + pos] = pt;
+      if (prune) skey[pos] = ((uint32_t)pt_out.rank[pt_out.cell[pt]] << 16) | (uint32_t)pos;
     }
   }
   __syncthreads();
+  if (prune) {
+    // the new landmarks sorted by (cell rank, position) — bitonic over 1024
+    // keys — and the cell masks of every 32-column chunk / 256-column tile
+    for (int k = 2; k <= 1024; k <<= 1) {
+      for (int sj = k >> 1; sj > 0; sj >>= 1) {
+        const int o = tid ^ sj;
+        if (o > tid) {
+          const uint32_t a = skey[tid], b = skey[o];
+          if ((a > b) == ((tid & k) == 0)) {
+            skey[tid] = b;
+            skey[o] = a;
+          }
+        }
+        __syncthreads();
+      }
+    }
+    const int dL = wpre[nb];
+    if (tid < dL) {
+      const int src = (int)(skey[tid] & 0xffffu);
+      const int32_t p = new_lm[src];   // written above by this CTA
+      pt_out.col_pt[tid] = p;
+      pt_out.col_pos[tid] = src;
+      const int c = pt_out.cell[p];
+      atomicOr(&scm[(tid >> 5) * 8 + (c >> 5)], 1u << (c & 31));
+    }
+    __syncthreads();
+    if (tid < 32 * 8) pt_out.cmask[tid] = scm[tid];
+    if (tid < 4 * 8) {
+      const int t = tid >> 3, wd = tid & 7;
+      uint32_t v = 0u;
+      for (int c = 0; c < 8; ++c) v |= scm[(t * 8 + c) * 8 + wd];
+      pt_out.tmask[tid] = v;
+    }
+  }
   if (tid == 0) {
     const int dL = wpre[nb];
     *dL_dev = dL;
@@ -152,7 +195,8 @@ __global__ void __launch_bounds__(1024) k_resolve_debug(const uint32_t* __restri
 cudaError_t launch_resolve(const uint32_t* adj, int adj_words, const int32_t* unc,
                            const int32_t* n_unc, int T, int32_t* lm_out, int32_t* L_dev,
                            int32_t* new_lm, int32_t* dL_dev, DevStats* stats, int32_t* ticket,
-                           unsigned long long* band_count, cudaStream_t s, int64_t* launches) {
+                           unsigned long long* band_count, cudaStream_t s, int64_t* launches,
+                           PruneTile pt_out) {
   ++*launches;
   const size_t smem = sizeof(uint32_t) * 32 * (size_t)adj_words * adj_words;
   static bool attr = false;   // (one attribute call per process; T <= 1024)
@@ -166,7 +210,7 @@ cudaError_t launch_resolve(const uint32_t* adj, int adj_words, const int32_t* un
     attr = true;
   }
   return launch_pdl(k_resolve, dim3(1), dim3(1024), smem, s, adj, adj_words, unc, n_unc, T,
-                    lm_out, L_dev, new_lm, dL_dev, stats, ticket, band_count);
+                    lm_out, L_dev, new_lm, dL_dev, stats, ticket, band_count, pt_out);
 }
 
 cudaError_t launch_resolve_debug(const uint32_t* adj, int adj_words, int nc, uint8_t* lm,

@@ -163,11 +163,21 @@ cudaError_t launch_l1_quantize(const float* X, int64_t n, int d, int nq, double*
                                uint32_t* qrows, cudaStream_t s, int64_t* launches);
 
 // A3; also resets the per-tile device counters (*ticket = 0, *band_count = 0).
+// pruning outputs of A3 (cells.cu): the tile's landmarks sorted by cell rank
+// and the chunk / tile cell masks (all null: no pruning)
+struct PruneTile {
+  const int32_t* cell;
+  const int32_t* rank;
+  int32_t* col_pt;
+  int32_t* col_pos;
+  uint32_t* cmask;
+  uint32_t* tmask;
+};
 cudaError_t launch_resolve(const uint32_t* adj, int adj_words, const int32_t* unc,
                            const int32_t* n_unc, int T, int32_t* lm_out, int32_t* L_dev,
                            int32_t* new_lm, int32_t* dL_dev, DevStats* stats,
                            int32_t* ticket, unsigned long long* band_count,
-                           cudaStream_t s, int64_t* launches);
+                           cudaStream_t s, int64_t* launches, PruneTile pt_out = PruneTile{});
 
 // Order-preserving compaction of the uncovered list after a tile: keeps
 // unc[i], nc <= i < n_unc, with covered[unc[i]] == 0 (single pass, decoupled

@@ -1322,9 +1322,33 @@ __global__ void k_tc_tile_lm(const uint8_t* __restrict__ xop, int64_t row_bytes,
                              const int32_t* __restrict__ l_count_dev, int kind, int cosine,
                              const void* __restrict__ nrm, double C2, uint8_t* __restrict__ lop,
                              float* __restrict__ ca, float* __restrict__ cb,
-                             float* __restrict__ colk, int32_t* __restrict__ cc) {
+                             float* __restrict__ colk, int32_t* __restrict__ cc,
+                             int64_t n_lm_blocks, const uint32_t* __restrict__ bmask,
+                             const uint32_t* __restrict__ cmask, int64_t nblk,
+                             uint32_t* __restrict__ act) {
   pdl_wait();
   pdl_trigger();   // one wave
+  if (blockIdx.x >= n_lm_blocks) {
+    // pruning (cells.cu): per row block, which 32-column chunks of this tile
+    // may hold an in-ball pair — one word per block for k_tc
+    __shared__ uint32_t scm[32 * 8];
+    for (int t = threadIdx.x; t < 32 * 8; t += blockDim.x) scm[t] = cmask[t];
+    __syncthreads();
+    const int64_t b = (blockIdx.x - n_lm_blocks) * (int64_t)blockDim.x + threadIdx.x;
+    if (b >= nblk) return;
+    uint32_t bm[8];
+#pragma unroll
+    for (int w = 0; w < 8; ++w) bm[w] = bmask[b * 8 + w];
+    uint32_t bits = 0u;
+    for (int c = 0; c < 32; ++c) {
+      uint32_t x = 0u;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) x |= bm[w] & scm[c * 8 + w];
+      bits |= (x != 0u ? 1u : 0u) << c;
+    }
+    act[b] = bits;
+    return;
+  }
   const int64_t j = blockIdx.x;
   const int64_t cnt = *l_count_dev;
   const bool live = j < cnt;
@@ -1348,11 +1372,16 @@ cudaError_t launch_tc_tile_landmarks(const TcPlan& P, const void* nrm, const int
                                      const int32_t* l_count_dev, double C2, TcArgs& a,
                                      cudaStream_t s, int64_t* launches) {
   ++*launches;
-  return launch_pdl(k_tc_tile_lm, dim3((unsigned)P.l_rows), dim3(64), 0, s,
+  // (pruned launches: extra CTAs fold the row-block and chunk cell masks into
+  // a.act in the same launch)
+  const int64_t nblk = a.act ? (P.n_rows + 127) / 128 : 0;
+  const int64_t extra = (nblk + 63) / 64;
+  return launch_pdl(k_tc_tile_lm, dim3((unsigned)(P.l_rows + extra)), dim3(64), 0, s,
                     (const uint8_t*)P.xop, P.row_bytes, new_lm, l_count_dev, P.kind, P.cosine,
                     nrm, C2,
                     (uint8_t*)P.lop, (float*)a.col_a, (float*)a.col_b, (float*)a.colk,
-                    (int32_t*)a.col_c);
+                    (int32_t*)a.col_c, (int64_t)P.l_rows, a.act_bmask, a.act_cmask, nblk,
+                    (uint32_t*)a.act);
 }
 
 

@@ -85,6 +85,8 @@ struct TcArgs {
   const int32_t* row_pt;
   const int32_t* col_pos;
   const uint32_t* act;     // [row block]: bit 8 t + c = chunk c of tile t is live
+  const uint32_t* act_bmask;   // its inputs (cells.cu), folded by the landmark-operand
+  const uint32_t* act_cmask;   //   launch of each greedy tile
 };
 
 int tc_bn_for(int kind, int katoms);
