@@ -230,7 +230,7 @@ cudaError_t launch_resolve_debug(const uint32_t* adj, int adj_words, int nc, uin
 // publishes its count, and derives its output offset by looking back over the
 // predecessors' published (aggregate | inclusive prefix) words.  Words carry the
 // launch tag, so the state array never needs clearing between tiles.
-constexpr int CP_NT = 256, CP_ROUNDS = 16, CP_TILE = CP_NT * CP_ROUNDS;
+constexpr int CP_NT = 256, CP_ROUNDS = 8, CP_TILE = CP_NT * CP_ROUNDS;
 
 __global__ void __launch_bounds__(CP_NT) k_compact(const uint8_t* __restrict__ covered,
                                                    const int32_t* __restrict__ unc,
