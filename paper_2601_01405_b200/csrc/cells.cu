@@ -12,8 +12,9 @@
 // and if they are not near every pair (p in a, l in b) has
 //   d(p, l) >= |c_a - c_b| - r_a - r_b >= eps (1 + 4e-6):
 // out, and outside the 1e-6 eps near-tie band, so it may be skipped.
-// Per greedy tile the new landmarks are sorted by cell rank (stable) and each
-// 32-column chunk gets the bit set of its landmarks' cells; the contraction
+// Per greedy tile the new landmarks are sorted by cell rank (stable; in the
+// resolve CTA, greedy.cu) and each 32-column chunk gets the bit set of its
+// landmarks' cells; the contraction
 // skips a chunk whose cells are near none of the row block's cells (no TMEM
 // read) and a whole 256-column tile whose chunks are all skipped (no MMA).
 #include <math.h>
@@ -295,58 +296,6 @@ __global__ void k_gather_f64(const double* __restrict__ src, const int32_t* __re
   if (r < n) dst[r] = src[perm[r]];
 }
 
-// One greedy tile: sort its dL new landmarks by (cell rank, position) —
-// bitonic over 1024 keys in shared memory — and build the per-chunk and
-// per-256-column-tile cell masks.
-__global__ void __launch_bounds__(1024) k_tile_sort(const int32_t* __restrict__ new_lm,
-                                                    const int32_t* __restrict__ dL_dev,
-                                                    const int32_t* __restrict__ cell,
-                                                    const int32_t* __restrict__ rank,
-                                                    int32_t* __restrict__ col_pt,
-                                                    int32_t* __restrict__ col_pos,
-                                                    uint32_t* __restrict__ cmask,
-                                                    uint32_t* __restrict__ tmask) {
-  __shared__ uint32_t key[1024];
-  __shared__ uint32_t scm[32 * KW];
-  pdl_wait();
-  pdl_trigger();   // one CTA
-  const int j = threadIdx.x;
-  const int dL = min(*dL_dev, 1024);
-  key[j] = j < dL ? ((uint32_t)rank[cell[new_lm[j]]] << 16) | (uint32_t)j : 0xffffffffu;
-  if (j < 32 * KW) scm[j] = 0u;
-  __syncthreads();
-  for (int k = 2; k <= 1024; k <<= 1) {
-    for (int s = k >> 1; s > 0; s >>= 1) {
-      const int o = j ^ s;
-      if (o > j) {
-        const uint32_t a = key[j], b = key[o];
-        const bool up = (j & k) == 0;
-        if ((a > b) == up) {
-          key[j] = b;
-          key[o] = a;
-        }
-      }
-      __syncthreads();
-    }
-  }
-  if (j < dL) {
-    const int src = (int)(key[j] & 0xffffu);
-    const int32_t pt = new_lm[src];
-    col_pt[j] = pt;
-    col_pos[j] = src;
-    const int c = cell[pt];
-    atomicOr(&scm[(j >> 5) * KW + (c >> 5)], 1u << (c & 31));
-  }
-  __syncthreads();
-  if (j < 32 * KW) cmask[j] = scm[j];
-  if (j < 4 * KW) {   // tile t = j / KW: OR of its eight chunks
-    const int t = j / KW, w = j - t * KW;
-    uint32_t v = 0u;
-    for (int c = 0; c < 8; ++c) v |= scm[(t * 8 + c) * KW + w];
-    tmask[j] = v;
-  }
-}
-
 cudaError_t prune_prepare(const float* xrows, int xstride, int d, int64_t n, double eps,
                           const uint8_t* xop, int64_t row_bytes, const double* nrm, PruneState& ps,
                           void* sort_temp, unsigned long long* keys, unsigned long long* alt,
@@ -413,14 +362,6 @@ cudaError_t prune_prepare(const float* xrows, int xstride, int d, int64_t n, dou
     for (int i = 0; i < npe; ++i) cudaEventDestroy(pe[i]);
   }
   return cudaGetLastError();
-}
-
-cudaError_t launch_tile_sort(const int32_t* new_lm, const int32_t* dL_dev, const PruneState& ps,
-                             int64_t n, cudaStream_t s, int64_t* launches) {
-  ++*launches;
-  (void)n;   // the live-chunk words are folded by the landmark-operand launch (tc.cu)
-  return launch_pdl(k_tile_sort, dim3(1), dim3(1024), 0, s, new_lm, dL_dev, ps.cell, ps.rank,
-                    ps.col_pt, ps.col_pos, ps.cmask, ps.tmask);
 }
 
 }  // namespace bm

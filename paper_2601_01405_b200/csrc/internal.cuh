@@ -245,14 +245,13 @@ struct PruneState {
   uint32_t* cmask;      // [32 chunks][K/32] cells of each 32-column chunk
   uint32_t* tmask;      // [4 tiles][K/32] cells of each 256-column tile
   uint32_t* act;        // [ceil(n/128)] per row block: bit 8 t + c = chunk c of tile t may
-                        // hold an in-ball pair (from bmask and cmask, per greedy tile)
+                        // hold an in-ball pair (from bmask and cmask, per greedy tile,
+                        // folded by the landmark-operand launch, tc.cu)
 };
 cudaError_t prune_prepare(const float* xrows, int xstride, int d, int64_t n, double eps,
                           const uint8_t* xop, int64_t row_bytes, const double* nrm, PruneState& ps,
                           void* sort_temp, unsigned long long* keys, unsigned long long* alt,
                           cudaStream_t s, int64_t* launches);
-cudaError_t launch_tile_sort(const int32_t* new_lm, const int32_t* dL_dev, const PruneState& ps,
-                             int64_t n, cudaStream_t s, int64_t* launches);
 
 // fps.cu (NEXT-2)
 int fps_max_candidates();
