@@ -873,9 +873,28 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
     TRY(pool.alloc(&cval, (size_t)2 * g));
     TRY(pool.alloc(&cidx, (size_t)2 * g));
     const double thr = metric == BM_L2 ? eps * eps : eps;
+    // float L2 / L1: points in spatial (cell) order so that each warp of the
+    // selection kernel can skip the landmarks that cannot lower its minima
+    int32_t* fperm = nullptr;
+    if ((kind == K_L2F || kind == K_L1F) && d <= 128 && n >= 4 * kPruneCells &&
+        !(o.flags & BM_FLAG_NO_PRUNE)) {
+      int32_t *fcell = nullptr, *frank = nullptr;
+      float* fpd = nullptr;
+      unsigned long long *fk = nullptr, *fa = nullptr;
+      void* ftemp = nullptr;
+      TRY(pool.alloc(&fperm, (size_t)n));
+      TRY(pool.alloc(&fcell, (size_t)n));
+      TRY(pool.alloc(&frank, (size_t)kPruneCells));
+      TRY(pool.alloc(&fpd, (size_t)kPruneCells * kPruneCells));
+      TRY(pool.alloc(&fk, (size_t)n));
+      TRY(pool.alloc(&fa, (size_t)n));
+      TRY(pool.alloc((uint8_t**)&ftemp, radix_temp_bytes(n)));
+      CK(cell_order((const float*)rows, 2 * nu, d, n, fcell, frank, fpd, &fk, &fa, ftemp, fperm, s,
+                    &launches));
+    }
     tm.mark(6);
     CK(launch_fps(rows, inorm, nu, d, kind, n, thr, o.fps_start, mind, seq, cnt + 2, cval, cidx,
-                  s));
+                  fperm, s));
     tm.mark(7);
     ++launches;
     int32_t hl = 0;

@@ -296,6 +296,34 @@ __global__ void k_gather_f64(const double* __restrict__ src, const int32_t* __re
   if (r < n) dst[r] = src[perm[r]];
 }
 
+// The spatial order alone (also used by the FPS kernel): cells, pivot chain,
+// points sorted by (cell rank, index) into perm; keys hold the sorted keys.
+cudaError_t cell_order(const float* xrows, int xstride, int d, int64_t n, int32_t* cell,
+                       int32_t* rank, float* pdist, unsigned long long** keys,
+                       unsigned long long** alt, void* sort_temp, int32_t* perm, cudaStream_t s,
+                       int64_t* launches) {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int dmax = d <= 32 ? 32 : (d <= 64 ? 64 : 128);
+  const size_t smem = sizeof(float) * KC * dmax;
+  auto kern = d <= 32 ? k_cell_assign<32> : (d <= 64 ? k_cell_assign<64> : k_cell_assign<128>);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  kern<<<sms * 2, 256, smem, s>>>(xrows, xstride, d, n, cell);
+  k_pivot_dist<<<KC, KC, 0, s>>>(xrows, xstride, d, n, pdist);
+  k_pivot_chain<<<1, 32, 0, s>>>(pdist, rank);
+  k_cell_keys<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(cell, rank, n, *keys);
+  *launches += 4;
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const BitRange br[2] = {{0, 32}, {32, 40}};
+  e = radix_sort_u64(keys, alt, n, br, 2, sort_temp, s, launches);
+  if (e != cudaSuccess) return e;
+  return launch_unpack_low(*keys, n, 0xffffffffull, perm, s, launches);
+}
+
 cudaError_t prune_prepare(const float* xrows, int xstride, int d, int64_t n, double eps,
                           const uint8_t* xop, int64_t row_bytes, const double* nrm, PruneState& ps,
                           void* sort_temp, unsigned long long* keys, unsigned long long* alt,

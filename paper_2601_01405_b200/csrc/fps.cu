@@ -14,6 +14,8 @@
 // taken in the same precision as the oracle's (F3).
 #include <cooperative_groups.h>
 #include <math.h>
+#include <stdio.h>
+#include <stdlib.h>
 
 #include "internal.cuh"
 
@@ -33,6 +35,8 @@ struct FpsArgs {
   int32_t* L_out;
   double* cval;        // [2][grid] candidate values
   int64_t* cidx;       // [2][grid] candidate indices
+  const int32_t* perm; // spatial order (null: strided ownership, no pruning)
+  unsigned long long* dbg;   // diagnostics (BM_FPS_DEBUG): [0] warp-steps, [1] skipped
 };
 
 // d(x_p, l) with l's units in shared memory.  Float kinds: the oracle's fp64
@@ -105,6 +109,15 @@ constexpr int FPS_MAX_CAND = 1024;   // grid size bound
 
 // PPT > 0: each thread owns points gt + k * gs (k < PPT) with their running
 // minimum in registers; PPT == 0: any n, running minimum in a.mind.
+__device__ __forceinline__ double warp_sum_d(double x) {
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+__device__ __forceinline__ double warp_max_d(double x) {
+  for (int o = 16; o > 0; o >>= 1) x = fmax(x, __shfl_xor_sync(0xffffffffu, x, o));
+  return x;
+}
+
 template <int KIND, int PPT>
 __global__ void __launch_bounds__(FPS_NT) k_fps(FpsArgs a) {
   cg::grid_group grid = cg::this_grid();
@@ -112,11 +125,67 @@ __global__ void __launch_bounds__(FPS_NT) k_fps(FpsArgs a) {
   __shared__ double sv[FPS_NT / 32];
   __shared__ int64_t si[FPS_NT / 32];
   __shared__ int64_t s_next;
+  // pruning (a.perm): the bounding ball of each warp's points (centre, radius)
+  constexpr bool FLT = KIND == K_L2F || KIND == K_L1F;
+  __shared__ double scen[FLT ? FPS_NT / 32 : 1][FLT ? 128 : 1];
+  __shared__ double srad[FPS_NT / 32];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int64_t gt = (int64_t)blockIdx.x * FPS_NT + tid, gs = (int64_t)gridDim.x * FPS_NT;
   double mr[PPT > 0 ? PPT : 1];
+  int32_t pidx[PPT > 0 ? PPT : 1];   // owned points (original indices; >= n: none)
 #pragma unroll
   for (int k = 0; k < (PPT > 0 ? PPT : 1); ++k) mr[k] = INFINITY;
+  const bool prune = FLT && PPT > 0 && a.perm != nullptr && a.d <= 128;
+  if constexpr (PPT > 0) {
+    // this warp's run of the spatial order: neighbouring runs go to different
+    // CTAs (run = warp * grid + CTA), so the few warps near a landmark — the
+    // ones that cannot skip it — are spread over the SMs instead of sharing one
+    const int64_t wbase = ((int64_t)w * gridDim.x + blockIdx.x) * 32 * PPT;
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) {
+      if (prune) {
+        const int64_t r = wbase + lane + 32 * k;
+        pidx[k] = r < a.n ? __ldg(a.perm + r) : (int32_t)a.n;
+      } else {
+        const int64_t p = gt + k * gs;
+        pidx[k] = p < a.n ? (int32_t)p : (int32_t)a.n;
+      }
+    }
+    if (prune) {
+      // centre: mean of the warp's points; radius: max distance, fp64, rounded up
+      double cnt = 0.0;
+#pragma unroll
+      for (int k = 0; k < PPT; ++k) cnt += pidx[k] < a.n ? 1.0 : 0.0;
+      cnt = warp_sum_d(cnt);
+      for (int j = 0; j < a.d; ++j) {
+        double sj = 0.0;
+#pragma unroll
+        for (int k = 0; k < PPT; ++k)
+          if (pidx[k] < a.n)
+            sj += (double)reinterpret_cast<const float*>(a.rows + pidx[k] * (int64_t)a.nu)[j];
+        sj = warp_sum_d(sj);
+        if (lane == 0) scen[w][j] = cnt > 0.0 ? sj / cnt : 0.0;
+      }
+      __syncwarp();
+      double rmax = 0.0;
+#pragma unroll
+      for (int k = 0; k < PPT; ++k) {
+        if (pidx[k] >= a.n) continue;
+        const float* x = reinterpret_cast<const float*>(a.rows + pidx[k] * (int64_t)a.nu);
+        double t2 = 0.0;
+        for (int j = 0; j < a.d; ++j) {
+          const double t = (double)x[j] - scen[w][j];
+          t2 += KIND == K_L2F ? t * t : fabs(t);
+        }
+        rmax = fmax(rmax, KIND == K_L2F ? sqrt(t2) : t2);
+      }
+      rmax = warp_max_d(rmax);
+      if (lane == 0) srad[w] = rmax * (1.0 + 1e-12) + 1e-300;
+      __syncwarp();
+    }
+  }
+  double bv = -INFINITY;   // this lane's (max running minimum, index): kept while skipped
+  int64_t bi = a.n;
   int64_t cur = a.start;
   int64_t L = 0;
   for (int step = 0;; ++step) {
@@ -126,22 +195,49 @@ __global__ void __launch_bounds__(FPS_NT) k_fps(FpsArgs a) {
     for (int u = tid; u < a.nue; u += FPS_NT) slm[u] = lrow[u];
     const int32_t lnorm = KIND == K_L2I ? __ldg(a.inorm + cur) : 0;
     __syncthreads();
-    double bv = -INFINITY;
-    int64_t bi = a.n;
     if constexpr (PPT > 0) {
+      // pruning: d(p, l) >= |l - c| - r for every p of the warp; if that bound
+      // is at least the warp's largest running minimum no minimum can change
+      // (margins cover the fp64 rounding of the centre, the radius and the
+      // oracle-formula distance, all relative 1e-13 or less), so the warp
+      // keeps its minima and its argmax candidate
+      bool skip = false;
+      if (prune && step > 0) {
+        const float* lf = reinterpret_cast<const float*>(slm);
+        double part = 0.0;
+        for (int j = lane; j < a.d; j += 32) {
+          const double t = (double)lf[j] - scen[w][j];
+          part += KIND == K_L2F ? t * t : fabs(t);
+        }
+        double dc = warp_sum_d(part);
+        if (KIND == K_L2F) dc = sqrt(dc);
+        const double lb = dc * (1.0 - 1e-12) - srad[w] * (1.0 + 1e-12);
+        const double mx = warp_max_d(bv);
+        skip = lb > 0.0 && (KIND == K_L2F ? lb * lb * (1.0 - 1e-12) >= mx : lb * (1.0 - 1e-12) >= mx);
+        if (a.dbg && lane == 0) {
+          atomicAdd(&a.dbg[0], 1ull);
+          if (skip) atomicAdd(&a.dbg[1], 1ull);
+        }
+      }
+      if (!skip) {
+        bv = -INFINITY;
+        bi = a.n;
 #pragma unroll
-      for (int k = 0; k < PPT; ++k) {
-        const int64_t p = gt + k * gs;
-        if (p < a.n) {
-          const double v = fps_dist<KIND>(a, p, slm, lnorm);
-          if (v < mr[k]) mr[k] = v;
-          if (better(mr[k], p, bv, bi)) {
-            bv = mr[k];
-            bi = p;
+        for (int k = 0; k < PPT; ++k) {
+          const int64_t p = pidx[k];
+          if (p < a.n) {
+            const double v = fps_dist<KIND>(a, p, slm, lnorm);
+            if (v < mr[k]) mr[k] = v;
+            if (better(mr[k], p, bv, bi)) {
+              bv = mr[k];
+              bi = p;
+            }
           }
         }
       }
     } else {
+      bv = -INFINITY;
+      bi = a.n;
       for (int64_t p = gt; p < a.n; p += gs) {
         const double v = fps_dist<KIND>(a, p, slm, lnorm);
         const double m = step == 0 ? v : fmin(a.mind[p], v);
@@ -229,48 +325,65 @@ static cudaError_t fps_go(const FpsArgs& a0, int grid, cudaStream_t s) {
 // Grid: CTAs co-resident for every instance of the kind (cooperative launch),
 // at most FPS_MAX_CAND, and no more than one CTA per 256 points (a small
 // problem pays a smaller barrier).
-template <int KIND>
-static int fps_grid_for(int64_t n, int nue) {
-  int dev = 0, sms = 0;
+// co-resident CTAs of one instance (cooperative launch), capped at
+// FPS_MAX_CAND and at one CTA per 256 points (a small problem pays a smaller
+// barrier)
+template <int KIND, int PPT>
+static int fps_grid_of(int64_t n, int nue) {
+  int dev = 0, sms = 0, q = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const size_t smem = (size_t)nue * sizeof(uint2);
-  const void* fs[] = {(const void*)k_fps<KIND, 0>, (const void*)k_fps<KIND, 1>,
-                      (const void*)k_fps<KIND, 2>, (const void*)k_fps<KIND, 4>,
-                      (const void*)k_fps<KIND, 8>, (const void*)k_fps<KIND, 16>};
-  int per = 1 << 30;
-  for (const void* f : fs) {
-    int q = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&q, f, FPS_NT, smem);
-    per = q < per ? q : per;
-  }
-  if (per < 1) per = 1;
-  int64_t g = (int64_t)sms * per;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&q, k_fps<KIND, PPT>, FPS_NT,
+                                                (size_t)nue * sizeof(uint2));
+  int64_t g = (int64_t)sms * (q > 0 ? q : 1);
   if (g > FPS_MAX_CAND) g = FPS_MAX_CAND;
   const int64_t want = (n + FPS_NT - 1) / FPS_NT;
   if (g > want) g = want;
   return (int)(g > 0 ? g : 1);
 }
 
+// the smallest register-resident PPT whose own grid covers n; else global minima
+template <int KIND, int PPT>
+static cudaError_t fps_try(const FpsArgs& a, cudaStream_t s, bool* done) {
+  const int g = fps_grid_of<KIND, PPT>(a.n, a.nue);
+  if ((int64_t)g * FPS_NT * PPT < a.n) return cudaSuccess;
+  *done = true;
+  return fps_go<KIND, PPT>(a, g, s);
+}
+
 template <int KIND>
 static cudaError_t fps_kind(const FpsArgs& a, cudaStream_t s) {
-  const int grid = fps_grid_for<KIND>(a.n, a.nue);
-  const int64_t per = (a.n + (int64_t)grid * FPS_NT - 1) / ((int64_t)grid * FPS_NT);
-  if (per <= 1) return fps_go<KIND, 1>(a, grid, s);
-  if (per <= 2) return fps_go<KIND, 2>(a, grid, s);
-  if (per <= 4) return fps_go<KIND, 4>(a, grid, s);
-  if (per <= 8) return fps_go<KIND, 8>(a, grid, s);
-  if (per <= 16) return fps_go<KIND, 16>(a, grid, s);
-  return fps_go<KIND, 0>(a, grid, s);
+  bool done = false;
+  cudaError_t e = fps_try<KIND, 1>(a, s, &done);
+  if (!done && e == cudaSuccess) e = fps_try<KIND, 2>(a, s, &done);
+  if (!done && e == cudaSuccess) e = fps_try<KIND, 4>(a, s, &done);
+  if (!done && e == cudaSuccess) e = fps_try<KIND, 8>(a, s, &done);
+  if (!done && e == cudaSuccess) e = fps_try<KIND, 16>(a, s, &done);
+  if (!done && e == cudaSuccess) e = fps_try<KIND, 32>(a, s, &done);
+  if (!done && e == cudaSuccess) return fps_go<KIND, 0>(a, fps_grid_of<KIND, 0>(a.n, a.nue), s);
+  return e;
 }
 
 cudaError_t launch_fps(const uint2* rows, const int32_t* inorm, int nu, int d, int kind, int64_t n,
                        double thr, int64_t start, double* mind, int32_t* seq, int32_t* L_out,
-                       double* cval, int64_t* cidx, cudaStream_t s) {
+                       double* cval, int64_t* cidx, const int32_t* perm, cudaStream_t s) {
   const int nue = (kind == K_L2I || kind == K_L1I) ? (d + 7) / 8 : (d + 1) / 2;
-  FpsArgs a{rows, inorm, nu, nue, d, n, thr, start, mind, seq, L_out, cval, cidx};
+  static unsigned long long* dbg = nullptr;
+  if (getenv("BM_FPS_DEBUG") && !dbg) {
+    cudaMallocManaged(&dbg, 16);
+  }
+  if (dbg) dbg[0] = dbg[1] = 0ull;
+  FpsArgs a{rows, inorm, nu, nue, d, n, thr, start, mind, seq, L_out, cval, cidx, perm, dbg};
   switch (kind) {
-    case K_L2F: return fps_kind<K_L2F>(a, s);
+    case K_L2F: {
+      cudaError_t e = fps_kind<K_L2F>(a, s);
+      if (dbg) {
+        cudaStreamSynchronize(s);
+        fprintf(stderr, "fps debug: warp-steps %llu skipped %llu (%.3f)\n", dbg[0], dbg[1],
+                dbg[0] ? (double)dbg[1] / dbg[0] : 0.0);
+      }
+      return e;
+    }
     case K_L1F: return fps_kind<K_L1F>(a, s);
     case K_COSF: return fps_kind<K_COSF>(a, s);
     case K_L2I: return fps_kind<K_L2I>(a, s);

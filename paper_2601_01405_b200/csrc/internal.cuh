@@ -248,6 +248,10 @@ struct PruneState {
                         // hold an in-ball pair (from bmask and cmask, per greedy tile,
                         // folded by the landmark-operand launch, tc.cu)
 };
+cudaError_t cell_order(const float* xrows, int xstride, int d, int64_t n, int32_t* cell,
+                       int32_t* rank, float* pdist, unsigned long long** keys,
+                       unsigned long long** alt, void* sort_temp, int32_t* perm, cudaStream_t s,
+                       int64_t* launches);
 cudaError_t prune_prepare(const float* xrows, int xstride, int d, int64_t n, double eps,
                           const uint8_t* xop, int64_t row_bytes, const double* nrm, PruneState& ps,
                           void* sort_temp, unsigned long long* keys, unsigned long long* alt,
@@ -255,9 +259,12 @@ cudaError_t prune_prepare(const float* xrows, int xstride, int d, int64_t n, dou
 
 // fps.cu (NEXT-2)
 int fps_max_candidates();
+// perm (may be null): the points in spatial (cell) order; each warp then owns
+// a contiguous run of it and skips a landmark whose distance to the run's
+// bounding ball proves no running minimum can change (float L2 / L1, d <= 128)
 cudaError_t launch_fps(const uint2* rows, const int32_t* inorm, int nu, int d, int kind, int64_t n,
                        double thr, int64_t start, double* mind, int32_t* seq, int32_t* L_out,
-                       double* cval, int64_t* cidx, cudaStream_t s);
+                       double* cval, int64_t* cidx, const int32_t* perm, cudaStream_t s);
 cudaError_t launch_fps_keys(const int32_t* seq, int64_t L, unsigned long long* keys,
                             cudaStream_t s, int64_t* launches);
 

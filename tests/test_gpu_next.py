@@ -143,3 +143,21 @@ def test_fps_degenerate(bm):
     assert _fps_case(bm, far, "l2", 1.0)["L"] == 40
     with pytest.raises(Exception):
         bm.cover_build(torch.from_numpy(far).cuda(), "l2", 1.0, select="fps", fps_start=40)
+
+
+@pytest.mark.parametrize("metric,eps", [("l2", 0.35), ("l1", 0.6)])
+def test_fps_pruned_equals_unpruned(bm, metric, eps):
+    """FPS with the spatial order and per-warp bounding balls (fps.cu) against
+    the unpruned kernel and the oracle, on clustered data where most warps skip."""
+    from paper_2601_01405_b200 import bm as B
+    rng = np.random.default_rng(31)
+    centres = rng.normal(size=(20, 6)) * 8.0
+    X_ = (centres[rng.integers(0, 20, size=12000)] + rng.normal(size=(12000, 6)) * 0.3).astype(np.float32)
+    t = torch.from_numpy(X_).cuda()
+    a = bm.cover_build(t, metric, eps, select="fps")
+    b = bm.cover_build(t, metric, eps, select="fps", flags=B.FLAG_NO_PRUNE)
+    na, nb = a.numpy(), b.numpy()
+    for k in na:
+        assert np.array_equal(na[k], nb[k]), k
+    want = np.sort(O.fps(X_, metric, eps))
+    assert np.array_equal(np.asarray(na["landmarks"], dtype=np.int64), want)

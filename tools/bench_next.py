@@ -133,7 +133,12 @@ def bench_fps(name, reps, n=None):
          E_fps=c.E, E_greedy=g.E, greedy_build_ms=round(tg, 3), fps_build_ms=round(tf, 3),
          fps_select_ms=round(sel, 3), select_us_per_landmark=round(sel / c.L * 1e3, 3),
          algorithmic_bytes_select=byts, achieved_gbs=round(byts / sel / 1e6, 1),
-         hbm_peak_gbs=PEAK, frac=round(byts / sel / 1e6 / PEAK, 4),
+         hbm_peak_gbs=PEAK,
+         # float L2 / L1 FPS skips warps by bounding balls (fps.cu): the unpruned
+         # bytes then overstate the traffic, so no fraction is claimed for them
+         frac=None if (w.dtype == "f32" and w.metric in ("l2", "l1"))
+         else round(byts / sel / 1e6 / PEAK, 4),
+         warp_pruning=w.dtype == "f32" and w.metric in ("l2", "l1"),
          oracle_prefix_n=m, oracle_prefix_L=int(len(so)), oracle_select_s=round(oracle_s, 3),
          oracle_evals_per_s=round(m * len(so) / oracle_s, 1),
          gpu_evals_per_s=round(nn * c.L / (sel * 1e-3), 1),
