@@ -118,13 +118,17 @@ __device__ __forceinline__ double warp_max_d(double x) {
   return x;
 }
 
-template <int KIND, int PPT>
+// CL: the whole grid is one thread-block cluster (small n): candidates are
+// exchanged through distributed shared memory and the per-landmark barrier is
+// the cluster barrier instead of a grid-wide one.
+template <int KIND, int PPT, bool CL>
 __global__ void __launch_bounds__(FPS_NT) k_fps(FpsArgs a) {
-  cg::grid_group grid = cg::this_grid();
   extern __shared__ uint2 slm[];   // the current landmark's units
   __shared__ double sv[FPS_NT / 32];
   __shared__ int64_t si[FPS_NT / 32];
   __shared__ int64_t s_next;
+  __shared__ double ccv[2];    // CL: this CTA's candidate per buffer
+  __shared__ int64_t cci[2];
   // pruning (a.perm): the bounding ball of each warp's points (centre, radius)
   constexpr bool FLT = KIND == K_L2F || KIND == K_L1F;
   __shared__ double scen[FLT ? FPS_NT / 32 : 1][FLT ? 128 : 1];
@@ -271,12 +275,35 @@ __global__ void __launch_bounds__(FPS_NT) k_fps(FpsArgs a) {
           v = sv[k];
           i = si[k];
         }
-      a.cval[buf * gridDim.x + blockIdx.x] = v;
-      a.cidx[buf * gridDim.x + blockIdx.x] = i;
+      if constexpr (CL) {
+        ccv[buf] = v;
+        cci[buf] = i;
+      } else {
+        a.cval[buf * gridDim.x + blockIdx.x] = v;
+        a.cidx[buf * gridDim.x + blockIdx.x] = i;
+      }
     }
-    grid.sync();
+    if constexpr (CL) cg::this_cluster().sync();
+    else cg::this_grid().sync();
     // every CTA reduces all candidates the same way (loads issued before the compares)
-    if (w == 0) {
+    if (w == 0 && CL) {
+      cg::cluster_group cl = cg::this_cluster();
+      double v = -INFINITY;
+      int64_t i = a.n;
+      if (lane < (int)gridDim.x) {
+        v = *cl.map_shared_rank(&ccv[buf], (unsigned)lane);
+        i = *cl.map_shared_rank(&cci[buf], (unsigned)lane);
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+        const int64_t oi = __shfl_xor_sync(0xffffffffu, i, o);
+        if (better(ov, oi, v, i)) {
+          v = ov;
+          i = oi;
+        }
+      }
+      if (lane == 0) s_next = (i < a.n && v >= a.thr) ? i : -1;   // reading F1: >= eps
+    } else if (w == 0) {
       double v = -INFINITY;
       int64_t i = a.n;
       for (int base = 0; base < (int)gridDim.x; base += 256) {
@@ -310,6 +337,8 @@ __global__ void __launch_bounds__(FPS_NT) k_fps(FpsArgs a) {
     cur = s_next;
     if (cur < 0) break;
   }
+  // CL: no CTA leaves while another may still read its candidates
+  if constexpr (CL) cg::this_cluster().sync();
   if (blockIdx.x == 0 && tid == 0) *a.L_out = (int32_t)L;
 }
 
@@ -318,8 +347,30 @@ static cudaError_t fps_go(const FpsArgs& a0, int grid, cudaStream_t s) {
   FpsArgs a = a0;
   void* args[] = {&a};
   const size_t smem = (size_t)a.nue * sizeof(uint2);
-  return cudaLaunchCooperativeKernel((void*)k_fps<KIND, PPT>, dim3(grid), dim3(FPS_NT), args,
-                                     smem, s);
+  return cudaLaunchCooperativeKernel((void*)k_fps<KIND, PPT, false>, dim3(grid), dim3(FPS_NT),
+                                     args, smem, s);
+}
+
+// one cluster of FPS_CL CTAs (non-portable size 16): small problems
+constexpr int FPS_CL = 16;
+template <int KIND, int PPT>
+static cudaError_t fps_go_cluster(const FpsArgs& a, cudaStream_t s) {
+  auto kern = k_fps<KIND, PPT, true>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(FPS_CL);
+  cfg.blockDim = dim3(FPS_NT);
+  cfg.dynamicSmemBytes = (size_t)a.nue * sizeof(uint2);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = FPS_CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
 // Grid: CTAs co-resident for every instance of the kind (cooperative launch),
@@ -333,7 +384,7 @@ static int fps_grid_of(int64_t n, int nue) {
   int dev = 0, sms = 0, q = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&q, k_fps<KIND, PPT>, FPS_NT,
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&q, k_fps<KIND, PPT, false>, FPS_NT,
                                                 (size_t)nue * sizeof(uint2));
   int64_t g = (int64_t)sms * (q > 0 ? q : 1);
   if (g > FPS_MAX_CAND) g = FPS_MAX_CAND;
@@ -353,6 +404,17 @@ static cudaError_t fps_try(const FpsArgs& a, cudaStream_t s, bool* done) {
 
 template <int KIND>
 static cudaError_t fps_kind(const FpsArgs& a, cudaStream_t s) {
+  // small problems: one cluster, register-resident minima (the cluster barrier
+  // costs a fraction of a grid barrier); falls through when it cannot launch
+  static const bool no_cl = getenv("BM_FPS_NO_CLUSTER") != nullptr;   // diagnostics
+  const int64_t cl_cap = (int64_t)FPS_CL * FPS_NT;
+  // (measured: C1, n = 2000, 3.35 -> 2.36 us per landmark; at C2's n = 1e5
+  // the 16 SMs are too few — 22 vs 5.6 us — so only up to 4 points per thread)
+  if (!no_cl && a.n <= cl_cap * 4) {
+    const cudaError_t e = fps_go_cluster<KIND, 4>(a, s);
+    if (e == cudaSuccess) return e;
+    cudaGetLastError();   // no cluster of this size: the cooperative path below
+  }
   bool done = false;
   cudaError_t e = fps_try<KIND, 1>(a, s, &done);
   if (!done && e == cudaSuccess) e = fps_try<KIND, 2>(a, s, &done);
