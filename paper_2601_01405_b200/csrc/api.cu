@@ -218,9 +218,19 @@ struct Pool {
 
 struct Priv {
   cudaStream_t stream;
-  void* pinned;        // host-buffer covers: the pinned block holding all arrays
+  void* pinned;        // host-buffer covers: pinned block of landmarks + both CSRs
   size_t pinned_cls;
+  void* pinned_e;      //   ... and of the edge list
+  size_t pinned_e_cls;
 };
+
+// A per-thread side stream for the host-buffer API's result copies (they
+// overlap the edge construction on the caller's stream)
+static cudaStream_t side_stream() {
+  static thread_local cudaStream_t s2 = nullptr;
+  if (!s2 && cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking) != cudaSuccess) s2 = nullptr;
+  return s2;
+}
 
 int bits_for(int64_t v) {  // number of bits to represent 0..v (>= 1)
   int b = 1;
@@ -1097,6 +1107,43 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
   tm.mark(4);
   tr("csr rest");
 
+  // host-buffer API: landmarks and both CSRs go back on a side stream while
+  // the edges are built (one pinned block; the edges follow at the end)
+  uint8_t* hblk = nullptr;
+  size_t hcls = 0, hoff[5] = {0, 0, 0, 0, 0};
+  cudaStream_t s2 = nullptr;
+  // on any early return: let the side-stream copies finish before the pool
+  // releases the device arrays, and give the pinned block back
+  struct SideGuard {
+    cudaStream_t& st;
+    uint8_t*& blk;
+    size_t& cls;
+    ~SideGuard() {
+      if (st) cudaStreamSynchronize(st);
+      if (blk) g_pinned.put(blk, cls);
+    }
+  } side_guard{s2, hblk, hcls};
+  if (host_in) {
+    const size_t hsz[5] = {sizeof(int32_t) * (size_t)L, sizeof(int64_t) * (size_t)(L + 1),
+                           sizeof(int32_t) * (size_t)M, sizeof(int64_t) * (size_t)(n + 1),
+                           sizeof(int32_t) * (size_t)M};
+    const void* hsrc[5] = {lm, ball_ptr, ball_idx, pt_ptr, pt_lm};
+    size_t total = 0;
+    for (int i = 0; i < 5; ++i) {
+      hoff[i] = total;
+      total += (hsz[i] + 255) & ~(size_t)255;
+    }
+    hblk = (uint8_t*)g_pinned.get(total, &hcls);
+    if (!hblk) return set_err(BM_ENOMEM, "pinned host allocation for the results failed");
+    s2 = side_stream();
+    cudaEvent_t ev = cached_event(8100);
+    if (!s2 || !ev) return set_err(BM_ECUDA, "side stream / event creation failed");
+    CK(cudaEventRecord(ev, s));
+    CK(cudaStreamWaitEvent(s2, ev, 0));
+    for (int i = 0; i < 5; ++i)
+      if (hsz[i]) CK(cudaMemcpyAsync(hblk + hoff[i], hsrc[i], hsz[i], cudaMemcpyDeviceToHost, s2));
+  }
+
   // ---- D1-D3 edges (edges.cu)
   int64_t NP = 0;  // P = sum_p C(t_p, 2) witnessed pairs
   int64_t E = 0;
@@ -1265,32 +1312,27 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
   c->n_launches = launches;
   if (host_in) {
     c->on_host = 1;
-    // all six arrays in one pinned block (256-byte aligned parts), queued
-    // copies, one synchronisation
-    const size_t sz[6] = {sizeof(int32_t) * (size_t)L, sizeof(int64_t) * (size_t)(L + 1),
-                          sizeof(int32_t) * (size_t)M, sizeof(int64_t) * (size_t)(n + 1),
-                          sizeof(int32_t) * (size_t)M, sizeof(int32_t) * 2 * (size_t)E};
-    const void* src[6] = {landmarks, ball_ptr, ball_idx, pt_ptr, pt_lm, edges};
-    size_t off[6], total = 0;
-    for (int i = 0; i < 6; ++i) {
-      off[i] = total;
-      total += (sz[i] + 255) & ~(size_t)255;
-    }
-    uint8_t* blk = (uint8_t*)g_pinned.get(total, &pv->pinned_cls);
-    if (!blk) {
+    pv->pinned = hblk;
+    pv->pinned_cls = hcls;
+    c->landmarks = (int32_t*)(hblk + hoff[0]);
+    c->ball_ptr = (int64_t*)(hblk + hoff[1]);
+    c->ball_idx = (int32_t*)(hblk + hoff[2]);
+    c->pt_ptr = (int64_t*)(hblk + hoff[3]);
+    c->pt_lm = (int32_t*)(hblk + hoff[4]);
+    hblk = nullptr;   // owned by the cover now
+    // the edge list (its size is known now), then both streams
+    const size_t esz = sizeof(int32_t) * 2 * (size_t)E;
+    uint8_t* eblk = (uint8_t*)g_pinned.get(esz, &pv->pinned_e_cls);
+    pv->pinned_e = eblk;
+    if (!eblk) {
       bm_free(c);
       return set_err(BM_ENOMEM, "pinned host allocation for the results failed");
     }
-    pv->pinned = blk;
-    for (int i = 0; i < 6; ++i)
-      if (sz[i]) CK(cudaMemcpyAsync(blk + off[i], src[i], sz[i], cudaMemcpyDeviceToHost, s));
+    c->edges = (int32_t*)eblk;
+    if (esz) CK(cudaMemcpyAsync(eblk, edges, esz, cudaMemcpyDeviceToHost, s));
     cudaError_t e = cudaStreamSynchronize(s);
-    c->landmarks = (int32_t*)(blk + off[0]);
-    c->ball_ptr = (int64_t*)(blk + off[1]);
-    c->ball_idx = (int32_t*)(blk + off[2]);
-    c->pt_ptr = (int64_t*)(blk + off[3]);
-    c->pt_lm = (int32_t*)(blk + off[4]);
-    c->edges = (int32_t*)(blk + off[5]);
+    const cudaError_t e2 = cudaStreamSynchronize(s2);
+    if (e == cudaSuccess) e = e2;
     if (e != cudaSuccess) {
       bm_free(c);
       return set_err(BM_ECUDA, "device-to-host copy of the results failed");
@@ -1347,6 +1389,7 @@ void bm_free(bm_cover* c) {
   if (c->on_host) {
     if (pv && pv->pinned) {
       g_pinned.put(pv->pinned, pv->pinned_cls);
+      if (pv->pinned_e) g_pinned.put(pv->pinned_e, pv->pinned_e_cls);
     } else {
       free(c->landmarks);
       free(c->ball_ptr);
