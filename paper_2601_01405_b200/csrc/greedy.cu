@@ -91,8 +91,9 @@ __global__ void __launch_bounds__(1024) k_resolve(const uint32_t* __restrict__ a
                                                   PruneTile pt_out) {
   __shared__ volatile uint32_t lmw[32];
   __shared__ int wpre[33];
-  __shared__ uint32_t skey[1024];      // pruning: (cell rank << 16 | position) sort keys
+  __shared__ uint32_t skey[1024];      // pruning: positions in cell-rank order
   __shared__ uint32_t scm[32 * 8];     // pruning: cell masks of the 32-column chunks
+  __shared__ int shist[256];           // pruning: landmarks per cell rank, then slots
   extern __shared__ uint32_t sadj[];
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
   pdl_wait();
@@ -123,7 +124,7 @@ __global__ void __launch_bounds__(1024) k_resolve(const uint32_t* __restrict__ a
   }
   const bool prune = pt_out.cell != nullptr;
   if (prune) {
-    skey[tid] = 0xffffffffu;
+    if (tid < 256) shist[tid] = 0;
     if (tid < 32 * 8) scm[tid] = 0u;
   }
   __syncthreads();
@@ -135,29 +136,50 @@ __global__ void __launch_bounds__(1024) k_resolve(const uint32_t* __restrict__ a
       const int32_t pt = unc[tid];
       new_lm[pos] = pt;
       lm_out[L0 + pos] = pt;
-      if (prune) skey[pos] = ((uint32_t)pt_out.rank[pt_out.cell[pt]] << 16) | (uint32_t)pos;
     }
   }
   __syncthreads();
   if (prune) {
-    // the new landmarks sorted by (cell rank, position) — bitonic over 1024
-    // keys — and the cell masks of every 32-column chunk / 256-column tile
-    for (int k = 2; k <= 1024; k <<= 1) {
-      for (int sj = k >> 1; sj > 0; sj >>= 1) {
-        const int o = tid ^ sj;
-        if (o > tid) {
-          const uint32_t a = skey[tid], b = skey[o];
-          if ((a > b) == ((tid & k) == 0)) {
-            skey[tid] = b;
-            skey[o] = a;
-          }
-        }
-        __syncthreads();
+    // the new landmarks grouped by cell rank (counting sort; the order inside
+    // a cell only affects which chunk a landmark lands in, never a result:
+    // keys carry the original positions) and the cell masks of every
+    // 32-column chunk / 256-column tile
+    int my_rank = -1, my_pos = -1;
+    if (w < nb && tid < nc) {
+      const uint32_t S = lmw[w];
+      if ((S >> lane) & 1u) {
+        my_pos = wpre[w] + __popc(S & ((1u << lane) - 1u));
+        my_rank = pt_out.rank[pt_out.cell[unc[tid]]];
+        atomicAdd(&shist[my_rank], 1);
       }
     }
+    __syncthreads();
+    if (tid < 32) {   // exclusive scan of the 256 counts (8 per lane)
+      int v[8], t = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        v[i] = shist[tid * 8 + i];
+        t += v[i];
+      }
+      int incl = t;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(FULLMASK, incl, o);
+        if (lane >= o) incl += u;
+      }
+      int run = incl - t;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        shist[tid * 8 + i] = run;
+        run += v[i];
+      }
+    }
+    __syncthreads();
+    if (my_rank >= 0) skey[atomicAdd(&shist[my_rank], 1)] = (uint32_t)my_pos;
+    __syncthreads();
     const int dL = wpre[nb];
     if (tid < dL) {
-      const int src = (int)(skey[tid] & 0xffffu);
+      const int src = (int)skey[tid];
       const int32_t p = new_lm[src];   // written above by this CTA
       pt_out.col_pt[tid] = p;
       pt_out.col_pos[tid] = src;
