@@ -354,6 +354,9 @@ def run_ours(args):
     covs_stats = []
     L = 0
     launches = 0
+    import gc
+    gc.collect()
+    gc.disable()   # a collector pause between ev0 and the first launch would count
     for i in range(args.steps):
         flush.fill_(i & 0xFF)                 # L2 flush outside the timed bracket
         ev[i][0].record(stream)
@@ -363,6 +366,7 @@ def run_ours(args):
         launches += cov.stats.n_launches
         cov.free()
     barrier()
+    gc.enable()
     clocks = sampler.stop()
     # instrumented pass (not timed): per-step breakdown, membership kernel time
     for i in range(max(3, min(args.steps, 10))):
