@@ -201,8 +201,12 @@ __device__ __forceinline__ void pairs_block(const PairArgs& A, uint2* sl, int32_
       sln[t] = (KIND == K_L2I) ? A.inorm[pt] : 0;
     }
     if constexpr (QF) {
-      for (int t = tid; t < nl * NQ; t += NT) {
-        const int jj = t / NQ, w = t - jj * NQ;
+      // (rows nl .. up to the next multiple of 8 repeat the last landmark, so
+      // the group screen below needs no tail clamp; those columns are never
+      // classified)
+      const int nl8 = (nl + 7) & ~7;
+      for (int t = tid; t < nl8 * NQ; t += NT) {
+        const int jj = min(t / NQ, nl - 1), w = t % NQ;
         sq[t] = A.qrows[(int64_t)A.lidx[lb + jj] * NQ + w];
       }
     }
@@ -219,7 +223,7 @@ __device__ __forceinline__ void pairs_block(const PairArgs& A, uint2* sl, int32_
       uint32_t all_out = 0xffffffffu;
 #pragma unroll
       for (int u = 0; u < UG; ++u) {
-        const int jq = min(jg + u, nl - 1);   // tail: repeat the last landmark
+        const int jq = jg + u;   // (the staged rows are padded to a multiple of 8)
         uint32_t lq[NQ];
         if constexpr (NQ % 4 == 0) {   // 16-byte shared loads
 #pragma unroll
