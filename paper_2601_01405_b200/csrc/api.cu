@@ -865,7 +865,12 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
     if (e && cudaEventRecord(e, s) == cudaSuccess) lev.emplace_back(phase, e);
   };
   int64_t tile = 0;
-  int batch = 4;
+  // tiles per host check: 3 first (the C2-size covers finish in three), then
+  // the remaining count predicted from the rate at which the uncovered list
+  // has been shrinking (each check costs a round trip, each tile after the
+  // last one a few empty launches)
+  int batch = 3;
+  int64_t unc_start = n;
   int nonfinite_checked = 0;
   if (fps) {
     // NEXT-2: farthest point sampling selects the landmarks (fps.cu), then one
@@ -1010,8 +1015,11 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
       if (mb->hs.nonfinite) return set_err(BM_EINVAL, "points contain a non-finite coordinate");
       nonfinite_checked = 1;
     }
-    if (mb->hc[tile & 1] == 0) break;
-    if (batch < 64) batch *= 2;
+    const int64_t unc_now = mb->hc[tile & 1];
+    if (unc_now == 0) break;
+    const double per_tile = (double)(unc_start - unc_now) / (double)tile;
+    int64_t est = per_tile > 0.0 ? (int64_t)ceil((double)unc_now / per_tile) : 2 * batch;
+    batch = (int)std::min<int64_t>(64, std::max<int64_t>(1, std::min<int64_t>(est, 2 * batch)));
   }
   tm.mark(2);
   tr("greedy+membership loop");
