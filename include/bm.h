@@ -271,8 +271,8 @@ bm_status bm_debug_resolve_tile(const uint32_t *adj, int32_t nc, uint8_t *lm_out
 /* Raw tcgen05 Gram accumulators of the membership contraction (step B):
  * out[p*L + j] = bits of sum_k x_p[k] * x_{lm[j]}[k] as accumulated by the
  * tensor core (fp32 bits of the tf32 products for BM_F32, int32 for
- * BM_U8 / BM_I8).  points, lm and out are DEVICE pointers; d*elem <= 512
- * bytes (F32) or 896 bytes (int8). */
+ * BM_U8 / BM_I8).  points, lm and out are DEVICE pointers; d*elem <= 4096
+ * bytes. */
 bm_status bm_debug_tc_gram(const void *points, bm_dtype dtype, int64_t n, int32_t d,
                            const int32_t *lm, int64_t L, uint32_t *out, void *stream);
 

@@ -24,6 +24,44 @@
 #include "internal.cuh"
 #include "tc.cuh"
 
+// diagnostics: per-CTA %globaltimer phase stamps of one traced k_tc launch
+// (TC_STAMP slots, tc.cu), summarised to stderr
+static cudaError_t print_tc_trace(const unsigned long long* tr, int G, const char* tag,
+                                  cudaStream_t s) {
+  std::vector<unsigned long long> h((size_t)G * 16);
+  cudaError_t e = cudaMemcpyAsync(h.data(), tr, sizeof(unsigned long long) * G * 16,
+                                  cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return e;
+  unsigned long long t0 = ~0ull;
+  for (int b = 0; b < G; ++b) t0 = h[b * 16] && h[b * 16] < t0 ? h[b * 16] : t0;
+  static const char* names[12] = {"start", "prologue", "pdl", "A0 issued", "producer done",
+                                  "A0 landed", "mma done", "epi0 first", "epi1 first",
+                                  "epi0 done", "epi1 done", "end"};
+  fprintf(stderr, "trace [%s]\n", tag);
+  for (int k = 0; k < 12; ++k) {
+    std::vector<double> v;
+    for (int b = 0; b < G; ++b)
+      if (h[b * 16 + k]) v.push_back((double)(h[b * 16 + k] - t0) * 1e-3);
+    std::sort(v.begin(), v.end());
+    if (!v.empty())
+      fprintf(stderr, "trace %-14s min %8.2f  med %8.2f  max %8.2f us  (%zu CTAs)\n", names[k],
+              v.front(), v[v.size() / 2], v.back(), v.size());
+  }
+  std::vector<int> ord(G);
+  for (int b = 0; b < G; ++b) ord[b] = b;
+  std::sort(ord.begin(), ord.end(), [&](int x, int y) { return h[x * 16 + 11] > h[y * 16 + 11]; });
+  for (int i = 0; i < 4 && i < G; ++i) {
+    const int b = ord[i];
+    fprintf(stderr, "slow CTA %3d:", b);
+    for (int k = 0; k < 12; ++k)
+      fprintf(stderr, " %6.2f", h[b * 16 + k] ? (double)(h[b * 16 + k] - t0) * 1e-3 : -1.0);
+    fprintf(stderr, "\n");
+  }
+  return cudaSuccess;
+}
+
+
 namespace {
 
 thread_local std::string g_err;
@@ -592,7 +630,7 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
   if (o.path == BM_PATH_TENSOR && !use_tc)
     return set_err(BM_EUNSUPPORTED,
                    "tensor-core path supports L2 and cosine with d*elem <= %d bytes",
-                   dtype == BM_F32 ? 512 : 896);
+                   4096);
 
   int64_t launches = 0;
   Mailbox* mb = mailbox();
@@ -858,6 +896,8 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
   // BM_LOOP_PROFILE=1 (diagnostics): per-phase device time of the tile loop
   // (A2 / A3 / B incl. landmark operands / A4), printed to stderr
   static const bool loop_prof = getenv("BM_LOOP_PROFILE") != nullptr;
+  unsigned long long* tc_trace = nullptr;   // BM_TC_TRACE=1: stamp every membership launch
+  if (use_tc && getenv("BM_TC_TRACE")) TRY(pool.alloc(&tc_trace, (size_t)P.num_sms * 16));
   std::vector<std::pair<int, cudaEvent_t>> lev;
   auto loop_mark = [&](int phase) {
     if (!loop_prof) return;
@@ -976,8 +1016,18 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
         CK(tc::launch_tc_tile_landmarks(P, tc_nrm, prune ? ps.col_pt : new_lm, cnt + 3, C2, ta, s,
                                         &launches));
         CK(mark_member());
+        if (tc_trace) {   // diagnostics: phase stamps of this launch (synchronises)
+          CK(cudaMemsetAsync(tc_trace, 0, sizeof(unsigned long long) * P.num_sms * 16, s));
+          ta.trace = tc_trace;
+        }
         CK(tc::launch_tc(prune ? Pm : P, ta, s, &launches));
         CK(mark_member());
+        if (tc_trace) {
+          char tag[64];
+          snprintf(tag, sizeof tag, "membership tile %lld", (long long)tile);
+          CK(print_tc_trace(tc_trace, P.num_sms, tag, s));
+          ta.trace = nullptr;
+        }
       } else {
         PairArgs m = base;
         m.qidx = nullptr;
@@ -1678,34 +1728,7 @@ bm_status bm_debug_tc_probe(const float* points, int64_t n, int32_t d, int64_t L
     CK(cudaMemsetAsync(tr, 0, sizeof(unsigned long long) * G * 16, s));
     ta.trace = tr;
     CK(tc::launch_tc_probe(P, ta, mode & 255, s));
-    std::vector<unsigned long long> h((size_t)G * 16);
-    CK(cudaMemcpyAsync(h.data(), tr, sizeof(unsigned long long) * G * 16, cudaMemcpyDeviceToHost,
-                       s));
-    CK(cudaStreamSynchronize(s));
-    unsigned long long t0 = ~0ull;
-    for (int b = 0; b < G; ++b) t0 = h[b * 16] && h[b * 16] < t0 ? h[b * 16] : t0;
-    static const char* names[12] = {"start", "prologue", "pdl", "A0 issued", "producer done",
-                                    "A0 landed", "mma done", "epi0 first", "epi1 first",
-                                    "epi0 done", "epi1 done", "end"};
-    for (int k = 0; k < 12; ++k) {
-      std::vector<double> v;
-      for (int b = 0; b < G; ++b)
-        if (h[b * 16 + k]) v.push_back((double)(h[b * 16 + k] - t0) * 1e-3);
-      std::sort(v.begin(), v.end());
-      if (!v.empty())
-        fprintf(stderr, "trace %-14s min %8.2f  med %8.2f  max %8.2f us  (%zu CTAs)\n", names[k],
-                v.front(), v[v.size() / 2], v.back(), v.size());
-    }
-    std::vector<int> ord(G);
-    for (int b = 0; b < G; ++b) ord[b] = b;
-    std::sort(ord.begin(), ord.end(), [&](int x, int y) { return h[x * 16 + 11] > h[y * 16 + 11]; });
-    for (int i = 0; i < 6 && i < G; ++i) {
-      const int b = ord[i];
-      fprintf(stderr, "slow CTA %3d:", b);
-      for (int k = 0; k < 12; ++k)
-        fprintf(stderr, " %6.2f", h[b * 16 + k] ? (double)(h[b * 16 + k] - t0) * 1e-3 : -1.0);
-      fprintf(stderr, "\n");
-    }
+    CK(print_tc_trace(tr, G, "probe", s));
   }
   return BM_OK;
 }

@@ -231,8 +231,11 @@ constexpr uint32_t make_idesc(int M, int N) {
 template <int RA, int BN, int KATOMS, int STAGES, int ABUF, bool FOLD, bool BRES = false>
 struct Smem {
   static constexpr int A_ATOM = 128 * 128;                 // 128 rows x 128 B
-  static constexpr int A_BYTES = RA * KATOMS * A_ATOM;     // one A buffer
-  static constexpr int B_STAGE = BN * 128;
+  // ABUF == 0 (K streaming, wide rows): no resident A block; every stage
+  // carries the unit's A atom after the tile's B atom
+  static constexpr bool KS = ABUF == 0;
+  static constexpr int A_BYTES = KS ? 0 : RA * KATOMS * A_ATOM;   // one A buffer
+  static constexpr int B_STAGE = BN * 128 + (KS ? A_ATOM : 0);
   static constexpr int B_BYTES = STAGES * B_STAGE;
   static constexpr int EPI_WARPS = 8;                     // two epilogue warpgroups
   static constexpr int KW = FOLD ? 64 : (KATOMS > 4 ? 96 : 128);  // staging slots per warp
@@ -261,13 +264,28 @@ __device__ __noinline__ bool pair_in_fp64(const float* xrows, int xstride, int d
                                           double* dist) {
   const float* x = xrows + p * (int64_t)xstride;
   const float* y = xrows + q * (int64_t)xstride;
+  // coordinates are loaded 16 at a time (independent loads in flight together:
+  // one memory latency per 16 dimensions instead of one per dimension); the
+  // fp64 sums still run in ascending coordinate order
+  constexpr int G = 16;
   if (cosine) {
     double dot = 0.0, xx = 0.0, yy = 0.0;
-    for (int k = 0; k < dd; ++k) {
-      const double a = (double)x[k], b = (double)y[k];
-      dot = __dadd_rn(dot, __dmul_rn(a, b));
-      xx = __dadd_rn(xx, __dmul_rn(a, a));
-      yy = __dadd_rn(yy, __dmul_rn(b, b));
+    for (int k0 = 0; k0 < dd; k0 += G) {
+      float xa[G], ya[G];
+#pragma unroll
+      for (int i = 0; i < G; ++i) {
+        xa[i] = k0 + i < dd ? __ldg(x + k0 + i) : 0.f;
+        ya[i] = k0 + i < dd ? __ldg(y + k0 + i) : 0.f;
+      }
+#pragma unroll
+      for (int i = 0; i < G; ++i) {
+        if (k0 + i < dd) {
+          const double a = (double)xa[i], b = (double)ya[i];
+          dot = __dadd_rn(dot, __dmul_rn(a, b));
+          xx = __dadd_rn(xx, __dmul_rn(a, a));
+          yy = __dadd_rn(yy, __dmul_rn(b, b));
+        }
+      }
     }
     if (xx == 0.0 && yy == 0.0) *dist = 0.0;
     else if (xx == 0.0 || yy == 0.0) *dist = 1.0;
@@ -275,9 +293,20 @@ __device__ __noinline__ bool pair_in_fp64(const float* xrows, int xstride, int d
     return *dist < eps;
   }
   double sacc = 0.0;
-  for (int k = 0; k < dd; ++k) {
-    const double t = __dsub_rn((double)x[k], (double)y[k]);
-    sacc = __dadd_rn(sacc, __dmul_rn(t, t));
+  for (int k0 = 0; k0 < dd; k0 += G) {
+    float xa[G], ya[G];
+#pragma unroll
+    for (int i = 0; i < G; ++i) {
+      xa[i] = k0 + i < dd ? __ldg(x + k0 + i) : 0.f;
+      ya[i] = k0 + i < dd ? __ldg(y + k0 + i) : 0.f;
+    }
+#pragma unroll
+    for (int i = 0; i < G; ++i) {
+      if (k0 + i < dd) {
+        const double t = __dsub_rn((double)xa[i], (double)ya[i]);
+        sacc = __dadd_rn(sacc, __dmul_rn(t, t));
+      }
+    }
   }
   *dist = __dsqrt_rn(sacc);
   return sacc < eps2;
@@ -312,6 +341,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   static_assert(RA == 1, "one 128-row block per unit (N = BN MMAs, A double-buffered)");
   constexpr int ATOM_ELEMS = KIND == TC_TF32 ? 32 : 128;
   constexpr uint32_t IDESC = make_idesc<KIND>(128, BN);
+  constexpr bool KS = S::KS;
+  static_assert(!KS || (RA == 1 && !BRES && !PR), "K streaming: plain instances only");
+  // K streaming moves only the atoms the rows occupy (KATOMS is the maximum)
+  const int n_atoms = KS ? (args.ksteps + 3) / 4 : KATOMS;
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -448,32 +481,37 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const uint32_t uact = act_next;
         act_next = act_of(u + gridDim.x);
         if (!unit_active(uact, t0, t1)) continue;
-        const int ab = (int)(ui % ABUF);
-        if (ui >= ABUF) {             // wait until the MMAs of unit ui - ABUF released it
-          mbar_wait(&a_empty[ab], (a_ph >> ab) & 1u);
-          a_ph ^= 1u << ab;
-        }
-        uint8_t* sAb = sA + ab * S::A_BYTES;
-        mbar_expect_tx(&a_full[ab], (uint32_t)S::A_BYTES);
         if (ui == 0) TC_STAMP(3);
-        for (int r = 0; r < RA; ++r)
-          for (int ka = 0; ka < KATOMS; ++ka)
-            tma_load_2d(sAb + (r * KATOMS + ka) * S::A_ATOM, &tmA, &a_full[ab], ka * ATOM_ELEMS,
-                        (int)(mb * RA * 128 + r * 128));
+        if constexpr (!KS) {
+          const int ab = (int)(ui % ABUF);
+          if (ui >= ABUF) {             // wait until the MMAs of unit ui - ABUF released it
+            mbar_wait(&a_empty[ab], (a_ph >> ab) & 1u);
+            a_ph ^= 1u << ab;
+          }
+          uint8_t* sAb = sA + ab * S::A_BYTES;
+          mbar_expect_tx(&a_full[ab], (uint32_t)S::A_BYTES);
+          for (int r = 0; r < RA; ++r)
+            for (int ka = 0; ka < KATOMS; ++ka)
+              tma_load_2d(sAb + (r * KATOMS + ka) * S::A_ATOM, &tmA, &a_full[ab],
+                          ka * ATOM_ELEMS, (int)(mb * RA * 128 + r * 128));
+        }
         // warm L2 with the next unit's point block while this one computes
         const int64_t un = u + gridDim.x;
-        if (un < n_units && un / n_chunks != mb) {
+        if (!KS && un < n_units && un / n_chunks != mb) {
           for (int r = 0; r < RA; ++r)
             for (int ka = 0; ka < KATOMS; ++ka)
               tma_prefetch_2d(&tmA, ka * ATOM_ELEMS, (int)((un / n_chunks) * RA * 128 + r * 128));
         }
         for (int64_t t = t0; t < t1 && !BRES; ++t) {
           if (!tile_active(uact, t)) continue;
-          for (int ka = 0; ka < KATOMS; ++ka) {
+          for (int ka = 0; ka < n_atoms; ++ka) {
             mbar_wait(&empty[stage], phase ^ 1u);
             mbar_expect_tx(&full[stage], (uint32_t)S::B_STAGE);
             tma_load_2d(sB + stage * S::B_STAGE, &tmB, &full[stage], ka * ATOM_ELEMS,
                         (int)(t * BN));
+            if constexpr (KS)   // the unit's A atom ka rides in the same stage
+              tma_load_2d(sB + stage * S::B_STAGE + BN * 128, &tmA, &full[stage],
+                          ka * ATOM_ELEMS, (int)(mb * 128));
             if (++stage == STAGES) {
               stage = 0;
               phase ^= 1u;
@@ -517,10 +555,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           n_skip += t1 - t0;
           continue;
         }
-        const int ab = (int)(ui % ABUF);
-        mbar_wait(&a_full[ab], (a_ph >> ab) & 1u);
-        a_ph ^= 1u << ab;
-        fence_after();
+        const int ab = KS ? 0 : (int)(ui % (ABUF > 0 ? ABUF : 1));
+        if constexpr (!KS) {
+          mbar_wait(&a_full[ab], (a_ph >> ab) & 1u);
+          a_ph ^= 1u << ab;
+          fence_after();
+        }
         if (ui == 0) TC_STAMP(5);
         const uint8_t* sAb = sA + ab * S::A_BYTES;
         for (int64_t t = t0; t < t1; ++t) {
@@ -559,13 +599,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             if constexpr (FOLD)
               mma<KIND>(dcol, sdesc32(su32(sAK)), sdesc32(su32(sBK + t * S::BK_SLOT)), idesc, 1u);
           }
-          for (int ka = 0; ka < KATOMS && !BRES; ++ka) {
+          for (int ka = 0; ka < n_atoms && !BRES; ++ka) {
             mbar_wait(&full[stage], phase);
             fence_after();
             const uint32_t bbase = su32(sB + stage * S::B_STAGE);
 #pragma unroll
             for (int r = 0; r < RA; ++r) {
-              const uint32_t abase = su32(sAb + (r * KATOMS + ka) * S::A_ATOM);
+              const uint32_t abase = KS ? bbase + (uint32_t)(BN * 128)
+                                        : su32(sAb + (r * KATOMS + ka) * S::A_ATOM);
 #pragma unroll
               for (int ks = 0; ks < 4; ++ks) {
                 if (ka * 4 + ks < ksteps)
@@ -591,7 +632,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           ++use[buf];
           buf = buf + 1 == NBUF ? 0 : buf + 1;
         }
-        mma_commit(&a_empty[ab]);
+        if constexpr (!KS) mma_commit(&a_empty[ab]);
         ++ui;
       }
       if (MODE == TC_MODE_MEMBER && args.stats) {
@@ -1040,6 +1081,8 @@ static cudaError_t launch_cfg(const TcPlan& P, TcArgs a, cudaStream_t s) {
 //   K <= 256 bytes (tf32 d <= 64, int8 d <= 256): 4 stages, 2 A buffers
 //   K <= 512 bytes (tf32 d <= 128):               4 stages, 1 A buffer
 //   K <= 896 bytes (int8 d <= 896):               3 stages, 1 A buffer
+//   K <= 4096 bytes (tf32 d <= 1024, int8 d <= 4096): 4 stages of (B atom + A atom),
+//                                                 no resident A block (ABUF = 0)
 // resident B applies when every CTA's units share one column chunk (enough
 // point blocks: n_chunks = 1 for any column count) and the launch's columns
 // fit the stage ring (the fused greedy tile: <= 1024 columns)
@@ -1068,24 +1111,28 @@ static cudaError_t dispatch(const TcPlan& P, const TcArgs& a, cudaStream_t s) {
     if (P.katoms == 1) return launch_cfg<TC_TF32, 1, 256, 1, 4, 2, MODE>(P, a, s);
     if (P.katoms <= 2) return launch_cfg<TC_TF32, 1, 256, 2, 4, 2, MODE>(P, a, s);
     if (P.katoms <= 4) return launch_cfg<TC_TF32, 1, 256, 4, 4, 1, MODE>(P, a, s);
+    // wide rows (the paper's D up to 1000): A atoms stream with the B atoms
+    if (P.katoms <= 32) return launch_cfg<TC_TF32, 1, 256, 32, 4, 0, MODE>(P, a, s);
     return cudaErrorNotSupported;
   }
   if (P.kind == TC_U8) {
     if (P.katoms == 1) return launch_cfg<TC_U8, 1, 256, 1, 4, 2, MODE>(P, a, s);
     if (P.katoms <= 2) return launch_cfg<TC_U8, 1, 256, 2, 4, 2, MODE>(P, a, s);
     if (P.katoms <= 7) return launch_cfg<TC_U8, 1, 256, 7, 3, 1, MODE>(P, a, s);
+    if (P.katoms <= 32) return launch_cfg<TC_U8, 1, 256, 32, 4, 0, MODE>(P, a, s);
     return cudaErrorNotSupported;
   }
   if (P.katoms == 1) return launch_cfg<TC_S8, 1, 256, 1, 4, 2, MODE>(P, a, s);
   if (P.katoms <= 2) return launch_cfg<TC_S8, 1, 256, 2, 4, 2, MODE>(P, a, s);
   if (P.katoms <= 7) return launch_cfg<TC_S8, 1, 256, 7, 3, 1, MODE>(P, a, s);
+  if (P.katoms <= 32) return launch_cfg<TC_S8, 1, 256, 32, 4, 0, MODE>(P, a, s);
   return cudaErrorNotSupported;
 }
 
 int tc_bn_for(int kind, int katoms) { return 256; }
 int tc_rows_for(int kind, int katoms) { return 128; }
 bool tc_supported(int kind, int katoms) {
-  return kind == TC_TF32 ? katoms <= 4 : katoms <= 7;
+  return katoms <= 32;   // 4096-byte rows: tf32 d <= 1024, int8 d <= 4096
 }
 
 // mode: TC_MODE_MEMBER / TC_MODE_PROBE_LDONLY / TC_MODE_PROBE_NOLD on the

@@ -30,7 +30,10 @@ def tf32_rna(x: np.ndarray) -> np.ndarray:
 
 
 @pytest.mark.parametrize("n,d,L", [(300, 3, 70), (1000, 17, 333), (1500, 64, 700),
-                                   (700, 100, 257), (129, 128, 65)])
+                                   (700, 100, 257), (129, 128, 65),
+                                   # wide rows: A atoms streamed with the B atoms (ABUF = 0)
+                                   (300, 129, 70), (600, 200, 300), (600, 500, 513),
+                                   (400, 1000, 129), (130, 1024, 33)])
 def test_tc_gram_tf32(bm, n, d, L):
     from paper_2601_01405_b200 import bm as B
     rng = np.random.default_rng(n + d)
@@ -47,7 +50,8 @@ def test_tc_gram_tf32(bm, n, d, L):
 
 @pytest.mark.parametrize("dtype", ["u8", "i8"])
 @pytest.mark.parametrize("n,d,L", [(300, 3, 70), (1000, 32, 257), (777, 100, 300),
-                                   (600, 784, 513), (513, 896, 77)])
+                                   (600, 784, 513), (513, 896, 77), (300, 1000, 100),
+                                   (200, 4096, 50)])
 def test_tc_gram_int8_exact(bm, dtype, n, d, L):
     from paper_2601_01405_b200 import bm as B
     rng = np.random.default_rng(n * 7 + d)
@@ -71,7 +75,7 @@ def test_tensor_path_parity(bm, name, m):
     compare(X, w.metric, w.eps, cov, float_path=w.dtype == "f32", tie_rate_limit=True)
 
 
-@pytest.mark.parametrize("d", [32, 33, 64, 100, 128])
+@pytest.mark.parametrize("d", [32, 33, 64, 100, 128, 200, 513, 1000])
 @pytest.mark.parametrize("dtype", ["f32", "u8", "i8"])
 def test_tensor_path_random(bm, d, dtype):
     n = 3000
@@ -91,7 +95,7 @@ def test_tensor_path_random(bm, d, dtype):
         compare(Y, "l2", eps, cov, float_path=True)
 
 
-@pytest.mark.parametrize("d", [3, 16, 64, 100])
+@pytest.mark.parametrize("d", [3, 16, 64, 100, 300])
 def test_tensor_path_cosine(bm, d):
     """Cosine distance on tcgen05 (Gram of the normalised rows, rigorous band,
     fp64 recheck with the zero-vector rule): equal to the oracle, with zero

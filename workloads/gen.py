@@ -210,3 +210,26 @@ def random_cloud(n: int, d: int, dtype: str = "f32", seed: int = 0, scale: float
     if dtype == "u8":
         return rng.integers(max(lo, 0), min(hi, 255) + 1, size=(n, d)).astype(np.uint8)
     raise ValueError(dtype)
+
+
+# --------------------------------------------------------------- paper grid
+# PAPER.md:263 ("Datasets were generated"; n in {100, 500, 1000, 2000, 5000},
+# D in {10, 50, 100, 200, 500, 1000}, 65 trials per cell).  The paper states
+# no distribution or radius; SPEC.md:131 fixes uniform on [0,1)^D and
+# SPEC.md:529 eps = 0.5 sqrt(D/6) (reading G1).
+PAPER_GRID_N = (100, 500, 1000, 2000, 5000)
+PAPER_GRID_D = (10, 50, 100, 200, 500, 1000)
+
+
+def cube_eps(D: int) -> float:
+    """The grid's radius for dimension D: half the RMS distance
+    sqrt(D/6) of two uniform points of the unit cube."""
+    return 0.5 * math.sqrt(D / 6.0)
+
+
+def cube_cloud(n: int, D: int, trial: int = 0) -> np.ndarray:
+    """Trial ``trial`` of grid cell (n, D): n x D float32 uniform on [0,1)^D,
+    seeded by (n, D, trial) so every cell and trial is reproducible."""
+    rng = np.random.default_rng([0xB1, int(n), int(D), int(trial)])
+    return rng.random((int(n), int(D))).astype(np.float32)
+
