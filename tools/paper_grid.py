@@ -2,8 +2,8 @@
 
 PAPER.md:263 [§4]: n in {100, 500, 1000, 2000, 5000} x D in {10, 50, 100,
 200, 500, 1000}, 65 trials per cell, Euclidean eps-net; §4.1 reports median
-runtimes and speedups; §4.3 (P:318-356) fits T(D) = k D^p by least squares on
-log T = log k + p log D and reports p with R^2 (Table 1).  Inputs: uniform on
+runtimes and speedups; §4.3 (P:318-338) fits T(D) = k D^p by least squares on
+log T = log k + p log D and reports p with R^2 (Table 1, P:340-356).  Inputs: uniform on
 [0,1)^D, eps = 0.5 sqrt(D/6) (workloads/gen.py cube_cloud / cube_eps; DESIGN.md
 reading G1).  The paper's comparison systems (Ball Tree, FAISS, pyBallMapper)
 are out of scope; the oracle (C, OpenMP) is timed beside the GPU instead.
@@ -20,6 +20,7 @@ Fits: T(D) at each n and T(n) at each D, for e2e and device time (fit_power_law)
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import math
 import os
@@ -36,9 +37,9 @@ from workloads import gen  # noqa: E402
 
 
 def fit_power_law(xs, ys) -> dict:
-    """Least-squares line through (log x, log y) (P:330-338 [§4.3]): p = slope,
+    """Least-squares line through (log x, log y) (P:326-332 [§4.3]): p = slope,
     k = exp(intercept), R^2 = 1 - SS_res / SS_tot in log space on the fit's own
-    residuals (P:340-346)."""
+    residuals (P:334-338)."""
     x = np.asarray(xs, dtype=np.float64)
     y = np.asarray(ys, dtype=np.float64)
     if x.size < 2 or x.size != y.size:
@@ -65,6 +66,10 @@ def median(v):
 def run(trials: int, oracle_trials: int, ns, ds, out):
     import torch
 
+    # the oracle's OpenMP threads must not spin on the host cores while the
+    # GPU cells are timed (measured: 3x outliers in the cell after an oracle
+    # call); the oracle runs in a second pass, after every GPU cell
+    os.environ.setdefault("OMP_WAIT_POLICY", "PASSIVE")
     import paper_2601_01405_b200 as bm
     from oracle import oracle as O
 
@@ -74,16 +79,26 @@ def run(trials: int, oracle_trials: int, ns, ds, out):
     for n in ns:
         for D in ds:
             eps = gen.cube_eps(D)
-            dev, e2e, orc = [], [], []
+            dev, e2e = [], []
             L = M = E = None
             # every trial's cloud is generated (and uploaded) before the timed
             # runs, so they run back to back (host generation between runs let
             # the idle GPU change clocks: 10x outliers)
             Xh_all = [gen.cube_cloud(n, D, t) for t in range(trials)]
             Xd_all = [torch.from_numpy(x).cuda() for x in Xh_all]
-            # warm-up (untimed): one trial per cell
-            bm.cover_build(Xd_all[0], "l2", eps).free()
-            torch.cuda.synchronize()
+            # warm-up (untimed): at least 3 covers and 0.3 s of
+            # back-to-back GPU work, so the GPU leaves its idle clocks first
+            # (the host-side generation above leaves it idle for up to a second)
+            tw = time.perf_counter()
+            for i in range(1000):
+                bm.cover_build(Xd_all[i % trials], "l2", eps).free()
+                torch.cuda.synchronize()
+                if i >= 2 and time.perf_counter() - tw > 0.3:
+                    break
+            # no collector pass inside a timed call (the wrapper's Python work
+            # after the library returns sits inside the event bracket)
+            gc.collect()
+            gc.disable()
             for t in range(trials):
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record()
@@ -100,23 +115,30 @@ def run(trials: int, oracle_trials: int, ns, ds, out):
                 h = bm.cover_build_host(Xh_all[t], "l2", eps)
                 e2e.append((time.perf_counter() - t0) * 1e3)
                 del h
+            gc.enable()
             del Xd_all
-            for t in range(oracle_trials):
-                Xh = gen.cube_cloud(n, D, t)
-                t0 = time.perf_counter()
-                o = O.cover(Xh, "l2", eps)
-                orc.append((time.perf_counter() - t0) * 1e3)
-                if t == 0:
-                    assert o.L == L, f"cell ({n}, {D}): oracle L {o.L} != GPU L {L}"
             rec = {"row": "NEXT-4 paper grid", "n": n, "D": D, "eps": eps, "L": L, "M": M, "E": E,
                    "trials": trials, "device_ms": round(median(dev), 4),
-                   "e2e_ms": round(median(e2e), 4), "oracle_trials": oracle_trials,
-                   "oracle_ms": round(median(orc), 3) if orc else None,
-                   "speedup_e2e": round(median(orc) / median(e2e), 1) if orc else None}
+                   "device_ms_min": round(min(dev), 4), "device_ms_all": [round(x, 2) for x in dev],
+                   "device_ms_p90": round(sorted(dev)[int(0.9 * (len(dev) - 1))], 4),
+                   "e2e_ms": round(median(e2e), 4),
+                   "oracle_trials": oracle_trials}
             cells.append(rec)
-            print(json.dumps(rec), flush=True)
-            if out:
-                out.write(json.dumps(rec) + "\n")
+    for rec in cells:   # second pass: the oracle beside every cell
+        n, D, eps = rec["n"], rec["D"], rec["eps"]
+        orc = []
+        for t in range(oracle_trials):
+            Xh = gen.cube_cloud(n, D, t)
+            t0 = time.perf_counter()
+            o = O.cover(Xh, "l2", eps)
+            orc.append((time.perf_counter() - t0) * 1e3)
+            if t == 0:
+                assert o.L == rec["L"], f"cell ({n}, {D}): oracle L {o.L} != GPU L {rec['L']}"
+        rec["oracle_ms"] = round(median(orc), 3) if orc else None
+        rec["speedup_e2e"] = round(median(orc) / rec["e2e_ms"], 1) if orc else None
+        print(json.dumps(rec), flush=True)
+        if out:
+            out.write(json.dumps(rec) + "\n")
     fits = []
     for key in ("e2e_ms", "device_ms", "oracle_ms"):
         for n in ns:
