@@ -14,7 +14,8 @@ from dataclasses import dataclass
 import numpy as np
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libbm_b200.so")
+# BM_LIB_PATH (diagnostics only): load another build of the library, e.g. for A/B runs
+LIB_PATH = os.environ.get("BM_LIB_PATH") or os.path.join(PKG, "libbm_b200.so")
 
 BM_OK, BM_EINVAL, BM_EUNSUPPORTED, BM_ENOMEM, BM_ECUDA, BM_EOVERFLOW = range(6)
 STATUS_NAMES = {0: "BM_OK", 1: "BM_EINVAL", 2: "BM_EUNSUPPORTED", 3: "BM_ENOMEM",

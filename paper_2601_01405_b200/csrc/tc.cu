@@ -910,35 +910,84 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             if (__any_sync(FULLM, surv)) {
               // rare path: column masks of candidates (not certainly out) and
               // certain-in pairs, then one append per set bit
-              uint32_t cand = 0u;
-              if (surv) {
+              if constexpr (!PR) {
+                // unpruned instances: candidate mask only; the certain-in
+                // test per candidate column (select tree + one d_j load)
+                uint32_t cand = 0u;
+                if (surv) {
 #pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                  if constexpr (KIND == TC_TF32) {
-                    cand |= (__uint_as_float(v[i]) > rlo[r] ? 1u : 0u) << i;
-                  } else {
-                    cand |= (2 * (int)v[i] - __ldg(args.col_c + j0 + i) > rint[r] ? 1u : 0u) << i;
+                  for (int i = 0; i < 32; ++i) {
+                    if constexpr (KIND == TC_TF32) {
+                      cand |= (__uint_as_float(v[i]) > rlo[r] ? 1u : 0u) << i;
+                    } else {
+                      cand |= (2 * (int)v[i] - __ldg(args.col_c + j0 + i) > rint[r] ? 1u : 0u) << i;
+                    }
                   }
                 }
-              }
-              // candidates only (a few per chunk): the certain-in test of
-              // column i takes its accumulator by a select tree and its d_j by
-              // one load, instead of testing all 32 columns
-              while (cand) {
-                const int i = __ffs(cand) - 1;
-                cand &= cand - 1u;
-                const int64_t j = j0 + i;
-                bool in = true;
-                if constexpr (KIND == TC_TF32) {
-                  const float dji = S::DJ_BYTES > 0 ? sdj[j] : __ldg(args.col_a + j);
-                  in = __uint_as_float(sel32(v, i)) - dji > rhi[r];
+                // candidates only (a few per chunk): the certain-in test of
+                // column i takes its accumulator by a select tree and its d_j by
+                // one load, instead of testing all 32 columns
+                while (cand) {
+                  const int i = __ffs(cand) - 1;
+                  cand &= cand - 1u;
+                  const int64_t j = j0 + i;
+                  bool in = true;
+                  if constexpr (KIND == TC_TF32) {
+                    const float dji = S::DJ_BYTES > 0 ? sdj[j] : __ldg(args.col_a + j);
+                    in = __uint_as_float(sel32(v, i)) - dji > rhi[r];
+                  }
+                  if (in) {
+                    if (args.covered) args.covered[ppt[r]] = 1;
+                    append(1, ((unsigned long long)ppt[r] << args.lbits) |
+                                  (unsigned long long)(lpos0 + kpos(j)));
+                  } else {
+                    append(2, ((unsigned long long)ppt[r] << 32) | (unsigned long long)j);
+                  }
                 }
-                if (in) {
-                  if (args.covered) args.covered[ppt[r]] = 1;
-                  append(1, ((unsigned long long)ppt[r] << args.lbits) |
-                                (unsigned long long)(lpos0 + kpos(j)));
-                } else {
-                  append(2, ((unsigned long long)ppt[r] << 32) | (unsigned long long)j);
+              } else {
+                // pruned instances (sparse survivors): both masks at once
+                // (measured: the per-candidate form slowed C3's pruned kernel
+                // 71 -> 80 ms)
+                uint32_t cand = 0u, inm = 0u;
+                float dj[32];   // tf32 in-test offsets of the chunk (warp-uniform loads)
+                if constexpr (KIND == TC_TF32) {
+                  const float4* d4 = reinterpret_cast<const float4*>(
+                      S::DJ_BYTES > 0 ? (const float*)(sdj + j0) : args.col_a + j0);
+#pragma unroll
+                  for (int i4 = 0; i4 < 8; ++i4) {
+                    float4 q4;
+                    if constexpr (S::DJ_BYTES > 0) q4 = d4[i4];   // shared memory
+                    else q4 = __ldg(d4 + i4);
+                    dj[4 * i4] = q4.x;
+                    dj[4 * i4 + 1] = q4.y;
+                    dj[4 * i4 + 2] = q4.z;
+                    dj[4 * i4 + 3] = q4.w;
+                  }
+                }
+                if (surv) {
+#pragma unroll
+                  for (int i = 0; i < 32; ++i) {
+                    if constexpr (KIND == TC_TF32) {
+                      const float a = __uint_as_float(v[i]);
+                      cand |= (a > rlo[r] ? 1u : 0u) << i;
+                      inm |= (a - dj[i] > rhi[r] ? 1u : 0u) << i;
+                    } else {
+                      cand |= (2 * (int)v[i] - __ldg(args.col_c + j0 + i) > rint[r] ? 1u : 0u) << i;
+                    }
+                  }
+                  if constexpr (KIND != TC_TF32) inm = cand;
+                }
+                while (cand) {
+                  const int i = __ffs(cand) - 1;
+                  cand &= cand - 1u;
+                  const int64_t j = j0 + i;
+                  if ((inm >> i) & 1u) {
+                    if (args.covered) args.covered[ppt[r]] = 1;
+                    append(1, ((unsigned long long)ppt[r] << args.lbits) |
+                                  (unsigned long long)(lpos0 + kpos(j)));
+                  } else {
+                    append(2, ((unsigned long long)ppt[r] << 32) | (unsigned long long)j);
+                  }
                 }
               }
               __syncwarp();
