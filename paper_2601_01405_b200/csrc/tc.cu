@@ -1518,8 +1518,11 @@ cudaError_t launch_tc_prep(const void* X, int dtype, int64_t n, int d, const TcP
                            void* nrm, DevStats* stats, cudaStream_t s, int64_t* launches) {
   ++*launches;
   const unsigned g = (unsigned)((n * 32 + 255) / 256);   // one warp per row
+  // G lanes per row, each striding over its row: 8 lanes cover a 32-float
+  // (128-byte) row in four coalesced 32-byte passes with a quarter of the
+  // threads and shuffles a warp per row would need
   int G = 1;
-  while (G < 32 && G < (int)(P.row_bytes / 4)) G *= 2;
+  while (G < 8 && G < (int)(P.row_bytes / 4)) G *= 2;
   if (dtype == BM_F32)
     k_tc_prep_f32<<<(unsigned)((n * G + 255) / 256), 256, 0, s>>>(
         (const float*)X, n, d, (int)(P.row_bytes / 4), P.cosine, G, (float*)P.xop,
