@@ -151,8 +151,8 @@ cudaError_t launch_prep(const void* X, int dtype, int64_t n, int d, int kind, in
   int bs = 256;
   int64_t g = (n * 32 + bs - 1) / bs;   // one warp per row
   if (dtype == BM_F32) {
-    int G = 1;
-    while (G < 32 && G < 2 * nu) G *= 2;
+    int G = 1;   // lanes per row (each strides over the row's 2 nu floats)
+    while (G < 8 && G < 2 * nu) G *= 2;
     g = (n * G + bs - 1) / bs;
     k_prep_f32<<<(unsigned)g, bs, 0, s>>>((const float*)X, n, d, nu, kind == K_COSF, G, rows,
                                           xhat, stats);
