@@ -462,12 +462,36 @@ void set_recheck(bm::tc::TcArgs& ta, const void* xrows, int xstride, int d, cons
 }
 
 // tf32 column-constant fold operands: B constants [l_rows][8] and the A ones tile.
+// The fold's constant A tile ({1,1,1,0,...} x 128 rows) is the same for every
+// build: one copy per device, written once (synchronously) on first use.
+static const float* fold_ones_tile() {
+  static std::mutex mu;
+  static const float* tiles[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!tiles[dev]) {
+    float h[128 * 8];
+    for (int i = 0; i < 128 * 8; ++i) h[i] = (i & 7) < 3 ? 1.f : 0.f;
+    float* d = nullptr;
+    if (cudaMalloc(&d, sizeof h) != cudaSuccess) return nullptr;
+    if (cudaMemcpy(d, h, sizeof h, cudaMemcpyHostToDevice) != cudaSuccess) {
+      cudaFree(d);
+      return nullptr;
+    }
+    tiles[dev] = d;
+  }
+  return tiles[dev];
+}
+
 bm_status alloc_fold(Pool& pool, bm::tc::TcPlan& P, bm::tc::TcArgs& ta, cudaStream_t s,
                      int64_t* launches) {
-  float *colk = nullptr, *ones = nullptr;
+  (void)s;
+  (void)launches;
+  float* colk = nullptr;
   TRY(pool.alloc(&colk, (size_t)P.l_rows * 8));
-  TRY(pool.alloc(&ones, (size_t)128 * 8));
-  CK(bm::tc::launch_tc_ones(ones, s, launches));
+  const float* ones = fold_ones_tile();
+  if (!ones) return set_err(BM_ENOMEM, "fold constant tile allocation failed");
   ta.colk = colk;
   P.ones = ones;
   return BM_OK;

@@ -1504,16 +1504,6 @@ cudaError_t launch_tc_tile_cand(const TcPlan& P, const TcPlan& Pc, const void* n
                     (float*)ac.col_a, (float*)ac.col_b, (float*)ac.colk, (int32_t*)ac.col_c);
 }
 
-__global__ void k_tc_ones(float* o) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < 128 * 8) o[i] = (i & 7) < 3 ? 1.f : 0.f;
-}
-cudaError_t launch_tc_ones(float* ones, cudaStream_t s, int64_t* launches) {
-  ++*launches;
-  k_tc_ones<<<4, 256, 0, s>>>(ones);
-  return cudaGetLastError();
-}
-
 cudaError_t launch_tc_prep(const void* X, int dtype, int64_t n, int d, const TcPlan& P,
                            void* nrm, DevStats* stats, cudaStream_t s, int64_t* launches) {
   ++*launches;

@@ -94,7 +94,6 @@ int tc_rows_for(int kind, int katoms);
 bool tc_supported(int kind, int katoms);
 
 // fill the [128][8] constant A tile of the column-constant fold ({1,1,1,0,...})
-cudaError_t launch_tc_ones(float* ones, cudaStream_t s, int64_t* launches);
 cudaError_t launch_tc_prep(const void* X, int dtype, int64_t n, int d, const TcPlan& P,
                            void* nrm, DevStats* stats, cudaStream_t s, int64_t* launches);
 cudaError_t launch_tc_rows(const TcPlan& P, const void* nrm, int64_t n, double C2, double eps2,
