@@ -6,9 +6,12 @@
     python bench.py --impl reference ...        # the CPU oracle arm
 
 One step = one full bm_cover_build (greedy eps-net, membership, CSR, edges) of
-the workload.  The default workload is BASELINE.json configs[1] (C2).  Inputs
-are resident in HBM before the timed region; L2 is flushed (a 256 MiB write)
-before every timed step, outside the step's CUDA-event bracket.  N > 1 runs N
+the workload.  BASELINE.json's metric names no config, so the default workload
+is the largest single-GPU config, configs[4] (C5: 1e7 x 16 fp32) with its
+first metric, L1 (eps 2.0); --workload selects the others (c1, c2, c3_e2,
+c3_e4, c3_e8, c4, c5_cos).  Inputs are resident in HBM before the timed
+region; L2 is flushed (a 256 MiB write) before every timed step, outside the
+step's CUDA-event bracket.  N > 1 runs N
 independent replicas (the path does not shard across
 GPUs in this build), one per rank, timed on the device, max over ranks.
 
@@ -34,10 +37,10 @@ UNIT = "evals/s"
 def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c2")
+    ap.add_argument("--workload", default="c5_l1")
     ap.add_argument("--n", type=int, default=0, help="prefix size (0 = the full workload)")
     ap.add_argument("--tile", type=int, default=0)
     ap.add_argument("--path", default="auto")
@@ -125,51 +128,68 @@ def _traffic(w):
     return None
 
 
-def roofline_tensor(w, L, kernel_ms, n, peaks, step_ms, st=None):
-    """tcgen05 contraction, two ceilings:
-      tensor: 2*d algorithmic ops per pair (true d, not the padded K) against
-        the measured bf16 peak x the nominal ratio (tf32 0.5, int8 2.0); burst
-        figure for short steps, sustained for steps > 0.5 s;
-      tmem: every pair's 4-byte accumulator is read from tensor memory once,
-        against 64 B/clk/SM x 148 SMs x sm_max_mhz (the guide's LDTM rate,
-        confirmed on this B200: 61 B/clk/SM with a TMEM-read-only epilogue,
-        tools/tc_probe_c2.py mode 2).
-    The reported bound is the ceiling the kernel is closer to (the binding
-    one); the other is kept under "other"."""
-    sustained = step_ms > 500.0
+def tc_peaks(peaks, sustained):
+    """Dense tensor peaks for the contraction's own dtype.  Preferred: the
+    tcgen05 microbenchmark committed under profiles/ (tools/ubench/tc_peak.cu,
+    kind::tf32 / kind::i8 / kind::f16-bf16, M128 N256 back to back on every
+    SM); its bf16 figure is checked against MEASURED_PEAKS' cuBLAS one and the
+    ratio carries the sustained/burst choice over.  Fallback: MEASURED_PEAKS'
+    bf16 x the guide's nominal ratio (tf32 0.5, int8 2)."""
     bf16 = float(peaks["bf16_tflops_sustained" if sustained else "bf16_tflops"])
-    ratio = 0.5 if w.dtype == "f32" else 2.0
-    peak = bf16 * ratio
+    p = os.path.join(ROOT, "profiles", "tc_peak.json")
+    if os.path.exists(p):
+        try:
+            m = {r["kind"]: float(r["tflops"]) for r in map(json.loads, open(p)) if "tflops" in r}
+            if "tf32" in m and "i8" in m:
+                scale = 1.0
+                if sustained and "bf16" in m and m["bf16"] > 0:
+                    scale = min(1.0, float(peaks["bf16_tflops_sustained"]) / m["bf16"])
+                return ({"tf32": m["tf32"] * scale, "i8": m["i8"] * scale},
+                        "measured tcgen05 microbenchmark (profiles/tc_peak.json)" +
+                        (f" x sustained/burst {scale:.3f}" if scale != 1.0 else ""))
+        except Exception:
+            pass
+    return ({"tf32": 0.5 * bf16, "i8": 2.0 * bf16},
+            f"MEASURED_PEAKS bf16 {'sustained' if sustained else 'burst'} {bf16} x nominal ratio")
+
+
+def roofline_tensor(w, L, kernel_ms, n, peaks, step_ms, st=None):
+    """tcgen05 contraction on the SURVEY §8(d) basis: 2*d algorithmic ops per
+    decided (point, landmark) pair (true d, not the padded K), n*L pairs per
+    cover, divided by the membership kernel's time and the measured dense peak
+    of its dtype (tf32 for float rows, int8 for integer rows; burst figure
+    for short steps, sustained for steps > 0.5 s).  With the tile-level
+    pruning the kernel decides pairs it never multiplies, so this fraction can
+    exceed what the MMA alone could do; the executed-tile basis (MMA work
+    actually issued) and the TMEM-read volume are kept under "other"."""
+    sustained = step_ms > 500.0
+    pk, basis = tc_peaks(peaks, sustained)
+    dt = "tf32" if w.dtype == "f32" else "i8"
+    peak = pk[dt]
     ks = kernel_ms * 1e-3
-    # executed work: with the tile-level pruning (cells.cu) only the contracted
-    # 128 x 256 tiles and the 128 x 32 chunks read from TMEM count against the
-    # ceilings; without it (or on paths that do not report) every pair does
+    ops = 2.0 * w.d * float(n) * L
+    achieved = ops / ks / 1e12 if kernel_ms > 0 else 0.0
     tiles = getattr(st, "tc_tiles_run", 0) if st is not None else 0
     chunks = getattr(st, "tc_chunks_run", 0) if st is not None else 0
-    ops = 2.0 * w.d * (tiles * 128.0 * 256.0 if tiles else float(n) * L)
-    achieved = ops / ks / 1e12 if kernel_ms > 0 else 0.0
+    ex_ops = 2.0 * w.d * (tiles * 128.0 * 256.0 if tiles else float(n) * L)
+    ex = ex_ops / ks / 1e12 if kernel_ms > 0 else 0.0
     clk = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
-    tmem_peak = 64.0 * 148 * clk / 1e9                      # GB/s
     tmem_bytes = (chunks * 128.0 * 32.0 if chunks else float(n) * L) * 4.0
     tmem_ach = tmem_bytes / ks / 1e9 if kernel_ms > 0 else 0.0
-    kern = "k_tc (tcgen05 " + ("tf32" if w.dtype == "f32" else "int8") + ", per-tile)"
-    tensor = {"bound": "tensor", "achieved": round(achieved, 3), "peak": round(peak, 3),
-              "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
-              "ops_per_pair": 2 * w.d,
-              "peak_basis": f"measured bf16 {'sustained' if sustained else 'burst'} "
-                            f"{bf16} x {ratio} (nominal {'tf32' if ratio == 0.5 else 'int8'} "
-                            f"ratio)"}
-    tmem = {"bound": "tmem", "achieved": round(tmem_ach, 1), "peak": round(tmem_peak, 1),
-            "unit": "GB/s", "frac": round(tmem_ach / tmem_peak, 4),
-            "bytes_per_pair": 4,
-            "peak_basis": "64 B/clk/SM TMEM read (guide; 61 B/clk measured here) x 148 x "
-                          f"{clk / 1e6:.0f} MHz"}
-    main, other = (tmem, tensor) if tmem["frac"] > tensor["frac"] else (tensor, tmem)
-    out = dict(main)
-    out.update({"kernel": kern, "traffic": _traffic(w), "kernel_ms": round(kernel_ms, 5),
-                "other": other,
-                "work_basis": "executed tiles / TMEM chunks" if tiles else "n x L pairs",
-                "decided_pairs_per_s": round(float(n) * L / ks, 1) if ks > 0 else None})
+    kern = "k_tc (tcgen05 " + dt + ", membership)"
+    out = {"bound": "tensor", "achieved": round(achieved, 3), "peak": round(peak, 3),
+           "unit": "TFLOP/s" if dt == "tf32" else "TOP/s", "frac": round(achieved / peak, 4),
+           "ops_per_pair": 2 * w.d, "work_basis": "n x L decided pairs x 2d (SURVEY §8(d))",
+           "peak_basis": basis, "kernel": kern, "traffic": _traffic(w),
+           "kernel_ms": round(kernel_ms, 5),
+           "other": {
+               "executed_tiles": {"achieved": round(ex, 3), "frac": round(ex / peak, 4),
+                                  "basis": "128 x 256 tiles actually multiplied x 2d"},
+               "tmem_read": {"achieved_gbs": round(tmem_ach, 1),
+                             "bytes": "4 B per accumulator read (chunks actually read)",
+                             "note": "64 B/clk/SM guide rate; see profiles/tc_peak.json "
+                                     "tmem_read for the measured rate"}},
+           "decided_pairs_per_s": round(float(n) * L / ks, 1) if ks > 0 else None}
     if st is not None and (getattr(st, "tc_tiles_skipped", 0) or getattr(st, "tc_chunks_skipped", 0)):
         tt = st.tc_tiles_run + st.tc_tiles_skipped
         cc = st.tc_chunks_run + st.tc_chunks_skipped
@@ -209,10 +229,21 @@ def roofline_alu(w, L, kernel_ms, n, peaks):
             "peak_basis": f"148 SM x {lanes} lanes x sm_max_mhz, {what} (DESIGN.md §7)"}
 
 
-def cpu_baseline(w, X, budget_s: float):
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_baseline(w, X, budget_s: float, L_full: int = 0):
     """The oracle as it stands on the host cores, bounded sample of the workload:
     the largest prefix whose greedy finishes within ~budget_s (full workload when
-    it fits).  value = sample pairs (n_s * L_s) / oracle seconds."""
+    it fits).  value = sample pairs (n_s * L_s) / oracle seconds; the full-size
+    oracle time is extrapolated as n * L_full / value."""
     from oracle import oracle as O
     cores = O.set_threads(0)
     n = X.shape[0]
@@ -228,9 +259,15 @@ def cpu_baseline(w, X, budget_s: float):
         grow = max(2.0, min(8.0, (budget_s / 4) / max(dt, 1e-3)))
         m = min(n, int(m * math.sqrt(grow)))
     m, L, dt = res
-    return {"value": m * L / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"{'full' if m == n else 'prefix'} {w.name} n={m} (L={L}), 1 run, "
-                      f"{dt:.2f}s", "seconds": round(dt, 3)}
+    v = m * L / dt
+    out = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+           "sample": f"{'full' if m == n else 'prefix'} {w.name} n={m} (L={L}), 1 run, "
+                     f"{dt:.2f}s", "seconds": round(dt, 3), "cpu_model": cpu_model(),
+           "threads": cores}
+    if m < n and L_full:
+        out["extrapolated_full_s"] = round(n * L_full / v, 1)
+        out["extrapolation"] = "n * L_gpu / (prefix pairs per second), labelled extrapolated"
+    return out
 
 
 # ----------------------------------------------------------------- arms
@@ -290,7 +327,7 @@ def run_reference(args):
             "config": {"workload": w.name, "n": int(m), "d": w.d, "metric": w.metric,
                        "eps": w.eps, "L": int(L)},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
-                             "sample": sample},
+                             "sample": sample, "cpu_model": cpu_model()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -335,8 +372,18 @@ def run_ours(args):
         torch.cuda.synchronize()
 
     warm = max(args.warmup, 3)            # timing rule: >= 3 warm-up steps
+    wt = []
     for _ in range(warm):
+        t0 = time.perf_counter()
         bm.cover_build(X, w.metric, w.eps, **kw).free()
+        wt.append(time.perf_counter() - t0)
+    # long steps (>= 20 ms: C3, C5) are timed WITH the library's per-launch
+    # membership events, so the dominant kernel's time is measured live inside
+    # the timed region (the events cost < 0.5% there); short steps (C1, C2,
+    # C4) lose their PDL overlap to the events, so they are timed plain and
+    # the kernel time comes from separate instrumented steps
+    live = min(wt) >= 0.020
+    kw_timed = kw_t if live else kw
     sampler = ClockSampler(local)
     sampler.start()
     time.sleep(0.25)
@@ -346,7 +393,7 @@ def run_ours(args):
         flush.fill_(i & 0xFF)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        bm.cover_build(X, w.metric, w.eps, **kw).free()
+        bm.cover_build(X, w.metric, w.eps, **kw_timed).free()
         e1.record(stream)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
@@ -360,20 +407,23 @@ def run_ours(args):
     for i in range(args.steps):
         flush.fill_(i & 0xFF)                 # L2 flush outside the timed bracket
         ev[i][0].record(stream)
-        cov = bm.cover_build(X, w.metric, w.eps, **kw)
+        cov = bm.cover_build(X, w.metric, w.eps, **kw_timed)
         ev[i][1].record(stream)
         L, M, E, NPW = cov.L, cov.M, cov.E, cov.P
         launches += cov.stats.n_launches
+        if live:
+            covs_stats.append(cov.stats)
         cov.free()
     barrier()
     gc.enable()
     clocks = sampler.stop()
-    # instrumented pass (not timed): per-step breakdown, membership kernel time
-    for i in range(max(3, min(args.steps, 10))):
-        flush.fill_(i & 0xFF)
-        cov = bm.cover_build(X, w.metric, w.eps, **kw_t)
-        covs_stats.append(cov.stats)
-        cov.free()
+    if not live:
+        # instrumented pass (not timed): per-step breakdown, membership kernel time
+        for i in range(max(3, min(args.steps, 10))):
+            flush.fill_(i & 0xFF)
+            cov = bm.cover_build(X, w.metric, w.eps, **kw_t)
+            covs_stats.append(cov.stats)
+            cov.free()
     torch.cuda.synchronize()
     step_ms = [a.elapsed_time(b) for a, b in ev]
     ms = sum(step_ms) / len(step_ms)
@@ -395,9 +445,11 @@ def run_ours(args):
     roof["share_of_step"] = round(kern_ms / ms, 4) if ms > 0 else None
     roof["launches_per_step"] = int(kern_launches)
     roof["avg_launch_ms"] = round(kern_ms / max(1, kern_launches), 5)
-    roof["timing"] = ("CUDA events on the launch stream around every membership launch "
-                      "(one per greedy tile), summed per step, median over the instrumented "
-                      "steps (share_of_step relative to the uninstrumented step time)")
+    roof["timing"] = ("CUDA events on the launch stream around every membership launch, "
+                      "summed per step, median over " +
+                      ("the timed steps themselves" if live else
+                       "separate instrumented steps (short steps lose PDL overlap to the "
+                       "events; share_of_step relative to the plain step time)"))
 
     # e2e through the public host-buffer entry point (H2D + D2H inside the timing)
     pinned = torch.from_numpy(Xh).pin_memory()
@@ -416,7 +468,7 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(w, Xh, args.cpu_sample_seconds)
+        cpu = cpu_baseline(w, Xh, args.cpu_sample_seconds, L_full=L)
 
     last = covs_stats[-1]
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -432,9 +484,10 @@ def run_ours(args):
             "cover_ms": round(ms, 4),
             "step_ms_stats": step_stats, "step_ms_all": [round(x, 4) for x in step_ms],
             "breakdown_ms": breakdown,
-            "breakdown_note": "library CUDA events per sub-step, separate instrumented steps "
-                              "(the events break the tile loop's PDL overlap, so these sum to "
-                              "more than ms_per_step)",
+            "breakdown_note": "library CUDA events per sub-step (" +
+                              ("the timed steps" if live else
+                               "separate instrumented steps: the events break the tile loop's "
+                               "PDL overlap, so these sum to more than ms_per_step") + ")",
             "greedy": {"tiles": int(last.n_greedy_tiles), "evals": int(last.n_greedy_evals),
                        "band_pairs": int(last.n_band_pairs), "near_ties": int(last.n_near_ties)},
             "roofline": roof,

@@ -104,8 +104,7 @@ typedef struct bm_options {
   int64_t near_tie_cap;  /* max near-tie pairs stored (0 = default 65536); all are counted      */
   int32_t key_cap;       /* initial membership key capacity (0 = default 16 n); a smaller M
                             fits, a larger one costs one exact-capacity recount             */
-  int32_t band_cap;      /* ignored (kept for layout): band pairs are re-decided in fp64
-                            inside the contraction kernels, no queue is needed              */
+  int32_t reserved0;     /* must be 0 (layout slot)                                           */
   int32_t flags;         /* BM_FLAG_* (diagnostics)                                           */
   int32_t select;        /* bm_select: landmark selection (default greedy in point order)     */
   int32_t fps_start;     /* BM_SELECT_FPS: index of the initial landmark x_0 (default 0)      */

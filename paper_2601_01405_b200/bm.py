@@ -47,7 +47,7 @@ class _Options(ctypes.Structure):
     _fields_ = [("struct_size", ctypes.c_int32), ("tile", ctypes.c_int32),
                 ("path", ctypes.c_int32), ("timing", ctypes.c_int32),
                 ("near_tie_cap", ctypes.c_int64), ("key_cap", ctypes.c_int32),
-                ("band_cap", ctypes.c_int32), ("flags", ctypes.c_int32),
+                ("reserved0", ctypes.c_int32), ("flags", ctypes.c_int32),
                 ("select", ctypes.c_int32), ("fps_start", ctypes.c_int32),
                 ("reserved", ctypes.c_int32 * 3)]
 
@@ -128,7 +128,7 @@ SELECT = {"greedy": 0, "fps": 1}
 
 
 def _options(tile=0, path="auto", timing=False, near_tie_cap=0, key_cap=0,
-             band_cap=0, flags=0, select="greedy", fps_start=0) -> _Options:
+             flags=0, select="greedy", fps_start=0) -> _Options:
     o = _Options()
     o.struct_size = ctypes.sizeof(_Options)
     o.tile = int(tile)
@@ -136,7 +136,6 @@ def _options(tile=0, path="auto", timing=False, near_tie_cap=0, key_cap=0,
     o.timing = 1 if timing else 0
     o.near_tie_cap = int(near_tie_cap)
     o.key_cap = int(key_cap)
-    o.band_cap = int(band_cap)
     o.flags = int(flags)
     o.select = SELECT[select] if isinstance(select, str) else int(select)
     o.fps_start = int(fps_start)
@@ -144,9 +143,14 @@ def _options(tile=0, path="auto", timing=False, near_tie_cap=0, key_cap=0,
 
 
 class _DevArray:
-    """__cuda_array_interface__ view of a library-owned device array."""
+    """__cuda_array_interface__ view of a library-owned device array.  Holds a
+    reference to the owning Cover, so a torch view (which keeps its source
+    object alive) keeps the cover's memory from being handed back to the
+    library's block cache while the view exists.  An explicit Cover.free()
+    still releases it: views must not be used after that call."""
 
-    def __init__(self, ptr, shape, typestr):
+    def __init__(self, ptr, shape, typestr, owner=None):
+        self._owner = owner
         self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
                                          "data": (int(ptr or 0), False), "version": 3,
                                          "strides": None}
@@ -214,7 +218,7 @@ class Cover:
                 dt = torch.int32 if ts == "<i4" else torch.int64
                 out[name] = torch.zeros(shape, dtype=dt, device="cuda")
             else:
-                out[name] = torch.as_tensor(_DevArray(p, shape, ts), device="cuda")
+                out[name] = torch.as_tensor(_DevArray(p, shape, ts, owner=self), device="cuda")
         return out
 
     def numpy(self) -> dict:
@@ -256,7 +260,7 @@ def _dtype_of(t) -> str:
 
 def cover_build(points, metric: str, eps: float, stream=None, tile: int = 0,
                 path: str = "auto", timing: bool = False, near_tie_cap: int = 0,
-                key_cap: int = 0, band_cap: int = 0, flags: int = 0, select: str = "greedy",
+                key_cap: int = 0, flags: int = 0, select: str = "greedy",
                 fps_start: int = 0) -> Cover:
     """bm_cover_build_ex on a CUDA torch tensor [n, d] (row-major, contiguous)."""
     import torch
@@ -270,7 +274,7 @@ def cover_build(points, metric: str, eps: float, stream=None, tile: int = 0,
         stream = torch.cuda.current_stream(points.device)
     sp = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
     out = ctypes.POINTER(_Cover)()
-    o = _options(tile, path, timing, near_tie_cap, key_cap, band_cap, flags, select,
+    o = _options(tile, path, timing, near_tie_cap, key_cap, flags, select,
                  fps_start)
     lib = load()
     with torch.cuda.device(points.device):
@@ -283,7 +287,7 @@ def cover_build(points, metric: str, eps: float, stream=None, tile: int = 0,
 
 def cover_build_host(points: np.ndarray, metric: str, eps: float, stream=None, tile: int = 0,
                      path: str = "auto", timing: bool = False, near_tie_cap: int = 0,
-                     key_cap: int = 0, band_cap: int = 0, flags: int = 0, select: str = "greedy",
+                     key_cap: int = 0, flags: int = 0, select: str = "greedy",
                      fps_start: int = 0) -> Cover:
     """bm_cover_build_host on a host buffer (numpy array or CPU torch tensor,
     ideally pinned): copies in, builds, copies every result back to host."""
@@ -302,7 +306,7 @@ def cover_build_host(points: np.ndarray, metric: str, eps: float, stream=None, t
         stream = torch.cuda.current_stream()
     sp = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
     out = ctypes.POINTER(_Cover)()
-    o = _options(tile, path, timing, near_tie_cap, key_cap, band_cap, flags, select,
+    o = _options(tile, path, timing, near_tie_cap, key_cap, flags, select,
                  fps_start)
     rc = load().bm_cover_build_host(ctypes.c_void_p(ptr), DTYPE[dt], n, d, METRIC[metric],
                                     float(eps), ctypes.c_void_p(sp), ctypes.byref(o),

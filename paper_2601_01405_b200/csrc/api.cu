@@ -331,8 +331,9 @@ bm::Thresh make_thresh(int kind, int d, double eps) {
 // (membership_full).  Bounded by a quarter of the free device memory.
 int64_t initial_key_cap(int64_t n) {
   int64_t cap = n * 16 > (1 << 20) ? n * 16 : (1 << 20);
-  static int64_t lim = -1;   // an eighth of the device memory, in keys (queried once)
-  if (lim < 0) {
+  static int64_t lim_of[bm::kMaxDevices] = {};   // an eighth of the device memory, in keys
+  int64_t& lim = lim_of[bm::cur_device()];
+  if (lim <= 0) {
     int dev = 0;
     cudaDeviceProp pr;
     lim = (cudaGetDevice(&dev) == cudaSuccess &&
@@ -463,19 +464,24 @@ void set_recheck(bm::tc::TcArgs& ta, const void* xrows, int xstride, int d, cons
 
 // tf32 column-constant fold operands: B constants [l_rows][8] and the A ones tile.
 // The fold's constant A tile ({1,1,1,0,...} x 128 rows) is the same for every
-// build: one copy per device, written once (synchronously) on first use.
-static const float* fold_ones_tile() {
+// build: one copy per device, written once on first use by an async copy on
+// the caller's stream followed by a synchronisation of that stream, so the
+// pointer is published only after the data has landed (a plain cudaMemcpy from
+// pageable memory may return before the DMA completes and is not ordered
+// against a non-blocking stream).
+static const float* fold_ones_tile(cudaStream_t s) {
   static std::mutex mu;
   static const float* tiles[64] = {};
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
   std::lock_guard<std::mutex> lk(mu);
   if (!tiles[dev]) {
-    float h[128 * 8];
+    static float h[128 * 8];
     for (int i = 0; i < 128 * 8; ++i) h[i] = (i & 7) < 3 ? 1.f : 0.f;
     float* d = nullptr;
     if (cudaMalloc(&d, sizeof h) != cudaSuccess) return nullptr;
-    if (cudaMemcpy(d, h, sizeof h, cudaMemcpyHostToDevice) != cudaSuccess) {
+    if (cudaMemcpyAsync(d, h, sizeof h, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess) {
       cudaFree(d);
       return nullptr;
     }
@@ -486,11 +492,10 @@ static const float* fold_ones_tile() {
 
 bm_status alloc_fold(Pool& pool, bm::tc::TcPlan& P, bm::tc::TcArgs& ta, cudaStream_t s,
                      int64_t* launches) {
-  (void)s;
   (void)launches;
   float* colk = nullptr;
   TRY(pool.alloc(&colk, (size_t)P.l_rows * 8));
-  const float* ones = fold_ones_tile();
+  const float* ones = fold_ones_tile(s);
   if (!ones) return set_err(BM_ENOMEM, "fold constant tile allocation failed");
   ta.colk = colk;
   P.ones = ones;
@@ -1407,6 +1412,9 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
     uint8_t* eblk = (uint8_t*)g_pinned.get(esz, &pv->pinned_e_cls);
     pv->pinned_e = eblk;
     if (!eblk) {
+      // the side stream may still be copying into the block the cover now
+      // owns: let it finish before bm_free hands the block back to the cache
+      cudaStreamSynchronize(s2);
       bm_free(c);
       return set_err(BM_ENOMEM, "pinned host allocation for the results failed");
     }

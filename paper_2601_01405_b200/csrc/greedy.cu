@@ -221,7 +221,8 @@ cudaError_t launch_resolve(const uint32_t* adj, int adj_words, const int32_t* un
                            PruneTile pt_out) {
   ++*launches;
   const size_t smem = sizeof(uint32_t) * 32 * (size_t)adj_words * adj_words;
-  static bool attr = false;   // (one attribute call per process; T <= 1024)
+  static bool attr_set[kMaxDevices] = {};   // per device (attributes are per context)
+  bool& attr = attr_set[cur_device()];
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(k_resolve, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)(sizeof(uint32_t) * 32 * 32 * 32));
@@ -332,7 +333,8 @@ cudaError_t launch_compact_unc(const uint8_t* covered, const int32_t* unc, const
                                int64_t n, cudaStream_t s, int64_t* launches) {
   const int64_t nblk = (n + CP_TILE - 1) / CP_TILE;
   ++*launches;
-  static int cap = 0;   // CTAs resident at once
+  static int cap_of[kMaxDevices] = {};   // CTAs resident at once, per device
+  int& cap = cap_of[cur_device()];
   if (cap == 0) {
     int dev = 0, sms = 0, per = 0;
     cudaGetDevice(&dev);

@@ -329,6 +329,16 @@ cudaError_t launch_resolve_debug(const uint32_t* adj, int adj_words, int nc, uin
 namespace bm {
 // Instantiated register-row widths of the CUDA-core pair kernel (8-byte units);
 // 0 = wide variant (rows re-read from L1/global).
+// Index of the current device for per-device caches of launch settings
+// (function attributes and occupancy are per context, so a process driving
+// several GPUs must not reuse one device's values on another).
+constexpr int kMaxDevices = 64;
+inline int cur_device() {
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= kMaxDevices) d = 0;
+  return d;
+}
+
 inline int pick_nu(int nu_needed) {
   static const int widths[] = {1, 2, 4, 5, 8, 12, 16, 24, 32};
   for (int w : widths)

@@ -451,7 +451,10 @@ cudaError_t launch_pairs_nu(const PairArgs& a, int64_t q_rows_max, cudaStream_t 
   } else {
     // persistent: as many CTAs as fit on the GPU at once (or fewer if there
     // is less work than that); the kernel strides over the work items
-    static int per_sm = 0, sms = 0;
+    static int per_sm_of[kMaxDevices] = {}, sms_of[kMaxDevices] = {};   // per device
+    const int dv = cur_device();
+    int& per_sm = per_sm_of[dv];
+    int& sms = sms_of[dv];
     if (per_sm == 0) {
       int dev = 0;
       cudaGetDevice(&dev);

@@ -13,8 +13,8 @@
 
 namespace bm {
 
-// G lanes per row (G = 1..32, a power of two >= the row's float count up to
-// a warp): lanes stride over the row, coalesced for wide rows.
+// G lanes per row (G = 1..8, the smallest power of two >= the row's float
+// count, capped at 8): lanes stride over the row, coalesced for wide rows.
 __global__ void k_prep_f32(const float* __restrict__ X, int64_t n, int d, int nu, int cosine,
                            int G, uint2* __restrict__ rows, uint2* __restrict__ xhat,
                            DevStats* stats) {
@@ -149,14 +149,14 @@ cudaError_t launch_prep(const void* X, int dtype, int64_t n, int d, int kind, in
                         uint2* rows, uint2* xhat, int32_t* inorm, DevStats* stats,
                         cudaStream_t s, int64_t* launches) {
   int bs = 256;
-  int64_t g = (n * 32 + bs - 1) / bs;   // one warp per row
   if (dtype == BM_F32) {
     int G = 1;   // lanes per row (each strides over the row's 2 nu floats)
     while (G < 8 && G < 2 * nu) G *= 2;
-    g = (n * G + bs - 1) / bs;
+    const int64_t g = (n * G + bs - 1) / bs;
     k_prep_f32<<<(unsigned)g, bs, 0, s>>>((const float*)X, n, d, nu, kind == K_COSF, G, rows,
                                           xhat, stats);
   } else {
+    const int64_t g = (n * 32 + bs - 1) / bs;   // integer rows: one warp per row
     k_prep_int<<<(unsigned)g, bs, 0, s>>>((const uint8_t*)X, n, d, nu, dtype == BM_U8, rows,
                                           inorm);
   }

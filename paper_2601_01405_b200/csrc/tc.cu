@@ -2,7 +2,7 @@
 // contraction (d^2(q,x) = d^2(q,0) + d^2(x,0) - 2 sum_j q_j x_j,
 // with the norms "precomputed and stored").
 //
-// Structure (one persistent CTA per SM, 8 warps):
+// Structure (one persistent CTA per SM, 12 warps):
 //   warp 0      TMA producer: the CTA's resident A block (RA x 128 point rows,
 //               all K atoms) once per work unit, then B (landmark) tiles of
 //               BN rows one 128-byte K atom per pipeline stage.
@@ -17,11 +17,11 @@
 //               one max against a per-row / per-column constant ("out for sure"
 //               test); the rare survivors are classified in / band and staged
 //               in shared memory, flushed to global with one atomic per flush.
-// Float exactness: with x, l rounded to tf32 and
-// fp32 accumulation, |acc - x.l| <= C (|x|^2 + |l|^2)/2 with a global constant
-// C; the per-row/per-column thresholds fold that bound in, so "out" and "in"
-// decisions are certain and every other pair is queued for the fp64 recheck
-// (k_tc_recheck) that reproduces the oracle's formula exactly.
+// Float exactness: with x, l rounded to tf32 and fp32
+// accumulation, |acc - x.l| <= C (|x|^2 + |l|^2)/2 with a global constant C;
+// the per-row/per-column thresholds fold that bound in, so "out" and "in"
+// decisions are certain and every other pair is re-decided inline by the
+// epilogue lanes with the oracle's fp64 formula (pair_in_fp64, B').
 #include <cuda.h>
 #include <math.h>
 
@@ -1229,7 +1229,7 @@ cudaError_t launch_tc(const TcPlan& P, const TcArgs& a, cudaStream_t s, int64_t*
 // ------------------------------------------------------------ prep kernels
 // Operand rows: fp32 rounded to tf32 (cvt.rna) or raw int8 bytes, K padded
 // with zeros to row_bytes; norms in fp64 (float) / int32 (int).
-// G lanes per row (power of two up to a warp), lanes stride over the row
+// G lanes per row (a power of two, at most 8), lanes stride over the row
 __global__ void k_tc_prep_f32(const float* __restrict__ X, int64_t n, int d, int row_elems,
                               int cosine, int G, float* __restrict__ xop,
                               double* __restrict__ nrm, DevStats* stats) {
@@ -1507,7 +1507,6 @@ cudaError_t launch_tc_tile_cand(const TcPlan& P, const TcPlan& Pc, const void* n
 cudaError_t launch_tc_prep(const void* X, int dtype, int64_t n, int d, const TcPlan& P,
                            void* nrm, DevStats* stats, cudaStream_t s, int64_t* launches) {
   ++*launches;
-  const unsigned g = (unsigned)((n * 32 + 255) / 256);   // one warp per row
   // G lanes per row, each striding over its row: 8 lanes cover a 32-float
   // (128-byte) row in four coalesced 32-byte passes with a quarter of the
   // threads and shuffles a warp per row would need
@@ -1517,8 +1516,8 @@ cudaError_t launch_tc_prep(const void* X, int dtype, int64_t n, int d, const TcP
     k_tc_prep_f32<<<(unsigned)((n * G + 255) / 256), 256, 0, s>>>(
         (const float*)X, n, d, (int)(P.row_bytes / 4), P.cosine, G, (float*)P.xop,
         (double*)nrm, stats);
-  else
-    k_tc_prep_int<<<g, 256, 0, s>>>((const uint8_t*)X, n, d, (int)P.row_bytes, dtype == BM_U8,
+  else   // integer rows: one warp per row
+    k_tc_prep_int<<<(unsigned)((n * 32 + 255) / 256), 256, 0, s>>>((const uint8_t*)X, n, d, (int)P.row_bytes, dtype == BM_U8,
                                     (uint8_t*)P.xop, (int32_t*)nrm);
   return cudaGetLastError();
 }

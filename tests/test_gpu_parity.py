@@ -1,8 +1,11 @@
 """GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
 
 Marked `gpu`; run on a B200.  Sizes span several greedy tiles (T down to 32)
-and ragged tails; full-size configs use the LFMIS certificate plus sampled
-pairs re-decided by the oracle.
+and ragged tails.  Full C1 and C2 are compared array by array here; full C4
+and the full-size C3 / C5 validity checks (LFMIS certificate, CSR transpose,
+>= 1e7 sampled pairs re-decided by the oracle, complete rows / columns,
+sampled edges) and the near-tie completeness tests are in
+test_gpu_fullsize.py.
 """
 import math
 

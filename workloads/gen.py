@@ -132,7 +132,10 @@ def _c3_chunk(seed, c, rows):
 
 
 # --------------------------------------------------------------------------- C4
-C4_TAU = 40.0  # intensity floor zeroed (tau ~40-70 for ~75-80% zeros)
+# intensity floor zeroed: BASELINE.json configs[3] asks for "~80% zeros"; with
+# this stroke model tau = 40 gave 74.9% and tau = 90 gives 80.1% (measured on
+# the first 8000 rows; SURVEY §8(d) guessed 40-70, which tops out at 78%)
+C4_TAU = 90.0
 
 
 def _c4_chunk(seed, c, rows):
