@@ -98,7 +98,8 @@ typedef enum bm_path {
 /* Optional knobs.  Zero-initialise, set struct_size = sizeof(bm_options). */
 typedef struct bm_options {
   int32_t struct_size;
-  int32_t tile;          /* greedy candidate tile T: 0 = default (1024); 32..1024, multiple of 32 */
+  int32_t tile;          /* greedy candidate tile T: 0 = default (8192 on pruned tensor-core
+                            launches, else 1024); 32..8192, multiple of 32                  */
   int32_t path;          /* bm_path                                                             */
   int32_t timing;        /* 1 = record per-step CUDA events into step_ms                        */
   int64_t near_tie_cap;  /* max near-tie pairs stored (0 = default 65536); all are counted      */
@@ -123,6 +124,7 @@ typedef enum bm_select {
 #define BM_FLAG_NO_EDGE_TRIANGLE 2  /* L > 4096: build edges by sort + unique, not the bit triangle */
 #define BM_FLAG_NO_PRUNE 4          /* tensor path: no tile-level pruning of the membership contraction */
 #define BM_FLAG_FORCE_PRUNE 8       /* tensor path: prune even below the size where it pays (tests) */
+#define BM_FLAG_DENSE_RESOLVE 16    /* tiles > 1024: resolve from the dense words, not the sparse list (tests) */
 
 /*
  * Result of one cover construction.  All arrays are owned by the library and

@@ -29,6 +29,7 @@ FLAG_NO_L1_PREFILTER = 1
 FLAG_NO_EDGE_TRIANGLE = 2
 FLAG_NO_PRUNE = 4
 FLAG_FORCE_PRUNE = 8
+FLAG_DENSE_RESOLVE = 16
 STEPS = ("prep", "greedy", "member", "csr", "edges", "total", "member_kernel", "select")
 
 EXPORTED = ("bm_cover_build", "bm_cover_build_ex", "bm_cover_build_host", "bm_free",

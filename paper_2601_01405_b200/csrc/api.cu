@@ -620,9 +620,8 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
                     ? (size_t)opts->struct_size : sizeof o;
     memcpy(&o, opts, sz);
   }
-  int T = o.tile > 0 ? o.tile : 1024;
-  if (T < 32 || T > 1024 || (T % 32) != 0)
-    return set_err(BM_EINVAL, "tile must be a multiple of 32 in [32, 1024]");
+  if (o.tile != 0 && (o.tile < 32 || o.tile > kBigT || (o.tile % 32) != 0))
+    return set_err(BM_EINVAL, "tile must be a multiple of 32 in [32, %d]", kBigT);
   const int64_t tie_cap = o.near_tie_cap > 0 ? o.near_tie_cap : 65536;
   if (o.select != BM_SELECT_GREEDY && o.select != BM_SELECT_FPS)
     return set_err(BM_EINVAL, "unknown landmark selection %d", o.select);
@@ -721,6 +720,15 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
   const bool prune = use_tc && dtype == BM_F32 && metric == BM_L2 && P.katoms <= 2 &&
                      n >= 4 * kPruneCells && !(o.flags & BM_FLAG_NO_PRUNE) &&
                      (n >= 262144 || (o.flags & BM_FLAG_FORCE_PRUNE));
+  // Greedy tile T (A11: the result does not depend on it).  Pruned tensor
+  // launches (C3) take 8192 candidates: each tile's membership launch streams
+  // the whole point operand from HBM once, so 8x fewer tiles move 8x fewer
+  // bytes, and a row block meets ~8x more live landmarks per A load; A2 then
+  // lists its non-zero words and k_resolve_big decides the sparse in-tile
+  // graph in rounds.  Elsewhere 1024 (the single-CTA in-order resolve).
+  const int T = o.tile > 0 ? o.tile : (prune ? kBigT : 1024);
+  const bool big_tile = T > 1024;
+  const int aw = (int)(((T + 255) / 256 + 3) / 4);   // live-chunk words per row block
   PruneState ps{};
   tc::TcPlan Pm{};   // the member kernel's plan: A operand in permuted order
   if (prune) {
@@ -737,11 +745,12 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
     TRY(pool.alloc(&ps.bmask, (size_t)nblk * KWd));
     TRY(pool.alloc(&ps.xop_perm, (size_t)n * P.row_bytes));
     TRY(pool.alloc(&ps.nrm_perm, (size_t)n));
-    TRY(pool.alloc(&ps.col_pt, 1024));
-    TRY(pool.alloc(&ps.col_pos, 1024));
-    TRY(pool.alloc(&ps.cmask, (size_t)32 * KWd));
-    TRY(pool.alloc(&ps.tmask, (size_t)4 * KWd));
-    TRY(pool.alloc(&ps.act, (size_t)nblk));
+    const int64_t Tq = ((T + 255) / 256) * 256;
+    TRY(pool.alloc(&ps.col_pt, (size_t)Tq));
+    TRY(pool.alloc(&ps.col_pos, (size_t)Tq));
+    TRY(pool.alloc(&ps.cmask, (size_t)(Tq / 32) * KWd));
+    TRY(pool.alloc(&ps.tmask, (size_t)(Tq / 256) * KWd));
+    TRY(pool.alloc(&ps.act, (size_t)nblk * aw));
     unsigned long long *pk = nullptr, *pa = nullptr;
     void* ptemp = nullptr;
     TRY(pool.alloc(&pk, (size_t)n));
@@ -776,6 +785,13 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
   TRY(pool.alloc(&cstate, (size_t)compact_state_words(n)));
   TRY(pool.alloc(&keys, (size_t)key_cap));
   TRY(pool.alloc(&ties_dev, (size_t)tie_cap * 3));
+  AdjList nz{};   // A2's non-zero word list for k_resolve_big (big tiles only)
+  if (big_tile) {
+    TRY(pool.alloc(&nz.e, (size_t)kBigNzCap));
+    TRY(pool.alloc(&nz.count, 1));
+    nz.cap = (uint32_t)kBigNzCap;
+    CK(cudaMemsetAsync(nz.count, 0, sizeof(uint32_t), s));
+  }
   CK(cudaMemsetAsync(covered, 0, (size_t)n, s));
   CK(cudaMemsetAsync(cstate, 0, sizeof(unsigned long long) * compact_state_words(n), s));
   {
@@ -859,6 +875,8 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
       ta.act = ps.act;
       ta.act_bmask = ps.bmask;
       ta.act_cmask = ps.cmask;
+      ta.act_tmask = ps.tmask;
+      ta.act_words = aw;
     }
   }
   if (tc_adj) {
@@ -885,6 +903,7 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
     ac.ksteps = ta.ksteps;
     ac.adj = adj;
     ac.adj_T = T;
+    ac.nz = nz;
     if (rp.tf32) {
       float *rlo, *rhi, *ca, *cb, *colk;
       TRY(pool.alloc(&rlo, (size_t)Tp));
@@ -1023,6 +1042,7 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
       a.l_end_dev = cnt + cur;
       a.adj = adj;
       a.adj_words = adj_words;
+      a.nz = nz;
       if (tc_adj) {
         ac.l_count_dev = cnt + cur;
         ac.lm_idx = uncb[cur];
@@ -1034,11 +1054,18 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
       }
       loop_mark(1);
       // A3: in-order resolve, append landmarks (resets the tile's counters)
-      CK(launch_resolve(adj, adj_words, uncb[cur], cnt + cur, T, lm, cnt + 2, new_lm, cnt + 3,
-                        stats, cnt + 4, nullptr, s, &launches,
-                        prune ? PruneTile{ps.cell, ps.rank, ps.col_pt, ps.col_pos, ps.cmask,
-                                          ps.tmask}
-                              : PruneTile{}));
+      {
+        const PruneTile pt = prune ? PruneTile{ps.cell, ps.rank, ps.col_pt, ps.col_pos, ps.cmask,
+                                               ps.tmask}
+                                   : PruneTile{};
+        if (big_tile)
+          CK(launch_resolve_big(adj, nz, uncb[cur], cnt + cur, T, lm, cnt + 2, new_lm, cnt + 3,
+                                stats, cnt + 4, nullptr, s, &launches, pt,
+                                (o.flags & BM_FLAG_DENSE_RESOLVE) ? 1 : 0));
+        else
+          CK(launch_resolve(adj, adj_words, uncb[cur], cnt + cur, T, lm, cnt + 2, new_lm,
+                            cnt + 3, stats, cnt + 4, nullptr, s, &launches, pt));
+      }
       loop_mark(2);
       // B (+A4 marks): membership of every point in the new balls
       if (use_tc) {

@@ -27,23 +27,25 @@ constexpr unsigned FULLMASK = 0xffffffffu;
 // a 32-warp wavefront that handed each block's word to the next warp through
 // shared-memory flags or mbarriers took ~20 us per 1024-candidate tile, almost
 // all of it cross-warp hand-off latency.)
-// sadj: [nb][T] words, T = 32 * adj_words.
-__device__ __forceinline__ void resolve_tile_core(const uint32_t* __restrict__ adj,
-                                                  int adj_words, int nc, volatile uint32_t* lmw,
-                                                  uint32_t* sadj) {
+// adj: word v of candidate a at adj[v * gstride + a] (global); sadj: the
+// staged lower triangle, word v of candidate a at sadj[v * sstride + a];
+// preb (optional, shared): bit a set = candidate a is already dominated by a
+// landmark outside this block of <= 1024 candidates (k_resolve_big's sub-tiles).
+__device__ __forceinline__ void resolve_core(const uint32_t* __restrict__ adj, int64_t gstride,
+                                             int nc, volatile uint32_t* lmw, uint32_t* sadj,
+                                             int sstride, const uint32_t* preb) {
   const int tid = threadIdx.x, lane = tid & 31;
   const int nb = (nc + 31) >> 5;
-  const int T = adj_words * 32;
   // stage the lower triangle (word v of candidate a is needed for v <= a / 32):
   // thread a issues its (up to 32) independent loads before any store
   if (tid < nc) {
     const int wa = tid >> 5;
     uint32_t x[32];
 #pragma unroll
-    for (int v = 0; v < 32; ++v) x[v] = v <= wa ? __ldcg(adj + (int64_t)v * T + tid) : 0u;
+    for (int v = 0; v < 32; ++v) x[v] = v <= wa ? __ldcg(adj + (int64_t)v * gstride + tid) : 0u;
 #pragma unroll
     for (int v = 0; v < 32; ++v)
-      if (v <= wa) sadj[v * T + tid] = x[v];
+      if (v <= wa) sadj[v * sstride + tid] = x[v];
   }
   __syncthreads();
   if (tid < 32) {
@@ -53,15 +55,16 @@ __device__ __forceinline__ void resolve_tile_core(const uint32_t* __restrict__ a
       // fold in the earlier blocks' landmark words (independent loads, 8 in flight)
       uint32_t conf = 0u;
       if (valid) {
+        if (preb) conf = (preb[w] >> lane) & 1u;
         for (int v0 = 0; v0 < w; v0 += 8) {
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
             const int v = v0 + k;
-            if (v < w) conf |= sadj[v * T + a] & lmw[v];
+            if (v < w) conf |= sadj[v * sstride + a] & lmw[v];
           }
         }
       }
-      const uint32_t inrow = valid ? (sadj[w * T + a] & ((1u << lane) - 1u)) : 0u;
+      const uint32_t inrow = valid ? (sadj[w * sstride + a] & ((1u << lane) - 1u)) : 0u;
       unsigned undecided = __ballot_sync(FULLMASK, valid && conf == 0u);
       unsigned S = 0u;
       while (undecided) {
@@ -77,6 +80,13 @@ __device__ __forceinline__ void resolve_tile_core(const uint32_t* __restrict__ a
       __syncwarp();
     }
   }
+}
+
+// sadj: [nb][T] words, T = 32 * adj_words.
+__device__ __forceinline__ void resolve_tile_core(const uint32_t* __restrict__ adj,
+                                                  int adj_words, int nc, volatile uint32_t* lmw,
+                                                  uint32_t* sadj) {
+  resolve_core(adj, 32 * adj_words, nc, lmw, sadj, 32 * adj_words, nullptr);
 }
 
 __global__ void __launch_bounds__(1024) k_resolve(const uint32_t* __restrict__ adj, int adj_words,
@@ -212,6 +222,266 @@ __global__ void __launch_bounds__(1024) k_resolve_debug(const uint32_t* __restri
   resolve_tile_core(adj, adj_words, nc, lmw, sadj);
   __syncthreads();
   if (tid < nc) lm[tid] = (lmw[tid >> 5] >> (tid & 31)) & 1u;
+}
+
+// ---------------------------------------------------------------------------
+// A3 for tiles of 1024 < T <= kBigT candidates (k_resolve_big, one CTA).
+//
+// Sparse path (the BASELINE workloads: a candidate has an earlier in-tile
+// neighbour with probability ~T x ball size / n): A2 also listed its non-zero
+// lower-triangle words (AdjList).  A candidate with no listed word has no
+// earlier neighbour and is a landmark; the "contested" rest are decided by
+// rounds: an undecided candidate with a landmark neighbour is covered, one
+// whose earlier neighbours are all decided non-landmarks is a landmark.  The
+// smallest undecided candidate is decided in every round (its neighbours are
+// all earlier), so the rounds reproduce the in-order greedy exactly; they stop
+// when every candidate is decided (usually 1-3 rounds).
+// Dense path (list overflow, or more than kBigRounds rounds): the tile is
+// resolved in sub-tiles of 1024 candidates in order, each first folding in
+// its rows' words against the landmarks of the earlier sub-tiles (coalesced
+// loads of the word-major matrix), then the in-order core above.
+// Output as k_resolve: landmarks appended in order, new_lm / counts, and with
+// pruning the landmarks sorted by cell rank with chunk / tile cell masks.
+constexpr int kBigW = kBigT / 32;
+constexpr uint32_t kBigNz = (uint32_t)kBigNzCap;   // list entries staged in shared memory
+constexpr int kBigRounds = 48;
+struct BigSmem {
+  static constexpr int BITS = 0;                               // 5 x kBigW words
+  static constexpr int WPRE = BITS + 5 * kBigW * 4;            // kBigW + 1 ints
+  static constexpr int REG = (WPRE + (kBigW + 1) * 4 + 15) & ~15;
+  static constexpr int REG_BYTES = 32 * 1024 * 4;              // sadj (dense) / entries (sparse)
+  static constexpr int SKEY = REG + REG_BYTES;                 // kBigT words
+  static constexpr int SCM = SKEY + kBigT * 4;                 // (kBigT / 32) x 8 words
+  static constexpr int SHIST = SCM + kBigW * 8 * 4;            // 256 ints
+  static constexpr int MISC = SHIST + 256 * 4;                 // 64 words
+  static constexpr int TOTAL = MISC + 64 * 4;
+};
+static_assert(kBigNz * 8 <= BigSmem::REG_BYTES, "sparse entries fit the shared region");
+
+__global__ void __launch_bounds__(1024) k_resolve_big(
+    const uint32_t* __restrict__ adj, AdjList nz, const int32_t* __restrict__ unc,
+    const int32_t* __restrict__ n_unc_dev, int T, int32_t* __restrict__ lm_out,
+    int32_t* __restrict__ L_dev, int32_t* __restrict__ new_lm, int32_t* __restrict__ dL_dev,
+    DevStats* stats, int32_t* __restrict__ ticket, unsigned long long* __restrict__ band_count,
+    PruneTile pt_out, int force_dense) {
+  extern __shared__ __align__(16) uint8_t bsm[];
+  uint32_t* lmb = reinterpret_cast<uint32_t*>(bsm + BigSmem::BITS);   // landmark bits
+  uint32_t* decb = lmb + kBigW;                                        // decided bits
+  uint32_t* killb = decb + kBigW;                                      // round: has landmark nb
+  uint32_t* blkb = killb + kBigW;                                      // round: undecided nb
+  uint32_t* conb = blkb + kBigW;                                       // contested
+  int* wpre = reinterpret_cast<int*>(bsm + BigSmem::WPRE);
+  uint2* ent = reinterpret_cast<uint2*>(bsm + BigSmem::REG);
+  uint32_t* sadj = reinterpret_cast<uint32_t*>(bsm + BigSmem::REG);
+  uint32_t* skey = reinterpret_cast<uint32_t*>(bsm + BigSmem::SKEY);
+  uint32_t* scm = reinterpret_cast<uint32_t*>(bsm + BigSmem::SCM);
+  int* shist = reinterpret_cast<int*>(bsm + BigSmem::SHIST);
+  uint32_t* misc = reinterpret_cast<uint32_t*>(bsm + BigSmem::MISC);
+  const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
+  pdl_wait();
+  pdl_trigger();   // a single CTA
+  const int n_unc = *n_unc_dev;
+  const int nc = min(T, n_unc);
+  const uint32_t cnt = *nz.count;
+  if (tid == 0) {
+    if (ticket) *ticket = 0;
+    if (band_count) *band_count = 0ull;
+    *nz.count = 0u;   // the next tile's A2 starts a fresh list (stream order)
+  }
+  if (nc == 0) {
+    if (tid == 0) *dL_dev = 0;
+    return;
+  }
+  const int W = (nc + 31) >> 5;
+  bool dense = force_dense || cnt > kBigNz || cnt > nz.cap;
+  // ---- sparse path
+  if (!dense) {
+    for (uint32_t k = tid; k < cnt; k += blockDim.x) ent[k] = __ldcg(nz.e + k);
+    for (int i = tid; i < W; i += blockDim.x) conb[i] = 0u;
+    __syncthreads();
+    for (uint32_t k = tid; k < cnt; k += blockDim.x) {
+      const uint32_t a = ent[k].x >> 16;
+      atomicOr(&conb[a >> 5], 1u << (a & 31));
+    }
+    __syncthreads();
+    for (int i = tid; i < W; i += blockDim.x) {
+      const uint32_t valid = (32 * i + 32 <= nc) ? 0xffffffffu : ((1u << (nc - 32 * i)) - 1u);
+      lmb[i] = valid & ~conb[i];
+      decb[i] = ~conb[i];          // contested candidates start undecided
+    }
+    __syncthreads();
+    int rounds = 0;
+    while (true) {
+      for (int i = tid; i < W; i += blockDim.x) {
+        killb[i] = 0u;
+        blkb[i] = 0u;
+      }
+      __syncthreads();
+      for (uint32_t k = tid; k < cnt; k += blockDim.x) {
+        const uint2 e = ent[k];
+        const uint32_t a = e.x >> 16, v = e.x & 0xffffu;
+        if ((decb[a >> 5] >> (a & 31)) & 1u) continue;
+        if (e.y & lmb[v]) atomicOr(&killb[a >> 5], 1u << (a & 31));
+        if (e.y & ~decb[v]) atomicOr(&blkb[a >> 5], 1u << (a & 31));
+      }
+      __syncthreads();
+      int still = 0;
+      for (int i = tid; i < W; i += blockDim.x) {
+        const uint32_t und = ~decb[i];
+        const uint32_t nn = und & killb[i];
+        const uint32_t nl = und & ~killb[i] & ~blkb[i];
+        lmb[i] |= nl;
+        decb[i] |= nn | nl;
+        still |= (und & ~(nn | nl)) != 0u;
+      }
+      ++rounds;
+      if (!__syncthreads_or(still)) break;
+      if (rounds >= kBigRounds) {
+        dense = true;   // a long in-tile dependency chain: the dense in-order path
+        break;
+      }
+    }
+  }
+  // ---- dense path: sub-tiles of 1024 in order
+  if (dense) {
+    for (int i = tid; i < W; i += blockDim.x) lmb[i] = 0u;
+    __syncthreads();
+    for (int base = 0; base < nc; base += 1024) {
+      const int ncs = min(1024, nc - base);
+      const int a = base + tid;
+      uint32_t pre = 0u;
+      if (tid < ncs) {
+        const int wb = base >> 5;
+        for (int v = 0; v < wb && !pre; ++v)
+          pre |= __ldcg(adj + (int64_t)v * T + a) & lmb[v];
+      }
+      const unsigned bal = __ballot_sync(FULLMASK, pre != 0u);
+      if (lane == 0) misc[wp] = bal;   // preb: 32 words, one per warp of the sub-tile
+      __syncthreads();
+      resolve_core(adj + (int64_t)(base >> 5) * T + base, T, ncs, lmb + (base >> 5), sadj, 1024,
+                   misc);
+      __syncthreads();
+    }
+  }
+  // ---- output: landmarks in order
+  if (tid < 32) {   // exclusive scan of the per-word counts (8 words per lane)
+    int v[8], t = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int wd = tid * 8 + i;
+      v[i] = wd < W ? __popc(lmb[wd]) : 0;
+      t += v[i];
+    }
+    int incl = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(FULLMASK, incl, o);
+      if (lane >= o) incl += u;
+    }
+    int run = incl - t;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      wpre[tid * 8 + i] = run;
+      run += v[i];
+    }
+    if (tid == 31) wpre[kBigW] = run;
+  }
+  const bool prune = pt_out.cell != nullptr;
+  if (prune) {
+    for (int i = tid; i < 256; i += blockDim.x) shist[i] = 0;
+    for (int i = tid; i < ((nc + 255) >> 8) * 64; i += blockDim.x) scm[i] = 0u;
+  }
+  __syncthreads();
+  const int L0 = *L_dev;
+  const int dL = wpre[kBigW];
+  for (int a = tid; a < nc; a += blockDim.x) {
+    const uint32_t S = lmb[a >> 5];
+    if ((S >> (a & 31)) & 1u) {
+      const int pos = wpre[a >> 5] + __popc(S & ((1u << (a & 31)) - 1u));
+      const int32_t pt = unc[a];
+      new_lm[pos] = pt;
+      lm_out[L0 + pos] = pt;
+      if (prune) atomicAdd(&shist[pt_out.rank[pt_out.cell[pt]]], 1);
+    }
+  }
+  __syncthreads();
+  if (prune) {
+    // landmarks grouped by cell rank (counting sort; positions kept in keys)
+    if (tid < 32) {
+      int v[8], t = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        v[i] = shist[tid * 8 + i];
+        t += v[i];
+      }
+      int incl = t;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(FULLMASK, incl, o);
+        if (lane >= o) incl += u;
+      }
+      int run = incl - t;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        shist[tid * 8 + i] = run;
+        run += v[i];
+      }
+    }
+    __syncthreads();
+    for (int a = tid; a < nc; a += blockDim.x) {
+      const uint32_t S = lmb[a >> 5];
+      if ((S >> (a & 31)) & 1u) {
+        const int pos = wpre[a >> 5] + __popc(S & ((1u << (a & 31)) - 1u));
+        const int r = pt_out.rank[pt_out.cell[unc[a]]];
+        skey[atomicAdd(&shist[r], 1)] = (uint32_t)pos;
+      }
+    }
+    __syncthreads();
+    for (int k = tid; k < dL; k += blockDim.x) {
+      const int src = (int)skey[k];
+      const int32_t p = new_lm[src];   // written above by this CTA
+      pt_out.col_pt[k] = p;
+      pt_out.col_pos[k] = src;
+      const int c = pt_out.cell[p];
+      atomicOr(&scm[(k >> 5) * 8 + (c >> 5)], 1u << (c & 31));
+    }
+    __syncthreads();
+    const int nch = (dL + 31) >> 5, ntl = (dL + 255) >> 8;
+    for (int i = tid; i < ntl * 64; i += blockDim.x) pt_out.cmask[i] = scm[i];   // whole tiles
+    for (int i = tid; i < ntl * 8; i += blockDim.x) {
+      const int t = i >> 3, wd = i & 7;
+      uint32_t v = 0u;
+      for (int c = 0; c < 8; ++c)
+        if (t * 8 + c < nch) v |= scm[(t * 8 + c) * 8 + wd];
+      pt_out.tmask[i] = v;
+    }
+  }
+  if (tid == 0) {
+    *dL_dev = dL;
+    *L_dev = L0 + dL;
+    stats->greedy_evals += (unsigned long long)nc * (unsigned long long)(nc - 1) / 2ull;
+    stats->tiles += 1ull;
+  }
+}
+
+cudaError_t launch_resolve_big(const uint32_t* adj, AdjList nz, const int32_t* unc,
+                               const int32_t* n_unc, int T, int32_t* lm_out, int32_t* L_dev,
+                               int32_t* new_lm, int32_t* dL_dev, DevStats* stats,
+                               int32_t* ticket, unsigned long long* band_count, cudaStream_t s,
+                               int64_t* launches, PruneTile pt_out, int force_dense) {
+  ++*launches;
+  if (T > kBigT || (T % 32) != 0) return cudaErrorInvalidValue;
+  static bool attr_set[kMaxDevices] = {};
+  bool& attr = attr_set[cur_device()];
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_resolve_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         BigSmem::TOTAL);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  return launch_pdl(k_resolve_big, dim3(1), dim3(1024), (size_t)BigSmem::TOTAL, s, adj, nz, unc,
+                    n_unc, T, lm_out, L_dev, new_lm, dL_dev, stats, ticket, band_count, pt_out,
+                    force_dense);
 }
 
 cudaError_t launch_resolve(const uint32_t* adj, int adj_words, const int32_t* unc,

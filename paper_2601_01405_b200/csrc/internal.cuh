@@ -115,6 +115,22 @@ struct DevStats {
   int overflow;                      // fused greedy: a tile's band queue overflowed
 };
 
+// A2's non-zero adjacency words as a list (the in-tile graph is sparse on the
+// BASELINE workloads: k_resolve_big decides the tile from it).  Entry k =
+// {a << 16 | v, word}: word v of candidate a; *count may exceed cap (then
+// the list is incomplete and the resolve falls back to the dense words).
+struct AdjList {
+  uint2* e;
+  uint32_t* count;
+  uint32_t cap;
+};
+__device__ __forceinline__ void adj_list_push(const AdjList& L, int64_t a, int64_t v,
+                                              uint32_t word) {
+  if (word == 0u || L.e == nullptr) return;
+  const uint32_t k = atomicAdd(L.count, 1u);
+  if (k < L.cap) L.e[k] = make_uint2(((uint32_t)a << 16) | (uint32_t)v, word);
+}
+
 struct PairArgs {
   const uint2* rows;        // [n][nu] scoring rows (xhat for cosine)
   const uint2* xrows;       // [n][nu] fp32 rows for the fp64 recheck (== rows except cosine)
@@ -138,6 +154,7 @@ struct PairArgs {
   // outputs
   uint32_t* adj; int adj_words;                 // MODE_ADJ: word v of candidate a at
                                                 //   adj[v * (32 * adj_words) + a]
+  AdjList nz;                                   // MODE_ADJ: list of the non-zero words
   uint8_t* covered;                             // MODE_MEMBER: covered[p] = 1 for in-ball pairs
   // L1 prefilter (K_L1F, MODE_MEMBER): 8-bit quantised rows, nq 32-bit words
   // per row; qparam = {min, max} of all coordinates (device, fp64)
@@ -178,6 +195,19 @@ cudaError_t launch_resolve(const uint32_t* adj, int adj_words, const int32_t* un
                            int32_t* new_lm, int32_t* dL_dev, DevStats* stats,
                            int32_t* ticket, unsigned long long* band_count,
                            cudaStream_t s, int64_t* launches, PruneTile pt_out = PruneTile{});
+
+// A3 for 1024 < T <= kBigT (greedy.cu k_resolve_big): decides the tile from
+// A2's non-zero word list when it is complete (sparse rounds), otherwise (or
+// with force_dense) from the dense words in sub-tiles of 1024; resets
+// *nz.count for the next tile.  pt_out arrays hold T entries (col_pt,
+// col_pos), T/32 x 8 (cmask) and T/256 x 8 (tmask) words.
+constexpr int kBigT = 8192;
+constexpr int64_t kBigNzCap = 8192;   // list entries (= the resolve's shared-memory stage)
+cudaError_t launch_resolve_big(const uint32_t* adj, AdjList nz, const int32_t* unc,
+                               const int32_t* n_unc, int T, int32_t* lm_out, int32_t* L_dev,
+                               int32_t* new_lm, int32_t* dL_dev, DevStats* stats,
+                               int32_t* ticket, unsigned long long* band_count, cudaStream_t s,
+                               int64_t* launches, PruneTile pt_out, int force_dense);
 
 // Order-preserving compaction of the uncovered list after a tile: keeps
 // unc[i], nc <= i < n_unc, with covered[unc[i]] == 0 (single pass, decoupled

@@ -372,7 +372,10 @@ __device__ __forceinline__ void pairs_block(const PairArgs& A, uint2* sl, int32_
     const int64_t wcol = l0 / 32;
 #pragma unroll
     for (int r = 0; r < R; ++r)
-      if (act[r]) A.adj[wcol * (int64_t)A.adj_words * 32 + qi[r]] = word[r];   // word-major
+      if (act[r]) {
+        A.adj[wcol * (int64_t)A.adj_words * 32 + qi[r]] = word[r];   // word-major
+        adj_list_push(A.nz, qi[r], wcol, word[r]);
+      }
   }
 }
 

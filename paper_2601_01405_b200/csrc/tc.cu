@@ -447,24 +447,48 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   n_chunks = n_tiles > 0 ? (n_tiles + tiles_per_chunk - 1) / tiles_per_chunk : 0;
   const int64_t n_units = args.n_mblk * n_chunks;
   // pruning: may the unit's row block hold an in-ball pair with a landmark of
-  // tile t?  ab = the unit's live-chunk word args.act[mb]; every role
-  // evaluates the same predicate, so they skip the same tiles.  (Only the
-  // fused greedy tile, <= 4 tiles, is pruned: t < 4.)
-  auto tile_active = [&](uint32_t ab, int64_t t) -> bool {
-    if constexpr (!PR) return true;
-    return ((ab >> (8 * t)) & 0xffu) != 0u;
+  // tile t?  The row block's live-chunk bitmap (args.act_words words: byte t =
+  // the 8 chunks of tile t) is loaded once per unit, one unit ahead, by every
+  // role; every role evaluates the same predicate, so they skip the same tiles.
+  constexpr int AWM = PR ? 8 : 1;   // <= 32 tiles of 256 columns (kBigT)
+  struct ActW {
+    uint32_t w[AWM];
+  };
+  auto tile_bits = [&](const ActW& ab, int64_t t) -> uint32_t {
+    if constexpr (!PR) return 0xffu;
+    const int i = (int)(t >> 2);
+    uint32_t x = ab.w[0];
+#pragma unroll
+    for (int k = 1; k < AWM; ++k) x = i == k ? ab.w[k] : x;
+    return (x >> (8 * (int)(t & 3))) & 0xffu;
+  };
+  // A2 (adjacency): a tile whose first column is at or after the row block's
+  // last row holds no strictly-lower pair and is skipped (its words are
+  // never read: the resolve kernels read only words v <= a / 32 of row a)
+  auto tile_active = [&](const ActW& ab, int64_t mb, int64_t t) -> bool {
+    if constexpr (MODE == TC_MODE_ADJ) return t * BN < (mb + 1) * RA * 128;
+    return tile_bits(ab, t) != 0u;
   };
   // a unit none of whose tiles is live is skipped whole (no A block load)
-  auto unit_active = [&](uint32_t ab, int64_t t0, int64_t t1) -> bool {
-    if constexpr (!PR) return true;
+  auto unit_active = [&](const ActW& ab, int64_t mb, int64_t t0, int64_t t1) -> bool {
+    if constexpr (!PR && MODE != TC_MODE_ADJ) return true;
     for (int64_t t = t0; t < t1; ++t)
-      if (tile_active(ab, t)) return true;
+      if (tile_active(ab, mb, t)) return true;
     return false;
   };
-  // the live-chunk word of unit u (prefetched one unit ahead by every role)
-  auto act_of = [&](int64_t u) -> uint32_t {
-    if constexpr (!PR) return 0xffffffffu;
-    return u < n_units ? __ldg(args.act + u / n_chunks) : 0u;
+  // the live-chunk words of unit u
+  auto act_of = [&](int64_t u) -> ActW {
+    ActW r;
+#pragma unroll
+    for (int k = 0; k < AWM; ++k) r.w[k] = PR ? 0u : 0xffffffffu;
+    if constexpr (PR) {
+      if (u < n_units) {
+        const uint32_t* p = args.act + (u / n_chunks) * (int64_t)args.act_words;
+#pragma unroll
+        for (int k = 0; k < AWM; ++k) r.w[k] = k < args.act_words ? __ldg(p + k) : 0u;
+      }
+    }
+    return r;
   };
 
   if (warp == 0) {
@@ -488,13 +512,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               tma_load_2d(sBK + t * S::BK_SLOT, &tmK, &full[t], 0, (int)(t * BN));
           }
       }
-      uint32_t act_next = act_of(blockIdx.x);
+      ActW act_next = act_of(blockIdx.x);
       for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
         const int64_t mb = u / n_chunks, ch = u % n_chunks;
         const int64_t t0 = ch * tiles_per_chunk, t1 = min(n_tiles, t0 + tiles_per_chunk);
-        const uint32_t uact = act_next;
+        const ActW uact = act_next;
         act_next = act_of(u + gridDim.x);
-        if (!unit_active(uact, t0, t1)) continue;
+        if (!unit_active(uact, mb, t0, t1)) continue;
         if (ui == 0) TC_STAMP(3);
         if constexpr (!KS) {
           const int ab = (int)(ui % ABUF);
@@ -517,7 +541,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               tma_prefetch_2d(&tmA, ka * ATOM_ELEMS, (int)((un / n_chunks) * RA * 128 + r * 128));
         }
         for (int64_t t = t0; t < t1 && !BRES; ++t) {
-          if (!tile_active(uact, t)) continue;
+          if (!tile_active(uact, mb, t)) continue;
           for (int ka = 0; ka < n_atoms; ++ka) {
             mbar_wait(&empty[stage], phase ^ 1u);
             mbar_expect_tx(&full[stage], (uint32_t)S::B_STAGE);
@@ -559,13 +583,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       if constexpr (FOLD) mbar_wait(ak_full, 0u);
       uint32_t res_seen = 0u;   // BRES: resident tiles already waited for
       unsigned long long n_run = 0ull, n_skip = 0ull;
-      uint32_t act_next = act_of(blockIdx.x);
+      ActW act_next = act_of(blockIdx.x);
       for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
-        const int64_t ch = u % n_chunks;
+        const int64_t mb = u / n_chunks, ch = u % n_chunks;
         const int64_t t0 = ch * tiles_per_chunk, t1 = min(n_tiles, t0 + tiles_per_chunk);
-        const uint32_t uact = act_next;
+        const ActW uact = act_next;
         act_next = act_of(u + gridDim.x);
-        if (!unit_active(uact, t0, t1)) {
+        if (!unit_active(uact, mb, t0, t1)) {
           n_skip += t1 - t0;
           continue;
         }
@@ -578,7 +602,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         if (ui == 0) TC_STAMP(5);
         const uint8_t* sAb = sA + ab * S::A_BYTES;
         for (int64_t t = t0; t < t1; ++t) {
-          if (!tile_active(uact, t)) {
+          if (!tile_active(uact, mb, t)) {
             ++n_skip;
             continue;
           }
@@ -758,10 +782,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     };
     load_rows(blockIdx.x);
     unsigned long long ck_run = 0ull, ck_skip = 0ull;   // chunks of this warp's rows
-    uint32_t act_next = act_of(blockIdx.x);
+    ActW act_next = act_of(blockIdx.x);
     for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
       const int64_t mb = u / n_chunks, ch = u % n_chunks;
-      const uint32_t uact = act_next;
+      const ActW uact = act_next;
       act_next = act_of(u + gridDim.x);
       const int64_t t0 = ch * tiles_per_chunk, t1 = min(n_tiles, t0 + tiles_per_chunk);
       int64_t prow[RA];
@@ -786,7 +810,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         else ppt[r] = prow[r];
       }
       for (int64_t t = t0; t < t1; ++t) {
-        if (!tile_active(uact, t)) continue;
+        if (!tile_active(uact, mb, t)) continue;
         // both groups drain every tile: group g takes its half of the columns
         const int buf = (int)(tcount % NBUF);
         const uint32_t ph = (phase >> buf) & 1u;    // parity of buffer buf's next fill
@@ -876,7 +900,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 }
                 mask &= tri;
               }
-              if (a < n_cols) args.adj[(j0 >> 5) * (int64_t)args.adj_T + a] = mask;
+              if (a < n_cols) {
+                args.adj[(j0 >> 5) * (int64_t)args.adj_T + a] = mask;
+                adj_list_push(args.nz, a, j0 >> 5, mask);
+              }
               return;
             }
             // fast path: one compare per 32 pairs decides "all out"
@@ -1001,7 +1028,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           for (int c = cbeg; c < cend; c += 2) {
             if constexpr (PR) {
               const int nck = c + 1 < cend ? 2 : 1;
-              if (((uact >> (8 * t + c)) & (nck == 2 ? 3u : 1u)) == 0u) {
+              if (((tile_bits(uact, t) >> c) & (nck == 2 ? 3u : 1u)) == 0u) {
                 ck_skip += nck;
                 continue;   // no landmark of these 64 columns can be near this row block
               }
@@ -1153,8 +1180,10 @@ static cudaError_t dispatch(const TcPlan& P, const TcArgs& a, cudaStream_t s) {
     // resident for one-atom rows); for two atoms the A stream is the bound, so
     // more A buffers in flight at the cost of one B stage
     if constexpr (MODE == TC_MODE_MEMBER) {
-      if (a.act && P.katoms == 1)
+      if (a.act && P.katoms == 1 && a.L <= 4 * 256)
         return launch_cfg<TC_TF32, 1, 256, 1, 4, 3, MODE, true, true>(P, a, s);
+      if (a.act && P.katoms == 1)   // big greedy tiles (> 1024 columns): B streams
+        return launch_cfg<TC_TF32, 1, 256, 1, 4, 3, MODE, false, true>(P, a, s);
       if (a.act && P.katoms <= 2)
         return launch_cfg<TC_TF32, 1, 256, 2, 3, 3, MODE, false, true>(P, a, s);
       if (a.act) return cudaErrorNotSupported;
@@ -1371,29 +1400,46 @@ __global__ void k_tc_tile_lm(const uint8_t* __restrict__ xop, int64_t row_bytes,
                              float* __restrict__ ca, float* __restrict__ cb,
                              float* __restrict__ colk, int32_t* __restrict__ cc,
                              int64_t n_lm_blocks, const uint32_t* __restrict__ bmask,
-                             const uint32_t* __restrict__ cmask, int64_t nblk,
+                             const uint32_t* __restrict__ cmask,
+                             const uint32_t* __restrict__ tmask, int64_t nblk, int act_words,
                              uint32_t* __restrict__ act) {
   pdl_wait();
   pdl_trigger();   // one wave
   if (blockIdx.x >= n_lm_blocks) {
     // pruning (cells.cu): per row block, which 32-column chunks of this tile
-    // may hold an in-ball pair — one word per block for k_tc
-    __shared__ uint32_t scm[32 * 8];
-    for (int t = threadIdx.x; t < 32 * 8; t += blockDim.x) scm[t] = cmask[t];
+    // may hold an in-ball pair — act_words words per block for k_tc (byte t =
+    // the chunks of 256-column tile t); a tile whose cell mask misses the
+    // block's near cells is skipped without looking at its chunks
+    __shared__ uint32_t scm[(kBigT / 32) * 8];
+    __shared__ uint32_t stm[(kBigT / 256) * 8];
+    const int64_t cnt = *l_count_dev;
+    const int ntl = (int)((cnt + 255) / 256);
+    for (int t = threadIdx.x; t < ntl * 64; t += blockDim.x) scm[t] = cmask[t];
+    for (int t = threadIdx.x; t < ntl * 8; t += blockDim.x) stm[t] = tmask[t];
     __syncthreads();
     const int64_t b = (blockIdx.x - n_lm_blocks) * (int64_t)blockDim.x + threadIdx.x;
     if (b >= nblk) return;
     uint32_t bm[8];
 #pragma unroll
     for (int w = 0; w < 8; ++w) bm[w] = bmask[b * 8 + w];
-    uint32_t bits = 0u;
-    for (int c = 0; c < 32; ++c) {
-      uint32_t x = 0u;
+    for (int wd = 0; wd < act_words; ++wd) {
+      uint32_t bits = 0u;
+      for (int tt = 0; tt < 4; ++tt) {
+        const int t = 4 * wd + tt;
+        if (t >= ntl) break;
+        uint32_t any = 0u;
 #pragma unroll
-      for (int w = 0; w < 8; ++w) x |= bm[w] & scm[c * 8 + w];
-      bits |= (x != 0u ? 1u : 0u) << c;
+        for (int w = 0; w < 8; ++w) any |= bm[w] & stm[t * 8 + w];
+        if (!any) continue;
+        for (int c = 0; c < 8; ++c) {
+          uint32_t x = 0u;
+#pragma unroll
+          for (int w = 0; w < 8; ++w) x |= bm[w] & scm[(t * 8 + c) * 8 + w];
+          bits |= (x != 0u ? 1u : 0u) << (8 * tt + c);
+        }
+      }
+      act[b * act_words + wd] = bits;
     }
-    act[b] = bits;
     return;
   }
   const int64_t j = blockIdx.x;
@@ -1427,8 +1473,8 @@ cudaError_t launch_tc_tile_landmarks(const TcPlan& P, const void* nrm, const int
                     (const uint8_t*)P.xop, P.row_bytes, new_lm, l_count_dev, P.kind, P.cosine,
                     nrm, C2,
                     (uint8_t*)P.lop, (float*)a.col_a, (float*)a.col_b, (float*)a.colk,
-                    (int32_t*)a.col_c, (int64_t)P.l_rows, a.act_bmask, a.act_cmask, nblk,
-                    (uint32_t*)a.act);
+                    (int32_t*)a.col_c, (int64_t)P.l_rows, a.act_bmask, a.act_cmask,
+                    a.act_tmask, nblk, a.act_words, (uint32_t*)a.act);
 }
 
 

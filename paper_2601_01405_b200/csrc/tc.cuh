@@ -75,6 +75,7 @@ struct TcArgs {
   uint32_t* gram;      // debug: raw accumulators [n][L]
   uint32_t* adj;       // TC_MODE_ADJ: word-major adjacency, word v of candidate a at adj[v*adj_T + a]
   int adj_T;
+  AdjList nz;          // TC_MODE_ADJ: the non-zero words as a list (internal.cuh)
   uint8_t* covered;    // fused greedy: covered[p] = 1 for every in-ball pair (may be null)
   unsigned long long* trace;   // diagnostics: [grid][16] %globaltimer stamps (null: off)
   // tile-level pruning (cells.cu; all null when off): A rows are permuted
@@ -84,9 +85,11 @@ struct TcArgs {
   // skipped (no MMA / no TMEM read)
   const int32_t* row_pt;
   const int32_t* col_pos;
-  const uint32_t* act;     // [row block]: bit 8 t + c = chunk c of tile t is live
+  const uint32_t* act;     // [row block][act_words]: bit 8 t + c = chunk c of tile t is live
+  int act_words;           // words per row block (tiles / 4 rounded up, <= 8)
   const uint32_t* act_bmask;   // its inputs (cells.cu), folded by the landmark-operand
   const uint32_t* act_cmask;   //   launch of each greedy tile
+  const uint32_t* act_tmask;
 };
 
 int tc_bn_for(int kind, int katoms);

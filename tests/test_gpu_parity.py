@@ -287,3 +287,49 @@ def test_edges_triangle_path(bm, metric, eps):
     for k in na:
         assert np.array_equal(na[k], nb[k]), k
     compare(X, metric, eps, a, float_path=True)
+
+
+@pytest.mark.parametrize("tile", [2048, 8192])
+@pytest.mark.parametrize("dense", [False, True])
+def test_big_tile_invariance(bm, tile, dense):
+    """Tiles of more than 1024 candidates (k_resolve_big): the sparse-list
+    rounds and the dense sub-tile path both give the oracle's cover (A11)."""
+    from paper_2601_01405_b200 import bm as B
+    w = gen.get("c2")
+    X = gen.generate(w)
+    cov = run(bm, X, w.metric, w.eps, tile=tile, flags=B.FLAG_DENSE_RESOLVE if dense else 0)
+    assert cov.stats.tile_used == tile
+    compare(X, w.metric, w.eps, cov, float_path=True, tie_rate_limit=True)
+
+
+@pytest.mark.parametrize("path", ["cuda_core", "tensor"])
+def test_big_tile_chains(bm, path):
+    """A long in-tile dependency chain (collinear points at unit spacing, eps
+    1.5: candidate i is adjacent only to i - 1) exceeds the sparse rounds'
+    budget and must fall back to the in-order dense path; a dense clump
+    overflows the non-zero word list."""
+    X = np.arange(20000, dtype=np.float32).reshape(-1, 1)
+    a = run(bm, X, "l2", 1.5, tile=8192, path=path).numpy()
+    assert a["landmarks"].tolist() == list(range(0, 20000, 2))
+    rng = np.random.default_rng(9)
+    Y = (rng.random((12000, 3)) * 0.2).astype(np.float32)
+    Y[6000:] += 5.0 * rng.random((6000, 3)).astype(np.float32)
+    compare(Y, "l2", 0.05, run(bm, Y, "l2", 0.05, tile=8192, path=path), float_path=True)
+
+
+@pytest.mark.parametrize("name,m", [("c3_e8", 30000), ("c3_e4", 20000)])
+def test_big_tile_pruned(bm, name, m):
+    """The pruned contraction with 8192-column tiles (multi-word live-chunk
+    bitmaps, streamed landmark tiles) against the 1024 tiles and the oracle."""
+    from paper_2601_01405_b200 import bm as B
+    w = gen.get(name)
+    X = gen.generate(w, m)
+    t = torch.from_numpy(X).cuda()
+    big = bm.cover_build(t, w.metric, w.eps, path="tensor", tile=8192, flags=B.FLAG_FORCE_PRUNE)
+    small = bm.cover_build(t, w.metric, w.eps, path="tensor", tile=1024,
+                           flags=B.FLAG_FORCE_PRUNE)
+    nb, ns = big.numpy(), small.numpy()
+    for k in nb:
+        assert np.array_equal(nb[k], ns[k]), k
+    assert big.stats.tc_tiles_skipped > 0
+    compare(X, w.metric, w.eps, big, float_path=True)
