@@ -251,7 +251,8 @@ struct BigSmem {
   static constexpr int REG = (WPRE + (kBigW + 1) * 4 + 15) & ~15;
   static constexpr int REG_BYTES = 32 * 1024 * 4;              // sadj (dense) / entries (sparse)
   static constexpr int SKEY = REG + REG_BYTES;                 // kBigT words
-  static constexpr int SCM = SKEY + kBigT * 4;                 // (kBigT / 32) x 8 words
+  static constexpr int SPT = SKEY + kBigT * 4;                 // kBigT points
+  static constexpr int SCM = SPT + kBigT * 4;                  // (kBigT / 32) x 8 words
   static constexpr int SHIST = SCM + kBigW * 8 * 4;            // 256 ints
   static constexpr int MISC = SHIST + 256 * 4;                 // 64 words
   static constexpr int TOTAL = MISC + 64 * 4;
@@ -275,6 +276,7 @@ __global__ void __launch_bounds__(1024) k_resolve_big(
   uint32_t* sadj = reinterpret_cast<uint32_t*>(bsm + BigSmem::REG);
   uint32_t* skey = reinterpret_cast<uint32_t*>(bsm + BigSmem::SKEY);
   uint32_t* scm = reinterpret_cast<uint32_t*>(bsm + BigSmem::SCM);
+  int32_t* spt = reinterpret_cast<int32_t*>(bsm + BigSmem::SPT);
   int* shist = reinterpret_cast<int*>(bsm + BigSmem::SHIST);
   uint32_t* misc = reinterpret_cast<uint32_t*>(bsm + BigSmem::MISC);
   const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
@@ -394,14 +396,32 @@ __global__ void __launch_bounds__(1024) k_resolve_big(
   __syncthreads();
   const int L0 = *L_dev;
   const int dL = wpre[kBigW];
-  for (int a = tid; a < nc; a += blockDim.x) {
-    const uint32_t S = lmb[a >> 5];
-    if ((S >> (a & 31)) & 1u) {
+  // each thread's (up to kBigT / 1024) candidates: point and cell rank loaded
+  // once, all loads of a level in flight together (three memory latencies
+  // per tile instead of three per candidate)
+  constexpr int PER = kBigT / 1024;
+  int32_t cpt[PER];
+  int crk[PER], ccl[PER];
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int a = tid + 1024 * k;
+    cpt[k] = a < nc && ((lmb[a >> 5] >> (a & 31)) & 1u) ? __ldcg(unc + a) : -1;
+  }
+  if (prune) {
+#pragma unroll
+    for (int k = 0; k < PER; ++k) ccl[k] = cpt[k] >= 0 ? __ldg(pt_out.cell + cpt[k]) : 0;
+#pragma unroll
+    for (int k = 0; k < PER; ++k) crk[k] = cpt[k] >= 0 ? __ldg(pt_out.rank + ccl[k]) : -1;
+  }
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int a = tid + 1024 * k;
+    if (cpt[k] >= 0) {
+      const uint32_t S = lmb[a >> 5];
       const int pos = wpre[a >> 5] + __popc(S & ((1u << (a & 31)) - 1u));
-      const int32_t pt = unc[a];
-      new_lm[pos] = pt;
-      lm_out[L0 + pos] = pt;
-      if (prune) atomicAdd(&shist[pt_out.rank[pt_out.cell[pt]]], 1);
+      new_lm[pos] = cpt[k];
+      lm_out[L0 + pos] = cpt[k];
+      if (prune) atomicAdd(&shist[crk[k]], 1);
     }
   }
   __syncthreads();
@@ -428,21 +448,23 @@ __global__ void __launch_bounds__(1024) k_resolve_big(
       }
     }
     __syncthreads();
-    for (int a = tid; a < nc; a += blockDim.x) {
-      const uint32_t S = lmb[a >> 5];
-      if ((S >> (a & 31)) & 1u) {
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int a = tid + 1024 * k;
+      if (cpt[k] >= 0) {
+        const uint32_t S = lmb[a >> 5];
         const int pos = wpre[a >> 5] + __popc(S & ((1u << (a & 31)) - 1u));
-        const int r = pt_out.rank[pt_out.cell[unc[a]]];
-        skey[atomicAdd(&shist[r], 1)] = (uint32_t)pos;
+        const int slot = atomicAdd(&shist[crk[k]], 1);
+        skey[slot] = (uint32_t)pos | ((uint32_t)ccl[k] << 16);   // pos < 2^13, cell < 256
+        spt[slot] = cpt[k];
       }
     }
     __syncthreads();
     for (int k = tid; k < dL; k += blockDim.x) {
-      const int src = (int)skey[k];
-      const int32_t p = new_lm[src];   // written above by this CTA
-      pt_out.col_pt[k] = p;
-      pt_out.col_pos[k] = src;
-      const int c = pt_out.cell[p];
+      const uint32_t v = skey[k];
+      const int c = (int)(v >> 16);
+      pt_out.col_pt[k] = spt[k];
+      pt_out.col_pos[k] = (int32_t)(v & 0xffffu);
       atomicOr(&scm[(k >> 5) * 8 + (c >> 5)], 1u << (c & 31));
     }
     __syncthreads();

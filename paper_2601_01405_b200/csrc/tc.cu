@@ -228,7 +228,8 @@ constexpr uint32_t make_idesc(int M, int N) {
          ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
-template <int RA, int BN, int KATOMS, int STAGES, int ABUF, bool FOLD, bool BRES = false>
+template <int RA, int BN, int KATOMS, int STAGES, int ABUF, bool FOLD, bool BRES = false,
+          int MODE = TC_MODE_MEMBER>
 struct Smem {
   static constexpr int A_ATOM = 128 * 128;                 // 128 rows x 128 B
   // ABUF == 0 (K streaming, wide rows): no resident A block; every stage
@@ -246,8 +247,10 @@ struct Smem {
   static constexpr int BK_SLOT = BN * 32;
   static constexpr int NBK = BRES ? STAGES : 2;            // fold constant slots
   static constexpr int COL_OFF = AK_OFF + (FOLD ? 128 * 32 + NBK * BK_SLOT : 0);
-  static constexpr int COL_BYTES = BN * 4;   // int8: per-buffer column constants c_j
-  static constexpr int BAR_OFF = COL_OFF + (FOLD ? 0 : NBUF * COL_BYTES);
+  static constexpr int COL_BYTES = BN * 4;   // per-buffer column constants: c_j (int8) / d_j (tf32)
+  // (tf32 with resident B keeps every d_j of the launch in DJ below instead)
+  static constexpr bool COLSLOT = (MODE == TC_MODE_MEMBER || MODE == TC_MODE_ADJ) && !(FOLD && BRES);
+  static constexpr int BAR_OFF = COL_OFF + (COLSLOT ? NBUF * COL_BYTES : 0);
   static constexpr int NBARS = 2 * STAGES + 2 * ABUF + 3 * NBUF + 5;
   static constexpr int CNT_OFF = BAR_OFF + NBARS * 8;     // tmem slot + per-warp counts
   static constexpr int BUF_OFF = CNT_OFF + 128;
@@ -346,7 +349,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   // MMA per tile (ones x {-cb_hi, -cb_mid, -cb_lo}), so the epilogue's test is
   // a plain max over the accumulators
   constexpr bool FOLD = KIND == TC_TF32 && MODE != TC_MODE_GRAM;
-  using S = Smem<RA, BN, KATOMS, STAGES, ABUF, FOLD, BRES>;
+  using S = Smem<RA, BN, KATOMS, STAGES, ABUF, FOLD, BRES, MODE>;
   static_assert(!BRES || KATOMS == 1, "resident B: one K atom per tile");
   constexpr int BUFCOLS = RA * BN;
   constexpr int NBUF = 512 / BUFCOLS;   // TMEM accumulator buffers (2 at BN=256, 4 at BN=128)
@@ -476,6 +479,38 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       if (tile_active(ab, mb, t)) return true;
     return false;
   };
+  // Live tiles of a unit as a bit mask (bit t = tile t), so that the roles
+  // visit only the live tiles instead of testing every tile of the unit
+  // (pruned launches: <= 32 tiles, ~2 live; A2: the lower-triangle tiles).
+  const bool use_mask = (PR || MODE == TC_MODE_ADJ) && n_tiles <= 32;
+  auto live_tiles = [&](const ActW& ab, int64_t mb, int64_t t0, int64_t t1) -> uint32_t {
+    uint32_t m = 0u;
+    if constexpr (MODE == TC_MODE_ADJ) {
+      const int64_t te = min(t1, ((mb + 1) * RA * 128 + BN - 1) / BN);
+      m = te > 0 ? (te >= 32 ? 0xffffffffu : (1u << te) - 1u) : 0u;
+    } else if constexpr (PR) {
+#pragma unroll
+      for (int k = 0; k < AWM; ++k) {
+        const uint32_t x = ab.w[k];
+        const uint32_t nz = (((x & 0x7f7f7f7fu) + 0x7f7f7f7fu) | x) & 0x80808080u;  // byte != 0
+        const uint32_t b = ((nz >> 7) & 1u) | ((nz >> 14) & 2u) | ((nz >> 21) & 4u) |
+                           ((nz >> 28) & 8u);
+        m |= b << (4 * k);
+      }
+    }
+    const uint32_t lo = t0 >= 32 ? 0u : (0xffffffffu << t0);
+    const uint32_t hi = t1 >= 32 ? 0xffffffffu : ((1u << t1) - 1u);
+    return m & lo & hi;
+  };
+  // first live tile after t (or a sentinel past every range)
+  auto next_live = [&](uint32_t m, int64_t t) -> int64_t {
+    const uint32_t r = t >= 31 ? 0u : (m & ~((2u << t) - 1u));
+    return r ? (int64_t)(__ffs(r) - 1) : (int64_t)1 << 40;
+  };
+  auto first_live = [&](uint32_t m) -> int64_t {
+    return m ? (int64_t)(__ffs(m) - 1) : (int64_t)1 << 40;
+  };
+
   // the live-chunk words of unit u
   auto act_of = [&](int64_t u) -> ActW {
     ActW r;
@@ -540,8 +575,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             for (int ka = 0; ka < KATOMS; ++ka)
               tma_prefetch_2d(&tmA, ka * ATOM_ELEMS, (int)((un / n_chunks) * RA * 128 + r * 128));
         }
-        for (int64_t t = t0; t < t1 && !BRES; ++t) {
-          if (!tile_active(uact, mb, t)) continue;
+        const uint32_t lmask = use_mask ? live_tiles(uact, mb, t0, t1) : 0u;
+        for (int64_t t = use_mask ? first_live(lmask) : t0; t < t1 && !BRES;
+             t = use_mask ? next_live(lmask, t) : t + 1) {
+          if (!use_mask && !tile_active(uact, mb, t)) continue;
           for (int ka = 0; ka < n_atoms; ++ka) {
             mbar_wait(&empty[stage], phase ^ 1u);
             mbar_expect_tx(&full[stage], (uint32_t)S::B_STAGE);
@@ -601,8 +638,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
         if (ui == 0) TC_STAMP(5);
         const uint8_t* sAb = sA + ab * S::A_BYTES;
-        for (int64_t t = t0; t < t1; ++t) {
-          if (!tile_active(uact, mb, t)) {
+        const uint32_t lmask = use_mask ? live_tiles(uact, mb, t0, t1) : 0u;
+        if (use_mask) n_skip += (t1 - t0) - __popc(lmask);
+        for (int64_t t = use_mask ? first_live(lmask) : t0; t < t1;
+             t = use_mask ? next_live(lmask, t) : t + 1) {
+          if (!use_mask && !tile_active(uact, mb, t)) {
             ++n_skip;
             continue;
           }
@@ -610,9 +650,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           mbar_wait(&t_empty[buf], (use[buf] & 1u) ^ 1u);
           fence_after();
           // int8: the tile's per-column constants c_j into this buffer's slot
-          if constexpr ((MODE == TC_MODE_MEMBER || MODE == TC_MODE_ADJ) && !FOLD) {
+          // (tf32 without resident B: the tile's in-test offsets d_j, read by
+          // the epilogue's classification, land in the same slot)
+          if constexpr (S::COLSLOT) {
             mbar_expect_tx(&c_full[buf], (uint32_t)S::COL_BYTES);
-            bulk_load(scol + buf * BN, (const void*)(args.col_c + t * BN),
+            bulk_load(scol + buf * BN,
+                      FOLD ? (const void*)(args.col_a + t * BN) : (const void*)(args.col_c + t * BN),
                       (uint32_t)S::COL_BYTES, &c_full[buf]);
           }
           const uint32_t dcol = tmem + (uint32_t)(buf * BUFCOLS);
@@ -809,15 +852,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         if constexpr (PR) ppt[r] = prow[r] < args.n ? (int64_t)__ldg(args.row_pt + prow[r]) : prow[r];
         else ppt[r] = prow[r];
       }
-      for (int64_t t = t0; t < t1; ++t) {
-        if (!tile_active(uact, mb, t)) continue;
+      const uint32_t lmask = use_mask ? live_tiles(uact, mb, t0, t1) : 0u;
+      for (int64_t t = use_mask ? first_live(lmask) : t0; t < t1;
+           t = use_mask ? next_live(lmask, t) : t + 1) {
+        if (!use_mask && !tile_active(uact, mb, t)) continue;
         // both groups drain every tile: group g takes its half of the columns
         const int buf = (int)(tcount % NBUF);
         const uint32_t ph = (phase >> buf) & 1u;    // parity of buffer buf's next fill
         mbar_wait(&t_full[buf], ph);
         if (tcount < 2 && q == 0 && lane == 0) TC_STAMP(7 + grp);
-        if constexpr ((MODE == TC_MODE_MEMBER || MODE == TC_MODE_ADJ) && !FOLD)
-          mbar_wait(&c_full[buf], ph);
+        if constexpr (S::COLSLOT) mbar_wait(&c_full[buf], ph);
         phase ^= 1u << buf;
         fence_after();
         const float* colb = scol + buf * BN;   // tile's col_b (tf32) / col_c (int8) in smem
@@ -860,10 +904,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               uint32_t mask = 0u;
               if constexpr (KIND == TC_TF32) {
                 float dj[32];
-                const float4* d4 = reinterpret_cast<const float4*>(args.col_a + j0);
+                const float4* d4 = reinterpret_cast<const float4*>(colb + cc * 32);   // smem slot
 #pragma unroll
                 for (int i4 = 0; i4 < 8; ++i4) {
-                  const float4 q4 = __ldg(d4 + i4);
+                  const float4 q4 = d4[i4];
                   dj[4 * i4] = q4.x;
                   dj[4 * i4 + 1] = q4.y;
                   dj[4 * i4 + 2] = q4.z;
@@ -960,7 +1004,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                   const int64_t j = j0 + i;
                   bool in = true;
                   if constexpr (KIND == TC_TF32) {
-                    const float dji = S::DJ_BYTES > 0 ? sdj[j] : __ldg(args.col_a + j);
+                    const float dji = S::DJ_BYTES > 0 ? sdj[j] : colb[cc * 32 + i];
                     in = __uint_as_float(sel32(v, i)) - dji > rhi[r];
                   }
                   if (in) {
@@ -979,12 +1023,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 float dj[32];   // tf32 in-test offsets of the chunk (warp-uniform loads)
                 if constexpr (KIND == TC_TF32) {
                   const float4* d4 = reinterpret_cast<const float4*>(
-                      S::DJ_BYTES > 0 ? (const float*)(sdj + j0) : args.col_a + j0);
+                      S::DJ_BYTES > 0 ? (const float*)(sdj + j0) : colb + cc * 32);
 #pragma unroll
                   for (int i4 = 0; i4 < 8; ++i4) {
                     float4 q4;
-                    if constexpr (S::DJ_BYTES > 0) q4 = d4[i4];   // shared memory
-                    else q4 = __ldg(d4 + i4);
+                    q4 = d4[i4];   // shared memory (resident d_j or the tile's slot)
                     dj[4 * i4] = q4.x;
                     dj[4 * i4 + 1] = q4.y;
                     dj[4 * i4 + 2] = q4.z;
@@ -1119,7 +1162,7 @@ template <int KIND, int RA, int BN, int KATOMS, int STAGES, int ABUF, int MODE, 
           bool PR = false>
 static cudaError_t launch_cfg(const TcPlan& P, TcArgs a, cudaStream_t s) {
   constexpr bool FOLD = KIND == TC_TF32 && MODE != TC_MODE_GRAM;
-  using S = Smem<RA, BN, KATOMS, STAGES, ABUF, FOLD, BRES>;
+  using S = Smem<RA, BN, KATOMS, STAGES, ABUF, FOLD, BRES, MODE>;
   static_assert(S::TOTAL <= 232448, "shared memory");
   CUtensorMap tA, tB, tK, tO;
   cudaError_t e = make_tmap(&tA, P.xop, KIND, P.k_elems, P.n_rows, P.row_bytes, 128);
