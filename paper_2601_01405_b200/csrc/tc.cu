@@ -194,31 +194,6 @@ __device__ __forceinline__ void tmem_wait64(uint32_t (&v)[64]) {
       : "memory");
 }
 
-// 32 consecutive columns of the warp's 32 TMEM lanes (no wait: the registers
-// are valid only after tmem_wait32 on the same array)
-__device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t (&v)[32]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
-      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
-        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
-        "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-      : "r"(taddr)
-      : "memory");
-}
-__device__ __forceinline__ void tmem_wait32(uint32_t (&v)[32]) {
-  asm volatile("tcgen05.wait::ld.sync.aligned;"
-      : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7]),
-        "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]), "+r"(v[12]), "+r"(v[13]), "+r"(v[14]), "+r"(v[15]),
-        "+r"(v[16]), "+r"(v[17]), "+r"(v[18]), "+r"(v[19]), "+r"(v[20]), "+r"(v[21]), "+r"(v[22]), "+r"(v[23]),
-        "+r"(v[24]), "+r"(v[25]), "+r"(v[26]), "+r"(v[27]), "+r"(v[28]), "+r"(v[29]), "+r"(v[30]), "+r"(v[31])
-      :
-      : "memory");
-}
-__device__ __forceinline__ void prefetch_l2(const void* p) {
-  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-}
-
 // Shared-memory matrix descriptor: K-major, 128-byte swizzle, 8-row groups
 // 1024 B apart (SBO), sm_100 descriptor version 1.
 __device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
@@ -804,18 +779,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       g0 = __shfl_sync(FULLM, g0, 0);
       for (uint32_t i = lane; i < kn; i += 32)
         if ((int64_t)(g0 + i) < args.key_cap) args.keys[g0 + i] = kb[i];
-      // B' rows: prefetch every staged band pair's two rows into L2 first, so
-      // the fp64 re-decisions below wait for L2, not DRAM, per coordinate group
-      for (uint32_t i = lane; i < bn; i += 32) {
-        const int64_t p = (int64_t)(bb[i] >> 32), j = (int64_t)(bb[i] & 0xffffffffull);
-        if (j >= n_cols || p >= args.n) continue;
-        const float* xp = args.xrows + p * (int64_t)args.xstride;
-        const float* xq = args.xrows + (int64_t)args.lm_idx[j] * args.xstride;
-        for (int o = 0; o < args.d; o += 32) {
-          prefetch_l2(xp + o);
-          prefetch_l2(xq + o);
-        }
-      }
       for (uint32_t i = lane; i < bn; i += 32) recheck(bb[i]);
       __syncwarp();
       if (lane == 0) {
@@ -906,6 +869,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         // flight while this one is classified (va / vb ping-pong)
         const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * BUFCOLS);
         constexpr int NCH = RA * (BN / 32);
+        uint32_t vv[64];   // two chunks per TMEM load
         // chunks the (possibly narrower) MMA of this tile wrote, this group's half
         const int64_t left = n_cols - t * BN;
         const int nch = RA == 1 && left < BN ? (int)((left + 31) / 32) : NCH;
@@ -1102,43 +1066,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           }
         };
         if constexpr (MODE != TC_MODE_PROBE_NOLD) {
-          // this group's chunks of the tile (pruned: only the live ones), 32
-          // columns per TMEM load, the next chunk's load in flight while the
-          // current one is classified (two register sets, ping-pong)
-          uint32_t cm = (cend > cbeg) ? (((cend >= 32) ? 0xffffffffu : ((1u << cend) - 1u)) &
-                                         ~((1u << cbeg) - 1u))
-                                      : 0u;
-          if constexpr (PR) {
-            const uint32_t all = cm;
-            cm &= tile_bits(uact, t);
-            ck_run += __popc(cm);
-            ck_skip += __popc(all) - __popc(cm);
-          }
-          uint32_t va[32], vb[32];
-          int c = cm ? __ffs(cm) - 1 : -1;
-          if (c >= 0) {
-            cm &= cm - 1u;
-            tmem_ld32_nowait(caddr(c), va);
-            tmem_wait32(va);
-          }
-          while (c >= 0) {
-            const int cn = cm ? __ffs(cm) - 1 : -1;
-            if (cn >= 0) {
-              cm &= cm - 1u;
-              tmem_ld32_nowait(caddr(cn), vb);
+          // 64 columns per load (a past-the-end half is read and discarded)
+#pragma unroll 1
+          for (int c = cbeg; c < cend; c += 2) {
+            if constexpr (PR) {
+              const int nck = c + 1 < cend ? 2 : 1;
+              if (((tile_bits(uact, t) >> c) & (nck == 2 ? 3u : 1u)) == 0u) {
+                ck_skip += nck;
+                continue;   // no landmark of these 64 columns can be near this row block
+              }
+              ck_run += nck;
             }
-            chunk(c, va);
-            if (cn < 0) break;
-            tmem_wait32(vb);
-            const int cnn = cm ? __ffs(cm) - 1 : -1;
-            if (cnn >= 0) {
-              cm &= cm - 1u;
-              tmem_ld32_nowait(caddr(cnn), va);
-            }
-            chunk(cn, vb);
-            if (cnn < 0) break;
-            tmem_wait32(va);
-            c = cnn;
+            tmem_ld64_nowait(caddr(c), vv);
+            tmem_wait64(vv);
+            chunk(c, *reinterpret_cast<uint32_t(*)[32]>(&vv[0]));
+            if (c + 1 < cend) chunk(c + 1, *reinterpret_cast<uint32_t(*)[32]>(&vv[32]));
           }
         }
         fence_before();
