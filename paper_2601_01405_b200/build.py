@@ -19,13 +19,17 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-OBJ = os.path.join(PKG, "build")
-LIB = os.path.join(PKG, "libbm_b200.so")
+# BM_NVCC_EXTRA (diagnostics, e.g. "-DBM_TC_WTRACE"): extra nvcc flags; such a
+# build goes to its own object directory and library (load it with BM_LIB_PATH)
+EXTRA = os.environ.get("BM_NVCC_EXTRA", "").split()
+_TAG = ("_" + "".join(c for c in "_".join(EXTRA) if c.isalnum() or c == "_").lower()) if EXTRA else ""
+OBJ = os.path.join(PKG, "build" + _TAG)
+LIB = os.path.join(PKG, f"libbm_b200{_TAG}.so")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                      "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills",
-                     "-I" + os.path.join(ROOT, "include")]
+                     "-I" + os.path.join(ROOT, "include")] + EXTRA
 
 
 def nvcc() -> str:

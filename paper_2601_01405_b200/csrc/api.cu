@@ -26,6 +26,30 @@
 
 // diagnostics: per-CTA %globaltimer phase stamps of one traced k_tc launch
 // (TC_STAMP slots, tc.cu), summarised to stderr
+// diagnostics: per-role wait cycles of one traced k_tc launch (BM_TC_TRACE=2),
+// medians over the CTAs, in microseconds at the nominal clock
+static cudaError_t print_tc_wtrace(const unsigned long long* tr, int G, const char* tag,
+                                   cudaStream_t s) {
+  std::vector<unsigned long long> h((size_t)G * 16);
+  cudaError_t e = cudaMemcpyAsync(h.data(), tr, sizeof(unsigned long long) * G * 16,
+                                  cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return e;
+  static const char* names[10] = {"P wait B stage", "P wait A buf/fold slot", "M wait A",
+                                  "M wait TMEM buf", "M wait B data", "E wait acc (x8 warps)",
+                                  "E tmem ld (x8)", "E flush (x8)", "E loop total (x8)",
+                                  "M wait fold consts"};
+  fprintf(stderr, "wtrace [%s]", tag);
+  for (int k = 0; k < 10; ++k) {
+    std::vector<double> v;
+    for (int b = 0; b < G; ++b) v.push_back((double)h[b * 16 + k] / 1965.0);
+    std::sort(v.begin(), v.end());
+    fprintf(stderr, " | %s %.1f", names[k], v[v.size() / 2]);
+  }
+  fprintf(stderr, " us\n");
+  return cudaSuccess;
+}
+
 static cudaError_t print_tc_trace(const unsigned long long* tr, int G, const char* tag,
                                   cudaStream_t s) {
   std::vector<unsigned long long> h((size_t)G * 16);
@@ -750,7 +774,7 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
     TRY(pool.alloc(&ps.col_pos, (size_t)Tq));
     TRY(pool.alloc(&ps.cmask, (size_t)(Tq / 32) * KWd));
     TRY(pool.alloc(&ps.tmask, (size_t)(Tq / 256) * KWd));
-    TRY(pool.alloc(&ps.act, (size_t)nblk * aw));
+    TRY(pool.alloc(&ps.act, (size_t)nblk * (aw + 1)));   // [live-tile mask, chunk words]
     unsigned long long *pk = nullptr, *pa = nullptr;
     void* ptemp = nullptr;
     TRY(pool.alloc(&pk, (size_t)n));
@@ -946,6 +970,7 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
   static const bool loop_prof = getenv("BM_LOOP_PROFILE") != nullptr;
   unsigned long long* tc_trace = nullptr;   // BM_TC_TRACE=1: stamp every membership launch
   if (use_tc && getenv("BM_TC_TRACE")) TRY(pool.alloc(&tc_trace, (size_t)P.num_sms * 16));
+  const bool tc_wmode = tc_trace && atoi(getenv("BM_TC_TRACE")) == 2;
   std::vector<std::pair<int, cudaEvent_t>> lev;
   auto loop_mark = [&](int phase) {
     if (!loop_prof) return;
@@ -1074,15 +1099,18 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
         CK(mark_member());
         if (tc_trace) {   // diagnostics: phase stamps of this launch (synchronises)
           CK(cudaMemsetAsync(tc_trace, 0, sizeof(unsigned long long) * P.num_sms * 16, s));
-          ta.trace = tc_trace;
+          if (tc_wmode) ta.wtrace = tc_trace;
+          else ta.trace = tc_trace;
         }
         CK(tc::launch_tc(prune ? Pm : P, ta, s, &launches));
         CK(mark_member());
         if (tc_trace) {
           char tag[64];
           snprintf(tag, sizeof tag, "membership tile %lld", (long long)tile);
-          CK(print_tc_trace(tc_trace, P.num_sms, tag, s));
+          if (tc_wmode) CK(print_tc_wtrace(tc_trace, P.num_sms, tag, s));
+          else CK(print_tc_trace(tc_trace, P.num_sms, tag, s));
           ta.trace = nullptr;
+          ta.wtrace = nullptr;
         }
       } else {
         PairArgs m = base;

@@ -84,6 +84,26 @@ __device__ __forceinline__ unsigned long long gtimer() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
+// diagnostics (BM_TC_TRACE=2): cycles a role spends in wait k, accumulated per
+// thread and summed per CTA into args.wtrace[block][16] (off: wtrace null)
+// (compiled in only with -DBM_TC_WTRACE: a diagnostic build, BM_NVCC_EXTRA)
+#ifdef BM_TC_WTRACE
+#define TC_TWAIT(k, stmt)                      \
+  do {                                         \
+    if (args.wtrace) {                         \
+      const long long _t0 = clock64();         \
+      stmt;                                    \
+      wacc[k] += clock64() - _t0;              \
+    } else {                                   \
+      stmt;                                    \
+    }                                          \
+  } while (0)
+#else
+#define TC_TWAIT(k, stmt) \
+  do {                    \
+    stmt;                 \
+  } while (0)
+#endif
 // diagnostics: stamp slot k of this CTA (no-op unless a trace buffer is given)
 #define TC_STAMP(k) \
   do { \
@@ -164,6 +184,35 @@ __device__ __forceinline__ void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t
         "l"(a), "l"(b), "r"(idesc), "r"(acc)
         : "memory");
   }
+}
+// Warp-wide forms for the MMA role: the whole warp runs the issue loop
+// (convergent, so the descriptors stay in uniform registers) and one elected
+// lane issues the instruction (elect.sync inside the asm).
+template <int KIND>
+__device__ __forceinline__ void mma_w(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
+                                      uint32_t acc) {
+  if constexpr (KIND == TC_TF32) {
+    asm volatile(
+        "{\n\t.reg .pred p, q;\n\t.reg .b32 r;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "elect.sync r|q, 0xffffffff;\n\t"
+        "@q tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p, q;\n\t.reg .b32 r;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "elect.sync r|q, 0xffffffff;\n\t"
+        "@q tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void commit_w(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\t.reg .b32 r;\n\telect.sync r|q, 0xffffffff;\n\t"
+      "@q tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
+          su32(bar))
+      : "memory");
 }
 // 64 consecutive columns of the warp's 32 TMEM lanes in one load
 __device__ __forceinline__ void tmem_ld64_nowait(uint32_t taddr, uint32_t (&v)[64]) {
@@ -388,6 +437,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   unsigned long long* bbuf = kbuf + S::EPI_WARPS * S::KW;            // [EPI_WARPS][BW]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  long long wacc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};   // BM_TC_TRACE=2 wait cycles
+  // (slot 1 also counts the producer's fold-constant slot waits, 9 the MMA's)
+  auto wflush = [&](int k0, int k1) {
+    if (!args.wtrace) return;
+    for (int k = k0; k < k1; ++k)
+      if (wacc[k]) atomicAdd(args.wtrace + blockIdx.x * 16 + k, (unsigned long long)wacc[k]);
+  };
   if (threadIdx.x == 0) TC_STAMP(0);
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -455,7 +511,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   // role; every role evaluates the same predicate, so they skip the same tiles.
   constexpr int AWM = PR ? 8 : 1;   // <= 32 tiles of 256 columns (kBigT)
   struct ActW {
-    uint32_t w[AWM];
+    uint32_t m;        // live tiles (bit t: tile t has a live chunk)
+    uint32_t w[AWM];   // chunk bytes (loaded by the epilogue only)
   };
   auto tile_bits = [&](const ActW& ab, int64_t t) -> uint32_t {
     if constexpr (!PR) return 0xffu;
@@ -470,10 +527,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   // never read: the resolve kernels read only words v <= a / 32 of row a)
   auto tile_active = [&](const ActW& ab, int64_t mb, int64_t t) -> bool {
     if constexpr (MODE == TC_MODE_ADJ) return t * BN < (mb + 1) * RA * 128;
-    return tile_bits(ab, t) != 0u;
+    if constexpr (PR) return t < 32 && ((ab.m >> t) & 1u);
+    return true;
   };
   // a unit none of whose tiles is live is skipped whole (no A block load)
-  auto unit_active = [&](const ActW& ab, int64_t mb, int64_t t0, int64_t t1) -> bool {
+  auto unit_active_scan = [&](const ActW& ab, int64_t mb, int64_t t0, int64_t t1) -> bool {
     if constexpr (!PR && MODE != TC_MODE_ADJ) return true;
     for (int64_t t = t0; t < t1; ++t)
       if (tile_active(ab, mb, t)) return true;
@@ -489,14 +547,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const int64_t te = min(t1, ((mb + 1) * RA * 128 + BN - 1) / BN);
       m = te > 0 ? (te >= 32 ? 0xffffffffu : (1u << te) - 1u) : 0u;
     } else if constexpr (PR) {
-#pragma unroll
-      for (int k = 0; k < AWM; ++k) {
-        const uint32_t x = ab.w[k];
-        const uint32_t nz = (((x & 0x7f7f7f7fu) + 0x7f7f7f7fu) | x) & 0x80808080u;  // byte != 0
-        const uint32_t b = ((nz >> 7) & 1u) | ((nz >> 14) & 2u) | ((nz >> 21) & 4u) |
-                           ((nz >> 28) & 8u);
-        m |= b << (4 * k);
-      }
+      m = ab.m;
     }
     const uint32_t lo = t0 >= 32 ? 0u : (0xffffffffu << t0);
     const uint32_t hi = t1 >= 32 ? 0xffffffffu : ((1u << t1) - 1u);
@@ -510,15 +561,30 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   auto first_live = [&](uint32_t m) -> int64_t {
     return m ? (int64_t)(__ffs(m) - 1) : (int64_t)1 << 40;
   };
+  auto unit_active = [&](const ActW& ab, int64_t mb, int64_t t0, int64_t t1) -> bool {
+    if (use_mask) return live_tiles(ab, mb, t0, t1) != 0u;
+    return unit_active_scan(ab, mb, t0, t1);
+  };
 
   // the live-chunk words of unit u
+  // the live-tile mask of unit u (act layout per row block: [mask, chunk words])
+  const int64_t act_stride = (int64_t)args.act_words + 1;
   auto act_of = [&](int64_t u) -> ActW {
     ActW r;
+    r.m = PR ? 0u : 0xffffffffu;
 #pragma unroll
     for (int k = 0; k < AWM; ++k) r.w[k] = PR ? 0u : 0xffffffffu;
     if constexpr (PR) {
+      if (u < n_units) r.m = __ldg(args.act + (u / n_chunks) * act_stride);
+    }
+    return r;
+  };
+  // ... and, for the epilogue, its chunk words too
+  auto act_of_full = [&](int64_t u) -> ActW {
+    ActW r = act_of(u);
+    if constexpr (PR) {
       if (u < n_units) {
-        const uint32_t* p = args.act + (u / n_chunks) * (int64_t)args.act_words;
+        const uint32_t* p = args.act + (u / n_chunks) * act_stride + 1;
 #pragma unroll
         for (int k = 0; k < AWM; ++k) r.w[k] = k < args.act_words ? __ldg(p + k) : 0u;
       }
@@ -558,7 +624,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         if constexpr (!KS) {
           const int ab = (int)(ui % ABUF);
           if (ui >= ABUF) {             // wait until the MMAs of unit ui - ABUF released it
-            mbar_wait(&a_empty[ab], (a_ph >> ab) & 1u);
+            TC_TWAIT(1, mbar_wait(&a_empty[ab], (a_ph >> ab) & 1u));
             a_ph ^= 1u << ab;
           }
           uint8_t* sAb = sA + ab * S::A_BYTES;
@@ -580,7 +646,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
              t = use_mask ? next_live(lmask, t) : t + 1) {
           if (!use_mask && !tile_active(uact, mb, t)) continue;
           for (int ka = 0; ka < n_atoms; ++ka) {
-            mbar_wait(&empty[stage], phase ^ 1u);
+            TC_TWAIT(0, mbar_wait(&empty[stage], phase ^ 1u));
             mbar_expect_tx(&full[stage], (uint32_t)S::B_STAGE);
             tma_load_2d(sB + stage * S::B_STAGE, &tmB, &full[stage], ka * ATOM_ELEMS,
                         (int)(t * BN));
@@ -595,7 +661,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           if constexpr (FOLD) {   // the tile's column constants, two slots
             const int sl = (int)(tk & 1);
             if (tk >= 2) {
-              mbar_wait(&bk_empty[sl], (bk_ph >> sl) & 1u);
+              TC_TWAIT(1, mbar_wait(&bk_empty[sl], (bk_ph >> sl) & 1u));
               bk_ph ^= 1u << sl;
             }
             mbar_expect_tx(&bk_full[sl], (uint32_t)S::BK_SLOT);
@@ -606,10 +672,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         ++ui;
       }
       TC_STAMP(4);
+      wflush(0, 2);
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ---------------- MMA issuer
+    {
+      // ---------------- MMA issuer (the whole warp runs the loop; one elected
+      // lane issues each tcgen05 instruction)
       int stage = 0;
       uint32_t phase = 0, a_ph = 0;
       uint32_t use[NBUF] = {};
@@ -632,11 +700,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
         const int ab = KS ? 0 : (int)(ui % (ABUF > 0 ? ABUF : 1));
         if constexpr (!KS) {
-          mbar_wait(&a_full[ab], (a_ph >> ab) & 1u);
+          TC_TWAIT(2, mbar_wait(&a_full[ab], (a_ph >> ab) & 1u));
           a_ph ^= 1u << ab;
           fence_after();
         }
-        if (ui == 0) TC_STAMP(5);
+        if (ui == 0 && lane == 0) TC_STAMP(5);
         const uint8_t* sAb = sA + ab * S::A_BYTES;
         const uint32_t lmask = use_mask ? live_tiles(uact, mb, t0, t1) : 0u;
         if (use_mask) n_skip += (t1 - t0) - __popc(lmask);
@@ -647,7 +715,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             continue;
           }
           ++n_run;
-          mbar_wait(&t_empty[buf], (use[buf] & 1u) ^ 1u);
+          TC_TWAIT(3, mbar_wait(&t_empty[buf], (use[buf] & 1u) ^ 1u));
           fence_after();
           // int8: the tile's per-column constants c_j into this buffer's slot
           // (tf32 without resident B: the tile's in-test offsets d_j, read by
@@ -675,13 +743,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
             for (int ks = 0; ks < 4; ++ks)
               if (ks < ksteps)
-                mma<KIND>(dcol, sdesc(abase + ks * 32), sdesc(bbase + ks * 32), idesc,
+                mma_w<KIND>(dcol, sdesc(abase + ks * 32), sdesc(bbase + ks * 32), idesc,
                           ks != 0 ? 1u : 0u);
             if constexpr (FOLD)
-              mma<KIND>(dcol, sdesc32(su32(sAK)), sdesc32(su32(sBK + t * S::BK_SLOT)), idesc, 1u);
+              mma_w<KIND>(dcol, sdesc32(su32(sAK)), sdesc32(su32(sBK + t * S::BK_SLOT)), idesc, 1u);
           }
           for (int ka = 0; ka < n_atoms && !BRES; ++ka) {
-            mbar_wait(&full[stage], phase);
+            TC_TWAIT(4, mbar_wait(&full[stage], phase));
             fence_after();
             const uint32_t bbase = su32(sB + stage * S::B_STAGE);
 #pragma unroll
@@ -691,11 +759,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
               for (int ks = 0; ks < 4; ++ks) {
                 if (ka * 4 + ks < ksteps)
-                  mma<KIND>(dcol + (uint32_t)(r * BN), sdesc(abase + ks * 32),
+                  mma_w<KIND>(dcol + (uint32_t)(r * BN), sdesc(abase + ks * 32),
                             sdesc(bbase + ks * 32), idesc, (ka | ks) != 0 ? 1u : 0u);
               }
             }
-            mma_commit(&empty[stage]);
+            commit_w(&empty[stage]);
             if (++stage == STAGES) {
               stage = 0;
               phase ^= 1u;
@@ -703,24 +771,28 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           }
           if constexpr (FOLD && !BRES) {   // acc' = x.l - cb_j: ones x {-cb_hi, -cb_mid, -cb_lo}
             const int sl = (int)(tk & 1);
-            mbar_wait(&bk_full[sl], (uint32_t)((tk >> 1) & 1));
+            TC_TWAIT(9, mbar_wait(&bk_full[sl], (uint32_t)((tk >> 1) & 1)));
             fence_after();
-            mma<KIND>(dcol, sdesc32(su32(sAK)), sdesc32(su32(sBK + sl * S::BK_SLOT)), idesc, 1u);
-            mma_commit(&bk_empty[sl]);
+            mma_w<KIND>(dcol, sdesc32(su32(sAK)), sdesc32(su32(sBK + sl * S::BK_SLOT)), idesc, 1u);
+            commit_w(&bk_empty[sl]);
           }
           ++tk;
-          mma_commit(&t_full[buf]);
+          commit_w(&t_full[buf]);
           ++use[buf];
           buf = buf + 1 == NBUF ? 0 : buf + 1;
         }
-        if constexpr (!KS) mma_commit(&a_empty[ab]);
+        if constexpr (!KS) commit_w(&a_empty[ab]);
         ++ui;
       }
-      if (MODE == TC_MODE_MEMBER && args.stats) {
+      if (MODE == TC_MODE_MEMBER && args.stats && lane == 0) {
         if (n_run) atomicAdd(&args.stats->tc_tiles_run, n_run);
         if (n_skip) atomicAdd(&args.stats->tc_tiles_skip, n_skip);
       }
-      TC_STAMP(6);
+      if (lane == 0) {
+        TC_STAMP(6);
+        wflush(2, 5);
+        wflush(9, 10);
+      }
     }
   } else if (warp >= 4) {
     // ---------------- epilogue: warps 4-7 take the first half of every tile's
@@ -809,12 +881,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // row constants of the next unit are loaded one unit ahead
     float nlo[RA], nhi[RA];
     int32_t nint[RA];
+    int64_t nppt[RA];   // pruning: original point of each row, loaded one unit ahead
     auto load_rows = [&](int64_t u) {
       if (u >= n_units) return;
       const int64_t mbn = u / n_chunks;
 #pragma unroll
       for (int r = 0; r < RA; ++r) {
         const int64_t pr = mbn * RA * 128 + r * 128 + q * 32 + lane;
+        if constexpr (PR) nppt[r] = pr < args.n ? (int64_t)__ldg(args.row_pt + pr) : pr;
         if constexpr (KIND == TC_TF32) {
           nlo[r] = __ldcg(args.row_lo + pr);
           nhi[r] = __ldcg(args.row_hi + pr);
@@ -825,11 +899,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     };
     load_rows(blockIdx.x);
     unsigned long long ck_run = 0ull, ck_skip = 0ull;   // chunks of this warp's rows
-    ActW act_next = act_of(blockIdx.x);
+    ActW act_next = act_of_full(blockIdx.x);
+    const long long epi_t0 = args.wtrace ? clock64() : 0;
     for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
       const int64_t mb = u / n_chunks, ch = u % n_chunks;
       const ActW uact = act_next;
-      act_next = act_of(u + gridDim.x);
+      act_next = act_of_full(u + gridDim.x);
       const int64_t t0 = ch * tiles_per_chunk, t1 = min(n_tiles, t0 + tiles_per_chunk);
       int64_t prow[RA];
       float rlo[RA], rhi[RA];
@@ -844,14 +919,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           rint[r] = nint[r];
         }
       }
-      load_rows(u + gridDim.x);
-      // pruning: original point of each row; the row block's near-cell mask
+      // pruning: original point of each row (loaded with the row constants)
       int64_t ppt[RA];
 #pragma unroll
       for (int r = 0; r < RA; ++r) {
-        if constexpr (PR) ppt[r] = prow[r] < args.n ? (int64_t)__ldg(args.row_pt + prow[r]) : prow[r];
+        if constexpr (PR) ppt[r] = nppt[r];
         else ppt[r] = prow[r];
       }
+      load_rows(u + gridDim.x);
       const uint32_t lmask = use_mask ? live_tiles(uact, mb, t0, t1) : 0u;
       for (int64_t t = use_mask ? first_live(lmask) : t0; t < t1;
            t = use_mask ? next_live(lmask, t) : t + 1) {
@@ -859,9 +934,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         // both groups drain every tile: group g takes its half of the columns
         const int buf = (int)(tcount % NBUF);
         const uint32_t ph = (phase >> buf) & 1u;    // parity of buffer buf's next fill
-        mbar_wait(&t_full[buf], ph);
+        TC_TWAIT(5, mbar_wait(&t_full[buf], ph));
         if (tcount < 2 && q == 0 && lane == 0) TC_STAMP(7 + grp);
-        if constexpr (S::COLSLOT) mbar_wait(&c_full[buf], ph);
+        if constexpr (S::COLSLOT) TC_TWAIT(5, mbar_wait(&c_full[buf], ph));
         phase ^= 1u << buf;
         fence_after();
         const float* colb = scol + buf * BN;   // tile's col_b (tf32) / col_c (int8) in smem
@@ -1061,24 +1136,24 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 }
               }
               __syncwarp();
-              if (*kc > S::KW / 2 || *bc > S::BW / 2) flush();
+              if (*kc > S::KW / 2 || *bc > S::BW / 2) TC_TWAIT(7, flush());
             }
           }
         };
         if constexpr (MODE != TC_MODE_PROBE_NOLD) {
           // 64 columns per load (a past-the-end half is read and discarded)
 #pragma unroll 1
+          const uint32_t tb = tile_bits(uact, t);   // this tile's live chunks
           for (int c = cbeg; c < cend; c += 2) {
             if constexpr (PR) {
               const int nck = c + 1 < cend ? 2 : 1;
-              if (((tile_bits(uact, t) >> c) & (nck == 2 ? 3u : 1u)) == 0u) {
+              if (((tb >> c) & (nck == 2 ? 3u : 1u)) == 0u) {
                 ck_skip += nck;
                 continue;   // no landmark of these 64 columns can be near this row block
               }
               ck_run += nck;
             }
-            tmem_ld64_nowait(caddr(c), vv);
-            tmem_wait64(vv);
+            TC_TWAIT(6, tmem_ld64_nowait(caddr(c), vv); tmem_wait64(vv));
             chunk(c, *reinterpret_cast<uint32_t(*)[32]>(&vv[0]));
             if (c + 1 < cend) chunk(c + 1, *reinterpret_cast<uint32_t(*)[32]>(&vv[32]));
           }
@@ -1089,8 +1164,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         ++tcount;
       }
     }
+    if (args.wtrace) wacc[8] += clock64() - epi_t0;
     flush();
     if (q == 0 && lane == 0) TC_STAMP(9 + grp);
+    if (lane == 0) wflush(5, 9);
     // every chunk is read by the four warps of its group (32 rows each): count
     // it once, from warp q == 0
     if (MODE == TC_MODE_MEMBER && args.stats && q == 0 && lane == 0) {
@@ -1465,6 +1542,7 @@ __global__ void k_tc_tile_lm(const uint8_t* __restrict__ xop, int64_t row_bytes,
     uint32_t bm[8];
 #pragma unroll
     for (int w = 0; w < 8; ++w) bm[w] = bmask[b * 8 + w];
+    uint32_t live = 0u;   // word 0: the live tiles
     for (int wd = 0; wd < act_words; ++wd) {
       uint32_t bits = 0u;
       for (int tt = 0; tt < 4; ++tt) {
@@ -1480,9 +1558,11 @@ __global__ void k_tc_tile_lm(const uint8_t* __restrict__ xop, int64_t row_bytes,
           for (int w = 0; w < 8; ++w) x |= bm[w] & scm[(t * 8 + c) * 8 + w];
           bits |= (x != 0u ? 1u : 0u) << (8 * tt + c);
         }
+        if ((bits >> (8 * tt)) & 0xffu) live |= 1u << t;
       }
-      act[b * act_words + wd] = bits;
+      act[b * (act_words + 1) + 1 + wd] = bits;
     }
+    act[b * (act_words + 1)] = live;
     return;
   }
   const int64_t j = blockIdx.x;

@@ -78,6 +78,7 @@ struct TcArgs {
   AdjList nz;          // TC_MODE_ADJ: the non-zero words as a list (internal.cuh)
   uint8_t* covered;    // fused greedy: covered[p] = 1 for every in-ball pair (may be null)
   unsigned long long* trace;   // diagnostics: [grid][16] %globaltimer stamps (null: off)
+  unsigned long long* wtrace;  // diagnostics: [grid][16] wait cycles per role (null: off)
   // tile-level pruning (cells.cu; all null when off): A rows are permuted
   // (row r is point row_pt[r]); columns are the tile's landmarks sorted by
   // cell (key position lpos0 + col_pos[j]); a 256-column tile / 32-column
@@ -85,8 +86,9 @@ struct TcArgs {
   // skipped (no MMA / no TMEM read)
   const int32_t* row_pt;
   const int32_t* col_pos;
-  const uint32_t* act;     // [row block][act_words]: bit 8 t + c = chunk c of tile t is live
-  int act_words;           // words per row block (tiles / 4 rounded up, <= 8)
+  const uint32_t* act;     // [row block][1 + act_words]: word 0 bit t = tile t is live; then
+                           //   bit 8 t + c of the chunk words = chunk c of tile t is live
+  int act_words;           // chunk words per row block (tiles / 4 rounded up, <= 8)
   const uint32_t* act_bmask;   // its inputs (cells.cu), folded by the landmark-operand
   const uint32_t* act_cmask;   //   launch of each greedy tile
   const uint32_t* act_tmask;
