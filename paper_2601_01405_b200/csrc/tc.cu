@@ -721,10 +721,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           // (tf32 without resident B: the tile's in-test offsets d_j, read by
           // the epilogue's classification, land in the same slot)
           if constexpr (S::COLSLOT) {
-            mbar_expect_tx(&c_full[buf], (uint32_t)S::COL_BYTES);
-            bulk_load(scol + buf * BN,
-                      FOLD ? (const void*)(args.col_a + t * BN) : (const void*)(args.col_c + t * BN),
-                      (uint32_t)S::COL_BYTES, &c_full[buf]);
+            if (lane == 0) {   // one thread of the (convergent) MMA warp
+              mbar_expect_tx(&c_full[buf], (uint32_t)S::COL_BYTES);
+              bulk_load(scol + buf * BN,
+                        FOLD ? (const void*)(args.col_a + t * BN)
+                             : (const void*)(args.col_c + t * BN),
+                        (uint32_t)S::COL_BYTES, &c_full[buf]);
+            }
+            __syncwarp();
           }
           const uint32_t dcol = tmem + (uint32_t)(buf * BUFCOLS);
           // the last tile of a ragged column range issues a narrower MMA
