@@ -61,9 +61,6 @@ class ClockSampler:
         self.path = os.path.join("/tmp", f"bm_clocks_{os.getpid()}.csv")
 
     def start(self):
-        if os.environ.get("BM_NO_CLOCKS"):   # diagnostics: run without the sampler
-            self.proc = None
-            return
         try:
             self.f = open(self.path, "w")
             self.proc = subprocess.Popen(

@@ -162,12 +162,10 @@ __device__ __forceinline__ void pairs_block(const PairArgs& A, uint2* sl, int32_
   using acc_t = typename KindTraits<KIND>::acc_t;
   const int nu = NU > 0 ? NU : A.nu;
   const int tid = threadIdx.x, lane = tid & 31;
-  // prefilter: shared memory holds the quantised landmark rows of a whole
-  // 1024-landmark tile and, behind them, their fp32 rows for the rare exact
-  // check (a global load there stalls the warp for a memory round trip on
-  // every candidate group); otherwise the fp32 rows
+  // prefilter: shared memory holds only the quantised landmark rows (the rare
+  // exact check reads the landmark's fp32 row from global memory), so a whole
+  // 1024-landmark tile is staged at once; otherwise the fp32 rows
   uint32_t* sq = reinterpret_cast<uint32_t*>(sl);
-  const uint2* sfr = reinterpret_cast<const uint2*>(sq + (QF ? LC * NQ : 0));   // [LC][nu]
   // bias 2^15 - thr (thr > 2^15: the filter cannot prove anything, bias 0
   // makes every pair a candidate: SADs stay below 2^14 for d <= 64)
   uint32_t qbase = 0u;
@@ -195,8 +193,6 @@ __device__ __forceinline__ void pairs_block(const PairArgs& A, uint2* sl, int32_
     if constexpr (QF) {
 #pragma unroll
       for (int w = 0; w < NQ; ++w) qq[r][w] = act[r] ? A.qrows[qp[r] * NQ + w] : 0u;
-      // the exact check of a candidate reads this fp32 row: bring it into L1 now
-      if (act[r]) asm volatile("prefetch.global.L1 [%0];" ::"l"(src));
     }
     qn[r] = (KIND == K_L2I && act[r]) ? A.inorm[qp[r]] : 0;
   }
@@ -226,11 +222,6 @@ __device__ __forceinline__ void pairs_block(const PairArgs& A, uint2* sl, int32_
       for (int t = tid; t < nl8 * NQ; t += NT) {
         const int jj = min(t / NQ, nl - 1), w = t % NQ;
         sq[t] = A.qrows[(int64_t)A.lidx[lb + jj] * NQ + w];
-      }
-      uint2* sf = const_cast<uint2*>(sfr);
-      for (int t = tid; t < nl * nu; t += NT) {
-        const int jj = t / nu, u = t - jj * nu;
-        sf[t] = A.rows[(int64_t)A.lidx[lb + jj] * nu + u];
       }
     }
     __syncthreads();
@@ -291,8 +282,8 @@ __device__ __forceinline__ void pairs_block(const PairArgs& A, uint2* sl, int32_
           if (cls[r] == 3) {
             acc_t a = 0;
             const uint2* src = A.rows + qp[r] * (int64_t)nu;
-            const uint2* lrow = sfr + jj * nu;   // shared memory
-            for (int u = 0; u < nu; ++u) acc_unit<KIND>(a, __ldg(src + u), lrow[u]);
+            const uint2* lrow = A.rows + (int64_t)slp[jj] * nu;
+            for (int u = 0; u < nu; ++u) acc_unit<KIND>(a, __ldg(src + u), __ldg(lrow + u));
             cls[r] = classify<KIND>(a, qn[r], sln[jj], A.th);
           }
         }
@@ -447,8 +438,7 @@ cudaError_t launch_pairs_nu(const PairArgs& a, int64_t q_rows_max, cudaStream_t 
   // prefilter: a whole 1024-landmark tile of 8-bit rows per staging round
   constexpr int LC = NQ > 0 ? 1024 : (NU == 0 ? 32 : 64);
   constexpr int NT = 256;
-  size_t smem = NQ > 0 ? (size_t)LC * NQ * sizeof(uint32_t) + (size_t)LC * a.nu * sizeof(uint2)
-                       : (size_t)LC * a.nu * sizeof(uint2);
+  size_t smem = NQ > 0 ? (size_t)LC * NQ * sizeof(uint32_t) : (size_t)LC * a.nu * sizeof(uint2);
   auto kern = k_pairs<KIND, NU, R, MODE, LC, NQ>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
