@@ -50,6 +50,35 @@ static cudaError_t print_tc_wtrace(const unsigned long long* tr, int G, const ch
   return cudaSuccess;
 }
 
+// diagnostics (BM_TC_TRACE=3): CTA 0's per-tile timeline, mean cycles over
+// tiles 32..511: MMA wait for a free buffer, MMA issue, commit -> epilogue
+// sees the accumulator, epilogue hold of the buffer, tile period
+static cudaError_t print_tc_tline(const unsigned long long* tl, const char* tag, cudaStream_t s) {
+  std::vector<unsigned long long> h(512 * 5);
+  cudaError_t e = cudaMemcpyAsync(h.data(), tl, sizeof(unsigned long long) * 512 * 5,
+                                  cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return e;
+  double a[5] = {0, 0, 0, 0, 0};
+  int m = 0;
+  for (int i = 32; i + 1 < 512; ++i) {
+    const unsigned long long* r = &h[i * 5];
+    if (!r[0] || !r[4] || !h[(i + 1) * 5 + 3]) break;
+    a[0] += (double)(long long)(r[1] - r[0]);
+    a[1] += (double)(long long)(r[2] - r[1]);
+    a[2] += (double)(long long)(r[3] - r[2]);
+    a[3] += (double)(long long)(r[4] - r[3]);
+    a[4] += (double)(long long)(h[(i + 1) * 5 + 3] - r[3]);
+    ++m;
+  }
+  if (m)
+    fprintf(stderr,
+            "tline [%s] tiles %d | MMA wait buf %.0f | MMA issue %.0f | commit->epi %.0f | "
+            "epi hold %.0f | period %.0f clk\n",
+            tag, m, a[0] / m, a[1] / m, a[2] / m, a[3] / m, a[4] / m);
+  return cudaSuccess;
+}
+
 static cudaError_t print_tc_trace(const unsigned long long* tr, int G, const char* tag,
                                   cudaStream_t s) {
   std::vector<unsigned long long> h((size_t)G * 16);
@@ -969,8 +998,10 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
   // (A2 / A3 / B incl. landmark operands / A4), printed to stderr
   static const bool loop_prof = getenv("BM_LOOP_PROFILE") != nullptr;
   unsigned long long* tc_trace = nullptr;   // BM_TC_TRACE=1: stamp every membership launch
-  if (use_tc && getenv("BM_TC_TRACE")) TRY(pool.alloc(&tc_trace, (size_t)P.num_sms * 16));
-  const bool tc_wmode = tc_trace && atoi(getenv("BM_TC_TRACE")) == 2;
+  if (use_tc && getenv("BM_TC_TRACE"))
+    TRY(pool.alloc(&tc_trace, (size_t)P.num_sms * 16 + 512 * 5));
+  const bool tc_wmode = tc_trace && atoi(getenv("BM_TC_TRACE")) >= 2;
+  const bool tc_tline = tc_trace && atoi(getenv("BM_TC_TRACE")) == 3;
   std::vector<std::pair<int, cudaEvent_t>> lev;
   auto loop_mark = [&](int phase) {
     if (!loop_prof) return;
@@ -1098,9 +1129,10 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
                                         &launches));
         CK(mark_member());
         if (tc_trace) {   // diagnostics: phase stamps of this launch (synchronises)
-          CK(cudaMemsetAsync(tc_trace, 0, sizeof(unsigned long long) * P.num_sms * 16, s));
+          CK(cudaMemsetAsync(tc_trace, 0, sizeof(unsigned long long) * (P.num_sms * 16 + 512 * 5), s));
           if (tc_wmode) ta.wtrace = tc_trace;
           else ta.trace = tc_trace;
+          if (tc_tline) ta.tline = tc_trace + P.num_sms * 16;
         }
         CK(tc::launch_tc(prune ? Pm : P, ta, s, &launches));
         CK(mark_member());
@@ -1109,8 +1141,10 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
           snprintf(tag, sizeof tag, "membership tile %lld", (long long)tile);
           if (tc_wmode) CK(print_tc_wtrace(tc_trace, P.num_sms, tag, s));
           else CK(print_tc_trace(tc_trace, P.num_sms, tag, s));
+          if (tc_tline) CK(print_tc_tline(tc_trace + P.num_sms * 16, tag, s));
           ta.trace = nullptr;
           ta.wtrace = nullptr;
+          ta.tline = nullptr;
         }
       } else {
         PairArgs m = base;

@@ -2,21 +2,27 @@
 // contraction (d^2(q,x) = d^2(q,0) + d^2(x,0) - 2 sum_j q_j x_j,
 // with the norms "precomputed and stored").
 //
-// Structure (one persistent CTA per SM, 12 warps):
+// Structure (one persistent CTA per SM; 12 warps, or 20 for the lean tf32
+// membership instances):
 //   warp 0      TMA producer: the CTA's resident A block (RA x 128 point rows,
 //               all K atoms) once per work unit, then B (landmark) tiles of
-//               BN rows one 128-byte K atom per pipeline stage.
+//               BN rows one 128-byte K atom per pipeline stage (or, resident
+//               B, the launch's whole landmark operand once).
 //   warp 1      MMA issuer (one elected thread): tcgen05.mma kind::tf32 (fp32
 //               data pre-rounded to tf32) or kind::i8 (exact int32), A and B
 //               from 128B-swizzled K-major shared memory, D in TMEM; two TMEM
 //               accumulator buffers of RA x BN columns so the epilogue of tile
-//               t overlaps the MMAs of tile t+1.
+//               t overlaps the MMAs of tile t+1; tf32 adds one K=8 MMA per
+//               tile that folds the per-column constant into the accumulator.
 //   warp 2      TMEM allocator.
-//   warps 4-11  epilogue (two warpgroups, one half of each tile's columns each):
-//               tcgen05.ld 32 columns at a time, per pair one add and
-//               one max against a per-row / per-column constant ("out for sure"
-//               test); the rare survivors are classified in / band and staged
-//               in shared memory, flushed to global with one atomic per flush.
+//   warps 4..   epilogue warpgroups (2, or 4 when lean), each owning a slice of
+//               every tile's columns; warp w reads TMEM lanes 32 (w % 4)..:
+//               a max over the accumulators against a per-row constant is the
+//               "every pair out" test; the rare survivors are classified in /
+//               band and staged in shared memory, flushed to global with one
+//               atomic per flush.  Lean instances (tf32 membership, unpruned,
+//               e.g. C2 / C5 cosine): 32-column loads, the TMEM buffer released
+//               before staged keys are flushed and band pairs re-decided.
 // Float exactness: with x, l rounded to tf32 and fp32
 // accumulation, |acc - x.l| <= C (|x|^2 + |l|^2)/2 with a global constant C;
 // the per-row/per-column thresholds fold that bound in, so "out" and "in"
@@ -102,6 +108,19 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #define TC_TWAIT(k, stmt) \
   do {                    \
     stmt;                 \
+  } while (0)
+#endif
+// diagnostics (BM_TC_TRACE=3, diagnostic builds): CTA 0's clock64 at stage k
+// of tile i: 0 MMA before its buffer wait, 1 after it, 2 after the commit,
+// 3 epilogue warp 4 sees the accumulator, 4 it releases the buffer
+#ifdef BM_TC_WTRACE
+#define TC_TL(i, k)                                                               \
+  do {                                                                            \
+    if (args.tline && blockIdx.x == 0 && (i) < 512) args.tline[(i) * 5 + (k)] = clock64(); \
+  } while (0)
+#else
+#define TC_TL(i, k) \
+  do {              \
   } while (0)
 #endif
 // diagnostics: stamp slot k of this CTA (no-op unless a trace buffer is given)
@@ -277,8 +296,9 @@ constexpr uint32_t make_idesc(int M, int N) {
          ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
+// EG: epilogue warpgroups (2, or 4 for the lean tf32 membership instances)
 template <int RA, int BN, int KATOMS, int STAGES, int ABUF, bool FOLD, bool BRES = false,
-          int MODE = TC_MODE_MEMBER>
+          int MODE = TC_MODE_MEMBER, int EG = 2>
 struct Smem {
   static constexpr int A_ATOM = 128 * 128;                 // 128 rows x 128 B
   // ABUF == 0 (K streaming, wide rows): no resident A block; every stage
@@ -287,8 +307,9 @@ struct Smem {
   static constexpr int A_BYTES = KS ? 0 : RA * KATOMS * A_ATOM;   // one A buffer
   static constexpr int B_STAGE = BN * 128 + (KS ? A_ATOM : 0);
   static constexpr int B_BYTES = STAGES * B_STAGE;
-  static constexpr int EPI_WARPS = 8;                     // two epilogue warpgroups
-  static constexpr int KW = FOLD ? 64 : (KATOMS > 4 ? 96 : 128);  // staging slots per warp
+  static constexpr int EPI_WARPS = 4 * EG;                // epilogue warpgroups x 4
+  // staging slots per warp (the same total for 2 or 4 groups)
+  static constexpr int KW = (FOLD ? 64 : (KATOMS > 4 ? 96 : 128)) * 2 / EG;
   static constexpr int BW = KW;
   static constexpr int NBUF = 512 / (RA * BN);              // TMEM accumulator buffers
   // fold tiles (tf32): A ones [128 rows x 32 B], B constants [2 slots][BN rows x 32 B]
@@ -302,12 +323,58 @@ struct Smem {
   static constexpr int BAR_OFF = COL_OFF + (COLSLOT ? NBUF * COL_BYTES : 0);
   static constexpr int NBARS = 2 * STAGES + 2 * ABUF + 3 * NBUF + 5;
   static constexpr int CNT_OFF = BAR_OFF + NBARS * 8;     // tmem slot + per-warp counts
-  static constexpr int BUF_OFF = CNT_OFF + 128;
+  static constexpr int BUF_OFF = CNT_OFF + 256;   // tmem slot + 2 x 16 warp counts
   // resident B (tf32): the launch's in-test offsets d_j, staged once for the rare path
   static constexpr int DJ_OFF = (BUF_OFF + EPI_WARPS * (KW + BW) * 8 + 15) & ~15;
   static constexpr int DJ_BYTES = (BRES && FOLD) ? STAGES * BN * 4 : 0;
   static constexpr int TOTAL = DJ_OFF + DJ_BYTES + 1024;  // + align slack
 };
+
+// 32 consecutive columns of the warp's 32 TMEM lanes
+__device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+        "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait32(uint32_t (&v)[32]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+      : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7]),
+        "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]), "+r"(v[12]), "+r"(v[13]), "+r"(v[14]), "+r"(v[15]),
+        "+r"(v[16]), "+r"(v[17]), "+r"(v[18]), "+r"(v[19]), "+r"(v[20]), "+r"(v[21]), "+r"(v[22]), "+r"(v[23]),
+        "+r"(v[24]), "+r"(v[25]), "+r"(v[26]), "+r"(v[27]), "+r"(v[28]), "+r"(v[29]), "+r"(v[30]), "+r"(v[31])
+      :
+      : "memory");
+}
+
+// 3-input max (one FMNMX3); inline PTX keeps the caller's reduction tree as
+// written (the compiler re-associates fmaxf chains into two long chains)
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+
+// max of 32 accumulators: four independent 3-input chains
+__device__ __forceinline__ float max32(const uint32_t (&v)[32]) {
+  float m[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    m[k] = fmax3(__uint_as_float(v[k]), __uint_as_float(v[4 + k]), __uint_as_float(v[8 + k]));
+#pragma unroll
+  for (int i = 12; i < 28; i += 8) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      m[k] = fmax3(m[k], __uint_as_float(v[i + k]), __uint_as_float(v[i + 4 + k]));
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) m[k] = fmaxf(m[k], __uint_as_float(v[28 + k]));
+  return fmax3(fmax3(m[0], m[1], m[2]), m[3], m[3]);
+}
 
 // v[i] for a run-time i in [0, 32) without local memory: a 5-level select tree
 __device__ __forceinline__ uint32_t sel32(const uint32_t (&v)[32], int i) {
@@ -379,7 +446,7 @@ __device__ __noinline__ bool pair_in_fp64(const float* xrows, int xstride, int d
 }
 
 // ------------------------------------------------------------------ kernel
-constexpr int TC_THREADS = 384;   // warps 0-3 roles, 4-11 epilogue
+// warps 0-3 roles, 4.. epilogue (two or four warpgroups, tc_groups below)
 
 // BRES (B resident): the launch's whole landmark operand (<= STAGES tiles of
 // one K atom) and its fold constants are loaded once per CTA and stay in
@@ -388,9 +455,29 @@ constexpr int TC_THREADS = 384;   // warps 0-3 roles, 4-11 epilogue
 // bounded by the L2 slices that hold them (measured: C5 cosine, d = 16).
 // PR: the launch is pruned (cells.cu; args.act, row_pt, col_pos set) — a
 // separate instance, so the unpruned kernels carry none of its code.
+// Epilogue warpgroups of an instance: the lean tf32 membership instances (the
+// TMEM-read-latency-bound small-d contractions, e.g. C5 cosine at d = 16) run
+// four, so that each SM sub-partition has four warps' loads in flight
+template <int KIND, int BN, int MODE, bool PR>
+constexpr bool tc_lean() {
+#ifdef BM_TC_NOLEAN   // A/B diagnostics: every instance on the generic epilogue
+  return false;
+#else
+  return KIND == TC_TF32 && MODE == TC_MODE_MEMBER && !PR && BN == 256;
+#endif
+}
+template <int KIND, int BN, int MODE, bool PR>
+constexpr int tc_groups() {
+  return tc_lean<KIND, BN, MODE, PR>() ? 4 : 2;
+}
+template <int KIND, int BN, int MODE, bool PR>
+constexpr int tc_threads() {
+  return 128 + 128 * tc_groups<KIND, BN, MODE, PR>();
+}
+
 template <int KIND, int RA, int BN, int KATOMS, int STAGES, int ABUF, int MODE, bool BRES,
           bool PR>
-__global__ void __launch_bounds__(TC_THREADS, 1)
+__global__ void __launch_bounds__(tc_threads<KIND, BN, MODE, PR>(), 1)
     k_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
          const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmO,
          TcArgs args) {
@@ -398,7 +485,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   // MMA per tile (ones x {-cb_hi, -cb_mid, -cb_lo}), so the epilogue's test is
   // a plain max over the accumulators
   constexpr bool FOLD = KIND == TC_TF32 && MODE != TC_MODE_GRAM;
-  using S = Smem<RA, BN, KATOMS, STAGES, ABUF, FOLD, BRES, MODE>;
+  // LEAN (tf32 membership, unpruned, BN = 256): four epilogue groups, each
+  // reads its 64 columns of a tile in one load and releases the TMEM buffer
+  // before classifying
+  constexpr bool LEAN = tc_lean<KIND, BN, MODE, PR>();
+  constexpr int EG = tc_groups<KIND, BN, MODE, PR>();
+  using S = Smem<RA, BN, KATOMS, STAGES, ABUF, FOLD, BRES, MODE, EG>;
   static_assert(!BRES || KATOMS == 1, "resident B: one K atom per tile");
   constexpr int BUFCOLS = RA * BN;
   constexpr int NBUF = 512 / BUFCOLS;   // TMEM accumulator buffers (2 at BN=256, 4 at BN=128)
@@ -456,7 +548,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
     for (int b = 0; b < NBUF; ++b) {
       mbar_init(&t_full[b], 1);
-      mbar_init(&t_empty[b], 8);   // all 8 epilogue warps drain every buffer
+      mbar_init(&t_empty[b], S::EPI_WARPS);   // every epilogue warp drains every buffer
       mbar_init(&c_full[b], 1);
     }
     mbar_init(&bk_full[0], 1);
@@ -715,7 +807,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             continue;
           }
           ++n_run;
+          if (lane == 0) TC_TL(tk, 0);
           TC_TWAIT(3, mbar_wait(&t_empty[buf], (use[buf] & 1u) ^ 1u));
+          if (lane == 0) TC_TL(tk, 1);
           fence_after();
           // int8: the tile's per-column constants c_j into this buffer's slot
           // (tf32 without resident B: the tile's in-test offsets d_j, read by
@@ -744,13 +838,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             }
             const uint32_t bbase = su32(sB + t * S::B_STAGE);
             const uint32_t abase = su32(sAb);
+#ifndef BM_TC_DIAG_NODATA
 #pragma unroll
             for (int ks = 0; ks < 4; ++ks)
               if (ks < ksteps)
                 mma_w<KIND>(dcol, sdesc(abase + ks * 32), sdesc(bbase + ks * 32), idesc,
                           ks != 0 ? 1u : 0u);
+#endif
+#ifndef BM_TC_DIAG_NOFOLD
             if constexpr (FOLD)
               mma_w<KIND>(dcol, sdesc32(su32(sAK)), sdesc32(su32(sBK + t * S::BK_SLOT)), idesc, 1u);
+#endif
           }
           for (int ka = 0; ka < n_atoms && !BRES; ++ka) {
             TC_TWAIT(4, mbar_wait(&full[stage], phase));
@@ -780,8 +878,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             mma_w<KIND>(dcol, sdesc32(su32(sAK)), sdesc32(su32(sBK + sl * S::BK_SLOT)), idesc, 1u);
             commit_w(&bk_empty[sl]);
           }
-          ++tk;
           commit_w(&t_full[buf]);
+          if (lane == 0) TC_TL(tk, 2);
+          ++tk;
           ++use[buf];
           buf = buf + 1 == NBUF ? 0 : buf + 1;
         }
@@ -805,8 +904,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // resident B: the in-test offsets of all the launch's columns in shared memory
     float* sdj = reinterpret_cast<float*>(sm + S::DJ_OFF);
     if constexpr (S::DJ_BYTES > 0) {
-      for (int64_t j = threadIdx.x - 128; j < n_tiles * BN; j += 256) sdj[j] = __ldg(args.col_a + j);
-      asm volatile("bar.sync 1, 256;" ::: "memory");   // the 8 epilogue warps only
+      for (int64_t j = threadIdx.x - 128; j < n_tiles * BN; j += 128 * EG)
+        sdj[j] = __ldg(args.col_a + j);
+      asm volatile("bar.sync 1, %0;" ::"n"(128 * EG) : "memory");   // the epilogue warps only
     }
     unsigned long long* kb = kbuf + ew * S::KW;
     unsigned long long* bb = bbuf + ew * S::BW;
@@ -880,6 +980,96 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         recheck(key);
       }
     };
+    if constexpr (LEAN) {
+      // ---- lean tf32 membership epilogue (four groups; group g owns columns
+      // [g BN/4, (g + 1) BN/4) of every tile, warp q TMEM lanes 32 q ..).  Per
+      // tile: BN/128 32-column loads, a max over the accumulators (the column
+      // constant is folded into the MMA, so "every pair is out" is one
+      // compare), one vote; only a warp with a candidate re-reads its columns
+      // and classifies them.  32-bit state, 32 data registers: the 640-thread
+      // CTA stays within 96 registers without spills.
+      constexpr int NL = BN / EG / 32;   // 32-column loads per tile and warp
+      const long long epi_t0 = args.wtrace ? clock64() : 0;
+      uint32_t phase = 0;
+      uint32_t tcnt = 0;
+      const uint32_t tlane = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(grp * (BN / EG));
+      float nlo = 0.f, nhi = 0.f;
+      auto lrows = [&](int64_t u) {
+        if (u < n_units) {
+          const int64_t pr = (u / n_chunks) * 128 + q * 32 + lane;
+          nlo = __ldcg(args.row_lo + pr);
+          nhi = __ldcg(args.row_hi + pr);
+        }
+      };
+      lrows(blockIdx.x);
+      for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
+        const int64_t mb = u / n_chunks, ch = u % n_chunks;
+        const int t0 = (int)(ch * tiles_per_chunk), t1 = (int)min(n_tiles, t0 + tiles_per_chunk);
+        const int64_t prow = mb * 128 + q * 32 + lane;
+        const float rlo = nlo, rhi = nhi;
+        lrows(u + gridDim.x);
+        for (int t = t0; t < t1; ++t) {
+          const uint32_t buf = tcnt & (uint32_t)(NBUF - 1);
+          TC_TWAIT(5, mbar_wait(&t_full[buf], (phase >> buf) & 1u));
+          if (ew == 0 && lane == 0) TC_TL(tcnt, 3);
+          phase ^= 1u << buf;
+          fence_after();
+          const uint32_t ta = tlane + buf * (uint32_t)BUFCOLS;
+          uint32_t v[32];
+          float mx;
+          TC_TWAIT(6, tmem_ld32_nowait(ta, v); tmem_wait32(v));
+          mx = max32(v);
+          if constexpr (NL == 2) {
+            TC_TWAIT(6, tmem_ld32_nowait(ta + 32u, v); tmem_wait32(v));
+            mx = fmaxf(mx, max32(v));
+          }
+          // (columns past a ragged last tile hold stale values: they only send
+          // the warp down the rare path, which classifies columns < n_cols)
+#ifdef BM_TC_DIAG   // timing experiments only (results invalid): no rare path
+          if (false) {
+#else
+          if (__any_sync(FULLM, mx > rlo)) {
+#endif
+            // rare path: re-read the chunks (32 data registers keep the
+            // 640-thread CTA spill-free), candidates (not certainly out)
+            // become keys (certainly in) or staged band pairs (B')
+            for (int k = 0; k < NL; ++k) {
+              const int64_t j0 = (int64_t)t * BN + grp * (BN / EG) + k * 32;
+              if (j0 >= n_cols) break;
+              tmem_ld32_nowait(ta + 32u * k, v);
+              tmem_wait32(v);
+              uint32_t cand = 0u;
+#pragma unroll
+              for (int i = 0; i < 32; ++i) cand |= (__uint_as_float(v[i]) > rlo ? 1u : 0u) << i;
+              if (prow >= args.n || j0 + 32 > n_cols)   // padding rows / columns never qualify
+                cand &= prow >= args.n ? 0u : (uint32_t)((1ull << (n_cols - j0)) - 1ull);
+              while (cand) {
+                const int i = __ffs(cand) - 1;
+                cand &= cand - 1u;
+                const int64_t j = j0 + i;
+                const float dji = S::DJ_BYTES > 0 ? sdj[j] : __ldg(args.col_a + j);
+                if (__uint_as_float(sel32(v, i)) - dji > rhi) {
+                  if (args.covered) args.covered[prow] = 1;
+                  append(1, ((unsigned long long)prow << args.lbits) |
+                                (unsigned long long)(lpos0 + j));
+                } else {
+                  append(2, ((unsigned long long)prow << 32) | (unsigned long long)j);
+                }
+              }
+            }
+          }
+          // the buffer goes back to the MMA issuer before any staged keys are
+          // written out and band pairs re-decided (global atomics, fp64 rows)
+          fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&t_empty[buf]);
+          if (ew == 0 && lane == 0) TC_TL(tcnt, 4);
+          ++tcnt;
+          if (*kc > S::KW / 2 || *bc > S::BW / 2) TC_TWAIT(7, flush());
+        }
+      }
+      if (args.wtrace) wacc[8] += clock64() - epi_t0;
+    }
     uint32_t phase = 0;   // bit b: parity of the next completion of buffer b
     int64_t tcount = 0;   // tiles seen, in the MMA issuer's order (buffer = tcount % NBUF)
     // row constants of the next unit are loaded one unit ahead
@@ -905,7 +1095,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     unsigned long long ck_run = 0ull, ck_skip = 0ull;   // chunks of this warp's rows
     ActW act_next = act_of_full(blockIdx.x);
     const long long epi_t0 = args.wtrace ? clock64() : 0;
-    for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
+    for (int64_t u = LEAN ? n_units : (int64_t)blockIdx.x; u < n_units; u += gridDim.x) {
       const int64_t mb = u / n_chunks, ch = u % n_chunks;
       const ActW uact = act_next;
       act_next = act_of_full(u + gridDim.x);
@@ -939,6 +1129,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const int buf = (int)(tcount % NBUF);
         const uint32_t ph = (phase >> buf) & 1u;    // parity of buffer buf's next fill
         TC_TWAIT(5, mbar_wait(&t_full[buf], ph));
+        if (ew == 0 && lane == 0) TC_TL(tcount, 3);
         if (tcount < 2 && q == 0 && lane == 0) TC_STAMP(7 + grp);
         if constexpr (S::COLSLOT) TC_TWAIT(5, mbar_wait(&c_full[buf], ph));
         phase ^= 1u << buf;
@@ -952,7 +1143,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         // chunks the (possibly narrower) MMA of this tile wrote, this group's half
         const int64_t left = n_cols - t * BN;
         const int nch = RA == 1 && left < BN ? (int)((left + 31) / 32) : NCH;
-        const int cbeg = grp * (NCH / 2), cend = min(nch, (grp + 1) * (NCH / 2));
+        const int cbeg = grp * (NCH / EG), cend = min(nch, (grp + 1) * (NCH / EG));
         auto caddr = [&](int c) {
           return trow + (uint32_t)((c / (BN / 32)) * BN + (c % (BN / 32)) * 32);
         };
@@ -1165,10 +1356,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&t_empty[buf]);
+        if (ew == 0 && lane == 0) TC_TL(tcount, 4);
         ++tcount;
       }
     }
-    if (args.wtrace) wacc[8] += clock64() - epi_t0;
+    if (!LEAN && args.wtrace) wacc[8] += clock64() - epi_t0;
     flush();
     if (q == 0 && lane == 0) TC_STAMP(9 + grp);
     if (lane == 0) wflush(5, 9);
@@ -1243,7 +1435,7 @@ template <int KIND, int RA, int BN, int KATOMS, int STAGES, int ABUF, int MODE, 
           bool PR = false>
 static cudaError_t launch_cfg(const TcPlan& P, TcArgs a, cudaStream_t s) {
   constexpr bool FOLD = KIND == TC_TF32 && MODE != TC_MODE_GRAM;
-  using S = Smem<RA, BN, KATOMS, STAGES, ABUF, FOLD, BRES, MODE>;
+  using S = Smem<RA, BN, KATOMS, STAGES, ABUF, FOLD, BRES, MODE, tc_groups<KIND, BN, MODE, PR>()>;
   static_assert(S::TOTAL <= 232448, "shared memory");
   CUtensorMap tA, tB, tK, tO;
   cudaError_t e = make_tmap(&tA, P.xop, KIND, P.k_elems, P.n_rows, P.row_bytes, 128);
@@ -1274,7 +1466,8 @@ static cudaError_t launch_cfg(const TcPlan& P, TcArgs a, cudaStream_t s) {
     if (a.n_mblk * chunks < grid) grid = a.n_mblk * chunks;
   }
   if (grid < 1) grid = 1;
-  return launch_pdl(kern, dim3((unsigned)grid), dim3(TC_THREADS), (size_t)S::TOTAL, s, tA, tB,
+  return launch_pdl(kern, dim3((unsigned)grid), dim3(tc_threads<KIND, BN, MODE, PR>()),
+                    (size_t)S::TOTAL, s, tA, tB,
                     tK, tO, a);
 }
 
@@ -1290,9 +1483,9 @@ static cudaError_t launch_cfg(const TcPlan& P, TcArgs a, cudaStream_t s) {
 // resident B applies when every CTA's units share one column chunk (enough
 // point blocks: n_chunks = 1 for any column count) and the launch's columns
 // fit the stage ring (the fused greedy tile: <= 1024 columns)
-static bool bres_ok(const TcPlan& P, const TcArgs& a, int stages) {
+static bool bres_ok(const TcPlan& P, const TcArgs& a, int stages, int bn = 256) {
   const int64_t n_mblk = (P.n_rows + 127) / 128;
-  return n_mblk >= 4 * (int64_t)P.num_sms && (a.L + 255) / 256 <= stages;
+  return n_mblk >= 4 * (int64_t)P.num_sms && (a.L + bn - 1) / bn <= stages;
 }
 
 template <int MODE>

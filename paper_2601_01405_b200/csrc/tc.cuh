@@ -79,6 +79,7 @@ struct TcArgs {
   uint8_t* covered;    // fused greedy: covered[p] = 1 for every in-ball pair (may be null)
   unsigned long long* trace;   // diagnostics: [grid][16] %globaltimer stamps (null: off)
   unsigned long long* wtrace;  // diagnostics: [grid][16] wait cycles per role (null: off)
+  unsigned long long* tline;   // diagnostics: CTA 0's per-tile clock64 stamps [512][5] (null: off)
   // tile-level pruning (cells.cu; all null when off): A rows are permuted
   // (row r is point row_pt[r]); columns are the tile's landmarks sorted by
   // cell (key position lpos0 + col_pos[j]); a 256-column tile / 32-column
