@@ -121,10 +121,18 @@ typedef enum bm_select {
 
 /* bm_options.flags */
 #define BM_FLAG_NO_L1_PREFILTER 1   /* L1: score every pair in fp32 (no 8-bit SAD prefilter) */
-#define BM_FLAG_NO_EDGE_TRIANGLE 2  /* L > 4096: build edges by sort + unique, not the bit triangle */
+#define BM_FLAG_EDGE_POINT_PAIRS 2  /* L > 4096: D1 emits every witnessed pair per point (C(t_p, 2)),
+                                       not the row-union keys deduplicated per ball row item;
+                                       then the same sort + unique           */
+#define BM_FLAG_NO_EDGE_TRIANGLE BM_FLAG_EDGE_POINT_PAIRS   /* (former name)                 */
 #define BM_FLAG_NO_PRUNE 4          /* tensor path: no tile-level pruning of the membership contraction */
 #define BM_FLAG_FORCE_PRUNE 8       /* tensor path: prune even below the size where it pays (tests) */
 #define BM_FLAG_DENSE_RESOLVE 16    /* tiles > 1024: resolve from the dense words, not the sparse list (tests) */
+#define BM_FLAG_EDGE_TRIANGLE 32    /* L > 4096: edges from a strictly-upper L x L bit triangle (no
+                                       sort) when it fits in a quarter of free HBM (<= 8 GiB);
+                                       default only while it is <= 256 MiB                    */
+#define BM_FLAG_EDGE_ROWS 64        /* L > 4096: D1 always by row union (default: only when the
+                                       witnessed pairs are >= 512 per landmark)                */
 
 /*
  * Result of one cover construction.  All arrays are owned by the library and

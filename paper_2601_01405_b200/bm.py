@@ -26,10 +26,13 @@ AGG = {"mean": 0, "median": 1, "trimmed": 2, "min": 3, "max": 4, "mode": 5, "var
        "range": 7}
 PATH = {"auto": 0, "cuda_core": 1, "tensor": 2}
 FLAG_NO_L1_PREFILTER = 1
-FLAG_NO_EDGE_TRIANGLE = 2
+FLAG_EDGE_POINT_PAIRS = 2
+FLAG_NO_EDGE_TRIANGLE = FLAG_EDGE_POINT_PAIRS   # (former name)
 FLAG_NO_PRUNE = 4
 FLAG_FORCE_PRUNE = 8
 FLAG_DENSE_RESOLVE = 16
+FLAG_EDGE_TRIANGLE = 32
+FLAG_EDGE_ROWS = 64
 STEPS = ("prep", "greedy", "member", "csr", "edges", "total", "member_kernel", "select")
 
 EXPORTED = ("bm_cover_build", "bm_cover_build_ex", "bm_cover_build_host", "bm_free",

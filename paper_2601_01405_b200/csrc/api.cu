@@ -422,6 +422,14 @@ int64_t tc_row_bytes(int d, int esz) {
 }
 
 // D: the bit-triangle edge path when it fits min(8 GiB, free / 4) of HBM
+// D1 row-union emission pays when the witnessed pairs repeat across the
+// points two balls share: at least this many pairs per landmark (C5: ~2000,
+// C3 eps=8: 265, where the per-point emission is faster)
+constexpr int64_t kRowsMinPairs = 512;
+// the bit triangle is the default while it stays this small (L <~ 46000: its
+// random atomics then mostly hit L2; C4's L = 7935 takes 8 MB)
+constexpr double kTriAutoBytes = 256.0 * (1 << 20);
+
 bool use_tri_bitmap(int64_t L, int flags) {
   if (flags & BM_FLAG_NO_EDGE_TRIANGLE) return false;
   const double bytes = 4.0 * (double)bm::tri_bitmap_words(L);
@@ -1343,7 +1351,9 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
     pe_pending = true;
     pool.free_now(bits);
     pool.free_now(etemp);
-  } else if (L >= 2 && use_tri_bitmap(L, o.flags)) {
+  } else if (L >= 2 && !(o.flags & (BM_FLAG_EDGE_POINT_PAIRS | BM_FLAG_EDGE_ROWS)) &&
+             ((o.flags & BM_FLAG_EDGE_TRIANGLE) || 4.0 * (double)tri_bitmap_words(L) <= kTriAutoBytes) &&
+             use_tri_bitmap(L, o.flags)) {
     // strictly-upper bit triangle: no pair buffer, no sort (edges.cu)
     uint32_t* bits = nullptr;
     int64_t *rcnt = nullptr, *roff = nullptr;
@@ -1368,51 +1378,116 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
     pool.free_now(roff);
     pool.free_now(stemp);
   } else if (L >= 2) {
-    int64_t *pcnt = nullptr, *poff = nullptr;
+    // D1 -> D2 radix sort -> D3 unique.  D1 is the row-union emission
+    // (deduplicated per ball row item) when the points' landmark rows repeat
+    // their pairs enough for it to pay (P >= kRowsMinPairs L: C5), else the
+    // per-point emission of every witnessed pair (C3)
+    int64_t *pcnt = nullptr, *poff = nullptr, *icnt = nullptr, *ioff = nullptr;
     void* stemp = nullptr;
     TRY(pool.alloc(&pcnt, (size_t)n));
     TRY(pool.alloc(&poff, (size_t)n));
-    TRY(pool.alloc((uint8_t**)&stemp, scan_temp_bytes(n)));
+    TRY(pool.alloc((uint8_t**)&stemp, scan_temp_bytes(n > L ? n : L)));
     CK(launch_pair_counts(pt_ptr, n, pcnt, s, &launches));
     CK(exclusive_scan_i64(pcnt, poff, n, stemp, ptot, s, &launches));
     CK(cudaMemcpyAsync(&NP, ptot, sizeof NP, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     tr("edges count");
-    if (NP > 0) {
-      unsigned long long *ek = nullptr, *ea = nullptr;
-      int32_t* etmp = nullptr;
-      void *et = nullptr, *ct = nullptr;
-      TRY(pool.alloc(&ek, (size_t)NP));
-      TRY(pool.alloc(&ea, (size_t)NP));
-      TRY(pool.alloc((uint8_t**)&et, radix_temp_bytes(NP)));
-      tr("edges alloc");
-      CK(launch_pair_emit(pt_ptr, pt_lm, n, poff, lbits, ek, s, &launches));
-      tr("edges emit");
-      const BitRange er[1] = {{0, 2 * lbits}};
-      CK(radix_sort_u64(&ek, &ea, NP, er, 1, et, s, &launches));
-      tr("edges sort");
-      pool.free_now(et);
-      etmp = (int32_t*)ea;   // the sort's spare buffer holds 2 NP int32
-      TRY(pool.alloc((uint8_t**)&ct, edge_lb_temp_bytes(NP)));
-      CK(launch_unique_compact(ek, NP, lbits, etmp, ptot + 1, ct, s, &launches));
-      tr("edges: compact launched");
-      CK(cudaMemcpyAsync(&E, ptot + 1, sizeof E, cudaMemcpyDeviceToHost, s));
+    const bool rows = !(o.flags & BM_FLAG_EDGE_POINT_PAIRS) &&
+                      ((o.flags & BM_FLAG_EDGE_ROWS) || NP >= kRowsMinPairs * L);
+    unsigned long long* kc = nullptr;   // [0] keys emitted, [1] pairs met
+    int64_t n_items = 0;
+    if (rows && NP > 0) {
+      TRY(pool.alloc(&icnt, (size_t)L));
+      TRY(pool.alloc(&ioff, (size_t)L));
+      TRY(pool.alloc(&kc, 2));
+      CK(cudaMemsetAsync(kc, 0, 2 * sizeof(unsigned long long), s));
+      CK(launch_row_items(ball_ptr, L, icnt, s, &launches));
+      CK(exclusive_scan_i64(icnt, ioff, L, stemp, ptot + 1, s, &launches));
+      CK(cudaMemcpyAsync(&n_items, ptot + 1, sizeof n_items, cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
-      tr("edges: E readback");
-      TRY(pool.alloc(&edges, (size_t)(2 * E > 0 ? 2 * E : 1)));
-      tr("edges: alloc exact");
-      if (E > 0)
-        CK(cudaMemcpyAsync(edges, etmp, sizeof(int32_t) * 2 * E, cudaMemcpyDeviceToDevice, s));
-      tr("edges: copy");
-      pool.free_now(ek);
-      tr("edges: free ek");
-      pool.free_now(ea);
-      tr("edges: free ea");
-      pool.free_now(ct);
+    }
+    if (rows) {
+      if (NP > 0) {
+        unsigned long long *ek = nullptr, *ea = nullptr;
+        int32_t* irow = nullptr;
+        TRY(pool.alloc(&irow, (size_t)n_items));
+        CK(launch_item_rows(ioff, icnt, L, irow, s, &launches));
+        TRY(pool.alloc(&ek, (size_t)NP));   // at most one key per witnessed pair
+        CK(launch_row_pairs(ball_ptr, ball_idx, pt_ptr, pt_lm, n, L, ioff, irow, n_items, lbits, ek,
+                            NP, kc, kc + 1, s, &launches));
+        int64_t NK = 0, NV = 0;
+        CK(cudaMemcpyAsync(&NK, kc, sizeof NK, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(&NV, kc + 1, sizeof NV, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (getenv("BM_ROWS_TRACE"))
+          fprintf(stderr, "rows: L %lld M %lld items %lld pairs %lld visits %lld keys %lld\n",
+                  (long long)L, (long long)M, (long long)n_items, (long long)NP, (long long)NV,
+                  (long long)NK);
+        tr("edges: row pairs");
+        if (NK > NP || NV != NP)
+          return set_err(BM_ECUDA, "row-union edge emission: %lld keys / %lld pairs met for %lld pairs",
+                         (long long)NK, (long long)NV, (long long)NP);
+        void *et = nullptr, *ct = nullptr;
+        TRY(pool.alloc(&ea, (size_t)(NK > 0 ? NK : 1)));
+        TRY(pool.alloc((uint8_t**)&et, radix_temp_bytes(NK)));
+        const BitRange er[1] = {{0, 2 * lbits}};
+        CK(radix_sort_u64(&ek, &ea, NK, er, 1, et, s, &launches));
+        pool.free_now(et);
+        // (2 NK int32 fit the sort's spare buffer of NK keys)
+        int32_t* etmp = (int32_t*)ea;
+        TRY(pool.alloc((uint8_t**)&ct, edge_lb_temp_bytes(NK)));
+        CK(launch_unique_compact(ek, NK, lbits, etmp, ptot + 1, ct, s, &launches));
+        CK(cudaMemcpyAsync(&E, ptot + 1, sizeof E, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        TRY(pool.alloc(&edges, (size_t)(2 * E > 0 ? 2 * E : 1)));
+        if (E > 0)
+          CK(cudaMemcpyAsync(edges, etmp, sizeof(int32_t) * 2 * E, cudaMemcpyDeviceToDevice, s));
+        tr("edges: rows sorted, unique");
+        pool.free_now(ek);
+        pool.free_now(ea);
+        pool.free_now(ct);
+        pool.free_now(irow);
+      }
+    } else {
+      if (NP > 0) {
+        unsigned long long *ek = nullptr, *ea = nullptr;
+        int32_t* etmp = nullptr;
+        void *et = nullptr, *ct = nullptr;
+        TRY(pool.alloc(&ek, (size_t)NP));
+        TRY(pool.alloc(&ea, (size_t)NP));
+        TRY(pool.alloc((uint8_t**)&et, radix_temp_bytes(NP)));
+        tr("edges alloc");
+        CK(launch_pair_emit(pt_ptr, pt_lm, n, poff, lbits, ek, s, &launches));
+        tr("edges emit");
+        const BitRange er[1] = {{0, 2 * lbits}};
+        CK(radix_sort_u64(&ek, &ea, NP, er, 1, et, s, &launches));
+        tr("edges sort");
+        pool.free_now(et);
+        etmp = (int32_t*)ea;   // the sort's spare buffer holds 2 NP int32
+        TRY(pool.alloc((uint8_t**)&ct, edge_lb_temp_bytes(NP)));
+        CK(launch_unique_compact(ek, NP, lbits, etmp, ptot + 1, ct, s, &launches));
+        tr("edges: compact launched");
+        CK(cudaMemcpyAsync(&E, ptot + 1, sizeof E, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        tr("edges: E readback");
+        TRY(pool.alloc(&edges, (size_t)(2 * E > 0 ? 2 * E : 1)));
+        tr("edges: alloc exact");
+        if (E > 0)
+          CK(cudaMemcpyAsync(edges, etmp, sizeof(int32_t) * 2 * E, cudaMemcpyDeviceToDevice, s));
+        tr("edges: copy");
+        pool.free_now(ek);
+        tr("edges: free ek");
+        pool.free_now(ea);
+        tr("edges: free ea");
+        pool.free_now(ct);
+      }
     }
     pool.free_now(pcnt);
     pool.free_now(poff);
     pool.free_now(stemp);
+    if (icnt) pool.free_now(icnt);
+    if (ioff) pool.free_now(ioff);
+    if (kc) pool.free_now(kc);
     tr("edges: frees");
   }
   if (!edges) TRY(pool.alloc(&edges, 1));

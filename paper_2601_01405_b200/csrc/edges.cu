@@ -181,6 +181,201 @@ __global__ void __launch_bounds__(UQ_NT) k_unique_compact(const unsigned long lo
   }
 }
 
+// ---------------------------------------------------------------- row-union emission
+// D1 for large L (the default above 4096 landmarks): the pairs (i, j), j > i,
+// are emitted landmark row by landmark row — row i's pairs are the entries
+// j > i of pt_lm[p] over the members p of ball i (each pair of a point's row
+// is met exactly once, at its smaller landmark) — and deduplicated in a
+// per-warp shared-memory hash set before they reach HBM.  A point's C(t_p, 2)
+// pairs repeat across the points two balls share (C3 eps=8: P = 1.4e8 pairs
+// for E = 1.8e7 edges), so the radix sort (D2) and the unique pass (D3) then
+// run on a few keys per edge instead of every witnessed pair.  A row is cut
+// into items of RP_CH members (a ball of 5e6 points is spread over ~1e4
+// warps); pairs an item repeats from another item of the same row are removed
+// by D3, like every other duplicate.
+constexpr int RP_CH = 512;                 // members per item
+#ifndef BM_RP_H
+#define BM_RP_H 1024
+#endif
+constexpr int RP_H = BM_RP_H;              // hash slots per warp
+constexpr int kRpBits = RP_H == 2048 ? 11 : 10;
+static_assert(RP_H == (1 << kRpBits), "RP_H: 1024 or 2048 slots");
+constexpr int RP_U = 4;                    // row entries per lane per step (128 per warp)
+constexpr uint32_t RP_EMPTY = 0xffffffffu;
+constexpr int RP_NT = 128, RP_NW = RP_NT / 32;
+
+__global__ void k_row_items(const int64_t* __restrict__ ball_ptr, int64_t L,
+                            int64_t* __restrict__ cnt) {
+  pdl_wait();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < L) cnt[i] = (ball_ptr[i + 1] - ball_ptr[i] + RP_CH - 1) / RP_CH;
+}
+
+// item -> landmark row (item_row[item_off[i] + k] = i)
+__global__ void k_item_rows(const int64_t* __restrict__ item_off, const int64_t* __restrict__ cnt,
+                            int64_t L, int32_t* __restrict__ item_row) {
+  pdl_wait();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= L) return;
+  const int64_t o = item_off[i], c = cnt[i];
+  for (int64_t k = 0; k < c; ++k) item_row[o + k] = (int32_t)i;
+}
+
+// the warp writes the keys (i << lbits | j) of its set (slots listed in the
+// insertion log) and empties those slots
+__device__ __forceinline__ void rp_flush(uint32_t* tab, const uint16_t* log, int fill, int64_t i,
+                                         int lbits, unsigned long long* __restrict__ keys,
+                                         int64_t cap, unsigned long long* kcount, int lane) {
+  __syncwarp();
+  unsigned long long base = 0;
+  if (lane == 0) base = atomicAdd(kcount, (unsigned long long)fill);
+  base = __shfl_sync(FME, base, 0);
+  const unsigned long long hi = (unsigned long long)i << lbits;
+  for (int k = lane; k < fill; k += 32) {
+    const uint32_t h = log[k];
+    const uint32_t v = tab[h];
+    if ((int64_t)(base + k) < cap) keys[base + k] = hi | v;
+    tab[h] = RP_EMPTY;
+  }
+  __syncwarp();
+}
+
+// One warp per item.  The item's members are taken 32 at a time; their rows
+// (pt_lm[p], t_p entries each) are walked as one flattened run of entries,
+// 128 per step over all 32 lanes (lane-parallel whatever the row lengths, and
+// consecutive entries of a row are consecutive loads).  Entries j > i go into
+// the warp's open-addressing set; every new key's slot is appended to an
+// insertion log, so a flush visits only the occupied slots.  The set is
+// flushed before a step could fill it (the probe always finds a free slot).
+__global__ void __launch_bounds__(RP_NT) k_row_pairs(
+    const int64_t* __restrict__ ball_ptr, const int32_t* __restrict__ ball_idx,
+    const int64_t* __restrict__ pt_ptr, const int32_t* __restrict__ pt_lm, int64_t n, int64_t L,
+    const int64_t* __restrict__ item_off, const int32_t* __restrict__ item_row, int64_t n_items,
+    int lbits, unsigned long long* __restrict__ keys, int64_t cap, unsigned long long* kcount,
+    unsigned long long* npairs) {
+  __shared__ uint32_t s_tab[RP_NW][RP_H];
+  __shared__ uint16_t s_log[RP_NW][RP_H];
+  pdl_wait();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  uint32_t* tab = s_tab[w];
+  uint16_t* log = s_log[w];
+  for (int k = lane; k < RP_H; k += 32) tab[k] = RP_EMPTY;
+  __syncwarp();
+  unsigned long long mine = 0ull;
+  const int64_t nwarps = (int64_t)gridDim.x * RP_NW;
+  for (int64_t it = (int64_t)blockIdx.x * RP_NW + w; it < n_items; it += nwarps) {
+    const int64_t i = item_row[it];
+    const int64_t m0 = ball_ptr[i] + (it - item_off[i]) * RP_CH;
+    const int64_t m1 = min(ball_ptr[i + 1], m0 + RP_CH);
+    int fill = 0;   // keys in the set (warp-uniform)
+    for (int64_t mb = m0; mb < m1; mb += 32) {
+      const int64_t m = mb + lane;
+      int64_t b = 0;
+      int t = 0;
+      if (m < m1) {
+        const int64_t p = ball_idx[m];
+        b = pt_ptr[p];
+        t = (int)(pt_ptr[p + 1] - b);
+      }
+      // exclusive prefix of the row lengths over the lanes, and the total
+      int pre = t;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(FME, pre, o);
+        if (lane >= o) pre += v;
+      }
+      const int T = __shfl_sync(FME, pre, 31);
+      pre -= t;
+      for (int g0 = 0; g0 < T; g0 += 32 * RP_U) {
+        if (fill > RP_H - 32 * RP_U - 1) {
+          rp_flush(tab, log, fill, i, lbits, keys, cap, kcount, lane);
+          fill = 0;
+        }
+        uint32_t jv[RP_U];
+#pragma unroll
+        for (int u = 0; u < RP_U; ++u) {
+          const int g = g0 + u * 32 + lane;
+          // member k of entry g: the last lane with pre_k <= g
+          int k = 0;
+#pragma unroll
+          for (int st = 16; st > 0; st >>= 1) {
+            const int pk = __shfl_sync(FME, pre, (k + st) & 31);
+            if (k + st < 32 && pk <= g) k += st;
+          }
+          const int64_t bk = __shfl_sync(FME, b, k);
+          const int pk = __shfl_sync(FME, pre, k);
+          jv[u] = g < T ? (uint32_t)pt_lm[bk + (g - pk)] : 0xffffffffu;
+        }
+        int cnt = 0;
+        uint32_t slot[RP_U];
+#pragma unroll
+        for (int u = 0; u < RP_U; ++u) {
+          slot[u] = 0xffffffffu;
+          const uint32_t j = jv[u];
+          if (j == 0xffffffffu || (int64_t)j <= i) continue;
+          ++mine;
+          uint32_t h = (j * 2654435761u) >> (32 - kRpBits);
+          uint32_t old;
+          while ((old = atomicCAS(&tab[h], RP_EMPTY, j)) != RP_EMPTY && old != j)
+            h = (h + 1) & (RP_H - 1);
+          if (old == RP_EMPTY) {
+            slot[u] = h;
+            ++cnt;
+          }
+        }
+        // log positions: exclusive prefix of the per-lane counts (0..RP_U)
+        const unsigned b0 = __ballot_sync(FME, cnt & 1), b1 = __ballot_sync(FME, cnt & 2),
+                       b2 = __ballot_sync(FME, cnt & 4);
+        int pos = fill + __popc(b0 & lt) + 2 * __popc(b1 & lt) + 4 * __popc(b2 & lt);
+#pragma unroll
+        for (int u = 0; u < RP_U; ++u)
+          if (slot[u] != 0xffffffffu) log[pos++] = (uint16_t)slot[u];
+        fill += __popc(b0) + 2 * __popc(b1) + 4 * __popc(b2);
+      }
+    }
+    if (fill > 0) rp_flush(tab, log, fill, i, lbits, keys, cap, kcount, lane);
+  }
+  for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(FME, mine, o);
+  if (lane == 0 && mine) atomicAdd(npairs, mine);
+}
+
+size_t row_items_temp_bytes(int64_t L) { return sizeof(int64_t) * (size_t)(2 * L + 2); }
+
+cudaError_t launch_row_items(const int64_t* ball_ptr, int64_t L, int64_t* cnt, cudaStream_t s,
+                             int64_t* launches) {
+  ++*launches;
+  const int64_t g = (L + 255) / 256;
+  return launch_pdl(k_row_items, dim3((unsigned)(g > 0 ? g : 1)), dim3(256), 0, s, ball_ptr, L,
+                    cnt);
+}
+
+cudaError_t launch_item_rows(const int64_t* item_off, const int64_t* cnt, int64_t L,
+                             int32_t* item_row, cudaStream_t s, int64_t* launches) {
+  ++*launches;
+  const int64_t g = (L + 255) / 256;
+  return launch_pdl(k_item_rows, dim3((unsigned)(g > 0 ? g : 1)), dim3(256), 0, s, item_off, cnt,
+                    L, item_row);
+}
+
+cudaError_t launch_row_pairs(const int64_t* ball_ptr, const int32_t* ball_idx,
+                             const int64_t* pt_ptr, const int32_t* pt_lm, int64_t n, int64_t L,
+                             const int64_t* item_off, const int32_t* item_row, int64_t n_items,
+                             int lbits, unsigned long long* keys, int64_t cap,
+                             unsigned long long* kcount, unsigned long long* npairs,
+                             cudaStream_t s, int64_t* launches) {
+  ++*launches;
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int64_t g = (n_items + RP_NW - 1) / RP_NW;
+  const int64_t per_sm = (int64_t)(200 * 1024) / (RP_NW * RP_H * 6);   // sets + logs per SM
+  if (g > (int64_t)sms * per_sm) g = (int64_t)sms * per_sm;
+  return launch_pdl(k_row_pairs, dim3((unsigned)(g > 0 ? g : 1)), dim3(RP_NT), 0, s, ball_ptr,
+                    ball_idx, pt_ptr, pt_lm, n, L, item_off, item_row, n_items, lbits, keys, cap,
+                    kcount, npairs);
+}
+
 // ---------------------------------------------------------------- bitmap CSR
 // Step C for moderate n * L: the membership keys (point << 32 | position) set
 // bit (p, j) of a point-major [n][Wp] and bit (j, p) of a landmark-major [L][Wl]

@@ -246,6 +246,18 @@ cudaError_t launch_unpack_high(const unsigned long long* keys, int64_t m, int32_
 cudaError_t launch_rekey_landmark_major(const unsigned long long* pm_keys, int64_t m, int lbits,
                                         int pbits, unsigned long long* out, cudaStream_t s,
                                         int64_t* launches);
+// D1 row-union emission (edges.cu): items of <= 512 members per landmark row
+size_t row_items_temp_bytes(int64_t L);
+cudaError_t launch_row_items(const int64_t* ball_ptr, int64_t L, int64_t* cnt, cudaStream_t s,
+                             int64_t* launches);
+cudaError_t launch_item_rows(const int64_t* item_off, const int64_t* cnt, int64_t L,
+                             int32_t* item_row, cudaStream_t s, int64_t* launches);
+cudaError_t launch_row_pairs(const int64_t* ball_ptr, const int32_t* ball_idx,
+                             const int64_t* pt_ptr, const int32_t* pt_lm, int64_t n, int64_t L,
+                             const int64_t* item_off, const int32_t* item_row, int64_t n_items,
+                             int lbits, unsigned long long* keys, int64_t cap,
+                             unsigned long long* kcount, unsigned long long* npairs,
+                             cudaStream_t s, int64_t* launches);
 cudaError_t launch_pair_counts(const int64_t* pt_ptr, int64_t n, int64_t* cnt, cudaStream_t s,
                                int64_t* launches);
 cudaError_t launch_pair_emit(const int64_t* pt_ptr, const int32_t* pt_lm, int64_t n,

@@ -19,6 +19,8 @@
 //
 // Descriptor words carry a per-launch tag and the state arrays are cleared
 // once per sort / scan call, so no per-pass reset is needed.
+#include <stdlib.h>
+
 #include "internal.cuh"
 
 namespace bm {
@@ -160,7 +162,11 @@ cudaError_t exclusive_scan_i64(const int64_t* in, int64_t* out, int64_t n, void*
 constexpr int RS_NT = 256, RS_BINS = 256;
 constexpr int RS_MAXP = 8;   // 64 bits / 8
 constexpr int64_t RS_SMALL = (int64_t)1 << 22;
-static inline int rs_rounds(int64_t n) { return n < RS_SMALL ? 4 : 16; }
+static inline int rs_rounds(int64_t n) {
+  static const int ov = getenv("BM_RS_ROUNDS") ? atoi(getenv("BM_RS_ROUNDS")) : 0;   // A/B diagnostics
+  if (ov == 4 || ov == 8 || ov == 16) return ov;
+  return n < RS_SMALL ? 4 : 16;
+}
 
 struct RsPasses {
   int np;
@@ -353,6 +359,10 @@ cudaError_t radix_sort_u64(unsigned long long** keys, unsigned long long** alt, 
   for (int p = 0; p < P.np; ++p) {
     if (rs_rounds(n) == 4)
       e = launch_pdl(k_rs_scatter<4>, dim3((unsigned)t), dim3(RS_NT), 0, s, *keys, *alt, n,
+                     P.shift[p], P.bits[p], (const int64_t*)(off + p * RS_BINS), state,
+                     tickets + p, (uint32_t)(p + 1));
+    else if (rs_rounds(n) == 8)
+      e = launch_pdl(k_rs_scatter<8>, dim3((unsigned)t), dim3(RS_NT), 0, s, *keys, *alt, n,
                      P.shift[p], P.bits[p], (const int64_t*)(off + p * RS_BINS), state,
                      tickets + p, (uint32_t)(p + 1));
     else

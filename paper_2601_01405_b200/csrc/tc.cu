@@ -319,7 +319,10 @@ struct Smem {
   static constexpr int COL_OFF = AK_OFF + (FOLD ? 128 * 32 + NBK * BK_SLOT : 0);
   static constexpr int COL_BYTES = BN * 4;   // per-buffer column constants: c_j (int8) / d_j (tf32)
   // (tf32 with resident B keeps every d_j of the launch in DJ below instead)
-  static constexpr bool COLSLOT = (MODE == TC_MODE_MEMBER || MODE == TC_MODE_ADJ) && !(FOLD && BRES);
+  // (the lean epilogue, EG == 4, reads a candidate's d_j from global memory and
+  // needs no slot: no copy may be left in flight when the CTA exits)
+  static constexpr bool COLSLOT =
+      (MODE == TC_MODE_MEMBER || MODE == TC_MODE_ADJ) && !(FOLD && BRES) && EG != 4;
   static constexpr int BAR_OFF = COL_OFF + (COLSLOT ? NBUF * COL_BYTES : 0);
   static constexpr int NBARS = 2 * STAGES + 2 * ABUF + 3 * NBUF + 5;
   static constexpr int CNT_OFF = BAR_OFF + NBARS * 8;     // tmem slot + per-warp counts

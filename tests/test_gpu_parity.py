@@ -273,20 +273,39 @@ def test_l1_prefilter_equivalence(bm, seed):
 
 
 @pytest.mark.parametrize("metric,eps", [("l2", 0.006), ("l1", 0.008), ("cos", 4e-5)])
-def test_edges_triangle_path(bm, metric, eps):
-    """L > 4096: the strictly-upper bit triangle (edges.cu) against the
-    sort + unique keys path and the oracle."""
+def test_edges_large_L_paths(bm, metric, eps):
+    """L > 4096: the default row-union emission (per-row-item dedup, sort,
+    unique), the per-point pair emission and the strictly-upper bit triangle
+    (edges.cu) agree with each other and with the oracle."""
     from paper_2601_01405_b200 import bm as B
     rng = np.random.default_rng(17)
     X = rng.random((12000, 3 if metric == "cos" else 2)).astype(np.float32)
     t = torch.from_numpy(X).cuda()
-    a = bm.cover_build(t, metric, eps)
-    b = bm.cover_build(t, metric, eps, flags=B.FLAG_NO_EDGE_TRIANGLE)
+    a = bm.cover_build(t, metric, eps, flags=B.FLAG_EDGE_ROWS)
+    b = bm.cover_build(t, metric, eps, flags=B.FLAG_EDGE_POINT_PAIRS)
+    c = bm.cover_build(t, metric, eps, flags=B.FLAG_EDGE_TRIANGLE)
     assert a.L > 4096 and a.E > 100, (a.L, a.E)
-    na, nb = a.numpy(), b.numpy()
+    na, nb, nc = a.numpy(), b.numpy(), c.numpy()
     for k in na:
         assert np.array_equal(na[k], nb[k]), k
+        assert np.array_equal(na[k], nc[k]), k
+    assert a.P == b.P == c.P
     compare(X, metric, eps, a, float_path=True)
+
+
+def test_edges_row_union_heavy_rows(bm):
+    """Row items: a ball of 3000 points (six items of 512 members) whose
+    points all lie in several other balls, plus a sparse remainder — every
+    (i, j) a heavy row repeats across its items must still come out once."""
+    rng = np.random.default_rng(23)
+    blob = (0.5 + 0.01 * rng.standard_normal((3000, 2))).astype(np.float32)
+    rest = rng.random((9000, 2)).astype(np.float32)
+    X = np.concatenate([blob, rest])[rng.permutation(12000)]
+    t = torch.from_numpy(X).cuda()
+    from paper_2601_01405_b200 import bm as B
+    a = bm.cover_build(t, "l2", 0.0075, flags=B.FLAG_EDGE_ROWS)
+    assert a.L > 4096, a.L
+    compare(X, "l2", 0.0075, a, float_path=True)
 
 
 @pytest.mark.parametrize("tile", [2048, 8192])
