@@ -516,6 +516,7 @@ void set_recheck(bm::tc::TcArgs& ta, const void* xrows, int xstride, int d, cons
   ta.eps = th.eps;
   ta.eps2 = th.eps2;
   ta.tie_rel = th.tie_rel;
+  ta.tie_abs = th.tie_rel * th.eps;
   ta.lm_idx = lm_idx;
   ta.cosine = th.cosine;
   ta.ties = ties;
@@ -716,9 +717,25 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
                 tc::tc_supported(P.kind, P.katoms) &&
                 (o.path == BM_PATH_TENSOR ||
                  (o.path == BM_PATH_AUTO && (d >= 32 || n >= 32768)));
+  // L1 (fp32, d <= 16) on tensor cores: a signed int8
+  // contraction of thermometer codes proves most pairs out, the rest pass the
+  // 8-bit SAD bound and the fp64 decision; needs the 8-bit rows.  Taken on
+  // request (BM_PATH_TENSOR) only: on C5 it measured 1.01-1.09 s against
+  // 1.00 s for the CUDA-core SAD path, which AUTO keeps.
+  const int l1t_B = (metric == BM_L1 && dtype == BM_F32) ? l1t_bytes_per_coord(d) : 0;
+  const bool use_l1t = l1t_B > 0 && l1q_words(d) > 0 && !(o.flags & BM_FLAG_NO_L1_PREFILTER) &&
+                       o.path == BM_PATH_TENSOR;
+  if (use_l1t) {
+    use_tc = true;
+    P.kind = tc::TC_S8;
+    P.row_bytes = ((int64_t)d * l1t_B + 6 + 127) / 128 * 128;
+    P.k_elems = P.row_bytes;
+    P.katoms = (int)(P.row_bytes / 128);
+  }
   if (o.path == BM_PATH_TENSOR && !use_tc)
     return set_err(BM_EUNSUPPORTED,
-                   "tensor-core path supports L2 and cosine with d*elem <= %d bytes",
+                   "tensor-core path supports L2 and cosine with d*elem <= %d bytes, "
+                   "and fp32 L1 with d <= 16",
                    4096);
 
   int64_t launches = 0;
@@ -762,17 +779,24 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
     int dev = 0;
     CK(cudaGetDevice(&dev));
     CK(cudaDeviceGetAttribute(&P.num_sms, cudaDevAttrMultiProcessorCount, dev));
-    CK(tc::launch_tc_prep(dpoints, dtype, n, d, P, tc_nrm, stats, s, &launches));
+    if (!use_l1t) CK(tc::launch_tc_prep(dpoints, dtype, n, d, P, tc_nrm, stats, s, &launches));
   }
   // L1: 8-bit quantised rows for the membership prefilter (exact decisions unchanged)
   uint32_t* qrows = nullptr;
   double* qparam = nullptr;
-  const int nq = kind == K_L1F ? l1q_words(d) : 0;
+  // (the tensor path reads whole 4-word rows: d <= 16 is zero padded to 4 words)
+  const int nq = kind == K_L1F ? (use_l1t ? 4 : l1q_words(d)) : 0;
   if (nq > 0 && !(o.flags & BM_FLAG_NO_L1_PREFILTER)) {
-    TRY(pool.alloc(&qrows, (size_t)n * nq));
+    // (rows padded to a multiple of 128: the tensor path copies whole 128-row
+    // blocks of them; the padding rows are never read as candidates)
+    TRY(pool.alloc(&qrows, (size_t)((n + 127) / 128 * 128) * nq));
     TRY(pool.alloc(&qparam, 4));
     CK(launch_l1_quantize((const float*)dpoints, n, d, nq, qparam, qrows, s, &launches));
   }
+  // ... and, on tensor cores, the thermometer operand over the same range
+  if (use_l1t)
+    CK(tc::launch_l1t_prep((const float*)dpoints, n, d, P, qparam, eps, (int32_t*)tc_nrm, s,
+                           &launches));
 
   if (host_in) pool.free_now((void*)dpoints);
 
@@ -874,6 +898,9 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
   base.d = d;
   base.th = th;
   base.stats = stats;
+  base.qrows = qrows;   // (MODE_MEMBER with K_L1F only: the 8-bit prefilter)
+  base.nq = nq;
+  base.qparam = qparam;
 
   // tensor path: tile landmark operand [T_pad][row_bytes], column constants
   tc::TcArgs ta{};
@@ -881,7 +908,7 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
   // re-read wide rows from memory (no register-resident width fits, e.g. C4)
   // (also for d >= 32: measured on C3, d = 64: 9.0 ms of A2 over 572 tiles on
   // tensor cores vs 12.0 ms on CUDA cores; C2, d = 10, is faster on CUDA cores)
-  const bool tc_adj = use_tc && (pick_nu(nu_needed) == 0 || d >= 32);
+  const bool tc_adj = use_tc && !use_l1t && (pick_nu(nu_needed) == 0 || d >= 32);
   tc::TcArgs ac{};      // A2 on tensor cores: candidate contraction
   tc::TcPlan Pc{};
   tc::RowParams rp{};
@@ -894,7 +921,8 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
     P.n_pad = ((n + RB - 1) / RB) * RB;
     ta.n = n;
     ta.L = T;
-    ta.ksteps = (int)(((int64_t)d * (dtype == BM_F32 ? 4 : 1) + 31) / 32);
+    ta.ksteps = use_l1t ? (int)(((int64_t)d * l1t_B + 6 + 31) / 32)
+                        : (int)(((int64_t)d * (dtype == BM_F32 ? 4 : 1) + 31) / 32);
     ta.lbits = 32;
     ta.l_count_dev = cnt + 3;
     ta.l_total_dev = cnt + 2;
@@ -913,7 +941,7 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
       TRY(alloc_fold(pool, P, ta, s, &launches));
       C2 = tc_band_c2(ta.ksteps);
       tau = 1.0000005e-6 * th.eps2 + th.eps2 * ldexp(1.0, -21);
-    } else {
+    } else if (!use_l1t) {   // (L1T: the row and column constants are folded into the operands)
       int32_t *rr, *cc;
       TRY(pool.alloc(&rr, (size_t)P.n_pad));
       TRY(pool.alloc(&cc, (size_t)P.l_rows));
@@ -922,12 +950,20 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
     }
     if (P.cosine) CK(tc::launch_tc_rows_cos(P, tc_nrm, n, th.eps, tc_cos_margin(ta.ksteps), ta, s,
                                             &launches));
-    else CK(tc::launch_tc_rows(P, prune ? (const void*)ps.nrm_perm : tc_nrm, n, C2, th.eps2, tau,
-                               th.lo_i, ta, s, &launches));
+    else if (!use_l1t)
+      CK(tc::launch_tc_rows(P, prune ? (const void*)ps.nrm_perm : tc_nrm, n, C2, th.eps2, tau,
+                            th.lo_i, ta, s, &launches));
     ta.keys = keys;
     ta.key_count = &stats->key_count;
     ta.key_cap = key_cap;
     set_recheck(ta, rows, 2 * nu, d, th, prune ? ps.col_pt : new_lm, ties_dev, tie_cap, stats);
+    if (use_l1t) {
+      ta.l1 = 1;
+      ta.l1t = 1;
+      ta.qrows = qrows;
+      ta.nq = nq;
+      ta.qparam = qparam;
+    }
     if (prune) {
       Pm = P;
       Pm.xop = ps.xop_perm;
@@ -1078,14 +1114,14 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
     CK(launch_unpack_low(lk, hl, 0xffffffffull, lm, s, &launches));
     int64_t Mf = 0;
     CK(mark_member());
-    TRY(membership_full(pool, kind, base, P, use_tc, tc_nrm, lm, hl, n, d, dtype, nu, th, C2,
+    TRY(membership_full(pool, kind, base, P, use_tc && !use_l1t, tc_nrm, lm, hl, n, d, dtype, nu, th, C2,
                         keys, key_cap, ties_dev, tie_cap, stats, s, &launches, &Mf));
     CK(mark_member());
     if (Mf > key_cap) {
       pool.free_now(keys);
       key_cap = Mf;
       TRY(pool.alloc(&keys, (size_t)key_cap));
-      TRY(membership_full(pool, kind, base, P, use_tc, tc_nrm, lm, hl, n, d, dtype, nu, th, C2,
+      TRY(membership_full(pool, kind, base, P, use_tc && !use_l1t, tc_nrm, lm, hl, n, d, dtype, nu, th, C2,
                           keys, key_cap, ties_dev, tie_cap, stats, s, &launches, &Mf));
       if (Mf > key_cap) return set_err(BM_ECUDA, "membership recount exceeded its exact size");
     }
@@ -1133,8 +1169,12 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
       loop_mark(2);
       // B (+A4 marks): membership of every point in the new balls
       if (use_tc) {
-        CK(tc::launch_tc_tile_landmarks(P, tc_nrm, prune ? ps.col_pt : new_lm, cnt + 3, C2, ta, s,
-                                        &launches));
+        if (use_l1t)
+          CK(tc::launch_l1t_tile_landmarks(P, (const int32_t*)tc_nrm, new_lm, cnt + 3, d, s,
+                                           &launches));
+        else
+          CK(tc::launch_tc_tile_landmarks(P, tc_nrm, prune ? ps.col_pt : new_lm, cnt + 3, C2, ta,
+                                          s, &launches));
         CK(mark_member());
         if (tc_trace) {   // diagnostics: phase stamps of this launch (synchronises)
           CK(cudaMemsetAsync(tc_trace, 0, sizeof(unsigned long long) * (P.num_sms * 16 + 512 * 5), s));
@@ -1236,7 +1276,7 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
     pool.free_now(keys);
     key_cap = M;
     TRY(pool.alloc(&keys, (size_t)key_cap));
-    TRY(membership_full(pool, kind, base, P, use_tc, tc_nrm, lm, L, n, d, dtype, nu, th, C2,
+    TRY(membership_full(pool, kind, base, P, use_tc && !use_l1t, tc_nrm, lm, L, n, d, dtype, nu, th, C2,
                         keys, key_cap, ties_dev, tie_cap, stats, s, &launches, &M));
     if (M > key_cap) return set_err(BM_ECUDA, "membership recount exceeded its exact size");
     CK(cudaMemcpyAsync(&hs, stats, sizeof hs, cudaMemcpyDeviceToHost, s));

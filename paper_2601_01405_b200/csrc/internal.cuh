@@ -11,6 +11,7 @@
 //   inorm  : integer L2 only — exact int32 squared norms.
 #pragma once
 #include <cuda_runtime.h>
+#include <math.h>
 #include <stdint.h>
 
 #include "../../include/bm.h"
@@ -178,6 +179,51 @@ cudaError_t launch_pairs(int kind, int mode, const PairArgs& a, int64_t q_rows_m
 int l1q_words(int d);   // 0 if the prefilter does not apply (d > 64)
 cudaError_t launch_l1_quantize(const float* X, int64_t n, int d, int nq, double* qparam,
                                uint32_t* qrows, cudaStream_t s, int64_t* launches);
+
+// L1 prefilter threshold: with q = rint((x - min)/s)
+// every coordinate is within s (1/2 + 1e-6) of min + s q, so
+// L1(x, y) >= s (SAD(q_x, q_y) - d (1 + 2e-6)); SAD >= thr proves
+// L1 >= eps (1 + 1.001e-6): out, and not a near tie.
+__device__ __forceinline__ double l1q_scale(const double* qp) {
+  const double r = qp[1] - qp[0];
+  return r > 0.0 ? r / 255.0 : 1.0;
+}
+__device__ __forceinline__ uint32_t l1q_threshold(const double* qp, double eps, int d) {
+  const double t = ceil(eps * (1.0 + 1.001e-6) / l1q_scale(qp) + d * (1.0 + 2e-6)) + 1.0;
+  return t > 4.0e9 ? 0xffffffffu : (uint32_t)t;
+}
+__device__ __forceinline__ uint32_t vsad4(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("vabsdiff4.u32.u32.u32.add %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
+// L1 on tensor cores ("coarse L1 as a Hamming Gram"): every
+// coordinate is binned into B + 1 levels (s_t = (max - min) / (B + 1)) and
+// written as a B-byte thermometer code, so the squared L2 distance of two codes
+// is the sum of the absolute level differences SADq; since every coordinate
+// lies within its bin (1e-9 s_t of slack for the fp64 binning),
+// L1(x, y) >= s_t (SADq - d (1 + 2e-9)), and SADq >= cut proves
+// L1 >= eps (1 + 4e-6): out, and not a near tie.  Bytes per coordinate B
+// (0: the path does not apply): the row (d B bytes + 6 bytes of folded
+// constants, tc.cu k_l1t_prep) fills at most three 128-byte K atoms (C5,
+// d = 16: B = 23, 24 levels; measured on C5, 24 levels leave ~0.26% of the
+// pairs as candidates for the 8-bit bound, 16 levels ~1.2%).
+__host__ __device__ __forceinline__ int l1t_bytes_per_coord(int d) {
+  // (d <= 16: the 8-bit rows of the candidate filter are <= 4 words, staged
+  // for a whole greedy tile in shared memory)
+  if (d < 1 || d > 16) return 0;
+  int b = 378 / d;
+  if (b > 32) b = 32;
+  return b;
+}
+__device__ __forceinline__ int32_t l1t_cut(const double* qp, double eps, int d, int B) {
+  const double r = qp[1] - qp[0];
+  const double st = r > 0.0 ? r / (double)(B + 1) : 1.0;
+  const double c = ceil(eps * (1.0 + 4e-6) / st + (double)d * (1.0 + 2e-9)) + 1.0;
+  const double cmax = (double)d * B + 1.0;   // every pair a candidate
+  return (int32_t)(c < cmax ? c : cmax);
+}
 
 // A3; also resets the per-tile device counters (*ticket = 0, *band_count = 0).
 // pruning outputs of A3 (cells.cu): the tile's landmarks sorted by cell rank

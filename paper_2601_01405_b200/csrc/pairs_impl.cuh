@@ -127,24 +127,6 @@ __device__ __forceinline__ int classify(typename KindTraits<KIND>::acc_t acc, in
   }
 }
 
-// L1 prefilter threshold: with q = rint((x - min)/s)
-// every coordinate is within s (1/2 + 1e-6) of min + s q, so
-// L1(x, y) >= s (SAD(q_x, q_y) - d (1 + 2e-6)); SAD >= thr proves
-// L1 >= eps (1 + 1.001e-6): out, and not a near tie.
-__device__ __forceinline__ double l1q_scale(const double* qp) {
-  const double r = qp[1] - qp[0];
-  return r > 0.0 ? r / 255.0 : 1.0;
-}
-__device__ __forceinline__ uint32_t l1q_threshold(const double* qp, double eps, int d) {
-  const double t = ceil(eps * (1.0 + 1.001e-6) / l1q_scale(qp) + d * (1.0 + 2e-6)) + 1.0;
-  return t > 4.0e9 ? 0xffffffffu : (uint32_t)t;
-}
-__device__ __forceinline__ uint32_t vsad4(uint32_t a, uint32_t b, uint32_t c) {
-  uint32_t d;
-  asm("vabsdiff4.u32.u32.u32.add %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
-  return d;
-}
-
 // NU > 0: query rows live in registers (NU units).  NU == 0 ("wide"): rows of
 // any length; the query row is re-read from global/L1 for every landmark.
 // NQ > 0 (K_L1F, MODE_MEMBER): the 8-bit quantised rows (NQ words) score a

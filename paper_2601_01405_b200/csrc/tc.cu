@@ -154,6 +154,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// the same with a suspend-time hint: the waiting warp sleeps until the phase
+// completes (or the hint expires) instead of re-issuing try_wait, so many
+// waiting warps do not take issue slots from the working ones
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@P1 bra DONE_%=;\n\t"
+      "bra WAIT_%=;\n"
+      "DONE_%=:\n\t}" ::"r"(su32(b)),
+      "r"(parity), "r"(0x989680)
+      : "memory");
+}
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, uint64_t* bar, int x,
                                             int y) {
   asm volatile(
@@ -309,8 +323,11 @@ struct Smem {
   static constexpr int B_BYTES = STAGES * B_STAGE;
   static constexpr int EPI_WARPS = 4 * EG;                // epilogue warpgroups x 4
   // staging slots per warp (the same total for 2 or 4 groups)
-  static constexpr int KW = (FOLD ? 64 : (KATOMS > 4 ? 96 : 128)) * 2 / EG;
-  static constexpr int BW = KW;
+  // (L1T: every pair is staged as a band pair; in-ball keys are written by
+  // the fp64 decision itself, so the key slots go unused)
+  static constexpr int KW =
+      MODE == TC_MODE_L1T ? 8 : (FOLD ? 64 : (KATOMS > 4 ? 96 : 128)) * 2 / EG;
+  static constexpr int BW = MODE == TC_MODE_L1T ? 64 : KW;
   static constexpr int NBUF = 512 / (RA * BN);              // TMEM accumulator buffers
   // fold tiles (tf32): A ones [128 rows x 32 B], B constants [2 slots][BN rows x 32 B]
   static constexpr int AK_OFF = ABUF * A_BYTES + B_BYTES;
@@ -324,19 +341,39 @@ struct Smem {
   static constexpr bool COLSLOT =
       (MODE == TC_MODE_MEMBER || MODE == TC_MODE_ADJ) && !(FOLD && BRES) && EG != 4;
   static constexpr int BAR_OFF = COL_OFF + (COLSLOT ? NBUF * COL_BYTES : 0);
-  static constexpr int NBARS = 2 * STAGES + 2 * ABUF + 3 * NBUF + 5;
+  static constexpr int NQR = MODE == TC_MODE_L1T ? 4 : 0;   // L1T: unit row-word ring slots
+  static constexpr int NBARS = 2 * STAGES + 2 * ABUF + 3 * NBUF + 5 + 2 * NQR;
   static constexpr int CNT_OFF = BAR_OFF + NBARS * 8;     // tmem slot + per-warp counts
   static constexpr int BUF_OFF = CNT_OFF + 256;   // tmem slot + 2 x 16 warp counts
   // resident B (tf32): the launch's in-test offsets d_j, staged once for the rare path
   static constexpr int DJ_OFF = (BUF_OFF + EPI_WARPS * (KW + BW) * 8 + 15) & ~15;
   static constexpr int DJ_BYTES = (BRES && FOLD) ? STAGES * BN * 4 : 0;
-  static constexpr int TOTAL = DJ_OFF + DJ_BYTES + 1024;  // + align slack
+  // L1T: the launch's landmark 8-bit rows (<= 1024 columns x 4 words), column order
+  static constexpr int Q8_OFF = DJ_OFF + DJ_BYTES;
+  static constexpr int Q8_BYTES = MODE == TC_MODE_L1T ? 1024 * 16 : 0;
+  // L1T: the 8-bit rows of a unit's 128 points, a ring of NQR slots filled by
+  // the producer (one bulk copy per unit) and released by the epilogue warps
+  static constexpr int QR_OFF = Q8_OFF + Q8_BYTES;
+  static constexpr int QR_SLOT = 128 * 16;
+  static constexpr int TOTAL = QR_OFF + NQR * QR_SLOT + 1024;  // + align slack
 };
 
 // 32 consecutive columns of the warp's 32 TMEM lanes
 __device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+        "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr)
+      : "memory");
+}
+// 64 consecutive columns of the warp's 32 TMEM lanes, the low 16 bits of two
+// adjacent columns packed per register (column 2i in bits 0-15, 2i+1 in 16-31)
+__device__ __forceinline__ void tmem_ld64p_nowait(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.pack::16b.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
       : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
         "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
         "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
@@ -396,7 +433,7 @@ __device__ __forceinline__ uint32_t sel32(const uint32_t (&v)[32], int i) {
 // B': the oracle's fp64 decision for points p, q (ascending coordinates, no
 // contraction; cosine with the zero-vector rule, A6/A7).
 __device__ __noinline__ bool pair_in_fp64(const float* xrows, int xstride, int dd, int cosine,
-                                          double eps, double eps2, int64_t p, int64_t q,
+                                          int l1, double eps, double eps2, int64_t p, int64_t q,
                                           double* dist) {
   const float* x = xrows + p * (int64_t)xstride;
   const float* y = xrows + q * (int64_t)xstride;
@@ -440,9 +477,13 @@ __device__ __noinline__ bool pair_in_fp64(const float* xrows, int xstride, int d
     for (int i = 0; i < G; ++i) {
       if (k0 + i < dd) {
         const double t = __dsub_rn((double)xa[i], (double)ya[i]);
-        sacc = __dadd_rn(sacc, __dmul_rn(t, t));
+        sacc = l1 ? __dadd_rn(sacc, fabs(t)) : __dadd_rn(sacc, __dmul_rn(t, t));
       }
     }
+  }
+  if (l1) {   // Manhattan (reading A8): sum_j |x_j - y_j| in ascending j, against eps
+    *dist = sacc;
+    return sacc < eps;
   }
   *dist = __dsqrt_rn(sacc);
   return sacc < eps2;
@@ -466,7 +507,8 @@ constexpr bool tc_lean() {
 #ifdef BM_TC_NOLEAN   // A/B diagnostics: every instance on the generic epilogue
   return false;
 #else
-  return KIND == TC_TF32 && MODE == TC_MODE_MEMBER && !PR && BN == 256;
+  return (KIND == TC_TF32 && MODE == TC_MODE_MEMBER && !PR && BN == 256) ||
+         (MODE == TC_MODE_L1T && BN == 256);
 #endif
 }
 template <int KIND, int BN, int MODE, bool PR>
@@ -500,6 +542,7 @@ __global__ void __launch_bounds__(tc_threads<KIND, BN, MODE, PR>(), 1)
   static_assert(NBUF >= 2 && NBUF * BUFCOLS <= 512, "TMEM: accumulator buffers must fit 512 columns");
   static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "BN");
   static_assert(RA == 1, "one 128-row block per unit (N = BN MMAs, A double-buffered)");
+  static_assert(MODE != TC_MODE_L1T || LEAN, "L1T runs the lean epilogue");
   constexpr int ATOM_ELEMS = KIND == TC_TF32 ? 32 : 128;
   constexpr uint32_t IDESC = make_idesc<KIND>(128, BN);
   constexpr bool KS = S::KS;
@@ -522,6 +565,8 @@ __global__ void __launch_bounds__(tc_threads<KIND, BN, MODE, PR>(), 1)
   uint64_t* bk_full = c_full + NBUF;                // [2] fold: B constant slots
   uint64_t* bk_empty = bk_full + 2;                 // [2]
   uint64_t* ak_full = bk_empty + 2;                 // fold: A ones tile
+  uint64_t* qr_full = ak_full + 1;                  // L1T: [NQR] unit row words landed
+  uint64_t* qr_empty = qr_full + S::NQR;            // L1T: [NQR] released by the epilogue
   float* scol = (float*)(sm + S::COL_OFF);          // [NBUF][BN] (int8)
   uint8_t* sAK = sm + S::AK_OFF;                    // fold: [128][32 B]
   uint8_t* sBK = sAK + 128 * 32;                    // fold: [2][BN][32 B]
@@ -559,6 +604,10 @@ __global__ void __launch_bounds__(tc_threads<KIND, BN, MODE, PR>(), 1)
     mbar_init(&bk_empty[0], 1);
     mbar_init(&bk_empty[1], 1);
     mbar_init(ak_full, 1);
+    for (int b = 0; b < S::NQR; ++b) {
+      mbar_init(&qr_full[b], 1);
+      mbar_init(&qr_empty[b], S::EPI_WARPS);
+    }
     for (int w = 0; w < S::EPI_WARPS; ++w) {
       kcount[w] = 0;
       bcount[w] = 0;
@@ -729,6 +778,14 @@ __global__ void __launch_bounds__(tc_threads<KIND, BN, MODE, PR>(), 1)
               tma_load_2d(sAb + (r * KATOMS + ka) * S::A_ATOM, &tmA, &a_full[ab],
                           ka * ATOM_ELEMS, (int)(mb * RA * 128 + r * 128));
         }
+        if constexpr (S::NQR > 0) {   // L1T: the unit's 8-bit rows for the epilogue
+          const int qs = (int)(ui % S::NQR);
+          if (ui >= S::NQR) mbar_wait(&qr_empty[qs], (uint32_t)((ui / S::NQR - 1) & 1));
+          const uint32_t qb = (uint32_t)(128 * args.nq * 4);
+          mbar_expect_tx(&qr_full[qs], qb);
+          bulk_load(sm + S::QR_OFF + qs * S::QR_SLOT, args.qrows + mb * 128 * args.nq, qb,
+                    &qr_full[qs]);
+        }
         // warm L2 with the next unit's point block while this one computes
         const int64_t un = u + gridDim.x;
         if (!KS && un < n_units && un / n_chunks != mb) {
@@ -890,7 +947,7 @@ __global__ void __launch_bounds__(tc_threads<KIND, BN, MODE, PR>(), 1)
         if constexpr (!KS) commit_w(&a_empty[ab]);
         ++ui;
       }
-      if (MODE == TC_MODE_MEMBER && args.stats && lane == 0) {
+      if ((MODE == TC_MODE_MEMBER || MODE == TC_MODE_L1T) && args.stats && lane == 0) {
         if (n_run) atomicAdd(&args.stats->tc_tiles_run, n_run);
         if (n_skip) atomicAdd(&args.stats->tc_tiles_skip, n_skip);
       }
@@ -911,6 +968,26 @@ __global__ void __launch_bounds__(tc_threads<KIND, BN, MODE, PR>(), 1)
         sdj[j] = __ldg(args.col_a + j);
       asm volatile("bar.sync 1, %0;" ::"n"(128 * EG) : "memory");   // the epilogue warps only
     }
+    // L1T: the columns' 8-bit rows (4 words each, zero padded) staged once, so
+    // the candidate filter reads shared memory instead of two dependent
+    // global loads (launches of <= 1024 columns with <= 4 words per row)
+    uint32_t* sq8 = reinterpret_cast<uint32_t*>(sm + S::Q8_OFF);
+    // L1T: the 8-bit SAD bound of the CUDA-core path,
+    // computed once into shared memory (an fp64 divide: kept out of the loop)
+    uint32_t* sthr8 = bcount + S::EPI_WARPS;
+    const bool q8s = S::Q8_BYTES > 0;   // (dispatch_l1t: nq == 4, <= 1024 columns)
+    if constexpr (S::Q8_BYTES > 0) {
+      if (threadIdx.x == 128) *sthr8 = l1q_threshold(args.qparam, args.eps, args.d);
+      if (q8s) {
+        for (int64_t t = threadIdx.x - 128; t < n_cols * 4; t += 128 * EG) {
+          const int64_t j = t >> 2;
+          const int w = (int)(t & 3);
+          sq8[t] = w < args.nq ? __ldg(args.qrows + (int64_t)__ldg(args.lm_idx + j) * args.nq + w)
+                               : 0u;
+        }
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(128 * EG) : "memory");   // the epilogue warps only
+    }
     unsigned long long* kb = kbuf + ew * S::KW;
     unsigned long long* bb = bbuf + ew * S::BW;
     uint32_t* kc = kcount + ew;
@@ -929,9 +1006,9 @@ __global__ void __launch_bounds__(tc_threads<KIND, BN, MODE, PR>(), 1)
       if (j >= n_cols || p >= args.n) return;   // padding rows / columns never qualify
       const int64_t qp = args.lm_idx[j];
       double dist;
-      const bool in = pair_in_fp64(args.xrows, args.xstride, args.d, args.cosine, args.eps,
-                                   args.eps2, p, qp, &dist);
-      if (fabs(dist - args.eps) <= args.tie_rel * args.eps) {
+      const bool in = pair_in_fp64(args.xrows, args.xstride, args.d, args.cosine, args.l1,
+                                   args.eps, args.eps2, p, qp, &dist);
+      if (fabs(dist - args.eps) <= args.tie_abs) {
         const unsigned long long k = atomicAdd(&args.stats->near_ties, 1ull);
         if ((int64_t)k < args.tie_cap && args.ties) {
           args.ties[3 * k] = p;
@@ -983,7 +1060,133 @@ __global__ void __launch_bounds__(tc_threads<KIND, BN, MODE, PR>(), 1)
         recheck(key);
       }
     };
-    if constexpr (LEAN) {
+    // L1T: 8-bit SAD of this lane's row (w words in registers) against column j
+    auto l1t_sad = [&](const uint32_t (&rq)[4], int64_t j) -> uint32_t {
+      uint32_t sad = 0u;
+      {   // staged rows (nq <= 4: the padding words are zero on both sides)
+        uint32_t a, b, c, e;
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(a), "=r"(b), "=r"(c), "=r"(e)
+                     : "r"(su32(sq8 + j * 4)));
+        sad = vsad4(rq[0], a, sad);
+        sad = vsad4(rq[1], b, sad);
+        sad = vsad4(rq[2], c, sad);
+        sad = vsad4(rq[3], e, sad);
+      }
+      return sad;
+    };
+    if constexpr (LEAN && MODE == TC_MODE_L1T) {
+      // ---- lean L1 epilogue (four groups, group g owns
+      // columns [64 g, 64 g + 64) of every tile, warp q TMEM lanes 32 q ..):
+      // the sign bits of the folded accumulators (SADq - cut < 0: not proven
+      // out) become two 32-bit masks, the TMEM buffer goes back to the MMA
+      // issuer, then each candidate passes the 8-bit SAD bound (rows staged in
+      // shared memory) and the survivors are decided in fp64 (B')
+      static_assert(BN / EG == 64, "L1T: 64 columns per group and tile");
+      const long long epi_t0 = args.wtrace ? clock64() : 0;
+      uint32_t phase = 0;
+      uint32_t tcnt = 0;
+      const uint32_t tlane = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(grp * (BN / EG));
+      const uint32_t* qr_base = reinterpret_cast<const uint32_t*>(sm + S::QR_OFF);
+      uint32_t uu = 0;   // units seen (the producer's ring order)
+      for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x, ++uu) {
+        const int64_t mb = n_chunks == 1 ? u : u / n_chunks, ch = n_chunks == 1 ? 0 : u % n_chunks;
+        const int t0 = (int)(ch * tiles_per_chunk), t1 = (int)min(n_tiles, t0 + tiles_per_chunk);
+        const int64_t prow = mb * 128 + q * 32 + lane;
+        const int qs = (int)(uu % S::NQR);
+        // this lane's 8-bit row in the unit's ring slot (read on a candidate)
+        const uint32_t* qrow = qr_base + qs * (S::QR_SLOT / 4) + (q * 32 + lane) * args.nq;
+        // (every warp waits for the slot's copy before it releases the slot, so
+        // the producer never re-arms a barrier whose copy is still in flight;
+        // the copy was issued with the unit's A block and has long landed)
+        mbar_wait(&qr_full[qs], (uu / S::NQR) & 1u);
+        for (int t = t0; t < t1; ++t) {
+          const uint32_t buf = tcnt & (uint32_t)(NBUF - 1);
+          TC_TWAIT(5, mbar_wait(&t_full[buf], (phase >> buf) & 1u));
+          if (ew == 0 && lane == 0) TC_TL(tcnt, 3);
+          phase ^= 1u << buf;
+          fence_after();
+          const uint32_t ta = tlane + buf * (uint32_t)BUFCOLS;
+          // the group's 64 columns in one load, two 16-bit accumulators per
+          // register (|SADq - cut| < 2^15); per 4 columns one byte permute
+          // gathers the 4 sign bytes, and 8 of those make a 32-bit mask whose
+          // bit 8 i + m is the sign of column 4 m + i
+          uint32_t cm[2];
+#ifdef BM_TC_WTRACE
+          const long long s6 = clock64();
+#endif
+          {
+            uint32_t v[32];
+            tmem_ld64p_nowait(ta, v);
+            tmem_wait32(v);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              uint32_t m = 0u;
+#pragma unroll
+              for (int mm = 0; mm < 8; ++mm) {
+                const uint32_t r = __byte_perm(v[16 * h + 2 * mm], v[16 * h + 2 * mm + 1], 0x7531);
+                m |= (r >> (7 - mm)) & (0x01010101u << mm);
+              }
+              cm[h] = m;
+            }
+          }
+          // (columns past the tile's landmarks and rows past n hold zero
+          // operands: acc = 0, never a candidate)
+          fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&t_empty[buf]);
+          if (ew == 0 && lane == 0) TC_TL(tcnt, 4);
+#ifdef BM_TC_WTRACE
+          const long long s7 = clock64();
+          wacc[6] += s7 - s6;   // (L1T diagnostics: slot 6 = TMEM load + masks + release)
+#endif
+          ++tcnt;
+          const int64_t jg = (int64_t)t * BN + grp * (BN / EG);
+          if (jg + 64 > n_cols) {   // a ragged last tile: its MMA wrote the first
+            // columns only; the rest of the buffer holds an earlier tile's sums
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+              for (int b = 0; b < 32; ++b)
+                if (jg + 32 * h + 4 * (b & 7) + (b >> 3) >= n_cols) cm[h] &= ~(1u << b);
+          }
+          // candidates (a few per lane and tile): the 8-bit SAD bound, rows
+          // staged in shared memory; survivors go to the fp64 decision (one
+          // loop over both halves)
+          unsigned long long cand = ((unsigned long long)cm[1] << 32) | cm[0];
+          if (__any_sync(FULLM, cand != 0ull)) {
+            uint32_t rq[4];
+            {
+              uint32_t a, b2, c, e;
+              asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                           : "=r"(a), "=r"(b2), "=r"(c), "=r"(e)
+                           : "r"(su32(qrow)));
+              rq[0] = a;   // (dispatch_l1t: nq == 4)
+              rq[1] = b2;
+              rq[2] = c;
+              rq[3] = e;
+            }
+            const uint32_t th8 = *sthr8;
+            while (cand) {
+              const int b = __ffsll((long long)cand) - 1;
+              cand &= cand - 1ull;
+              // bit b of the 64-bit mask -> column
+              const int64_t j = jg + 32 * (b >> 5) + 4 * (b & 7) + ((b >> 3) & 3);
+              if (l1t_sad(rq, j) < th8)
+                append(2, ((unsigned long long)prow << 32) | (unsigned long long)j);
+            }
+          }
+          __syncwarp();
+          if (*kc > S::KW / 2 || *bc > S::BW / 2) flush();
+#ifdef BM_TC_WTRACE
+          wacc[7] += clock64() - s7;   // (L1T diagnostics: slot 7 = candidates + flush)
+#endif
+        }
+        __syncwarp();   // the unit's row words go back to the producer
+        if (lane == 0) mbar_arrive(&qr_empty[qs]);
+      }
+      if (args.wtrace) wacc[8] += clock64() - epi_t0;
+    } else if constexpr (LEAN) {
       // ---- lean tf32 membership epilogue (four groups; group g owns columns
       // [g BN/4, (g + 1) BN/4) of every tile, warp q TMEM lanes 32 q ..).  Per
       // tile: BN/128 32-column loads, a max over the accumulators (the column
@@ -1200,7 +1403,7 @@ __global__ void __launch_bounds__(tc_threads<KIND, BN, MODE, PR>(), 1)
                     const int i = __ffs(band) - 1;
                     band &= band - 1u;
                     double dist;
-                    if (pair_in_fp64(args.xrows, args.xstride, args.d, args.cosine, args.eps,
+                    if (pair_in_fp64(args.xrows, args.xstride, args.d, args.cosine, 0, args.eps,
                                      args.eps2, args.lm_idx[a], args.lm_idx[j0 + i], &dist))
                       mask |= 1u << i;
                   }
@@ -1569,8 +1772,21 @@ cudaError_t launch_tc_adj(const TcPlan& Pc, const TcArgs& ac, cudaStream_t s, in
   return dispatch<TC_MODE_ADJ>(Pc, ac, s);
 }
 
+// L1 on tensor cores: signed int8 thermometer operands of one or two K atoms
+static cudaError_t dispatch_l1t(const TcPlan& P, const TcArgs& a, cudaStream_t s) {
+  if (P.kind != TC_S8 || !a.qrows || !a.qparam || a.nq != 4 || a.L > 1024)
+    return cudaErrorInvalidValue;
+  if (P.katoms == 1 && bres_ok(P, a, 4))
+    return launch_cfg<TC_S8, 1, 256, 1, 4, 3, TC_MODE_L1T, true>(P, a, s);
+  if (P.katoms == 1) return launch_cfg<TC_S8, 1, 256, 1, 4, 2, TC_MODE_L1T>(P, a, s);
+  if (P.katoms == 2) return launch_cfg<TC_S8, 1, 256, 2, 3, 2, TC_MODE_L1T>(P, a, s);
+  if (P.katoms == 3) return launch_cfg<TC_S8, 1, 256, 3, 3, 2, TC_MODE_L1T>(P, a, s);
+  return cudaErrorNotSupported;
+}
+
 cudaError_t launch_tc(const TcPlan& P, const TcArgs& a, cudaStream_t s, int64_t* launches) {
   ++*launches;
+  if (a.l1t) return dispatch_l1t(P, a, s);
   if (a.gram) return dispatch<TC_MODE_GRAM>(P, a, s);
   return dispatch<TC_MODE_MEMBER>(P, a, s);
 }
@@ -1916,6 +2132,121 @@ cudaError_t launch_tc_landmarks(const TcPlan& P, const void* nrm, const int32_t*
   else
     k_tc_cols_int<<<g, 256, 0, s>>>((const int32_t*)nrm, lm, L, P.l_rows, (int32_t*)a.col_c);
   return cudaGetLastError();
+}
+
+// ---- L1 on tensor cores: thermometer operands
+// byte j B + k of a point row = -2 if level(x_j) > k else 0 (k < B); bytes
+// dB..dB+2 = 1 (they meet the landmark's n_l), dB+3..dB+5 = n_p - cut in
+// three signed bytes (they meet the landmark's 1s); a landmark row holds the
+// bits as 0/1, n_l in three bytes, then 1,1,1.  So the s8 contraction gives
+// acc = -2 <T(x), T(l)> + n_l + n_p - cut = SADq - cut.
+__device__ __forceinline__ int l1t_chunk(int v, int k) {   // v split into 3 signed bytes
+  const int c0 = v < -128 ? -128 : (v > 127 ? 127 : v);
+  const int v1 = v - c0;
+  const int c1 = v1 < -128 ? -128 : (v1 > 127 ? 127 : v1);
+  return k == 0 ? c0 : (k == 1 ? c1 : v1 - c1);
+}
+
+// one warp per point: lane j < d bins coordinate j; every lane writes 8 bytes
+// of the row (B >= 8, so 8 consecutive bytes span at most two coordinates)
+__global__ void k_l1t_prep(const float* __restrict__ X, int64_t n, int d, int B, int row_bytes,
+                           const double* __restrict__ qparam, double eps,
+                           uint8_t* __restrict__ xop, int32_t* __restrict__ nrm) {
+  const int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (p >= n) return;
+  const double mn = qparam[0], mx = qparam[1];
+  const double st = mx > mn ? (mx - mn) / (double)(B + 1) : 1.0;
+  int lv = 0;
+  if (lane < d) {
+    const double t = floor(((double)__ldg(X + p * (int64_t)d + lane) - mn) / st);
+    lv = t < 0.0 ? 0 : (t > (double)B ? B : (int)t);
+  }
+  int np = lv;
+  for (int o = 16; o > 0; o >>= 1) np += __shfl_xor_sync(0xffffffffu, np, o);
+  const int r = np - l1t_cut(qparam, eps, d, B);
+  const int dB = d * B;
+  for (int h = 0; h < row_bytes; h += 256) {   // (rows of up to 512 bytes: two passes)
+    const int b0 = h + lane * 8;
+    const int ja = min(b0 / B, 31), jb = min((b0 + 7) / B, 31);
+    const int la = __shfl_sync(0xffffffffu, lv, ja), lb = __shfl_sync(0xffffffffu, lv, jb);
+    if (b0 >= row_bytes) continue;
+    uint32_t w[2] = {0u, 0u};
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int b = b0 + k;
+      int v = 0;
+      if (b < dB) {
+        const int j = b / B;
+        v = (j == ja ? la : lb) > b - j * B ? -2 : 0;
+      } else if (b < dB + 3) {
+        v = 1;
+      } else if (b < dB + 6) {
+        v = l1t_chunk(r, b - dB - 3);
+      }
+      w[k >> 2] |= (uint32_t)(uint8_t)(int8_t)v << (8 * (k & 3));
+    }
+    *reinterpret_cast<uint2*>(xop + p * (int64_t)row_bytes + b0) = make_uint2(w[0], w[1]);
+  }
+  if (lane == 0) nrm[p] = np;
+}
+
+cudaError_t launch_l1t_prep(const float* X, int64_t n, int d, const TcPlan& P,
+                            const double* qparam, double eps, int32_t* nrm, cudaStream_t s,
+                            int64_t* launches) {
+  const int B = l1t_bytes_per_coord(d);
+  if (B == 0 || P.row_bytes > 512 || P.kind != TC_S8 || d * B + 6 > P.row_bytes)
+    return cudaErrorInvalidValue;
+  ++*launches;
+  k_l1t_prep<<<(unsigned)((n * 32 + 255) / 256), 256, 0, s>>>(
+      X, n, d, B, (int)P.row_bytes, qparam, eps, (uint8_t*)P.xop, nrm);
+  return cudaGetLastError();
+}
+
+// one warp per landmark row of the tile's operand (zero beyond the count)
+__global__ void k_l1t_tile_lm(const uint8_t* __restrict__ xop, int row_bytes,
+                              const int32_t* __restrict__ new_lm,
+                              const int32_t* __restrict__ l_count_dev,
+                              const int32_t* __restrict__ nrm, int d, int B, int64_t l_rows,
+                              uint8_t* __restrict__ lop) {
+  pdl_wait();
+  pdl_trigger();   // one wave
+  const int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (j >= l_rows) return;
+  const bool live = j < (int64_t)*l_count_dev;
+  for (int b0 = lane * 8; b0 < row_bytes; b0 += 256) {
+  uint2 out = make_uint2(0u, 0u);
+  if (live) {
+    const int32_t pt = new_lm[j];
+    const int nl = nrm[pt];
+    const uint2 a = *reinterpret_cast<const uint2*>(xop + (int64_t)pt * row_bytes + b0);
+    const int dB = d * B;
+    uint32_t w[2] = {(a.x >> 1) & 0x01010101u, (a.y >> 1) & 0x01010101u};   // -2 -> 1, 0 -> 0
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int b = b0 + k;
+      if (b < dB) continue;
+      int v = 0;
+      if (b < dB + 3) v = l1t_chunk(nl, b - dB);
+      else if (b < dB + 6) v = 1;
+      const uint32_t m = 0xffu << (8 * (k & 3));
+      w[k >> 2] = (w[k >> 2] & ~m) | ((uint32_t)(uint8_t)(int8_t)v << (8 * (k & 3)));
+    }
+    out = make_uint2(w[0], w[1]);
+  }
+  *reinterpret_cast<uint2*>(lop + j * (int64_t)row_bytes + b0) = out;
+  }
+}
+
+cudaError_t launch_l1t_tile_landmarks(const TcPlan& P, const int32_t* nrm, const int32_t* new_lm,
+                                      const int32_t* l_count_dev, int d, cudaStream_t s,
+                                      int64_t* launches) {
+  ++*launches;
+  const int B = l1t_bytes_per_coord(d);
+  return launch_pdl(k_l1t_tile_lm, dim3((unsigned)((P.l_rows * 32 + 255) / 256)), dim3(256), 0, s,
+                    (const uint8_t*)P.xop, (int)P.row_bytes, new_lm, l_count_dev, nrm, d, B,
+                    (int64_t)P.l_rows, (uint8_t*)P.lop);
 }
 
 

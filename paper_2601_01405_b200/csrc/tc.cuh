@@ -14,7 +14,9 @@ enum TcMode : int {
   TC_MODE_GRAM = 1,
   TC_MODE_PROBE_LDONLY = 2,   // diagnostics: epilogue reads TMEM, no classification
   TC_MODE_PROBE_NOLD = 3,     // diagnostics: epilogue releases buffers without reading
-  TC_MODE_ADJ = 4             // A2: candidate x candidate adjacency bits of a greedy tile
+  TC_MODE_ADJ = 4,            // A2: candidate x candidate adjacency bits of a greedy tile
+  TC_MODE_L1T = 5             // B for L1 (TC_S8): thermometer-code Gram, sign of the folded
+                              //   accumulator = "not proven out"; 8-bit SAD, then fp64 (B')
 };
 
 // Per-row thresholds of the contraction, shared by the point
@@ -67,8 +69,18 @@ struct TcArgs {
   int xstride;
   int d;
   double eps, eps2, tie_rel;
+  double tie_abs;          // tie_rel * eps (precomputed: no fp64 multiply in the epilogue)
   const int32_t* lm_idx;   // landmark column -> point index
-  int cosine;              // recheck with the cosine formula (else Euclidean)
+  int cosine;              // recheck with the cosine formula (else Euclidean, or L1 below)
+  int l1;                  // recheck with the L1 formula
+  // L1 on tensor cores (TC_MODE_L1T, l1t != 0): candidates (SADq < cut, the
+  // sign of the folded accumulator) pass the 8-bit SAD filter of the
+  // CUDA-core path (qrows: nq words per point, qparam: coordinate range)
+  // before the fp64 decision
+  int l1t;
+  const uint32_t* qrows;
+  int nq;
+  const double* qparam;
   int64_t* ties;           // near-tie triples (point, landmark point, decision)
   int64_t tie_cap;
   DevStats* stats;         // band_pairs / near_ties counters
@@ -123,6 +135,17 @@ cudaError_t launch_tc_tile_cand(const TcPlan& P, const TcPlan& Pc, const void* n
                                 const int32_t* unc, const int32_t* n_unc_dev, int T, double C2,
                                 const RowParams& rp, TcArgs& ac, cudaStream_t s,
                                 int64_t* launches);
+// L1 on tensor cores (internal.cuh l1t_bytes_per_coord): point operand rows
+// (-2 x thermometer bits, then the folded constants 1,1,1 and n_p - cut in
+// three bytes) and n_p = sum of the levels; qparam from launch_l1_quantize.
+cudaError_t launch_l1t_prep(const float* X, int64_t n, int d, const TcPlan& P,
+                            const double* qparam, double eps, int32_t* nrm, cudaStream_t s,
+                            int64_t* launches);
+// ... and the greedy tile's landmark operand (thermometer bits, n_l in three
+// bytes, then 1,1,1), rows >= *l_count_dev zero
+cudaError_t launch_l1t_tile_landmarks(const TcPlan& P, const int32_t* nrm, const int32_t* new_lm,
+                                      const int32_t* l_count_dev, int d, cudaStream_t s,
+                                      int64_t* launches);
 cudaError_t launch_tc_adj(const TcPlan& Pc, const TcArgs& ac, cudaStream_t s, int64_t* launches);
 // diagnostics: the contraction with a probe epilogue (TC_MODE_PROBE_*), tf32 K <= 64 only
 cudaError_t launch_tc_probe(const TcPlan& P, const TcArgs& a, int mode, cudaStream_t s);

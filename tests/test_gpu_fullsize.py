@@ -45,11 +45,12 @@ def _log(rep):
             f.write(json.dumps(rep) + "\n")
 
 
-@pytest.mark.parametrize("name", ["c3_e2", "c3_e4", "c3_e8", "c5_l1", "c5_cos"])
-def test_fullsize_validity(bm, name):
+@pytest.mark.parametrize("name,path", [("c3_e2", "auto"), ("c3_e4", "auto"), ("c3_e8", "auto"),
+                                       ("c5_l1", "auto"), ("c5_l1", "tensor"), ("c5_cos", "auto")])
+def test_fullsize_validity(bm, name, path):
     w = gen.get(name)
     X = gen.generate(w)
-    cov = bm.cover_build(torch.from_numpy(X).cuda(), w.metric, w.eps)
+    cov = bm.cover_build(torch.from_numpy(X).cuda(), w.metric, w.eps, path=path)
     assert cov.stats.n_near_ties == len(cov.near_ties), "near-tie list truncated"
     a = cov.numpy()
     path = ["auto", "cuda_core", "tensor"][cov.stats.path_used]
@@ -107,8 +108,6 @@ def test_near_tie_completeness(bm, kind, metric, path):
     """north_star: near-tie pairs "are reported" — the GPU's near-tie list must
     equal the oracle's full set of in-band (point, landmark) pairs of the final
     cover, not merely a subset of the band."""
-    if path == "tensor" and metric == "l1":
-        pytest.skip("L1 has no tensor-core path")
     X, eps = _tie_cloud(kind, 3)
     t = torch.from_numpy(X).cuda()
     cov = bm.cover_build(t, metric, eps, path=path, tile=256)

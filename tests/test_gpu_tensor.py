@@ -119,6 +119,47 @@ def test_tensor_path_cosine_c5_prefix(bm):
     compare(X, w.metric, w.eps, cov, float_path=True, tie_rate_limit=True)
 
 
+@pytest.mark.parametrize("d", [1, 2, 3, 7, 8, 11, 16])
+def test_tensor_path_l1(bm, d):
+    """L1 on tcgen05 (thermometer-code Gram): the signed int8
+    contraction only proves pairs out; results equal the CUDA-core path and
+    the oracle for widths with one and two K atoms, also with exact-eps
+    shifts along one axis and a few far outliers (coarse levels)."""
+    rng = np.random.default_rng([d, 0x11])
+    n = 3000
+    X = rng.random((n, d)).astype(np.float32)
+    eps = 0.3 * d ** 0.75
+    X[1::7] = X[0::7][: len(X[1::7])]
+    X[1::7, 0] += np.float32(eps)                 # |dx| = eps exactly along axis 0
+    t = torch.from_numpy(X).cuda()
+    a = bm.cover_build(t, "l1", eps, path="tensor", tile=256)
+    b = bm.cover_build(t, "l1", eps, path="cuda_core", tile=256)
+    assert a.stats.path_used == 2 and b.stats.path_used == 1
+    na, nb = a.numpy(), b.numpy()
+    for k in na:
+        assert np.array_equal(na[k], nb[k]), k
+    compare(X, "l1", eps, a, float_path=True)
+    Y = X.copy()
+    Y[::61] *= 50.0                               # outliers widen the level spacing
+    a = bm.cover_build(torch.from_numpy(Y).cuda(), "l1", eps, path="tensor")
+    compare(Y, "l1", eps, a, float_path=True)
+
+
+def test_tensor_path_l1_unsupported_width(bm):
+    from paper_2601_01405_b200 import bm as B
+    X = torch.rand(100, 17, device="cuda")
+    with pytest.raises(B.BMError):
+        bm.cover_build(X, "l1", 1.0, path="tensor")
+
+
+def test_tensor_path_l1_c5_prefix(bm):
+    w = gen.get("c5_l1")
+    X = gen.generate(w, 60000)
+    cov = bm.cover_build(torch.from_numpy(X).cuda(), w.metric, w.eps, path="tensor")
+    assert cov.stats.path_used == 2
+    compare(X, w.metric, w.eps, cov, float_path=True, tie_rate_limit=True)
+
+
 @pytest.mark.parametrize("name,m", [("c3_e8", 20000), ("c3_e4", 12000), ("c3_e2", 6000),
                                     ("c2", None)])
 def test_pruned_contraction_parity(bm, name, m):
