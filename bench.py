@@ -132,8 +132,8 @@ def tc_peaks(peaks, sustained):
     """Dense tensor peaks for the contraction's own dtype.  Preferred: the
     tcgen05 microbenchmark committed under profiles/ (tools/ubench/tc_peak.cu,
     kind::tf32 / kind::i8 / kind::f16-bf16, M128 N256 back to back on every
-    SM); its bf16 figure is checked against MEASURED_PEAKS' cuBLAS one and the
-    ratio carries the sustained/burst choice over.  Fallback: MEASURED_PEAKS'
+    SM, ~5 ms bursts); for steps > 0.5 s it is scaled by MEASURED_PEAKS'
+    cuBLAS sustained / burst ratio.  Fallback: MEASURED_PEAKS'
     bf16 x the guide's nominal ratio (tf32 0.5, int8 2)."""
     bf16 = float(peaks["bf16_tflops_sustained" if sustained else "bf16_tflops"])
     p = os.path.join(ROOT, "profiles", "tc_peak.json")
@@ -142,9 +142,9 @@ def tc_peaks(peaks, sustained):
             rows = [json.loads(l) for l in open(p) if l.lstrip().startswith("{")]
             m = {r["kind"]: float(r["tflops"]) for r in rows if "tflops" in r}
             if "tf32" in m and "i8" in m:
-                scale = 1.0
-                if sustained and "bf16" in m and m["bf16"] > 0:
-                    scale = min(1.0, float(peaks["bf16_tflops_sustained"]) / m["bf16"])
+                scale = 1.0   # long steps: the cuBLAS sustained / burst ratio (clocks under load)
+                if sustained and float(peaks.get("bf16_tflops", 0)) > 0:
+                    scale = min(1.0, float(peaks["bf16_tflops_sustained"]) / float(peaks["bf16_tflops"]))
                 return ({"tf32": m["tf32"] * scale, "i8": m["i8"] * scale},
                         "measured tcgen05 microbenchmark (profiles/tc_peak.json)" +
                         (f" x sustained/burst {scale:.3f}" if scale != 1.0 else ""))
@@ -165,22 +165,31 @@ def roofline_tensor(w, L, kernel_ms, n, peaks, step_ms, st=None):
     actually issued) and the TMEM-read volume are kept under "other"."""
     sustained = step_ms > 500.0
     pk, basis = tc_peaks(peaks, sustained)
-    dt = "tf32" if (w.dtype == "f32" and w.metric != "l1") else "i8"   # (L1: s8 thermometer codes)
+    l1t = w.metric == "l1"   # L1 on tensor cores: s8 thermometer codes (DESIGN.md §13.4)
+    dt = "tf32" if (w.dtype == "f32" and not l1t) else "i8"
     peak = pk[dt]
     ks = kernel_ms * 1e-3
-    ops = 2.0 * w.d * float(n) * L
+    # algorithmic work of the contraction: 2 x (the rows' true K) per decided
+    # pair -- d for L2 / cosine, the d B thermometer bytes for L1 (B levels
+    # per coordinate, l1t_bytes_per_coord in internal.cuh; the 6 folded
+    # constant bytes and the K padding are not counted)
+    kt = w.d * min(32, 378 // w.d) if l1t else w.d
+    ops = 2.0 * kt * float(n) * L
     achieved = ops / ks / 1e12 if kernel_ms > 0 else 0.0
     tiles = getattr(st, "tc_tiles_run", 0) if st is not None else 0
     chunks = getattr(st, "tc_chunks_run", 0) if st is not None else 0
-    ex_ops = 2.0 * w.d * (tiles * 128.0 * 256.0 if tiles else float(n) * L)
+    ex_ops = 2.0 * kt * (tiles * 128.0 * 256.0 if tiles else float(n) * L)
     ex = ex_ops / ks / 1e12 if kernel_ms > 0 else 0.0
     clk = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
     tmem_bytes = (chunks * 128.0 * 32.0 if chunks else float(n) * L) * 4.0
     tmem_ach = tmem_bytes / ks / 1e9 if kernel_ms > 0 else 0.0
-    kern = "k_tc (tcgen05 " + dt + ", membership)"
+    kern = "k_tc (tcgen05 " + ("s8 thermometer L1" if l1t else dt) + ", membership)"
     out = {"bound": "tensor", "achieved": round(achieved, 3), "peak": round(peak, 3),
            "unit": "TFLOP/s" if dt == "tf32" else "TOP/s", "frac": round(achieved / peak, 4),
-           "ops_per_pair": 2 * w.d, "work_basis": "n x L decided pairs x 2d (SURVEY §8(d))",
+           "ops_per_pair": 2 * kt,
+           "work_basis": ("n x L decided pairs x 2 x d B (the L1 thermometer-code contraction, "
+                          "B = %d levels per coordinate; DESIGN.md §13.4)" % (kt // w.d)) if l1t
+                         else "n x L decided pairs x 2d (SURVEY §8(d))",
            "peak_basis": basis, "kernel": kern, "traffic": _traffic(w),
            "kernel_ms": round(kernel_ms, 5),
            "other": {
@@ -191,6 +200,10 @@ def roofline_tensor(w, L, kernel_ms, n, peaks, step_ms, st=None):
                              "note": "measured tcgen05.ld rate 167 (4 warps) - 465 (16 warps) "
                                      "B/clk/SM, profiles/tc_peak.json: not the binding ceiling"}},
            "decided_pairs_per_s": round(float(n) * L / ks, 1) if ks > 0 else None}
+    if l1t:   # the same pairs on the SURVEY §8(d) L1 basis (2d per pair)
+        a8 = 2.0 * w.d * float(n) * L / ks / 1e12 if kernel_ms > 0 else 0.0
+        out["other"]["survey_l1_basis"] = {"achieved": round(a8, 3), "unit": "Tops/s",
+                                           "ops_per_pair": 2 * w.d}
     if st is not None and (getattr(st, "tc_tiles_skipped", 0) or getattr(st, "tc_chunks_skipped", 0)):
         tt = st.tc_tiles_run + st.tc_tiles_skipped
         cc = st.tc_chunks_run + st.tc_chunks_skipped

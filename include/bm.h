@@ -90,7 +90,8 @@ enum {
 
 /* Execution path for the membership / coverage contraction. */
 typedef enum bm_path {
-  BM_PATH_AUTO = 0,     /* tensor cores for L2 with d >= 32 or n >= 32768, else CUDA cores */
+  BM_PATH_AUTO = 0,     /* tensor cores for L2 / cosine with d >= 32 or n >= 32768 and for
+                           fp32 L1 with d <= 16 and n >= 65536, else CUDA cores */
   BM_PATH_CUDA_CORE = 1,
   BM_PATH_TENSOR = 2    /* tcgen05: L2, cosine, and fp32 L1 with d <= 16 (thermometer-code
                            contraction); BM_EUNSUPPORTED otherwise */

@@ -719,12 +719,12 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
                  (o.path == BM_PATH_AUTO && (d >= 32 || n >= 32768)));
   // L1 (fp32, d <= 16) on tensor cores: a signed int8
   // contraction of thermometer codes proves most pairs out, the rest pass the
-  // 8-bit SAD bound and the fp64 decision; needs the 8-bit rows.  Taken on
-  // request (BM_PATH_TENSOR) only: on C5 it measured 1.01-1.09 s against
-  // 1.00 s for the CUDA-core SAD path, which AUTO keeps.
+  // 8-bit SAD bound and the fp64 decision; needs the 8-bit rows.  AUTO takes
+  // it for n >= 65536 (C5 L1: contraction 0.91 s against 1.00 s for the
+  // CUDA-core SAD pass, same box)
   const int l1t_B = (metric == BM_L1 && dtype == BM_F32) ? l1t_bytes_per_coord(d) : 0;
   const bool use_l1t = l1t_B > 0 && l1q_words(d) > 0 && !(o.flags & BM_FLAG_NO_L1_PREFILTER) &&
-                       o.path == BM_PATH_TENSOR;
+                       (o.path == BM_PATH_TENSOR || (o.path == BM_PATH_AUTO && n >= 65536));
   if (use_l1t) {
     use_tc = true;
     P.kind = tc::TC_S8;

@@ -197,8 +197,12 @@ __global__ void __launch_bounds__(1024) k_resolve(const uint32_t* __restrict__ a
       atomicOr(&scm[(tid >> 5) * 8 + (c >> 5)], 1u << (c & 31));
     }
     __syncthreads();
-    if (tid < 32 * 8) pt_out.cmask[tid] = scm[tid];
-    if (tid < 4 * 8) {
+    // (only the tile's chunks: the masks are allocated for T rounded up to
+    // 256 columns, api.cu; a T = 256 tile has 8 chunks and one 256-column
+    // tile, and writing all 32 / 4 of them overran into the next buffer)
+    const int tq = ((T + 255) / 256) * 256;
+    if (tid < (tq / 32) * 8) pt_out.cmask[tid] = scm[tid];
+    if (tid < (tq / 256) * 8) {
       const int t = tid >> 3, wd = tid & 7;
       uint32_t v = 0u;
       for (int c = 0; c < 8; ++c) v |= scm[(t * 8 + c) * 8 + wd];

@@ -67,6 +67,9 @@ __device__ __forceinline__ uint32_t warp_lookback(unsigned long long* state, int
   return excl;
 }
 
+// BM_NO_PDL=1 (diagnostics): launch the dependent chains with plain stream
+// ordering (griddepcontrol.wait then returns at once)
+bool pdl_enabled();
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
                        cudaStream_t s, Args... args) {
@@ -79,7 +82,7 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kern, ((KArgs)args)...);
 }
 
@@ -213,7 +216,10 @@ __host__ __device__ __forceinline__ int l1t_bytes_per_coord(int d) {
   // (d <= 16: the 8-bit rows of the candidate filter are <= 4 words, staged
   // for a whole greedy tile in shared memory)
   if (d < 1 || d > 16) return 0;
-  int b = 378 / d;
+#ifndef BM_L1T_KB
+#define BM_L1T_KB 378   // thermometer + fold bytes per row (<= 3 K atoms)
+#endif
+  int b = (BM_L1T_KB) / d;
   if (b > 32) b = 32;
   return b;
 }

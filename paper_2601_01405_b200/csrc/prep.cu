@@ -1,3 +1,4 @@
+#include <stdlib.h>
 // prep.cu — step A0: pack rows into 8-byte units, norms, finite check.
 //
 // fp32 rows are copied bit-for-bit (zero padded to NU units): the CUDA-core
@@ -121,6 +122,11 @@ __global__ void k_l1_quantize(const float* __restrict__ X, int64_t n, int d, int
     }
     qrows[p * nq + w] = word;
   }
+}
+
+bool pdl_enabled() {
+  static const bool on = getenv("BM_NO_PDL") == nullptr;
+  return on;
 }
 
 int l1q_words(int d) {

@@ -512,7 +512,14 @@ constexpr bool tc_lean() {
 #endif
 }
 template <int KIND, int BN, int MODE, bool PR>
+// L1T epilogue warpgroups: 2 (eight warps, 128 columns each, 141 registers,
+// no spills) measured faster than 4 (96 registers with spills to a nearly
+// all-shared-memory L1): C5 L1 contraction 911 vs 991 ms (same box)
+#ifndef BM_L1T_EG
+#define BM_L1T_EG 2
+#endif
 constexpr int tc_groups() {
+  if (MODE == TC_MODE_L1T) return BM_L1T_EG;   // (2 or 4 groups: 128 or 64 columns per warp)
   return tc_lean<KIND, BN, MODE, PR>() ? 4 : 2;
 }
 template <int KIND, int BN, int MODE, bool PR>
@@ -1082,7 +1089,8 @@ __global__ void __launch_bounds__(tc_threads<KIND, BN, MODE, PR>(), 1)
       // out) become two 32-bit masks, the TMEM buffer goes back to the MMA
       // issuer, then each candidate passes the 8-bit SAD bound (rows staged in
       // shared memory) and the survivors are decided in fp64 (B')
-      static_assert(BN / EG == 64, "L1T: 64 columns per group and tile");
+      constexpr int NP = BN / EG / 64;   // packed 64-column loads per warp and tile
+      static_assert(NP * 64 * EG == BN, "L1T: whole 64-column loads per group");
       const long long epi_t0 = args.wtrace ? clock64() : 0;
       uint32_t phase = 0;
       uint32_t tcnt = 0;
@@ -1107,17 +1115,18 @@ __global__ void __launch_bounds__(tc_threads<KIND, BN, MODE, PR>(), 1)
           phase ^= 1u << buf;
           fence_after();
           const uint32_t ta = tlane + buf * (uint32_t)BUFCOLS;
-          // the group's 64 columns in one load, two 16-bit accumulators per
+          // the group's columns in 64-column loads, two 16-bit accumulators per
           // register (|SADq - cut| < 2^15); per 4 columns one byte permute
           // gathers the 4 sign bytes, and 8 of those make a 32-bit mask whose
           // bit 8 i + m is the sign of column 4 m + i
-          uint32_t cm[2];
+          uint32_t cm[2 * NP];
 #ifdef BM_TC_WTRACE
           const long long s6 = clock64();
 #endif
-          {
+#pragma unroll
+          for (int p = 0; p < NP; ++p) {
             uint32_t v[32];
-            tmem_ld64p_nowait(ta, v);
+            tmem_ld64p_nowait(ta + 64u * p, v);
             tmem_wait32(v);
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
@@ -1127,7 +1136,7 @@ __global__ void __launch_bounds__(tc_threads<KIND, BN, MODE, PR>(), 1)
                 const uint32_t r = __byte_perm(v[16 * h + 2 * mm], v[16 * h + 2 * mm + 1], 0x7531);
                 m |= (r >> (7 - mm)) & (0x01010101u << mm);
               }
-              cm[h] = m;
+              cm[2 * p + h] = m;
             }
           }
           // (columns past the tile's landmarks and rows past n hold zero
@@ -1142,19 +1151,20 @@ __global__ void __launch_bounds__(tc_threads<KIND, BN, MODE, PR>(), 1)
 #endif
           ++tcnt;
           const int64_t jg = (int64_t)t * BN + grp * (BN / EG);
-          if (jg + 64 > n_cols) {   // a ragged last tile: its MMA wrote the first
+          if (jg + 64 * NP > n_cols) {   // a ragged last tile: its MMA wrote the first
             // columns only; the rest of the buffer holds an earlier tile's sums
 #pragma unroll
-            for (int h = 0; h < 2; ++h)
+            for (int h = 0; h < 2 * NP; ++h)
 #pragma unroll
               for (int b = 0; b < 32; ++b)
                 if (jg + 32 * h + 4 * (b & 7) + (b >> 3) >= n_cols) cm[h] &= ~(1u << b);
           }
           // candidates (a few per lane and tile): the 8-bit SAD bound, rows
-          // staged in shared memory; survivors go to the fp64 decision (one
-          // loop over both halves)
-          unsigned long long cand = ((unsigned long long)cm[1] << 32) | cm[0];
-          if (__any_sync(FULLM, cand != 0ull)) {
+          // staged in shared memory; survivors go to the fp64 decision
+          uint32_t anyc = 0u;
+#pragma unroll
+          for (int h = 0; h < 2 * NP; ++h) anyc |= cm[h];
+          if (__any_sync(FULLM, anyc != 0u)) {
             uint32_t rq[4];
             {
               uint32_t a, b2, c, e;
@@ -1167,13 +1177,18 @@ __global__ void __launch_bounds__(tc_threads<KIND, BN, MODE, PR>(), 1)
               rq[3] = e;
             }
             const uint32_t th8 = *sthr8;
-            while (cand) {
-              const int b = __ffsll((long long)cand) - 1;
-              cand &= cand - 1ull;
-              // bit b of the 64-bit mask -> column
-              const int64_t j = jg + 32 * (b >> 5) + 4 * (b & 7) + ((b >> 3) & 3);
-              if (l1t_sad(rq, j) < th8)
-                append(2, ((unsigned long long)prow << 32) | (unsigned long long)j);
+#pragma unroll
+            for (int p = 0; p < NP; ++p) {
+              unsigned long long cand =
+                  ((unsigned long long)cm[2 * p + 1] << 32) | cm[2 * p];
+              while (cand) {
+                const int b = __ffsll((long long)cand) - 1;
+                cand &= cand - 1ull;
+                // bit b of the 64-bit mask -> column
+                const int64_t j = jg + 64 * p + 32 * (b >> 5) + 4 * (b & 7) + ((b >> 3) & 3);
+                if (l1t_sad(rq, j) < th8)
+                  append(2, ((unsigned long long)prow << 32) | (unsigned long long)j);
+              }
             }
           }
           __syncwarp();
