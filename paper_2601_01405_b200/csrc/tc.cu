@@ -2187,19 +2187,21 @@ __global__ void k_l1t_prep(const float* __restrict__ X, int64_t n, int d, int B,
     const int la = __shfl_sync(0xffffffffu, lv, ja), lb = __shfl_sync(0xffffffffu, lv, jb);
     if (b0 >= row_bytes) continue;
     uint32_t w[2] = {0u, 0u};
+    int kk = b0 - ja * B;   // level of byte b0 within coordinate ja (no per-byte divide)
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       const int b = b0 + k;
       int v = 0;
+      const bool second = kk >= B;   // (bytes b0 .. b0 + 7 span at most two coordinates)
       if (b < dB) {
-        const int j = b / B;
-        v = (j == ja ? la : lb) > b - j * B ? -2 : 0;
+        v = (second ? lb : la) > (second ? kk - B : kk) ? -2 : 0;
       } else if (b < dB + 3) {
         v = 1;
       } else if (b < dB + 6) {
         v = l1t_chunk(r, b - dB - 3);
       }
       w[k >> 2] |= (uint32_t)(uint8_t)(int8_t)v << (8 * (k & 3));
+      ++kk;
     }
     *reinterpret_cast<uint2*>(xop + p * (int64_t)row_bytes + b0) = make_uint2(w[0], w[1]);
   }
