@@ -958,7 +958,6 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
     ta.key_cap = key_cap;
     set_recheck(ta, rows, 2 * nu, d, th, prune ? ps.col_pt : new_lm, ties_dev, tie_cap, stats);
     if (use_l1t) {
-      ta.l1 = 1;
       ta.l1t = 1;
       ta.qrows = qrows;
       ta.nq = nq;

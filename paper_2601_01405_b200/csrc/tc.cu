@@ -433,7 +433,7 @@ __device__ __forceinline__ uint32_t sel32(const uint32_t (&v)[32], int i) {
 // B': the oracle's fp64 decision for points p, q (ascending coordinates, no
 // contraction; cosine with the zero-vector rule, A6/A7).
 __device__ __noinline__ bool pair_in_fp64(const float* xrows, int xstride, int dd, int cosine,
-                                          int l1, double eps, double eps2, int64_t p, int64_t q,
+                                          double eps, double eps2, int64_t p, int64_t q,
                                           double* dist) {
   const float* x = xrows + p * (int64_t)xstride;
   const float* y = xrows + q * (int64_t)xstride;
@@ -477,16 +477,36 @@ __device__ __noinline__ bool pair_in_fp64(const float* xrows, int xstride, int d
     for (int i = 0; i < G; ++i) {
       if (k0 + i < dd) {
         const double t = __dsub_rn((double)xa[i], (double)ya[i]);
-        sacc = l1 ? __dadd_rn(sacc, fabs(t)) : __dadd_rn(sacc, __dmul_rn(t, t));
+        sacc = __dadd_rn(sacc, __dmul_rn(t, t));
       }
     }
   }
-  if (l1) {   // Manhattan (reading A8): sum_j |x_j - y_j| in ascending j, against eps
-    *dist = sacc;
-    return sacc < eps;
-  }
   *dist = __dsqrt_rn(sacc);
   return sacc < eps2;
+}
+
+// B' for L1 (the thermometer path): the oracle's fp64 Manhattan distance,
+// sum_j |x_j - y_j| in ascending j (reading A8).  A separate function: one
+// more argument on pair_in_fp64's call made the tf32 instances spill.
+__device__ __noinline__ bool pair_in_fp64_l1(const float* xrows, int xstride, int dd, double eps,
+                                             int64_t p, int64_t q, double* dist) {
+  const float* x = xrows + p * (int64_t)xstride;
+  const float* y = xrows + q * (int64_t)xstride;
+  constexpr int G = 16;
+  double sacc = 0.0;
+  for (int k0 = 0; k0 < dd; k0 += G) {
+    float xa[G], ya[G];
+#pragma unroll
+    for (int i = 0; i < G; ++i) {
+      xa[i] = k0 + i < dd ? __ldg(x + k0 + i) : 0.f;
+      ya[i] = k0 + i < dd ? __ldg(y + k0 + i) : 0.f;
+    }
+#pragma unroll
+    for (int i = 0; i < G; ++i)
+      if (k0 + i < dd) sacc = __dadd_rn(sacc, fabs(__dsub_rn((double)xa[i], (double)ya[i])));
+  }
+  *dist = sacc;
+  return sacc < eps;
 }
 
 // ------------------------------------------------------------------ kernel
@@ -1013,8 +1033,12 @@ __global__ void __launch_bounds__(tc_threads<KIND, BN, MODE, PR>(), 1)
       if (j >= n_cols || p >= args.n) return;   // padding rows / columns never qualify
       const int64_t qp = args.lm_idx[j];
       double dist;
-      const bool in = pair_in_fp64(args.xrows, args.xstride, args.d, args.cosine, args.l1,
-                                   args.eps, args.eps2, p, qp, &dist);
+      bool in;
+      if constexpr (MODE == TC_MODE_L1T)
+        in = pair_in_fp64_l1(args.xrows, args.xstride, args.d, args.eps, p, qp, &dist);
+      else
+        in = pair_in_fp64(args.xrows, args.xstride, args.d, args.cosine, args.eps, args.eps2, p,
+                          qp, &dist);
       if (fabs(dist - args.eps) <= args.tie_abs) {
         const unsigned long long k = atomicAdd(&args.stats->near_ties, 1ull);
         if ((int64_t)k < args.tie_cap && args.ties) {
@@ -1418,7 +1442,7 @@ __global__ void __launch_bounds__(tc_threads<KIND, BN, MODE, PR>(), 1)
                     const int i = __ffs(band) - 1;
                     band &= band - 1u;
                     double dist;
-                    if (pair_in_fp64(args.xrows, args.xstride, args.d, args.cosine, 0, args.eps,
+                    if (pair_in_fp64(args.xrows, args.xstride, args.d, args.cosine, args.eps,
                                      args.eps2, args.lm_idx[a], args.lm_idx[j0 + i], &dist))
                       mask |= 1u << i;
                   }

@@ -71,8 +71,7 @@ struct TcArgs {
   double eps, eps2, tie_rel;
   double tie_abs;          // tie_rel * eps (precomputed: no fp64 multiply in the epilogue)
   const int32_t* lm_idx;   // landmark column -> point index
-  int cosine;              // recheck with the cosine formula (else Euclidean, or L1 below)
-  int l1;                  // recheck with the L1 formula
+  int cosine;              // recheck with the cosine formula (else Euclidean; L1T: Manhattan)
   // L1 on tensor cores (TC_MODE_L1T, l1t != 0): candidates (SADq < cut, the
   // sign of the folded accumulator) pass the 8-bit SAD filter of the
   // CUDA-core path (qrows: nq words per point, qparam: coordinate range)
