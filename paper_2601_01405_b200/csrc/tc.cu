@@ -532,19 +532,31 @@ constexpr bool tc_lean() {
 #endif
 }
 template <int KIND, int BN, int MODE, bool PR>
-// L1T epilogue warpgroups: 2 (eight warps, 128 columns each, 141 registers,
-// no spills) measured faster than 4 (96 registers with spills to a nearly
-// all-shared-memory L1): C5 L1 contraction 911 vs 991 ms (same box)
+// L1T epilogue warpgroups: 4 (64 columns per warp) with two role warps
+// (576 threads, 92 registers, no spills): C5 L1 contraction 832 ms; 2 groups
+// (128 columns per warp, 137 registers): 891 ms; 4 groups beside four role
+// warps (640 threads, 96 registers with spills to a nearly all-shared-memory
+// L1): 991 ms (same box each)
 #ifndef BM_L1T_EG
-#define BM_L1T_EG 2
+#define BM_L1T_EG 4
 #endif
 constexpr int tc_groups() {
   if (MODE == TC_MODE_L1T) return BM_L1T_EG;   // (2 or 4 groups: 128 or 64 columns per warp)
   return tc_lean<KIND, BN, MODE, PR>() ? 4 : 2;
 }
+// role warps ahead of the epilogue: warp 0 TMA producer, warp 1 MMA issuer,
+// warp 2 TMEM allocator, warp 3 idle; the epilogue warps follow (TMEM lane
+// quadrant = warp % 4, so every four consecutive epilogue warps cover the 128
+// lanes).  L1T drops the two spare warps (the MMA warp allocates TMEM): with
+// four epilogue groups its 576 threads fit 92 registers without spills
+// (C5 L1 contraction 891 -> 832 ms against two groups)
+template <int MODE>
+constexpr int tc_rolew() {
+  return MODE == TC_MODE_L1T ? 2 : 4;
+}
 template <int KIND, int BN, int MODE, bool PR>
 constexpr int tc_threads() {
-  return 128 + 128 * tc_groups<KIND, BN, MODE, PR>();
+  return 32 * tc_rolew<MODE>() + 128 * tc_groups<KIND, BN, MODE, PR>();
 }
 
 template <int KIND, int RA, int BN, int KATOMS, int STAGES, int ABUF, int MODE, bool BRES,
@@ -646,7 +658,7 @@ __global__ void __launch_bounds__(tc_threads<KIND, BN, MODE, PR>(), 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
     if constexpr (FOLD) asm volatile("prefetch.tensormap [%0];" ::"l"(&tmK) : "memory");
   }
-  if (warp == 2) {
+  if (warp == (tc_rolew<MODE>() == 2 ? 1 : 2)) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      su32(tmem_slot)),
                  "r"(512)
@@ -984,14 +996,14 @@ __global__ void __launch_bounds__(tc_threads<KIND, BN, MODE, PR>(), 1)
         wflush(9, 10);
       }
     }
-  } else if (warp >= 4) {
+  } else if (warp >= tc_rolew<MODE>()) {
     // ---------------- epilogue: warps 4-7 take the first half of every tile's
     // columns, warps 8-11 the second half; warp w reads TMEM lanes 32*(w%4)..
-    const int ew = warp - 4, grp = ew >> 2, q = warp & 3;
+    const int ew = warp - tc_rolew<MODE>(), grp = ew >> 2, q = warp & 3;
     // resident B: the in-test offsets of all the launch's columns in shared memory
     float* sdj = reinterpret_cast<float*>(sm + S::DJ_OFF);
     if constexpr (S::DJ_BYTES > 0) {
-      for (int64_t j = threadIdx.x - 128; j < n_tiles * BN; j += 128 * EG)
+      for (int64_t j = threadIdx.x - 32 * tc_rolew<MODE>(); j < n_tiles * BN; j += 128 * EG)
         sdj[j] = __ldg(args.col_a + j);
       asm volatile("bar.sync 1, %0;" ::"n"(128 * EG) : "memory");   // the epilogue warps only
     }
@@ -1004,9 +1016,9 @@ __global__ void __launch_bounds__(tc_threads<KIND, BN, MODE, PR>(), 1)
     uint32_t* sthr8 = bcount + S::EPI_WARPS;
     const bool q8s = S::Q8_BYTES > 0;   // (dispatch_l1t: nq == 4, <= 1024 columns)
     if constexpr (S::Q8_BYTES > 0) {
-      if (threadIdx.x == 128) *sthr8 = l1q_threshold(args.qparam, args.eps, args.d);
+      if (threadIdx.x == 32 * tc_rolew<MODE>()) *sthr8 = l1q_threshold(args.qparam, args.eps, args.d);
       if (q8s) {
-        for (int64_t t = threadIdx.x - 128; t < n_cols * 4; t += 128 * EG) {
+        for (int64_t t = threadIdx.x - 32 * tc_rolew<MODE>(); t < n_cols * 4; t += 128 * EG) {
           const int64_t j = t >> 2;
           const int w = (int)(t & 3);
           sq8[t] = w < args.nq ? __ldg(args.qrows + (int64_t)__ldg(args.lm_idx + j) * args.nq + w)
@@ -1620,7 +1632,7 @@ __global__ void __launch_bounds__(tc_threads<KIND, BN, MODE, PR>(), 1)
   __syncthreads();
   fence_after();
   if (threadIdx.x == 0) TC_STAMP(11);
-  if (warp == 2) {
+  if (warp == (tc_rolew<MODE>() == 2 ? 1 : 2)) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512)
                  : "memory");
   }

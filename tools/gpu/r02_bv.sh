@@ -17,3 +17,7 @@ python tools/launch_summary.py gpurun_out/bv_launches_default.csv > gpurun_out/b
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:"^k_tc$" \
    --launch-skip 60 --launch-count 1 -o gpurun_out/bv_ncu_c5l1_member -f python tools/one_cover.py c5_l1 1 > gpurun_out/bv_ncu.log 2>&1
 python tools/ncu_summary.py gpurun_out/bv_ncu_c5l1_member.ncu-rep > gpurun_out/bv_ncu_c5l1_member.txt 2>&1; head -20 gpurun_out/bv_ncu_c5l1_member.txt
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:"^k_tc$" \
+   --launch-skip 9 --launch-count 1 -o gpurun_out/bv_ncu_c4_member -f python tools/one_cover.py c4 2 > gpurun_out/bv_ncu4.log 2>&1
+python tools/ncu_summary.py gpurun_out/bv_ncu_c4_member.ncu-rep > gpurun_out/bv_ncu_c4_member.txt 2>&1; head -3 gpurun_out/bv_ncu_c4_member.txt
+timeout 900 python tools/bench_next.py --reps 3 > gpurun_out/bv_next.jsonl 2> gpurun_out/bv_next.err; echo "next rc=$?"
