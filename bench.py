@@ -173,7 +173,7 @@ def roofline_tensor(w, L, kernel_ms, n, peaks, step_ms, st=None):
     # pair -- d for L2 / cosine, the d B thermometer bytes for L1 (B levels
     # per coordinate, l1t_bytes_per_coord in internal.cuh; the 6 folded
     # constant bytes and the K padding are not counted)
-    kt = w.d * min(32, 378 // w.d) if l1t else w.d
+    kt = w.d * min(32, 314 // w.d) if l1t else w.d   # (internal.cuh l1t_bytes_per_coord)
     ops = 2.0 * kt * float(n) * L
     achieved = ops / ks / 1e12 if kernel_ms > 0 else 0.0
     tiles = getattr(st, "tc_tiles_run", 0) if st is not None else 0

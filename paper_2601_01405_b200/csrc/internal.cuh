@@ -210,14 +210,16 @@ __device__ __forceinline__ uint32_t vsad4(uint32_t a, uint32_t b, uint32_t c) {
 // L1 >= eps (1 + 4e-6): out, and not a near tie.  Bytes per coordinate B
 // (0: the path does not apply): the row (d B bytes + 6 bytes of folded
 // constants, tc.cu k_l1t_prep) fills at most three 128-byte K atoms (C5,
-// d = 16: B = 23, 24 levels; measured on C5, 24 levels leave ~0.26% of the
-// pairs as candidates for the 8-bit bound, 16 levels ~1.2%).
+// d = 16: B = 19, 20 levels, 310 bytes = ten 32-byte K steps; measured on
+// C5, 24 levels leave ~0.26% of the pairs as candidates for the 8-bit bound,
+// 20 levels ~0.5%, 16 levels ~1.2%; the contraction took 836 / 810 / 855 ms
+// at B = 23 / 19 / 17, same box).
 __host__ __device__ __forceinline__ int l1t_bytes_per_coord(int d) {
   // (d <= 16: the 8-bit rows of the candidate filter are <= 4 words, staged
   // for a whole greedy tile in shared memory)
   if (d < 1 || d > 16) return 0;
 #ifndef BM_L1T_KB
-#define BM_L1T_KB 378   // thermometer + fold bytes per row (<= 3 K atoms)
+#define BM_L1T_KB 314   // thermometer + fold bytes per row (<= 3 K atoms)
 #endif
   int b = (BM_L1T_KB) / d;
   if (b > 32) b = 32;
