@@ -683,7 +683,10 @@ __global__ void __launch_bounds__(tc_threads<KIND, BN, MODE, PR>(), 1)
       args.l_count_dev ? min((int64_t)*args.l_count_dev, args.L) : args.L;
   const int64_t lpos0 = args.l_total_dev ? (int64_t)*args.l_total_dev - n_cols : 0;
   const int64_t n_tiles = (n_cols + BN - 1) / BN;
-  int64_t n_chunks = (4 * (int64_t)gridDim.x + args.n_mblk - 1) / args.n_mblk;
+  // (a single A buffer of wide rows (C4: 112 KB) is reloaded per unit without
+  // overlap, so those instances split the columns only below two row blocks per CTA)
+  constexpr int64_t UPC = (ABUF == 1 && KATOMS >= 4) ? 2 : 4;   // target units per CTA
+  int64_t n_chunks = (UPC * (int64_t)gridDim.x + args.n_mblk - 1) / args.n_mblk;
   n_chunks = max((int64_t)1, min(n_chunks, n_tiles));
   const int64_t tiles_per_chunk = n_tiles > 0 ? (n_tiles + n_chunks - 1) / n_chunks : 1;
   n_chunks = n_tiles > 0 ? (n_tiles + tiles_per_chunk - 1) / tiles_per_chunk : 0;

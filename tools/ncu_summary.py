@@ -5,6 +5,7 @@ roofline cares about: duration, DRAM bytes, pipe utilisation, issue, occupancy.
 """
 import csv
 import io
+import re
 import subprocess
 import sys
 
@@ -31,6 +32,14 @@ WANT = [
 ]
 
 
+# memory-hierarchy throughputs and the top stall reasons (any name matching)
+EXTRA = re.compile(r"^(lts__t_(bytes|sectors)[^,]*(sum|pct_of_peak_sustained_elapsed)$"
+                   r"|lts__throughput\.avg\.pct_of_peak_sustained_elapsed"
+                   r"|l1tex__m_xbar2l1tex_read_bytes\.sum(\.per_second)?"
+                   r"|l1tex__throughput\.avg\.pct_of_peak_sustained_active"
+                   r"|smsp__average_warp(s|_latency)_issue_stalled_[a-z_]+_per_issue_active\.ratio)")
+
+
 def main(path):
     raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
@@ -46,6 +55,18 @@ def main(path):
             if key in h:
                 i = h.index(key)
                 print(f"  {label:32s} {r[i]} {units[i]}")
+        stalls = []
+        for i, c in enumerate(h):
+            if EXTRA.match(c) and r[i] not in ("", "n/a"):
+                if "issue_stalled" in c:
+                    try:
+                        stalls.append((float(r[i].replace(",", "")), c))
+                    except ValueError:
+                        pass
+                else:
+                    print(f"  {c:60s} {r[i]} {units[i]}")
+        for v, c in sorted(stalls, reverse=True)[:8]:
+            print(f"  {c:60s} {v:.3f}")
         for c in tensor_cols:
             i = h.index(c)
             if r[i] not in ("", "0", "n/a"):
