@@ -23,6 +23,10 @@
 //               atomic per flush.  Lean instances (tf32 membership, unpruned,
 //               e.g. C2 / C5 cosine): 32-column loads, the TMEM buffer released
 //               before staged keys are flushed and band pairs re-decided.
+//   L1T (the L1 thermometer-code contraction): two role
+//   warps (producer; MMA issuer that also allocates TMEM) and four epilogue
+//   warpgroups (576 threads); the accumulator's sign is the candidate mask,
+//   candidates pass an 8-bit SAD bound, survivors get the fp64 decision.
 // Float exactness: with x, l rounded to tf32 and fp32
 // accumulation, |acc - x.l| <= C (|x|^2 + |l|^2)/2 with a global constant C;
 // the per-row/per-column thresholds fold that bound in, so "out" and "in"
@@ -2220,29 +2224,33 @@ __global__ void k_l1t_prep(const float* __restrict__ X, int64_t n, int d, int B,
   for (int o = 16; o > 0; o >>= 1) np += __shfl_xor_sync(0xffffffffu, np, o);
   const int r = np - l1t_cut(qparam, eps, d, B);
   const int dB = d * B;
+  // the folded constant bytes dB .. dB + 5 (1, 1, 1 and n_p - cut in three
+  // signed bytes), little-endian from byte dB
+  const uint64_t tail = 0x010101ull | ((uint64_t)(uint8_t)(int8_t)l1t_chunk(r, 0) << 24) |
+                        ((uint64_t)(uint8_t)(int8_t)l1t_chunk(r, 1) << 32) |
+                        ((uint64_t)(uint8_t)(int8_t)l1t_chunk(r, 2) << 40);
+  auto bytemask = [](int nb) -> uint64_t {   // the low nb bytes (clamped to 0 .. 8)
+    return nb >= 8 ? ~0ull : (nb <= 0 ? 0ull : ((1ull << (8 * nb)) - 1ull));
+  };
   for (int h = 0; h < row_bytes; h += 256) {   // (rows of up to 512 bytes: two passes)
     const int b0 = h + lane * 8;
     const int ja = min(b0 / B, 31), jb = min((b0 + 7) / B, 31);
     const int la = __shfl_sync(0xffffffffu, lv, ja), lb = __shfl_sync(0xffffffffu, lv, jb);
     if (b0 >= row_bytes) continue;
-    uint32_t w[2] = {0u, 0u};
-    int kk = b0 - ja * B;   // level of byte b0 within coordinate ja (no per-byte divide)
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int b = b0 + k;
-      int v = 0;
-      const bool second = kk >= B;   // (bytes b0 .. b0 + 7 span at most two coordinates)
-      if (b < dB) {
-        v = (second ? lb : la) > (second ? kk - B : kk) ? -2 : 0;
-      } else if (b < dB + 3) {
-        v = 1;
-      } else if (b < dB + 6) {
-        v = l1t_chunk(r, b - dB - 3);
-      }
-      w[k >> 2] |= (uint32_t)(uint8_t)(int8_t)v << (8 * (k & 3));
-      ++kk;
+    // byte i of the 8 is level kk + i of coordinate ja while kk + i < B (set
+    // iff i < la - kk), else level kk + i - B of coordinate jb (set iff
+    // i < lb + B - kk): two byte-prefix masks instead of a per-byte loop
+    const int kk = b0 - ja * B, e1 = B - kk;
+    uint64_t m = bytemask(max(0, min(min(8, e1), la - kk)));
+    if (e1 < 8) m |= bytemask(max(e1, min(8, e1 + lb))) & ~bytemask(e1);
+    uint64_t v = m & 0xfefefefefefefefeull;   // -2 per set level
+    if (b0 + 8 > dB) {   // past the coordinates: the constant bytes, then zeros
+      v &= bytemask(max(0, dB - b0));
+      const int off = b0 - dB;   // (-8, row_bytes)
+      if (off < 6) v |= off >= 0 ? (tail >> (8 * off)) : (tail << (8 * -off));
     }
-    *reinterpret_cast<uint2*>(xop + p * (int64_t)row_bytes + b0) = make_uint2(w[0], w[1]);
+    *reinterpret_cast<uint2*>(xop + p * (int64_t)row_bytes + b0) =
+        make_uint2((uint32_t)v, (uint32_t)(v >> 32));
   }
   if (lane == 0) nrm[p] = np;
 }
