@@ -826,6 +826,8 @@ bm_status build_impl(const void* points, bm_dtype dtype, int64_t n, int32_t d, b
     TRY(pool.alloc(&ps.seg, (size_t)kPruneCells + 1));
     TRY(pool.alloc(&ps.center, (size_t)kPruneCells * d));
     TRY(pool.alloc(&ps.radius, (size_t)kPruneCells));
+    TRY(pool.alloc(&ps.part, (size_t)kPruneCells * kPruneSplit * 128));
+    TRY(pool.alloc(&ps.rad2, (size_t)kPruneCells));
     TRY(pool.alloc(&ps.near, (size_t)kPruneCells * KWd));
     TRY(pool.alloc(&ps.bmask, (size_t)nblk * KWd));
     TRY(pool.alloc(&ps.xop_perm, (size_t)n * P.row_bytes));

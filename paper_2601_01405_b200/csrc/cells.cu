@@ -29,14 +29,19 @@ constexpr int KC = kPruneCells;          // 256 cells
 constexpr int KW = kPruneCells / 32;     // mask words
 
 // nearest pivot (pivot i = point i * (n / K)); fp32 rows, first d coordinates.
-// The point's row lives in registers (DMAX >= d, zero padded), the pivots in
-// shared memory read as float4 broadcasts (one LDS.128 per four FMAs).
+// Gram form: argmin_k |x - c_k|^2 = argmin_k (|c_k|^2 / 2 - x . c_k), one FMA
+// per coordinate.  Two points per thread live in registers (DMAX >= d, zero
+// padded), the pivots in shared memory read as float4 broadcasts (one LDS.128
+// per eight FMAs).  fp32 rounding may pick another pivot on a near tie: the
+// cells are only a grouping (centre and radius are exact enough in fp64,
+// k_cell_*), no decision depends on which cell a point falls in.
 template <int DMAX>
 __global__ void __launch_bounds__(256) k_cell_assign(const float* __restrict__ xrows, int xstride,
                                                      int d, int64_t n,
                                                      int32_t* __restrict__ cell) {
-  extern __shared__ float4 spiv4[];   // [KC][DMAX / 4]
+  extern __shared__ float4 spiv4[];   // [KC][DMAX / 4], then half norms [KC]
   constexpr int DQ = DMAX / 4;
+  float* shalf = reinterpret_cast<float*>(spiv4 + KC * DQ);
   const int64_t step = n / KC;
   for (int t = threadIdx.x; t < KC * DQ; t += blockDim.x) {
     const int k = t / DQ, q = t - k * DQ;
@@ -49,34 +54,63 @@ __global__ void __launch_bounds__(256) k_cell_assign(const float* __restrict__ x
     spiv4[t] = v;
   }
   __syncthreads();
-  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
-       p += (int64_t)gridDim.x * blockDim.x) {
-    const float* x = xrows + p * xstride;
-    float xr[DMAX];
+  for (int k = threadIdx.x; k < KC; k += blockDim.x) {
+    float h = 0.f;
+    for (int q = 0; q < DQ; ++q) {
+      const float4 v = spiv4[k * DQ + q];
+      h = fmaf(v.x, v.x, h);
+      h = fmaf(v.y, v.y, h);
+      h = fmaf(v.z, v.z, h);
+      h = fmaf(v.w, v.w, h);
+    }
+    shalf[k] = 0.5f * h;
+  }
+  __syncthreads();
+  constexpr bool TWO = DMAX <= 64;   // (two 128-coordinate rows do not fit the registers)
+  const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t p0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p0 < n;
+       p0 += (TWO ? 2 : 1) * nthr) {
+    const int64_t p1 = TWO ? p0 + nthr : n;
+    const float* x0 = xrows + p0 * xstride;
+    const float* x1 = xrows + (p1 < n ? p1 : p0) * xstride;
+    float xa[DMAX], xb[TWO ? DMAX : 1];
 #pragma unroll
-    for (int j = 0; j < DMAX; ++j) xr[j] = j < d ? x[j] : 0.f;
-    float best = INFINITY;
-    int bk = 0;
+    for (int j = 0; j < DMAX; ++j) {
+      xa[j] = j < d ? x0[j] : 0.f;
+      if constexpr (TWO) xb[j] = j < d ? x1[j] : 0.f;
+    }
+    float besta = INFINITY, bestb = INFINITY;
+    int ka = 0, kb = 0;
     for (int k = 0; k < KC; ++k) {
       const float4* c = spiv4 + k * DQ;
-      float s0 = 0.f, s1 = 0.f;
+      const float h = shalf[k];
+      float a0 = h, a1 = 0.f, b0 = h, b1 = 0.f;
 #pragma unroll
       for (int q = 0; q < DQ; ++q) {
         const float4 v = c[q];
-        const float t0 = xr[4 * q] - v.x, t1 = xr[4 * q + 1] - v.y;
-        const float t2 = xr[4 * q + 2] - v.z, t3 = xr[4 * q + 3] - v.w;
-        s0 = fmaf(t0, t0, s0);
-        s1 = fmaf(t1, t1, s1);
-        s0 = fmaf(t2, t2, s0);
-        s1 = fmaf(t3, t3, s1);
+        a0 = fmaf(-xa[4 * q], v.x, a0);
+        a1 = fmaf(-xa[4 * q + 1], v.y, a1);
+        a0 = fmaf(-xa[4 * q + 2], v.z, a0);
+        a1 = fmaf(-xa[4 * q + 3], v.w, a1);
+        if constexpr (TWO) {
+          b0 = fmaf(-xb[4 * q], v.x, b0);
+          b1 = fmaf(-xb[4 * q + 1], v.y, b1);
+          b0 = fmaf(-xb[4 * q + 2], v.z, b0);
+          b1 = fmaf(-xb[4 * q + 3], v.w, b1);
+        }
       }
-      const float sv = s0 + s1;
-      if (sv < best) {
-        best = sv;
-        bk = k;
+      const float sa = a0 + a1, sb = b0 + b1;
+      if (sa < besta) {
+        besta = sa;
+        ka = k;
+      }
+      if (sb < bestb) {
+        bestb = sb;
+        kb = k;
       }
     }
-    cell[p] = bk;
+    cell[p0] = ka;
+    if (TWO && p1 < n) cell[p1] = kb;
   }
 }
 
@@ -140,95 +174,145 @@ __global__ void k_cell_keys(const int32_t* __restrict__ cell, const int32_t* __r
   if (p < n) keys[p] = ((unsigned long long)(uint32_t)rank[cell[p]] << 32) | (uint64_t)p;
 }
 
-// one CTA per cell rank r: the segment of the sorted points with that rank.
-// Warps stride over the points, lanes over the coordinates (coalesced rows).
-__global__ void __launch_bounds__(512) k_cell_stats(const float* __restrict__ xrows, int xstride,
-                                                    int d, const int32_t* __restrict__ perm,
-                                                    const int64_t* __restrict__ seg,
-                                                    const int32_t* __restrict__ rank,
-                                                    double* __restrict__ center,
-                                                    double* __restrict__ radius) {
-  constexpr int NW = 16;   // warps
-  constexpr int UN = 4;    // rows in flight per warp
-  __shared__ double sacc[NW][128];
-  __shared__ double sc[128];
-  __shared__ double sred[NW];
-  __shared__ int s_cell;
-  const int r = blockIdx.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t b = seg[r], e = seg[r + 1];
-  if (threadIdx.x == 0) s_cell = -1;
+// Cell centre and radius (fp64).  The segment of rank r in the sorted order is
+// cut into CS_SPLIT slices, one CTA each (KC * CS_SPLIT CTAs keep every SM
+// busy whatever the cell sizes); warps stride over the slice's points with
+// CS_UN rows in flight, lanes over the coordinates (coalesced rows).
+//   k_cell_sum:    per-slice coordinate sums -> part[r][slice][128]
+//   k_cell_center: centre = sum of the slices in order / count; rad2 = 0
+//   k_cell_rad:    per slice the max squared distance to the centre ->
+//                  atomicMax on the bits of the non-negative double rad2[c]
+//                  (order-independent: the result is deterministic)
+//   k_cell_finish: radius = sqrt(rad2) rounded up; -1 for an empty cell
+constexpr int CS_SPLIT = kPruneSplit;
+constexpr int CS_NW = 8;   // warps per CTA
+constexpr int CS_UN = 8;   // rows in flight per warp
+
+__device__ __forceinline__ void cs_slice(const int64_t* __restrict__ seg, int r, int sp,
+                                         int64_t& b, int64_t& e) {
+  const int64_t sb = seg[r], len = seg[r + 1] - sb;
+  b = sb + len * sp / CS_SPLIT;
+  e = sb + len * (sp + 1) / CS_SPLIT;
+}
+
+__global__ void __launch_bounds__(CS_NW * 32) k_cell_sum(const float* __restrict__ xrows,
+                                                         int xstride, int d,
+                                                         const int32_t* __restrict__ perm,
+                                                         const int64_t* __restrict__ seg,
+                                                         double* __restrict__ part) {
+  __shared__ double sacc[CS_NW][128];
+  const int r = blockIdx.x / CS_SPLIT, sp = blockIdx.x % CS_SPLIT;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int64_t b, e;
+  cs_slice(seg, r, sp, b, e);
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};   // d <= 128: lane j holds coordinates j + 32 q
+  for (int64_t i0 = b + w; i0 < e; i0 += CS_NW * CS_UN) {
+    float v[CS_UN][4];
+#pragma unroll
+    for (int u = 0; u < CS_UN; ++u) {
+      const int64_t i = i0 + (int64_t)u * CS_NW;
+      const float* x = i < e ? xrows + (int64_t)__ldg(perm + i) * xstride : nullptr;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) v[u][q] = (x && lane + 32 * q < d) ? __ldg(x + lane + 32 * q) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < CS_UN; ++u)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[q] += (double)v[u][q];
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) sacc[w][lane + 32 * q] = acc[q];
   __syncthreads();
+  for (int j = threadIdx.x; j < 128; j += blockDim.x) {
+    double sum = 0.0;
+    for (int k = 0; k < CS_NW; ++k) sum += sacc[k][j];
+    part[((int64_t)r * CS_SPLIT + sp) * 128 + j] = sum;
+  }
+}
+
+// one CTA per cell c (128 threads over the coordinates)
+__global__ void k_cell_center(int d, const int64_t* __restrict__ seg,
+                              const int32_t* __restrict__ rank, const double* __restrict__ part,
+                              double* __restrict__ center, unsigned long long* __restrict__ rad2) {
+  const int c = blockIdx.x, r = rank[c], j = threadIdx.x;
+  const int64_t cnt = seg[r + 1] - seg[r];
+  if (j < d) {
+    double sum = 0.0;
+    for (int sp = 0; sp < CS_SPLIT; ++sp) sum += part[((int64_t)r * CS_SPLIT + sp) * 128 + j];
+    center[(int64_t)c * d + j] = cnt > 0 ? sum / (double)cnt : 0.0;
+  }
+  if (j == 0) rad2[c] = 0ull;
+}
+
+__global__ void __launch_bounds__(CS_NW * 32) k_cell_rad(const float* __restrict__ xrows,
+                                                         int xstride, int d,
+                                                         const int32_t* __restrict__ perm,
+                                                         const int64_t* __restrict__ seg,
+                                                         const int32_t* __restrict__ rank,
+                                                         const double* __restrict__ center,
+                                                         unsigned long long* __restrict__ rad2) {
+  __shared__ double sc[128];
+  __shared__ double sred[CS_NW];
+  __shared__ int s_cell;
+  const int r = blockIdx.x / CS_SPLIT, sp = blockIdx.x % CS_SPLIT;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int64_t b, e;
+  cs_slice(seg, r, sp, b, e);
+  if (e <= b) return;
   for (int k = threadIdx.x; k < KC; k += blockDim.x)
-    if (rank[k] == r) s_cell = k;
+    if (rank[k] == r) s_cell = k;   // (rank is a permutation: exactly one writer)
   __syncthreads();
   const int c = s_cell;
-  if (c < 0) return;
-  if (e <= b) {   // empty cell: never near anything
-    if (threadIdx.x == 0) radius[c] = -1.0;
-    for (int j = threadIdx.x; j < d; j += blockDim.x) center[(int64_t)c * d + j] = 0.0;
-    return;
-  }
-  // centre: per-warp partial sums (lane j: coordinates j, j + 32, ...), then across warps
-  double part[4] = {0.0, 0.0, 0.0, 0.0};   // d <= 128
-  for (int64_t i0 = b + w; i0 < e; i0 += NW * UN) {
-    float v[UN][4];
-#pragma unroll
-    for (int u = 0; u < UN; ++u) {
-      const int64_t i = i0 + (int64_t)u * NW;
-      const float* x = i < e ? xrows + (int64_t)__ldg(perm + i) * xstride : nullptr;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) v[u][q] = (x && lane + 32 * q < d) ? __ldg(x + lane + 32 * q) : 0.f;
-    }
-#pragma unroll
-    for (int u = 0; u < UN; ++u)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) part[q] += (double)v[u][q];
-  }
-#pragma unroll
-  for (int q = 0; q < 4; ++q)
-    if (lane + 32 * q < 128) sacc[w][lane + 32 * q] = part[q];
+  for (int j = threadIdx.x; j < 128; j += blockDim.x) sc[j] = j < d ? center[(int64_t)c * d + j] : 0.0;
   __syncthreads();
-  for (int j = threadIdx.x; j < d; j += blockDim.x) {
-    double sum = 0.0;
-    for (int k = 0; k < NW; ++k) sum += sacc[k][j];
-    const double m = sum / (double)(e - b);
-    center[(int64_t)c * d + j] = m;
-    sc[j] = m;
-  }
-  __syncthreads();
-  // radius: per point the squared distance (lanes over coordinates), max over points
+  double cq[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) cq[q] = sc[lane + 32 * q];
+  // per point the squared distance (lanes over coordinates), max over points
   double mx = 0.0;
-  for (int64_t i0 = b + w; i0 < e; i0 += NW * UN) {
-    float v[UN][4];
+  for (int64_t i0 = b + w; i0 < e; i0 += CS_NW * CS_UN) {
+    float v[CS_UN][4];
 #pragma unroll
-    for (int u = 0; u < UN; ++u) {
-      const int64_t i = i0 + (int64_t)u * NW;
+    for (int u = 0; u < CS_UN; ++u) {
+      const int64_t i = i0 + (int64_t)u * CS_NW;
       const float* x = i < e ? xrows + (int64_t)__ldg(perm + i) * xstride : nullptr;
 #pragma unroll
       for (int q = 0; q < 4; ++q) v[u][q] = (x && lane + 32 * q < d) ? __ldg(x + lane + 32 * q) : 0.f;
     }
 #pragma unroll
-    for (int u = 0; u < UN; ++u) {
-      if (i0 + (int64_t)u * NW >= e) break;
-      double s = 0.0;
+    for (int u = 0; u < CS_UN; ++u) {
+      // (a row past the slice holds zeros: it is excluded below)
+      double s2 = 0.0;
 #pragma unroll
       for (int q = 0; q < 4; ++q)
         if (lane + 32 * q < d) {
-          const double t = (double)v[u][q] - sc[lane + 32 * q];
-          s += t * t;
+          const double t = (double)v[u][q] - cq[q];
+          s2 += t * t;
         }
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      mx = fmax(mx, s);
+      for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+      if (i0 + (int64_t)u * CS_NW < e) mx = fmax(mx, s2);
     }
   }
   if (lane == 0) sred[w] = mx;
   __syncthreads();
   if (threadIdx.x == 0) {
     double m = 0.0;
-    for (int k = 0; k < NW; ++k) m = fmax(m, sred[k]);
-    // the fp64 sums above carry relative errors far below 1e-12
-    radius[c] = sqrt(m) * (1.0 + 1e-12) + 1e-300;
+    for (int k = 0; k < CS_NW; ++k) m = fmax(m, sred[k]);
+    // non-negative doubles order like their bit patterns
+    atomicMax(rad2 + c, (unsigned long long)__double_as_longlong(m));
   }
+}
+
+__global__ void k_cell_finish(const int64_t* __restrict__ seg, const int32_t* __restrict__ rank,
+                              const unsigned long long* __restrict__ rad2,
+                              double* __restrict__ radius) {
+  const int c = threadIdx.x;
+  const int r = rank[c];
+  // the fp64 sums above carry relative errors far below 1e-12; an empty cell
+  // is never near anything
+  radius[c] = seg[r + 1] > seg[r]
+                  ? sqrt(__longlong_as_double((long long)rad2[c])) * (1.0 + 1e-12) + 1e-300
+                  : -1.0;
 }
 
 // near[a][w]: bit b of word w set iff cells a and b may hold an in-ball pair
@@ -283,11 +367,12 @@ __global__ void k_block_masks(const int32_t* __restrict__ perm, const int32_t* _
 __global__ void k_gather_rows(const uint8_t* __restrict__ src, int64_t row_bytes,
                               const int32_t* __restrict__ perm, int64_t n,
                               uint8_t* __restrict__ dst) {
-  const int64_t r = blockIdx.x;
+  // 16 lanes per row (a 256-byte row is one 16-byte load per lane), 16 rows per CTA
+  const int64_t r = (int64_t)blockIdx.x * 16 + (threadIdx.x >> 4);
   if (r >= n) return;
   const uint4* s = reinterpret_cast<const uint4*>(src + (int64_t)perm[r] * row_bytes);
   uint4* t = reinterpret_cast<uint4*>(dst + r * row_bytes);
-  for (int i = threadIdx.x; i < (int)(row_bytes / 16); i += blockDim.x) t[i] = s[i];
+  for (int i = threadIdx.x & 15; i < (int)(row_bytes / 16); i += 16) t[i] = s[i];
 }
 
 __global__ void k_gather_f64(const double* __restrict__ src, const int32_t* __restrict__ perm,
@@ -306,7 +391,7 @@ cudaError_t cell_order(const float* xrows, int xstride, int d, int64_t n, int32_
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int dmax = d <= 32 ? 32 : (d <= 64 ? 64 : 128);
-  const size_t smem = sizeof(float) * KC * dmax;
+  const size_t smem = sizeof(float) * KC * (dmax + 1);
   auto kern = d <= 32 ? k_cell_assign<32> : (d <= 64 ? k_cell_assign<64> : k_cell_assign<128>);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
@@ -342,7 +427,7 @@ cudaError_t prune_prepare(const float* xrows, int xstride, int d, int64_t n, dou
   };
   pmark();
   const int dmax = d <= 32 ? 32 : (d <= 64 ? 64 : 128);
-  const size_t smem = sizeof(float) * KC * dmax;
+  const size_t smem = sizeof(float) * KC * (dmax + 1);
   auto kern = d <= 32 ? k_cell_assign<32> : (d <= 64 ? k_cell_assign<64> : k_cell_assign<128>);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
@@ -366,18 +451,21 @@ cudaError_t prune_prepare(const float* xrows, int xstride, int d, int64_t n, dou
   e = launch_segment_ptr(k, n, 32, 0xffull, KC, ps.seg, s, launches);
   if (e != cudaSuccess) return e;
   pmark();
-  k_cell_stats<<<KC, 512, 0, s>>>(xrows, xstride, d, ps.perm, ps.seg, ps.rank, ps.center,
-                                  ps.radius);
+  k_cell_sum<<<KC * CS_SPLIT, CS_NW * 32, 0, s>>>(xrows, xstride, d, ps.perm, ps.seg, ps.part);
+  k_cell_center<<<KC, 128, 0, s>>>(d, ps.seg, ps.rank, ps.part, ps.center, ps.rad2);
+  k_cell_rad<<<KC * CS_SPLIT, CS_NW * 32, 0, s>>>(xrows, xstride, d, ps.perm, ps.seg, ps.rank,
+                                                  ps.center, ps.rad2);
+  k_cell_finish<<<1, KC, 0, s>>>(ps.seg, ps.rank, ps.rad2, ps.radius);
   pmark();
   k_cell_near<<<KC * KC / 256, 256, 0, s>>>(ps.center, ps.radius, d, eps, ps.near);
   const int64_t nblk = (n + 127) / 128;
   k_block_masks<<<(unsigned)((nblk * 32 + 255) / 256), 256, 0, s>>>(ps.perm, ps.cell, n, nblk,
                                                                    ps.near, ps.bmask);
   pmark();
-  k_gather_rows<<<(unsigned)n, 64, 0, s>>>(xop, row_bytes, ps.perm, n, ps.xop_perm);
+  k_gather_rows<<<(unsigned)((n + 15) / 16), 256, 0, s>>>(xop, row_bytes, ps.perm, n, ps.xop_perm);
   k_gather_f64<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(nrm, ps.perm, n, ps.nrm_perm);
   pmark();
-  *launches += 5;
+  *launches += 8;
   if (ptr) {
     cudaEventSynchronize(pe[npe - 1]);
     static const char* nm[] = {"assign", "chain", "keys+sort+seg", "stats", "near+masks",

@@ -324,6 +324,7 @@ cudaError_t launch_unique_scatter(const unsigned long long* keys, int64_t m,
                                   cudaStream_t s, int64_t* launches);
 // cells.cu: tile-level pruning of the tensor-core membership contraction
 constexpr int kPruneCells = 256;
+constexpr int kPruneSplit = 8;   // slices per cell in the centre / radius passes
 struct PruneState {
   int32_t* cell;        // [n] cell of each point
   int32_t* rank;        // [K] position of each cell in the pivot chain
@@ -332,6 +333,8 @@ struct PruneState {
   int64_t* seg;         // [K+1] rank segments of perm
   double* center;       // [K*d]
   double* radius;       // [K] (-1: empty cell)
+  double* part;         // [K][kPruneSplit][128] per-slice coordinate sums (scratch)
+  unsigned long long* rad2;   // [K] bits of the max squared distance to the centre
   uint32_t* near;       // [K][K/32]
   uint32_t* bmask;      // [ceil(n/128)][K/32] cells near some row of the block
   uint8_t* xop_perm;    // [n][row_bytes] the A operand in permuted order
