@@ -129,13 +129,26 @@ __global__ void k_pivot_dist(const float* __restrict__ xrows, int xstride, int d
   dist[a * KC + b] = s;
 }
 
-// nearest-neighbour chain over the pivots from pivot 0 (one warp): rank[k]
-__global__ void k_pivot_chain(const float* __restrict__ dist /* [KC][KC] */,
-                              int32_t* __restrict__ rank) {
-  const int lane = threadIdx.x;
+// nearest-neighbour chain over the pivots from pivot 0: rank[k].  The chain is
+// serial (256 steps, each an argmin over one row of the distance matrix), so
+// the whole CTA first stages the matrix's upper triangle in shared memory
+// (128 KB) and one warp then walks it without a global round trip per step.
+constexpr int kTriWords = KC * (KC - 1) / 2;
+__device__ __forceinline__ int tri_index(int a, int b) {   // a < b
+  return a * (2 * KC - a - 1) / 2 + (b - a - 1);
+}
+__global__ void __launch_bounds__(1024) k_pivot_chain(const float* __restrict__ dist /* [KC][KC] */,
+                                                      int32_t* __restrict__ rank) {
+  extern __shared__ float stri[];   // [kTriWords]
   __shared__ uint32_t svis[KW];
-  if (lane < KW) svis[lane] = 0u;
-  __syncwarp();
+  for (int t = threadIdx.x; t < KC * KC; t += blockDim.x) {
+    const int a = t / KC, b = t - a * KC;
+    if (a < b) stri[tri_index(a, b)] = dist[t];
+  }
+  if (threadIdx.x < KW) svis[threadIdx.x] = 0u;
+  __syncthreads();
+  if (threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
   int cur = 0;
   for (int r = 0; r < KC; ++r) {
     if (lane == 0) {
@@ -148,11 +161,15 @@ __global__ void k_pivot_chain(const float* __restrict__ dist /* [KC][KC] */,
 #pragma unroll
     for (int i = 0; i < KC / 32; ++i) {
       const int k = lane + 32 * i;
-      const bool seen = (svis[k >> 5] >> (k & 31)) & 1u;
-      const float v = __ldcg(dist + cur * KC + k);
-      if (!seen && (v < bv || (v == bv && k < bi))) {
-        bv = v;
-        bi = k;
+      const bool seen = (svis[k >> 5] >> (k & 31)) & 1u;   // (cur itself is seen)
+      if (!seen) {
+        // dist[cur][k] and dist[k][cur] are the same fp32 sum (k_pivot_dist adds
+        // the squared differences in the same coordinate order)
+        const float v = cur < k ? stri[tri_index(cur, k)] : stri[tri_index(k, cur)];
+        if (v < bv || (v == bv && k < bi)) {
+          bv = v;
+          bi = k;
+        }
       }
     }
     for (int o = 16; o > 0; o >>= 1) {
@@ -279,20 +296,38 @@ __global__ void __launch_bounds__(CS_NW * 32) k_cell_rad(const float* __restrict
 #pragma unroll
       for (int q = 0; q < 4; ++q) v[u][q] = (x && lane + 32 * q < d) ? __ldg(x + lane + 32 * q) : 0.f;
     }
+    // each lane's partial squared distances of the 8 rows, then a transposing
+    // butterfly (4 + 2 + 1 + 1 + 1 exchanges instead of 5 per row): lane l
+    // ends with the whole sum of row 4 l[4] + 2 l[3] + l[2]
+    double s2[CS_UN];
 #pragma unroll
     for (int u = 0; u < CS_UN; ++u) {
-      // (a row past the slice holds zeros: it is excluded below)
-      double s2 = 0.0;
+      s2[u] = 0.0;
 #pragma unroll
       for (int q = 0; q < 4; ++q)
         if (lane + 32 * q < d) {
           const double t = (double)v[u][q] - cq[q];
-          s2 += t * t;
+          s2[u] += t * t;
         }
-      for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
-      if (i0 + (int64_t)u * CS_NW < e) mx = fmax(mx, s2);
     }
+    static_assert(CS_UN == 8, "the butterfly below folds eight rows");
+#pragma unroll
+    for (int h = 4, o = 16; h >= 1; h >>= 1, o >>= 1) {
+      const bool hi = (lane & o) != 0;
+#pragma unroll
+      for (int k = 0; k < h; ++k) {
+        const double send = hi ? s2[k] : s2[k + h];
+        const double keep = hi ? s2[k + h] : s2[k];
+        s2[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+      }
+    }
+    s2[0] += __shfl_xor_sync(0xffffffffu, s2[0], 2);
+    s2[0] += __shfl_xor_sync(0xffffffffu, s2[0], 1);
+    const int urow = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+    // (a row past the slice holds zeros: excluded)
+    if (i0 + (int64_t)urow * CS_NW < e) mx = fmax(mx, s2[0]);
   }
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   if (lane == 0) sred[w] = mx;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -398,7 +433,10 @@ cudaError_t cell_order(const float* xrows, int xstride, int d, int64_t n, int32_
   if (e != cudaSuccess) return e;
   kern<<<sms * 2, 256, smem, s>>>(xrows, xstride, d, n, cell);
   k_pivot_dist<<<KC, KC, 0, s>>>(xrows, xstride, d, n, pdist);
-  k_pivot_chain<<<1, 32, 0, s>>>(pdist, rank);
+  e = cudaFuncSetAttribute(k_pivot_chain, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)(kTriWords * sizeof(float)));
+  if (e != cudaSuccess) return e;
+  k_pivot_chain<<<1, 1024, kTriWords * sizeof(float), s>>>(pdist, rank);
   k_cell_keys<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(cell, rank, n, *keys);
   *launches += 4;
   e = cudaGetLastError();
@@ -435,7 +473,10 @@ cudaError_t prune_prepare(const float* xrows, int xstride, int d, int64_t n, dou
   kern<<<sms * 2, 256, smem, s>>>(xrows, xstride, d, n, ps.cell);
   pmark();
   k_pivot_dist<<<KC, KC, 0, s>>>(xrows, xstride, d, n, ps.pdist);
-  k_pivot_chain<<<1, 32, 0, s>>>(ps.pdist, ps.rank);
+  e = cudaFuncSetAttribute(k_pivot_chain, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)(kTriWords * sizeof(float)));
+  if (e != cudaSuccess) return e;
+  k_pivot_chain<<<1, 1024, kTriWords * sizeof(float), s>>>(ps.pdist, ps.rank);
   pmark();
   k_cell_keys<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(ps.cell, ps.rank, n, keys);
   *launches += 3;
