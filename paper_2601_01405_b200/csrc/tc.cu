@@ -194,6 +194,11 @@ __device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* tm, int x, in
                "r"(x), "r"(y)
                : "memory");
 }
+__device__ __forceinline__ uint32_t lds32(uint32_t saddr) {   // shared-space load (no generic path)
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(saddr) : "memory");
+  return v;
+}
 __device__ __forceinline__ void fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
@@ -1139,6 +1144,8 @@ __global__ void __launch_bounds__(tc_threads<KIND, BN, MODE, PR>(), 1)
       uint32_t tcnt = 0;
       const uint32_t tlane = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(grp * (BN / EG));
       const uint32_t* qr_base = reinterpret_cast<const uint32_t*>(sm + S::QR_OFF);
+      const uint32_t th8 = lds32(su32(sthr8));   // (constant per launch)
+      const uint32_t kc_a = su32(kc), bc_a = su32(bc), sq8_a = su32(sq8);
       uint32_t uu = 0;   // units seen (the producer's ring order)
       for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x, ++uu) {
         const int64_t mb = n_chunks == 1 ? u : u / n_chunks, ch = n_chunks == 1 ? 0 : u % n_chunks;
@@ -1150,7 +1157,7 @@ __global__ void __launch_bounds__(tc_threads<KIND, BN, MODE, PR>(), 1)
         // (every warp waits for the slot's copy before it releases the slot, so
         // the producer never re-arms a barrier whose copy is still in flight;
         // the copy was issued with the unit's A block and has long landed)
-        mbar_wait(&qr_full[qs], (uu / S::NQR) & 1u);
+        TC_TWAIT(9, mbar_wait(&qr_full[qs], (uu / S::NQR) & 1u));   // (L1T diagnostics: slot 9)
         for (int t = t0; t < t1; ++t) {
           const uint32_t buf = tcnt & (uint32_t)(NBUF - 1);
           TC_TWAIT(5, mbar_wait(&t_full[buf], (phase >> buf) & 1u));
@@ -1219,23 +1226,30 @@ __global__ void __launch_bounds__(tc_threads<KIND, BN, MODE, PR>(), 1)
               rq[2] = c;
               rq[3] = e;
             }
-            const uint32_t th8 = *sthr8;
+            // (32-bit masks, 32-bit column index, two independent SAD chains:
+            // the loop is per-lane and latency-bound)
+            const uint32_t jg32 = (uint32_t)jg;
 #pragma unroll
-            for (int p = 0; p < NP; ++p) {
-              unsigned long long cand =
-                  ((unsigned long long)cm[2 * p + 1] << 32) | cm[2 * p];
+            for (int h = 0; h < 2 * NP; ++h) {
+              uint32_t cand = cm[h];
               while (cand) {
-                const int b = __ffsll((long long)cand) - 1;
-                cand &= cand - 1ull;
-                // bit b of the 64-bit mask -> column
-                const int64_t j = jg + 64 * p + 32 * (b >> 5) + 4 * (b & 7) + ((b >> 3) & 3);
-                if (l1t_sad(rq, j) < th8)
+                const uint32_t b = 31u - (uint32_t)__clz((int)(cand & (0u - cand)));
+                cand &= cand - 1u;
+                // bit b of mask h -> column
+                const uint32_t j = jg32 + 32u * h + 4u * (b & 7u) + (b >> 3);
+                uint32_t a0, a1, a2, a3;
+                asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3)
+                             : "r"(sq8_a + j * 16u));
+                const uint32_t sad = vsad4(rq[1], a1, vsad4(rq[0], a0, 0u)) +
+                                     vsad4(rq[3], a3, vsad4(rq[2], a2, 0u));
+                if (sad < th8)
                   append(2, ((unsigned long long)prow << 32) | (unsigned long long)j);
               }
             }
           }
           __syncwarp();
-          if (*kc > S::KW / 2 || *bc > S::BW / 2) flush();
+          if (lds32(kc_a) > S::KW / 2 || lds32(bc_a) > S::BW / 2) flush();
 #ifdef BM_TC_WTRACE
           wacc[7] += clock64() - s7;   // (L1T diagnostics: slot 7 = candidates + flush)
 #endif
