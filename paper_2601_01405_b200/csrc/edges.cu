@@ -141,11 +141,22 @@ __global__ void __launch_bounds__(UQ_NT) k_unique_compact(const unsigned long lo
   const int64_t i0 = tile * UQ_TILE + (int64_t)threadIdx.x * UQ_IPT;
   unsigned long long kv[UQ_IPT];
   uint32_t keep = 0u, cnt = 0u;
+  const bool whole = i0 + UQ_IPT <= m;   // the thread's 64 bytes in four 16-byte loads
+  if (whole) {
+    const ulonglong2* kp = reinterpret_cast<const ulonglong2*>(keys + i0);
+#pragma unroll
+    for (int k = 0; k < UQ_IPT / 2; ++k) {
+      const ulonglong2 v = kp[k];
+      kv[2 * k] = v.x;
+      kv[2 * k + 1] = v.y;
+    }
+  }
+  const unsigned long long kprev = i0 > 0 && i0 < m ? keys[i0 - 1] : 0ull;
 #pragma unroll
   for (int k = 0; k < UQ_IPT; ++k) {
     const int64_t i = i0 + k;
-    kv[k] = i < m ? keys[i] : 0ull;
-    const bool f = i < m && (i == 0 || kv[k] != (k > 0 ? kv[k - 1] : keys[i - 1]));
+    if (!whole) kv[k] = i < m ? keys[i] : 0ull;
+    const bool f = i < m && (i == 0 || kv[k] != (k > 0 ? kv[k - 1] : kprev));
     keep |= (f ? 1u : 0u) << k;
     cnt += f ? 1u : 0u;
   }
