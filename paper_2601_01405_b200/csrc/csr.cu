@@ -100,9 +100,8 @@ cudaError_t launch_pair_counts(const int64_t* pt_ptr, int64_t n, int64_t* cnt, c
 }
 
 // One warp per point: the C(t,2) pairs (a, c), a < c, of the point's row in
-// row-major order over the strict upper triangle.  The lanes stride over the
-// flat pair index q (every lane busy, coalesced key stores) and decode
-// (a, c) from it: row a starts at S(a) = a (2 t - a - 1) / 2.
+// row-major order over the strict upper triangle; the warp walks the rows and
+// its lanes stride over the columns of each row (O(1) per pair).
 __global__ void k_pair_emit(const int64_t* __restrict__ pt_ptr, const int32_t* __restrict__ pt_lm,
                             int64_t n, const int64_t* __restrict__ off, int lbits,
                             unsigned long long* __restrict__ keys) {
@@ -111,17 +110,12 @@ __global__ void k_pair_emit(const int64_t* __restrict__ pt_ptr, const int32_t* _
   if (p >= n) return;
   const int64_t b = pt_ptr[p], t = pt_ptr[p + 1] - b;
   if (t < 2) return;
-  const int64_t o = off[p];
-  const int64_t np = t * (t - 1) / 2;
-  const double tw = (double)(2 * t - 1);
-  for (int64_t q = lane; q < np; q += 32) {
-    // a = floor((2t - 1 - sqrt((2t - 1)^2 - 8 q)) / 2), corrected for rounding
-    int64_t a = (int64_t)((tw - sqrt(tw * tw - 8.0 * (double)q)) * 0.5);
-    a = a < 0 ? 0 : (a > t - 2 ? t - 2 : a);
-    while (a * (2 * t - a - 1) / 2 > q) --a;
-    while ((a + 1) * (2 * t - a - 2) / 2 <= q) ++a;
-    const int64_t c = a + 1 + (q - a * (2 * t - a - 1) / 2);
-    keys[o + q] = ((unsigned long long)pt_lm[b + a] << lbits) | (unsigned long long)pt_lm[b + c];
+  int64_t o = off[p];
+  for (int64_t a = 0; a + 1 < t; ++a) {
+    const unsigned long long hi = (unsigned long long)pt_lm[b + a] << lbits;
+    for (int64_t c = a + 1 + lane; c < t; c += 32)
+      keys[o + (c - a - 1)] = hi | (unsigned long long)pt_lm[b + c];
+    o += t - 1 - a;
   }
 }
 
