@@ -324,7 +324,7 @@ cudaError_t launch_unique_scatter(const unsigned long long* keys, int64_t m,
                                   cudaStream_t s, int64_t* launches);
 // cells.cu: tile-level pruning of the tensor-core membership contraction
 constexpr int kPruneCells = 256;
-constexpr int kPruneSplit = 8;   // slices per cell in the centre / radius passes
+constexpr int kPruneSplit = 32;  // slices per cell in the centre / radius passes
 struct PruneState {
   int32_t* cell;        // [n] cell of each point
   int32_t* rank;        // [K] position of each cell in the pivot chain
